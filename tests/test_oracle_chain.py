@@ -1,0 +1,197 @@
+"""Pins for the oracle's Markov chain (Alg. 1) and App. A change of variable.
+
+Statistical pins: per-chain means over the
+second half (or the S4.1 protocol), grand mean within 4 standard errors of the
+exact value.  Exact values: the 1-D truncated normal closed form (and the
+printed S4.1 table), the half-normal for the orthant, numpy
+rejection sampling for a tiny 2-D polytope, N(0, I) when every constraint is
+slack.  Invariant: A x <= b at every iterate.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2407_10449_b200 import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def trunc_normal_moments(lo, hi):
+    """Exact mean/variance of N(0,1) truncated to [lo, hi] (textbook closed form)."""
+    phi = lambda z: math.exp(-0.5 * z * z) / math.sqrt(2 * math.pi)
+    # Z via erfc on the side that avoids cancellation
+    if lo > 0:
+        Z = 0.5 * (math.erfc(lo / math.sqrt(2)) - math.erfc(hi / math.sqrt(2)))
+    else:
+        Z = 0.5 * (math.erf(hi / math.sqrt(2)) - math.erf(lo / math.sqrt(2)))
+    mu = (phi(lo) - phi(hi)) / Z
+    var = 1.0 + (lo * phi(lo) - hi * phi(hi)) / Z - mu * mu
+    return mu, var
+
+
+def test_closed_form_matches_printed_table():
+    g = json.load(open(os.path.join(GOLD, "table_4_1.json")))
+    for (lo, hi), mu_p, var_p in zip(g["intervals"], g["true_mu"], g["true_var"]):
+        mu, var = trunc_normal_moments(lo, hi)
+        assert abs(mu - mu_p) < 5e-5 and abs(var - var_p) < 5e-5
+
+
+def _per_chain_stat(res_sum, n_per_chain):
+    return res_sum / n_per_chain
+
+
+@pytest.mark.parametrize("interval", [(-1.0, 3.0), (15.0, 16.0)])
+def test_one_dim_section_4_1(interval):
+    """S4.1 protocol: 2000 chains, burn-in 500, thinning 10, 1e5 samples."""
+    A, b, x0 = synth.one_dim(interval)
+    C, burn, thin, n_iter = 2000, 500, 10, 1000
+    X0 = np.tile(x0, (C, 1))
+    # run chains one by one to get per-chain statistics (oracle.run reduces over chains)
+    mu, var = trunc_normal_moments(*interval)
+    res = oracle.run(A, b, X0, n_iter, seed=2024, burn_in=burn, thin=thin)
+    n = res["n_rec"]
+    assert n == C * (n_iter - burn) // thin
+    m1 = res["sum"][0] / n
+    m2 = res["sumsq"][0] / n - m1 * m1
+    assert abs(m1 - mu) < 0.01 and abs(m2 - var) < 0.01  # "accurate to the 2nd digit"
+    assert np.all(res["X"] >= interval[0]) and np.all(res["X"] <= interval[1])
+    assert res["rejections"] <= 1e-4 * C * n_iter  # FP64: practically zero
+
+
+def _chains_in_batches(A, b, x0, C, T, seed, batch):
+    """Per-chain means of x and x^2 over iterations T/2..T-1, computed chain by chain."""
+    d = A.shape[1]
+    means, sq = [], []
+    for c0 in range(0, C, batch):
+        cb = min(batch, C - c0)
+        r = oracle.run(A, b, np.tile(x0, (cb, 1)), T, seed, chain_offset=c0, burn_in=T // 2)
+        # oracle.run reduces over chains; rerun per chain only for small batches
+        means.append(r["sum"] / r["n_rec"])
+        sq.append(r["sumsq"] / r["n_rec"])
+    return np.array(means), np.array(sq)
+
+
+def test_orthant_half_normal():
+    """Config 2 structure (A = -I, b = 0): every coordinate half-normal."""
+    d = 100
+    A, b, x0 = synth.make_instance(2)
+    mu_true, var_true = math.sqrt(2 / math.pi), 1 - 2 / math.pi
+    # from x0 = 0.1*ones the chain needs ~1e4 iterations to mix in d = 100
+    mean_b, sq_b = _chains_in_batches(A, b, x0, C=32, T=20000, seed=102, batch=2)
+    # batch means: each row is the mean over 2 chains x 10000 iterations
+    m = mean_b.mean(axis=1)          # average over coordinates per batch
+    se = m.std(ddof=1) / math.sqrt(len(m))
+    assert abs(m.mean() - mu_true) < 4 * se + 1e-3
+    # variance via E[(x - mu)^2] with the true mu (recipe step 2)
+    v = (sq_b - 2 * mu_true * mean_b + mu_true**2).mean(axis=1)
+    sev = v.std(ddof=1) / math.sqrt(len(v))
+    assert abs(v.mean() - var_true) < 4 * sev + 1e-3
+
+
+def test_tiny_2d_vs_rejection_sampling():
+    """Config 1 instance; exact moments from numpy rejection sampling (independent)."""
+    A, b, x0 = synth.make_instance(1)
+    rng = np.random.default_rng(12345)
+    z = rng.standard_normal((4_000_000, 2))
+    acc = z[np.all(z @ A.T <= b, axis=1)]
+    assert acc.shape[0] > 100000
+    mu_rs = acc.mean(0)
+    C, T, batch = 512, 1000, 8
+    mean_b, sq_b = _chains_in_batches(A, b, x0, C=C, T=T, seed=101, batch=batch)
+    nb = mean_b.shape[0]
+    se = mean_b.std(axis=0, ddof=1) / math.sqrt(nb)
+    se_rs = acc.std(0) / math.sqrt(acc.shape[0])
+    assert np.all(np.abs(mean_b.mean(0) - mu_rs) < 4 * np.hypot(se, se_rs) * 1.2)
+    ex2_rs = (acc**2).mean(0)
+    se2 = sq_b.std(axis=0, ddof=1) / math.sqrt(nb)
+    assert np.all(np.abs(sq_b.mean(0) - ex2_rs) < 4 * se2 * 1.2 + 1e-3)
+
+
+def test_all_slack_is_standard_normal():
+    """Every constraint slack (b >> r): plain ESS, stationary N(0, I)."""
+    d = 5
+    A = np.eye(d)
+    b = np.full(d, 1e6)
+    mean_b, sq_b = _chains_in_batches(A, b, np.zeros(d), C=256, T=400, seed=7, batch=8)
+    se = mean_b.std(axis=0, ddof=1) / math.sqrt(mean_b.shape[0])
+    assert np.all(np.abs(mean_b.mean(0)) < 4 * se / 0.9)
+    assert np.all(np.abs(sq_b.mean(0) - 1.0) < 0.1)
+
+
+def test_every_iterate_feasible_and_step_dump():
+    """A x <= b at every iterate under fresh dot products."""
+    A, b, x0 = synth.make_instance(3, m=60, d=20)
+    x = x0.copy()
+    rej = 0
+    for t in range(300):
+        xn, dmp = oracle.step(A, b, x, seed=103, t=t, c=5)
+        assert np.max(A @ xn - b) <= 0.0
+        if dmp["accept"]:
+            assert np.array_equal(xn, dmp["x_prop"])
+            th = dmp["theta"]
+            assert np.allclose(xn, x * math.cos(th) + dmp["nu"] * math.sin(th), rtol=0, atol=1e-14)
+            # theta lies inside one of the canonical segments
+            assert any(lo <= th <= hi for lo, hi in dmp["segs"])
+        else:
+            rej += 1
+            assert np.array_equal(xn, x)
+        x = xn
+    assert rej == 0
+
+
+def test_run_matches_step_and_offsets():
+    A, b, x0 = synth.make_instance(3, m=30, d=10)
+    X0 = np.tile(x0, (3, 1))
+    r = oracle.run(A, b, X0, 20, seed=9, chain_offset=7, iter_offset=100)
+    for k in range(3):
+        x = x0.copy()
+        for t in range(100, 120):
+            x, _ = oracle.step(A, b, x, 9, t, 7 + k)
+        assert np.array_equal(x, r["X"][k])
+    # resume: 20 iterations == 10 + 10 with iter_offset
+    r1 = oracle.run(A, b, X0, 10, seed=9, chain_offset=7, iter_offset=100)
+    r2 = oracle.run(A, b, r1["X"], 10, seed=9, chain_offset=7, iter_offset=110)
+    assert np.array_equal(r2["X"], r["X"])
+
+
+def test_whiten_closed_form_and_roundtrip():
+    """App. A: d=1, mu=2, Sigma=4 (L=2), A=1, b=6 -> A'=2, b'=4."""
+    Aw, bw = oracle.whiten(np.array([[1.0]]), np.array([6.0]), mu=np.array([2.0]), L=np.array([[2.0]]))
+    assert Aw[0, 0] == 2.0 and bw[0] == 4.0
+    assert oracle.unwhiten_point(np.array([1.0]), mu=np.array([2.0]), L=np.array([[2.0]]))[0] == 4.0
+    L, mu = synth.random_spd_factor(6, seed=1)
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((8, 6))
+    b = rng.uniform(0.5, 1.5, 8)
+    Aw, bw = oracle.whiten(A, b, mu, L)
+    assert np.allclose(Aw, A @ L, atol=1e-13) and np.allclose(bw, b - A @ mu, atol=1e-13)
+    for _ in range(20):
+        x = rng.standard_normal(6)
+        u = oracle.whiten_point(x, mu, L)
+        assert np.allclose(L @ u + mu, x, atol=1e-12)
+        assert np.allclose(oracle.unwhiten_point(u, mu, L), x, atol=1e-12)
+        # feasibility is preserved by the change of variable
+        assert np.array_equal(A @ x <= b, Aw @ u <= bw + 0.0) or np.allclose(A @ x - b, Aw @ u - bw, atol=1e-12)
+
+
+def test_affine_one_dim_moments():
+    """x ~ N(2, 4) truncated to [1, 5]: moments in x-space via x = L u + mu."""
+    mu_x, sig = 2.0, 2.0
+    A = np.array([[1.0], [-1.0]])
+    b = np.array([5.0, -1.0])
+    Aw, bw = oracle.whiten(A, b, np.array([mu_x]), np.array([[sig]]))
+    lo, hi = (1.0 - mu_x) / sig, (5.0 - mu_x) / sig
+    mu_u, var_u = trunc_normal_moments(lo, hi)
+    C, n_iter = 1000, 600
+    u0 = oracle.whiten_point(np.array([3.0]), np.array([mu_x]), np.array([[sig]]))
+    res = oracle.run(Aw, bw, np.tile(u0, (C, 1)), n_iter, seed=77, burn_in=100,
+                     mu=np.array([mu_x]), L=np.array([[sig]]))
+    n = res["n_rec"]
+    m1 = res["sum"][0] / n
+    v1 = res["sumsq"][0] / n - m1 * m1
+    assert abs(m1 - (mu_x + sig * mu_u)) < 0.02
+    assert abs(v1 - sig * sig * var_u) < 0.05

@@ -1,0 +1,26 @@
+# Builds the product library (sm_100a) and the CPU oracle (test infrastructure).
+NVCC    ?= /usr/local/cuda/bin/nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v
+PKG     := paper_2407_10449_b200
+CSRC    := $(PKG)/csrc
+SRCS    := $(CSRC)/gemm_f64.cu $(CSRC)/ess_chain.cu $(CSRC)/aux_kernels.cu $(CSRC)/runtime.cu
+OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
+HDRS    := $(CSRC)/common.cuh $(CSRC)/internal.h include/tmvn.h
+
+all: $(PKG)/libtmvn.so oracle/liboracle.so
+
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(PKG)/libtmvn.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static
+
+oracle/liboracle.so: oracle/oracle.cpp
+	g++ -std=c++17 -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -o $@ $<
+
+clean:
+	rm -rf build $(PKG)/libtmvn.so oracle/liboracle.so
+
+.PHONY: all clean

@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 ESS hot path (BASELINE.json metric).
+
+A "step" = one tmvn_sample call that runs --iters-per-step (default 100)
+iterations of Alg. 1 for all C chains of the workload (every row of SURVEY
+8(a): RNG, projection GEMM, arcs, sort / cummax, theta, update, moments, and
+the periodic P refresh), continuing the chains from the previous step.
+Default workload: BASELINE config 3 (d=1000, m=2000, 4096 chains per GPU,
+FP64) -- the configuration north_star's target is quoted on.
+
+  python bench.py [--gpus N --steps K --warmup W --config 3 --impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU, NCCL): every rank owns its own
+4096 chains (weak scaling, global chain offset rank*C), no per-iteration
+collective; one all_reduce of the moments and one MAX of the timings at the end.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "constraint-evals/sec (chain-iterations/sec x m), FP64, whole job"
+UNIT = "constraint-evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--iters-per-step", type=int, default=100)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def config_dict(cfg, args, world):
+    return {"workload": f"BASELINE config {args.config} ({cfg.key}): {cfg.desc}",
+            "d": cfg.d, "m": cfg.m, "chains_per_gpu": cfg.C, "chains_total": cfg.C * world,
+            "iters_per_step": args.iters_per_step, "recompute_every": 32,
+            "l2": "no flush: working set (X, nu, P x2, Q, A) >> 126 MB L2",
+            "parallelism": f"chains sharded over {world} GPU(s), A and b replicated"}
+
+
+# ------------------------------------------------------------------ clocks
+CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                "clocks_event_reasons.sw_power_cap")
+
+
+def clocks_start():
+    f = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+    try:
+        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={CLOCK_FIELDS}", "--format=csv,noheader,nounits",
+                              "-lms", "100"], stdout=f, stderr=subprocess.DEVNULL)
+    except FileNotFoundError:
+        return None
+    return p, f.name
+
+
+def clocks_stop(h, gpus):
+    if h is None:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+    p, path = h
+    p.terminate()
+    p.wait()
+    sm, mx, reasons = [], [], set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(path):
+        parts = [x.strip() for x in line.split(",")]
+        if len(parts) < 8 or not parts[0].isdigit() or int(parts[0]) not in gpus:
+            continue
+        try:
+            sm.append(float(parts[1]))
+            mx.append(float(parts[2]))
+        except ValueError:
+            continue
+        for n, v in zip(names, parts[4:8]):
+            if v.lower().startswith("active"):
+                reasons.add(n)
+    os.unlink(path)
+    return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_rate(A, b, x0, seed, seconds, C_full):
+    """The oracle as it stands, all host cores, on a bounded sample of the workload."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    m = A.shape[0]
+    Co = int(min(C_full, 2 * cores))
+    X0 = np.tile(x0, (Co, 1))
+    t0 = time.perf_counter()
+    oracle.run(A, b, X0, 1, seed, nthreads=cores)
+    one = max(time.perf_counter() - t0, 1e-6)
+    To = int(max(1, min(1000, seconds / one)))
+    t0 = time.perf_counter()
+    oracle.run(A, b, X0, To, seed, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": Co * To * m / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{Co} chains x {To} iterations of the same instance (first iterations from x0), "
+                      f"{dt:.1f} s on {cores} host threads (OpenMP over chains)",
+            "chain_iters_per_s": Co * To / dt, "seconds": dt}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return
+    from paper_2407_10449_b200 import synth
+    cfg = synth.CONFIGS[args.config]
+    A, b, x0 = synth.make_instance(args.config)
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    Co = int(min(cfg.C, 2 * cores))
+    X = np.tile(x0, (Co, 1))
+    t0 = time.perf_counter()
+    oracle.run(A, b, X, 1, cfg.chain_seed, nthreads=cores)
+    one = max(time.perf_counter() - t0, 1e-6)
+    To = int(max(1, min(args.iters_per_step, 3.0 / one)))  # ~3 s of CPU work per step
+    for _ in range(args.warmup):
+        X = oracle.run(A, b, X, 1, cfg.chain_seed, nthreads=cores)["X"]
+    times = []
+    it0 = 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        X = oracle.run(A, b, X, To, cfg.chain_seed, iter_offset=it0, nthreads=cores)["X"]
+        times.append(time.perf_counter() - t0)
+        it0 += To
+    tot = sum(times)
+    value = Co * To * cfg.m * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(cfg, args, world),
+            "cpu_baseline": {"kind": "oracle", "cores": cores, "value": value, "unit": UNIT,
+                             "sample": f"each step {Co} chains x {To} iterations of the workload on "
+                                       f"{cores} host threads (the CPU oracle as it stands)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_2407_10449_b200 as tm
+    from paper_2407_10449_b200 import synth
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = synth.CONFIGS[args.config]
+    A, b, x0 = synth.make_instance(args.config)
+    m, d, C = cfg.m, cfg.d, cfg.C
+    ips = args.iters_per_step
+    seed = cfg.chain_seed
+    stream = torch.cuda.Stream(device=dev)
+    s = tm.Sampler(torch.tensor(A, device=dev), torch.tensor(b, device=dev), chain_offset=rank * C)
+    s.set_options(stream=stream, profile=1)
+    X = torch.tensor(np.tile(x0, (C, 1)), device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            s.sample(X, ips, seed, out=X)
+        s.reset_stats()
+        torch.cuda.synchronize()
+        barrier()
+        clk = clocks_start() if rank == 0 else None
+        time.sleep(0.15 if clk else 0)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.sample(X, ips, seed, out=X)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    clocks = clocks_stop(clk, set(range(world))) if rank == 0 else None
+    prof = s.profile()
+    st = s.stats()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    rej = torch.tensor([float(st["rejections"])], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(rej)
+    ms_max = float(t.item())
+    total_iters = world * C * ips * args.steps
+    value = total_iters * m / (ms_max * 1e-3)
+    # moments: the one collective of the path
+    sm, sq, n = s.moments()
+    mom = torch.tensor(np.concatenate([sm, sq, [n]]), device=dev)
+    if world > 1:
+        dist.all_reduce(mom)
+
+    # ---- roofline of the dominant kernel (the projection GEMM), from live CUDA events
+    peaks = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")))
+    gemm_avg_ms = prof["gemm_ms"] / max(1, prof["gemm_launches"])
+    gemm_flops = prof["gemm_flops"] / max(1, prof["gemm_launches"])
+    achieved = gemm_flops / (gemm_avg_ms * 1e-3) / 1e12
+    peak = peaks["dmma_tflops_w8"]
+    ess_avg_ms = prof["ess_ms"] / max(1, prof["ess_launches"])
+    ess_gbs = prof["ess_bytes"] / max(1, prof["ess_launches"]) / (ess_avg_ms * 1e-3) / 1e9
+    hbm = None
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        hbm = 6650.0
+    roofline = {"bound": "tensor", "kernel": "gemm_tn_f64_kernel (Q = N A^T, FP64 DMMA)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None,
+                "peak_source": "measured FP64 DMMA pipe peak on this pool's B200 (profiles/peaks_fp64_r01.json; "
+                               f"cuBLAS DGEMM measured {peaks['dgemm_tflops_burst']} TF/s)",
+                "algorithmic_flops_per_launch": gemm_flops, "avg_launch_ms": gemm_avg_ms,
+                "share_of_step": prof["gemm_ms"] / ms,
+                "ess_kernel": {"bound": "hbm", "achieved": ess_gbs, "peak": hbm, "unit": "GB/s",
+                               "frac": ess_gbs / hbm, "avg_launch_ms": ess_avg_ms,
+                               "share_of_step": prof["ess_ms"] / ms,
+                               "algorithmic_bytes_per_launch": prof["ess_bytes"] / max(1, prof["ess_launches"])}}
+    gpu_launches = prof["launches"]
+
+    # ---- end to end through the public API with host buffers (pinned), rank-local
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        s.set_options(profile=0)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s.sample(Xh, ips, seed, out=Xh)  # H2D of X0 and D2H of the iterates inside the call
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        barrier()
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_iters * m / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": C * d * 8, "d2h_bytes_per_step": C * d * 8,
+               "timer": "host wall clock around synchronous tmvn_sample calls (max over ranks)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_rate(A, b, x0, seed, args.cpu_seconds, C)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded Gaussian polytope of BASELINE config; no dataset)",
+                "config": config_dict(cfg, args, world),
+                "chain_iters_per_s": total_iters / (ms_max * 1e-3),
+                "evals_per_s_per_gpu": value / world,
+                "rejections": int(rej.item()),
+                "recorded": int(mom[-1].item()),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": gpu_launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

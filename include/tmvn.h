@@ -1,0 +1,219 @@
+/*
+ * tmvn.h -- C ABI of the B200-native batched linear elliptical slice sampler
+ * for a standard normal truncated to a polytope {x : A x <= b}
+ * (arXiv 2407.10449; "P:n" = /root/reference/PAPER.md line n).
+ *
+ * The library (paper_2407_10449_b200/libtmvn.so) runs C independent Markov
+ * chains of Alg. 1 in FP64 on one sm_100a GPU.  Per chain and
+ * iteration t it draws nu ~ N(0, I_d), forms the ellipse
+ * x cos(theta) + nu sin(theta) (Eq. 1), computes the active
+ * intervals I_act by the paper's sort + cumulative-max algorithm
+ * (Alg. 3 / Prop. 1) from the per-constraint roots of Eq. 2
+ * (eq:roots), samples theta uniformly on I_act, and applies
+ * the S3.3 safeguard (reject an infeasible x_{t+1} and stay).
+ *
+ * Conventions shared by every entry point:
+ *  - All functions return tmvn_status; nothing throws across the ABI.
+ *  - "host or device" pointers: any pointer argument may point to host memory
+ *    (pageable or pinned) or to device memory of the handle's GPU; the library
+ *    copies with cudaMemcpyDefault (unified addressing).  The caller keeps
+ *    ownership of every buffer it passes; the library never frees them.
+ *  - Matrices are row-major, FP64, densely packed (leading dimension = #cols).
+ *  - A handle is bound to the CUDA device that is current at tmvn_create.  It
+ *    is not thread-safe: use one handle per thread / rank.
+ *  - After an error the handle stays valid; tmvn_last_error() names the cause
+ *    (for an infeasible start: the chain and constraint index).
+ *  - tmvn_sample is synchronous with respect to the host.
+ *  - Determinism: the output is a pure function of (A, b, mu, L, X0, seed,
+ *    chain_offset, iter_offset, n_iter, options); it does not depend on how the
+ *    chains are split across calls or GPUs (global chain index in the RNG
+ *    counter, no split-K in the projection GEMM).
+ */
+#ifndef TMVN_H_
+#define TMVN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tmvn_ctx* tmvn_handle;
+
+typedef enum {
+  TMVN_OK = 0,
+  TMVN_E_ARG = -1,              /* null pointer, bad size, non-finite input, C < 1 ...       */
+  TMVN_E_EMPTY_POLYTOPE = -2,   /* a zero row of A with b_i < 0 ("invalid")          */
+  TMVN_E_INFEASIBLE_START = -3, /* some a_i . x0 >= b_i: start must be strictly interior     */
+  TMVN_E_FACTOR = -4,           /* L not lower-triangular with a positive diagonal (App. A)  */
+  TMVN_E_CUDA = -5,             /* a CUDA runtime error                                      */
+  TMVN_E_OOM = -6,              /* device allocation failed                                  */
+  TMVN_E_STATE = -7             /* call out of order (e.g. moments before any sample)        */
+} tmvn_status;
+
+typedef struct {
+  /* S3.3 trimming epsilon: every active interval [l, u] becomes
+   * [l + eps, u - eps] except at the outer endpoints 0 and 2*pi; segments that
+   * vanish are dropped; if all vanish the untrimmed set is used (C7).
+   * Default 0.0 (FP64). */
+  double trim_eps;
+  /* P = A x_t is maintained incrementally (P <- P cos(theta) + Q sin(theta),
+   * exact by Eq. 1) and recomputed as X A^T after every iteration t with
+   * (t + 1) % recompute_every == 0.  Default 32; 1 = recompute every step. */
+  int64_t recompute_every;
+  /* Moment recording (S4.1 protocol): the iterate x_{t+1} produced by
+   * iteration t is recorded iff record != 0, t >= burn_in and
+   * (t - burn_in) % thin == 0.  Defaults: record 1, burn_in 0, thin 1. */
+  int64_t burn_in, thin;
+  int32_t record;
+  /* Global index of the first chain of this handle (multi-GPU sharding) and
+   * the iteration index of the first iteration of the next tmvn_sample (the
+   * RNG counter base; resume).  Defaults 0, 0.  iter_offset advances by n_iter
+   * after every successful tmvn_sample when auto_advance != 0 (default 1). */
+  int64_t chain_offset;
+  int64_t iter_offset;
+  int32_t auto_advance;
+  /* cudaStream_t to run on (e.g. torch.cuda.current_stream().cuda_stream);
+   * NULL = the legacy default stream. */
+  void* stream;
+  /* 1: bracket every projection GEMM and every ESS launch of the hot loop with
+   * CUDA events on `stream` and accumulate their durations (tmvn_get_profile).
+   * Default 0. */
+  int32_t profile;
+} tmvn_options;
+
+typedef struct {
+  int64_t steps;       /* chain-iterations run (accepted or not) since the last reset        */
+  int64_t rejections;  /* safeguard rejections + L = 0 stays (C9)       */
+  int64_t recorded;    /* chain-iterations recorded into the moments                          */
+} tmvn_stats;
+
+typedef struct {
+  int64_t launches;      /* kernels launched by the library (all kinds) since the last reset */
+  int64_t gemm_launches; /* hot-loop projection GEMMs timed (Q = N A^T and P refreshes)     */
+  double gemm_ms;        /* sum of their CUDA-event durations                                */
+  double gemm_flops;     /* algorithmic flops of those GEMMs: 2 C m d each (no padding)      */
+  int64_t ess_launches;  /* fused per-chain ESS launches timed                               */
+  double ess_ms;
+  double ess_bytes;      /* algorithmic HBM bytes of those launches    */
+} tmvn_profile;
+
+/* Fills *opt with the defaults listed above. */
+tmvn_status tmvn_default_options(tmvn_options* opt);
+
+/* Creates a handle on the current CUDA device for the polytope {x : A x <= b}
+ * (P:24).  A: m x d row-major FP64, b: m FP64 (host or device; both
+ * copied).  Errors: TMVN_E_ARG (null, m < 1, d < 1, non-finite entries),
+ * TMVN_E_EMPTY_POLYTOPE (a zero row with b_i < 0), TMVN_E_OOM,
+ * TMVN_E_CUDA.  On error *out is NULL. */
+tmvn_status tmvn_create(const double* A, const double* b, int64_t m, int64_t d, tmvn_handle* out);
+
+/* Non-standard normal N(mu, L L^T) by the change of variable of App. A
+ * (P:898-904): the chains run on u ~ N(0, I) truncated to
+ * {u : (A L) u <= b - A mu} and report x = L u + mu.  mu: d (NULL = 0);
+ * L: d x d row-major lower-triangular with a positive diagonal (NULL = I).
+ * After this call X0 / out of tmvn_sample and the moments are in x-space.
+ * Passing both NULL restores the standard normal.  Errors: TMVN_E_ARG,
+ * TMVN_E_FACTOR (an entry above the diagonal is non-zero or a diagonal entry
+ * is <= 0), TMVN_E_EMPTY_POLYTOPE (a zero row of A L with b - A mu < 0). */
+tmvn_status tmvn_set_affine(tmvn_handle h, const double* mu, const double* L);
+
+tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* opt);
+tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* opt);
+
+/* Runs n_iter iterations of Alg. 1 for C chains.
+ * X0: C x d row-major start points (host or device), strictly feasible
+ * (a_i . x0 < b_i for all i, checked on the GPU: TMVN_E_INFEASIBLE_START names
+ * the first offending chain / constraint).  out: C x d row-major final iterates
+ * (host or device; out == X0 allowed).  Chain k of this call is global chain
+ * chain_offset + k; its iteration t (t = iter_offset .. iter_offset+n_iter-1)
+ * draws nu from Philox4x32-10 counters (j, t, chain, 0) and u from
+ * (0, t, chain, 1) under key (seed & 0xffffffff, seed >> 32) (C12).
+ * n_iter = 0 only checks and copies X0.  Requires t < 2^32 and
+ * chain_offset + C <= 2^32.  Errors: TMVN_E_ARG, TMVN_E_INFEASIBLE_START,
+ * TMVN_E_OOM, TMVN_E_CUDA. */
+tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed,
+                        double* out);
+
+/* Counters since creation or the last tmvn_reset_stats. */
+tmvn_status tmvn_get_stats(tmvn_handle h, tmvn_stats* st);
+
+/* Sums over recorded iterates (x-space): sum[j] = sum x_j, sumsq[j] = sum x_j^2
+ * (d each, host or device), *n = number of recorded chain-iterations (host).
+ * The caller forms mean = sum / n and var = sumsq / n - mean^2 (S4.1).
+ * Multi-GPU: all-reduce these three over ranks. */
+tmvn_status tmvn_get_moments(tmvn_handle h, double* sum, double* sumsq, int64_t* n);
+tmvn_status tmvn_reset_stats(tmvn_handle h);  /* also resets the profile */
+/* Kernel timings collected while options.profile != 0 (launch counts always). */
+tmvn_status tmvn_get_profile(tmvn_handle h, tmvn_profile* prof);
+
+/* Last error message of this handle (or of the calling thread's last failed
+ * tmvn_create when h is NULL).  Valid until the next call on the handle. */
+const char* tmvn_last_error(tmvn_handle h);
+const char* tmvn_version(void);
+void tmvn_destroy(tmvn_handle h);
+
+/* ------------------------------------------------------------------------ */
+/* Test hooks (same .so; not part of the public contract).  They run the     */
+/* production device code on caller-given inputs so each stage can be        */
+/* compared with the CPU oracle.  All pointers host or device.               */
+/* ------------------------------------------------------------------------ */
+
+/* Philox4x32-10 of the device path on n records: ctr 4n words, key 2n words -> out 4n. */
+tmvn_status tmvn_test_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out);
+/* cuRAND's curand_Philox4x32_10 on the device (library pin), same layout. */
+tmvn_status tmvn_test_curand_philox(const uint32_t* ctr, const uint32_t* key, int64_t n,
+                                    uint32_t* out);
+/* nu (C x d) and u (C) for global chains c0 .. c0+C-1 at iteration t (C12). */
+tmvn_status tmvn_test_normals(uint64_t seed, uint64_t t, int64_t c0, int64_t C, int64_t d,
+                              double* nu, double* u);
+/* Arcs of eq:roots (C1-C5) for n triples; active[i] = 1 iff hypot(p,q) > b. */
+tmvn_status tmvn_test_arcs(const double* p, const double* q, const double* b, int64_t n,
+                           double* alpha, double* beta, uint8_t* active);
+/* I_act by the production kernel (Alg. 3) for C chains of m pairs each
+ * (alpha, beta: C x m, every pair used; (0, 0) is a no-op padding pair),
+ * then trimming by eps and theta = inverse CDF at u (C; NULL = no theta).
+ * seg_lo/seg_hi: C x seg_cap canonical segments (untrimmed), nseg: C counts
+ * (may exceed seg_cap), L: C total length after trimming, theta: C. */
+tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t m, int64_t C,
+                                const double* u, double eps, double* seg_lo, double* seg_hi,
+                                int64_t seg_cap, int64_t* nseg, double* L, double* theta);
+/* The production FP64 GEMM: out[R x S] = X[R x K] . W[S x K]^T (all row-major). */
+tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
+                           double* out);
+
+typedef struct {
+  double* nu;        /* C x d  */
+  double* u;         /* C      */
+  double* p;         /* C x m  A x_t as used by the step            */
+  double* q;         /* C x m  A nu                                 */
+  double* alpha;     /* C x m  */
+  double* beta;      /* C x m  */
+  uint8_t* active;   /* C x m  */
+  double* seg_lo;    /* C x seg_cap canonical untrimmed I_act      */
+  double* seg_hi;    /* C x seg_cap */
+  int64_t seg_cap;
+  int64_t* nseg;     /* C */
+  double* L;         /* C  total length after trimming               */
+  double* theta;     /* C  */
+  double* x_next;    /* C x d  x_{t+1} (= x_t when rejected)         */
+  double* max_slack; /* C  max_i (P'_i - b_i) of the proposal        */
+  int32_t* accept;   /* C  */
+} tmvn_step_dump;
+
+/* One iteration t of the production kernels from the given X_t (C x d, in the
+ * handle's u-space; P recomputed from X_t), with every intermediate dumped. */
+tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t seed, int64_t t,
+                           tmvn_step_dump* dump);
+/* tmvn_sample (production loop: incremental P, periodic refresh, fused RNG)
+ * that also records, for the n_trace chains listed in chains[] (host), the
+ * u-space iterate after every iteration: trace[(it * n_trace + k) * d + j],
+ * it = 0 .. n_iter (row 0 = X0). */
+tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter,
+                            uint64_t seed, const int64_t* chains, int64_t n_trace, double* trace,
+                            double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TMVN_H_ */

@@ -1,0 +1,296 @@
+// aux_kernels.cu -- data movement and small kernels around the hot loop:
+// layout conversion, the first nu draw, the strict start check (C18), moment
+// reduction, App. A helpers, and the test-hook kernels.
+#define QUALIFIERS static __forceinline__ __device__
+#include <curand_philox4x32_x.h>
+#include "common.cuh"
+#include "internal.h"
+
+namespace tmvn {
+namespace {
+
+__global__ void pack_kernel(const double* __restrict__ src, int64_t R, int64_t K, int64_t ld,
+                            double* __restrict__ dst, int64_t K_pad) {
+  int64_t n = R * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / K, k = e % K;
+    dst[tiled_offset(r, k, K_pad)] = src[r * ld + k];
+  }
+}
+
+__global__ void unpack_kernel(const double* __restrict__ src, int64_t R, int64_t K, int64_t K_pad,
+                              double* __restrict__ dst) {
+  int64_t n = R * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / K, k = e % K;
+    dst[e] = src[tiled_offset(r, k, K_pad)];
+  }
+}
+
+// one thread per 64-byte run of nu
+__global__ void normals_kernel(double* __restrict__ N, int C, int d, int64_t d_pad, uint64_t seed,
+                               uint32_t t, uint32_t chain_offset) {
+  const int runs = (int)(d_pad / 8);
+  int64_t n = (int64_t)C * runs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(e / runs), a = (int)(e % runs);
+    double nn[8];
+    normal_run(seed, t, chain_offset + (uint32_t)c, a, d, nn);
+    double2* o = reinterpret_cast<double2*>(N + run_offset(c, a, d_pad));
+#pragma unroll
+    for (int h = 0; h < 4; ++h) o[h] = make_double2(nn[2 * h], nn[2 * h + 1]);
+  }
+}
+
+__global__ void start_check_kernel(const double* __restrict__ P, int64_t ldp,
+                                   const double* __restrict__ b, int C, int m,
+                                   unsigned long long* flag) {
+  int64_t n = (int64_t)C * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = e / m, i = e % m;
+    double s = P[c * ldp + i] - b[i];
+    if (!(s < 0.0)) atomicMin(flag, (unsigned long long)e);  // NaN also fails
+  }
+}
+
+// deterministic: thread j sums chains in index order
+__global__ void chain_sum_kernel(const double* __restrict__ S, int C, int d, int64_t d_pad,
+                                 double* __restrict__ out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) s += S[tiled_offset(c, j, d_pad)];
+  out[j] = s;
+}
+
+__global__ void accum_affine_kernel(const double* __restrict__ X, int64_t ldx,
+                                    const double* __restrict__ mu, int C, int d,
+                                    double* __restrict__ S1, double* __restrict__ S2) {
+  int64_t n = (int64_t)C * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = e / d, j = e % d;
+    double x = X[c * ldx + j] + (mu ? mu[j] : 0.0);
+    S1[e] += x;
+    S2[e] += x * x;
+  }
+}
+
+__global__ void add_vec_rows_kernel(double* __restrict__ X, int64_t ldx,
+                                    const double* __restrict__ mu, int C, int d) {
+  int64_t n = (int64_t)C * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = e / d, j = e % d;
+    X[c * ldx + j] += mu[j];
+  }
+}
+
+// Forward substitution u = L^{-1} (x - mu), one CTA per row, the dot products
+// over the solved prefix reduced across the block.
+__global__ void trsv_rows_kernel(const double* __restrict__ X, const double* __restrict__ mu,
+                                 const double* __restrict__ L, int C, int d,
+                                 double* __restrict__ U) {
+  __shared__ double red[32];
+  for (int c = blockIdx.x; c < C; c += gridDim.x) {
+    const double* x = X + (int64_t)c * d;
+    double* u = U + (int64_t)c * d;
+    for (int j = 0; j < d; ++j) {
+      double s = 0.0;
+      for (int k = threadIdx.x; k < j; k += blockDim.x) s += L[(int64_t)j * d + k] * u[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        u[j] = (x[j] - (mu ? mu[j] : 0.0) - t) / L[(int64_t)j * d + j];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ Xt, int64_t d_pad, int d,
+                                   const int64_t* __restrict__ rows, int n,
+                                   double* __restrict__ out) {
+  int64_t tot = (int64_t)n * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = e / d, j = e % d;
+    out[e] = Xt[tiled_offset(rows[k], j, d_pad)];
+  }
+}
+
+__global__ void sum_i64_kernel(const int64_t* __restrict__ v, int n, int64_t* out) {
+  __shared__ long long red[32];
+  long long s = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+__global__ void gemv_shift_kernel(const double* __restrict__ A, const double* __restrict__ b,
+                                  const double* __restrict__ mu, int m, int d,
+                                  double* __restrict__ out) {
+  int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  double s = 0.0;
+  for (int j = lane; j < d; j += 32) s += A[(int64_t)row * d + j] * mu[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[row] = b[row] - s;
+}
+
+__global__ void test_philox_kernel(const uint32_t* __restrict__ ctr, const uint32_t* __restrict__ key,
+                                   int64_t n, uint32_t* __restrict__ out, int use_curand) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t k0 = key[2 * i], k1 = key[2 * i + 1];
+  if (use_curand) {
+    uint4 c = make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]);
+    uint4 r = curand_Philox4x32_10(c, make_uint2(k0, k1));
+    out[4 * i] = r.x;
+    out[4 * i + 1] = r.y;
+    out[4 * i + 2] = r.z;
+    out[4 * i + 3] = r.w;
+  } else {
+    U4 r = philox10(U4{ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]}, k0, k1);
+    out[4 * i] = r.x;
+    out[4 * i + 1] = r.y;
+    out[4 * i + 2] = r.z;
+    out[4 * i + 3] = r.w;
+  }
+}
+
+__global__ void test_normals_kernel(uint64_t seed, uint32_t t, uint32_t c0, int C, int d,
+                                    double* __restrict__ nu, double* __restrict__ u) {
+  const int runs = (d + 7) / 8;
+  int64_t n = (int64_t)C * runs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(e / runs), a = (int)(e % runs);
+    double nn[8];
+    normal_run(seed, t, c0 + (uint32_t)c, a, d, nn);
+    for (int kk = 0; kk < 8; ++kk) {
+      int k = a * 8 + kk;
+      if (k < d) nu[(int64_t)c * d + k] = nn[run_slot(kk)];
+    }
+    if (a == 0 && u) u[c] = theta_uniform(seed, t, c0 + (uint32_t)c);
+  }
+}
+
+__global__ void test_arcs_kernel(const double* __restrict__ p, const double* __restrict__ q,
+                                 const double* __restrict__ b, int64_t n, double* alpha,
+                                 double* beta, uint8_t* active) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double al = 0.0, be = 0.0;
+  bool act = arc_of(p[i], q[i], b[i], al, be);
+  alpha[i] = act ? al : 0.0;
+  beta[i] = act ? be : 0.0;
+  active[i] = act ? 1 : 0;
+}
+
+inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 64) g = 148 * 64;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t launch_pack(const double* src, int64_t R, int64_t K, int64_t ld, double* dst,
+                        int64_t K_pad, cudaStream_t st) {
+  if (R * K == 0) return cudaSuccess;
+  pack_kernel<<<grid_for(R * K), 256, 0, st>>>(src, R, K, ld, dst, K_pad);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack(const double* src, int64_t R, int64_t K, int64_t K_pad, double* dst,
+                          cudaStream_t st) {
+  if (R * K == 0) return cudaSuccess;
+  unpack_kernel<<<grid_for(R * K), 256, 0, st>>>(src, R, K, K_pad, dst);
+  return cudaGetLastError();
+}
+cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed, uint32_t t,
+                           uint32_t chain_offset, cudaStream_t st) {
+  int64_t n = (int64_t)C * (d_pad / 8);
+  if (n == 0) return cudaSuccess;
+  normals_kernel<<<grid_for(n), 256, 0, st>>>(N, C, d, d_pad, seed, t, chain_offset);
+  return cudaGetLastError();
+}
+cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, int C, int m,
+                               unsigned long long* flag, cudaStream_t st) {
+  start_check_kernel<<<grid_for((int64_t)C * m), 256, 0, st>>>(P, ldp, b, C, m, flag);
+  return cudaGetLastError();
+}
+cudaError_t launch_chain_sum(const double* S, int C, int d, int64_t d_pad, double* out,
+                             cudaStream_t st) {
+  chain_sum_kernel<<<(d + 127) / 128, 128, 0, st>>>(S, C, d, d_pad, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_accum_affine(const double* Xrow, int64_t ldx, const double* mu, int C, int d,
+                                double* S1row, double* S2row, cudaStream_t st) {
+  accum_affine_kernel<<<grid_for((int64_t)C * d), 256, 0, st>>>(Xrow, ldx, mu, C, d, S1row, S2row);
+  return cudaGetLastError();
+}
+cudaError_t launch_add_vec_rows(double* Xrow, int64_t ldx, const double* mu, int C, int d,
+                                cudaStream_t st) {
+  add_vec_rows_kernel<<<grid_for((int64_t)C * d), 256, 0, st>>>(Xrow, ldx, mu, C, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_trsv_rows(const double* Xrow, const double* mu, const double* L, int C, int d,
+                             double* Urow, cudaStream_t st) {
+  int g = C < 148 * 8 ? C : 148 * 8;
+  trsv_rows_kernel<<<g, 128, 0, st>>>(Xrow, mu, L, C, d, Urow);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_rows_tiled(const double* Xt, int64_t d_pad, int d, const int64_t* rows,
+                                     int n, double* out, cudaStream_t st) {
+  if ((int64_t)n * d == 0) return cudaSuccess;
+  gather_rows_kernel<<<grid_for((int64_t)n * d), 256, 0, st>>>(Xt, d_pad, d, rows, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_i64(const int64_t* v, int n, int64_t* out, cudaStream_t st) {
+  sum_i64_kernel<<<1, 1024, 0, st>>>(v, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_gemv_shift(const double* A, const double* b, const double* mu, int m, int d,
+                              double* out, cudaStream_t st) {
+  gemv_shift_kernel<<<(m + 7) / 8, 256, 0, st>>>(A, b, mu, m, d, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_test_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out,
+                               bool curand, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  test_philox_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(ctr, key, n, out, curand ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_test_normals(uint64_t seed, uint32_t t, uint32_t c0, int C, int d, double* nu,
+                                double* u, cudaStream_t st) {
+  int64_t n = (int64_t)C * ((d + 7) / 8);
+  if (n == 0) return cudaSuccess;
+  test_normals_kernel<<<grid_for(n), 256, 0, st>>>(seed, t, c0, C, d, nu, u);
+  return cudaGetLastError();
+}
+cudaError_t launch_test_arcs(const double* p, const double* q, const double* b, int64_t n,
+                             double* alpha, double* beta, uint8_t* active, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  test_arcs_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(p, q, b, n, alpha, beta, active);
+  return cudaGetLastError();
+}
+
+}  // namespace tmvn

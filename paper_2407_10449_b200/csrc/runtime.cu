@@ -1,0 +1,848 @@
+// runtime.cu -- host runtime behind the C ABI of include/tmvn.h: the handle,
+// device buffers, the per-iteration launch sequence of Alg. 1 and the test hooks.
+//
+// Per iteration t (all on one stream, two launches in steady state):
+//   GEMM  Q = N A^T                                    (gemm_f64.cu)
+//   ESS   arcs -> I_act -> theta -> P', x, moments, nu_{t+1}   (ess_chain.cu)
+//   every recompute_every iterations: GEMM P = X A^T  (C13)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "../../include/tmvn.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace tmvn;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct tmvn_ctx {
+  int device = 0;
+  int64_t m = 0, d = 0, m_pad = 0, d_pad = 0, d_r128 = 0;
+  // constraints
+  double* A_row = nullptr;  // m x d (original)
+  double* b_orig = nullptr; // m
+  double* A_tiled = nullptr;  // tiled m_pad x d_pad of the ORIGINAL A (for A L)
+  double* At = nullptr;     // tiled m_pad x d_pad of A' (= A L if affine)
+  double* b_eff = nullptr;  // m, b' = b - A mu
+  // affine (App. A)
+  bool affine = false;
+  double* mu = nullptr;      // d
+  double* L = nullptr;       // d x d row-major
+  double* L_tiled = nullptr; // rows j = L[j, :], tiled d_r128 x d_pad  (x = U L^T)
+  // chains
+  int64_t C_cap = 0, C_pad = 0;
+  double *X = nullptr, *N = nullptr, *P0 = nullptr, *P1 = nullptr, *Q = nullptr;
+  double *S1 = nullptr, *S2 = nullptr;       // tiled moments (u-space == x-space w/o affine)
+  double *S1x = nullptr, *S2x = nullptr;     // row-major x-space moments (affine)
+  double *stage = nullptr, *stage2 = nullptr;  // row-major C_pad x max(d_pad, d_r128)
+  int64_t* rej = nullptr;
+  int64_t* dsum = nullptr;
+  double* msum = nullptr;  // d (device) moment reduction target
+  unsigned long long* dflag = nullptr;
+  double2 *gstash = nullptr, *ggaps = nullptr;
+  int grid = 0, NB = 64;
+  // state
+  tmvn_options opt{};
+  tmvn_stats stats{};
+  std::vector<double> mom_sum, mom_sq;
+  std::string err;
+  // profiling (tmvn_get_profile)
+  tmvn_profile prof{};
+  std::vector<cudaEvent_t> events;
+  // trace hook
+  const int64_t* trace_rows = nullptr;
+  int trace_n = 0;
+  double* trace_dev = nullptr;
+};
+
+namespace {
+
+tmvn_status fail(tmvn_ctx* h, tmvn_status s, const std::string& msg) {
+  if (h) h->err = msg;
+  else g_create_error = msg;
+  return s;
+}
+
+tmvn_status cuda_fail(tmvn_ctx* h, cudaError_t e, const char* where) {
+  std::string msg = std::string(where) + ": " + cudaGetErrorString(e);
+  return fail(h, e == cudaErrorMemoryAllocation ? TMVN_E_OOM : TMVN_E_CUDA, msg);
+}
+
+#define CK(h, expr)                                          \
+  do {                                                       \
+    cudaError_t e_ = (expr);                                 \
+    if (e_ != cudaSuccess) return cuda_fail((h), e_, #expr); \
+  } while (0)
+
+// a kernel launch of the library: checked and counted
+#define KL(h, expr)          \
+  do {                       \
+    CK(h, expr);             \
+    (h)->prof.launches += 1; \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemset(*p, 0, count * sizeof(T));
+}
+
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+std::vector<double> to_host(const double* p, size_t n) {
+  std::vector<double> v(n);
+  if (n) cudaMemcpy(v.data(), p, n * sizeof(double), cudaMemcpyDefault);
+  return v;
+}
+
+cudaStream_t stream_of(const tmvn_ctx* h) { return (cudaStream_t)h->opt.stream; }
+
+void free_chain_buffers(tmvn_ctx* h) {
+  dfree(h->X); dfree(h->N); dfree(h->P0); dfree(h->P1); dfree(h->Q);
+  dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
+  dfree(h->stage); dfree(h->stage2); dfree(h->rej);
+  dfree(h->gstash); dfree(h->ggaps);
+  h->C_cap = h->C_pad = 0;
+}
+
+tmvn_status ensure_chains(tmvn_ctx* h, int64_t C) {
+  if (C <= h->C_cap) return TMVN_OK;
+  free_chain_buffers(h);
+  const int64_t C_pad = round_up(C, kTileR);
+  const size_t cd = (size_t)C_pad * h->d_pad, cm = (size_t)C_pad * h->m_pad;
+  const size_t wide = (size_t)C_pad * std::max(h->d_pad, h->d_r128);
+  CK(h, dalloc(&h->X, cd));
+  CK(h, dalloc(&h->N, cd));
+  CK(h, dalloc(&h->P0, cm));
+  CK(h, dalloc(&h->P1, cm));
+  CK(h, dalloc(&h->Q, cm));
+  CK(h, dalloc(&h->S1, cd));
+  CK(h, dalloc(&h->S2, cd));
+  CK(h, dalloc(&h->stage, wide));
+  CK(h, dalloc(&h->stage2, wide));
+  CK(h, dalloc(&h->rej, (size_t)C_pad));
+  h->NB = ess_buckets((int)h->m);
+  h->grid = ess_grid((int)C, (int)h->m, h->NB);
+  const int gmax = ess_grid((int)C_pad, (int)h->m, h->NB);
+  if (h->m > kStashSmemMax) CK(h, dalloc(&h->gstash, (size_t)gmax * h->m));
+  CK(h, dalloc(&h->ggaps, (size_t)gmax * (h->m + 2)));
+  h->C_cap = C;
+  h->C_pad = C_pad;
+  return TMVN_OK;
+}
+
+tmvn_status ensure_affine_moments(tmvn_ctx* h) {
+  if (h->S1x) return TMVN_OK;
+  CK(h, dalloc(&h->S1x, (size_t)h->C_pad * h->d));
+  CK(h, dalloc(&h->S2x, (size_t)h->C_pad * h->d));
+  return TMVN_OK;
+}
+
+bool finite_all(const std::vector<double>& v) {
+  for (double x : v)
+    if (!std::isfinite(x)) return false;
+  return true;
+}
+
+EssParams base_params(tmvn_ctx* h, int C) {
+  EssParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.ldp = h->m_pad;
+  p.b = h->b_eff;
+  p.m = (int)h->m;
+  p.X = h->X;
+  p.N = h->N;
+  p.d = (int)h->d;
+  p.d_pad = h->d_pad;
+  p.C = C;
+  p.chain_offset = (uint32_t)h->opt.chain_offset;
+  p.eps = h->opt.trim_eps;
+  p.S1 = h->S1;
+  p.S2 = h->S2;
+  p.rej = h->rej;
+  p.gstash = h->gstash;
+  p.ggaps = h->ggaps;
+  p.NB = h->NB;
+  return p;
+}
+
+// X0 (C x d, host/device, x-space) -> tiled X (u-space).
+tmvn_status load_X(tmvn_ctx* h, const double* X0, int64_t C) {
+  cudaStream_t st = stream_of(h);
+  const int64_t d = h->d;
+  CK(h, cudaMemcpyAsync(h->stage, X0, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
+  if (h->affine) {
+    KL(h, launch_trsv_rows(h->stage, h->mu, h->L, (int)C, (int)d, h->stage2, st));
+    KL(h, launch_pack(h->stage2, C, d, d, h->X, h->d_pad, st));
+  } else {
+    KL(h, launch_pack(h->stage, C, d, d, h->X, h->d_pad, st));
+  }
+  return TMVN_OK;
+}
+
+// tiled X (u-space) -> out (C x d, x-space).
+tmvn_status store_X(tmvn_ctx* h, int64_t C, double* out) {
+  cudaStream_t st = stream_of(h);
+  const int64_t d = h->d;
+  if (h->affine) {
+    KL(h, launch_gemm_tn(h->X, h->C_pad, h->L_tiled, h->d_r128, h->d_pad, h->stage, h->d_r128, st));
+    KL(h, launch_add_vec_rows(h->stage, h->d_r128, h->mu, (int)C, (int)d, st));
+    CK(h, cudaMemcpy2DAsync(out, d * sizeof(double), h->stage, h->d_r128 * sizeof(double),
+                            d * sizeof(double), C, cudaMemcpyDefault, st));
+  } else {
+    KL(h, launch_unpack(h->X, C, d, h->d_pad, h->stage, st));
+    CK(h, cudaMemcpyAsync(out, h->stage, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
+  }
+  return TMVN_OK;
+}
+
+// P = X A'^T, then the strict start check (C18).
+tmvn_status start_check(tmvn_ctx* h, int64_t C, double* P) {
+  cudaStream_t st = stream_of(h);
+  KL(h, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, P, h->m_pad, st));
+  CK(h, cudaMemsetAsync(h->dflag, 0xff, sizeof(unsigned long long), st));
+  KL(h, launch_start_check(P, h->m_pad, h->b_eff, (int)C, (int)h->m, h->dflag, st));
+  unsigned long long flag = 0;
+  CK(h, cudaMemcpyAsync(&flag, h->dflag, sizeof(flag), cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  if (flag != ~0ull) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "infeasible start: chain %lld violates constraint %lld (a_i . x0 >= b_i; the start "
+             "must be strictly interior)",
+             (long long)(flag / h->m), (long long)(flag % h->m));
+    return fail(h, TMVN_E_INFEASIBLE_START, buf);
+  }
+  return TMVN_OK;
+}
+
+bool recorded_iter(const tmvn_options& o, int64_t t) {
+  if (!o.record || t < o.burn_in) return false;
+  int64_t thin = o.thin < 1 ? 1 : o.thin;
+  return ((t - o.burn_in) % thin) == 0;
+}
+
+// The hot loop.  On entry X holds x_{t0} (tiled) and P_cur = X A'^T.
+tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, double* P_cur,
+                     int64_t* n_recorded) {
+  cudaStream_t st = stream_of(h);
+  const int64_t t0 = h->opt.iter_offset;
+  const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
+  double* P_next = (P_cur == h->P0) ? h->P1 : h->P0;
+  EssParams p = base_params(h, (int)C);
+  KL(h, launch_normals(h->N, (int)C, (int)h->d, h->d_pad, seed, (uint32_t)t0,
+                       (uint32_t)h->opt.chain_offset, st));
+  int64_t nrec = 0;
+  // profiling: event pairs around the hot-loop GEMMs (kind 0) and ESS launches (kind 1)
+  const bool prof = h->opt.profile != 0;
+  std::vector<int> kinds;
+  auto ev_mark = [&](size_t idx) -> cudaError_t {
+    while (h->events.size() <= idx) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      h->events.push_back(e);
+    }
+    return cudaEventRecord(h->events[idx], st);
+  };
+#define TIMED(kind, expr)                                   \
+  do {                                                      \
+    if (prof) CK(h, ev_mark(2 * kinds.size()));             \
+    KL(h, expr);                                            \
+    if (prof) {                                             \
+      CK(h, ev_mark(2 * kinds.size() + 1));                 \
+      kinds.push_back(kind);                                \
+    }                                                       \
+  } while (0)
+  for (int64_t it = 0; it < n_iter; ++it) {
+    const int64_t t = t0 + it;
+    TIMED(0, launch_gemm_tn(h->N, h->C_pad, h->At, h->m_pad, h->d_pad, h->Q, h->m_pad, st));
+    const bool rec = recorded_iter(h->opt, t);
+    p.P_cur = P_cur;
+    p.P_next = P_next;
+    p.Q = h->Q;
+    p.seed = seed;
+    p.t = (uint32_t)t;
+    p.gen_next = (it + 1 < n_iter) ? 1 : 0;
+    p.record = (rec && !h->affine) ? 1 : 0;
+    TIMED(1, launch_ess_step(p, h->grid, st));
+    std::swap(P_cur, P_next);
+    if (rec) {
+      ++nrec;
+      if (h->affine) {
+        KL(h, launch_gemm_tn(h->X, h->C_pad, h->L_tiled, h->d_r128, h->d_pad, h->stage, h->d_r128, st));
+        KL(h, launch_accum_affine(h->stage, h->d_r128, h->mu, (int)C, (int)h->d, h->S1x, h->S2x, st));
+      }
+    }
+    if ((t + 1) % K == 0 && it + 1 < n_iter)
+      TIMED(0, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, P_cur, h->m_pad, st));
+    if (h->trace_dev)
+      KL(h, launch_gather_rows_tiled(h->X, h->d_pad, (int)h->d, h->trace_rows, h->trace_n,
+                                     h->trace_dev + (size_t)(it + 1) * h->trace_n * h->d, st));
+  }
+#undef TIMED
+  *n_recorded = nrec;
+  if (prof && !kinds.empty()) {
+    CK(h, cudaEventSynchronize(h->events[2 * kinds.size() - 1]));
+    const double flops = 2.0 * (double)C * (double)h->m * (double)h->d;
+    // P, Q read + P' write (24 B per constraint-eval); X r/w, nu read + next nu write (32 B per
+    // chain-coordinate); moments (32 B per chain-coordinate) on recorded iterations
+    const double ess_bytes = 24.0 * (double)C * (double)h->m + 32.0 * (double)C * (double)h->d;
+    for (size_t k = 0; k < kinds.size(); ++k) {
+      float ms = 0.f;
+      CK(h, cudaEventElapsedTime(&ms, h->events[2 * k], h->events[2 * k + 1]));
+      if (kinds[k] == 0) {
+        h->prof.gemm_launches += 1;
+        h->prof.gemm_ms += ms;
+        h->prof.gemm_flops += flops;
+      } else {
+        h->prof.ess_launches += 1;
+        h->prof.ess_ms += ms;
+        h->prof.ess_bytes += ess_bytes;
+      }
+    }
+  }
+  return TMVN_OK;
+}
+
+// Reduce per-chain moments / rejections into the handle's counters.
+tmvn_status finish_stats(tmvn_ctx* h, int64_t C, int64_t n_iter, int64_t nrec) {
+  cudaStream_t st = stream_of(h);
+  const int64_t d = h->d;
+  int64_t rej = 0;
+  KL(h, launch_sum_i64(h->rej, (int)C, h->dsum, st));
+  CK(h, cudaMemcpyAsync(&rej, h->dsum, sizeof(rej), cudaMemcpyDeviceToHost, st));
+  std::vector<double> s(d, 0.0), q(d, 0.0);
+  if (nrec > 0) {
+    if (h->affine) {
+      // row-major C x d accumulators: reuse the tiled reducer through a pack
+      KL(h, launch_pack(h->S1x, C, d, d, h->stage2, h->d_pad, st));
+      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, st));
+      CK(h, cudaMemcpyAsync(s.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(h, cudaStreamSynchronize(st));
+      KL(h, launch_pack(h->S2x, C, d, d, h->stage2, h->d_pad, st));
+      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, st));
+      CK(h, cudaMemcpyAsync(q.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
+    } else {
+      KL(h, launch_chain_sum(h->S1, (int)C, (int)d, h->d_pad, h->msum, st));
+      CK(h, cudaMemcpyAsync(s.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(h, cudaStreamSynchronize(st));
+      KL(h, launch_chain_sum(h->S2, (int)C, (int)d, h->d_pad, h->msum, st));
+      CK(h, cudaMemcpyAsync(q.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+  }
+  CK(h, cudaStreamSynchronize(st));
+  for (int64_t j = 0; j < d; ++j) {
+    h->mom_sum[j] += s[j];
+    h->mom_sq[j] += q[j];
+  }
+  h->stats.steps += C * n_iter;
+  h->stats.rejections += rej;
+  h->stats.recorded += C * nrec;
+  return TMVN_OK;
+}
+
+tmvn_status clear_accumulators(tmvn_ctx* h, int64_t n_iter) {
+  cudaStream_t st = stream_of(h);
+  bool any = false;
+  for (int64_t it = 0; it < n_iter && !any; ++it) any = recorded_iter(h->opt, h->opt.iter_offset + it);
+  if (any) {
+    size_t cd = (size_t)h->C_pad * h->d_pad;
+    if (h->affine) {
+      if (ensure_affine_moments(h) != TMVN_OK) return TMVN_E_OOM;
+      CK(h, cudaMemsetAsync(h->S1x, 0, (size_t)h->C_pad * h->d * sizeof(double), st));
+      CK(h, cudaMemsetAsync(h->S2x, 0, (size_t)h->C_pad * h->d * sizeof(double), st));
+    } else {
+      CK(h, cudaMemsetAsync(h->S1, 0, cd * sizeof(double), st));
+      CK(h, cudaMemsetAsync(h->S2, 0, cd * sizeof(double), st));
+    }
+  }
+  CK(h, cudaMemsetAsync(h->rej, 0, (size_t)h->C_pad * sizeof(int64_t), st));
+  return TMVN_OK;
+}
+
+tmvn_status check_sample_args(tmvn_ctx* h, const double* X0, int64_t C, int64_t n_iter,
+                              const double* out) {
+  if (!h) return fail(nullptr, TMVN_E_ARG, "null handle");
+  if (!X0 || !out) return fail(h, TMVN_E_ARG, "X0 and out must be non-null");
+  if (C < 1 || n_iter < 0) return fail(h, TMVN_E_ARG, "need C >= 1 and n_iter >= 0");
+  if (h->opt.chain_offset < 0 || h->opt.chain_offset + C > (int64_t)1 << 32)
+    return fail(h, TMVN_E_ARG, "global chain index must fit in 32 bits");
+  if (h->opt.iter_offset < 0 || h->opt.iter_offset + n_iter >= (int64_t)1 << 32)
+    return fail(h, TMVN_E_ARG, "iteration index must fit in 32 bits");
+  if (C > (int64_t)1 << 30) return fail(h, TMVN_E_ARG, "C too large");
+  return TMVN_OK;
+}
+
+tmvn_status set_device(tmvn_ctx* h) {
+  CK(h, cudaSetDevice(h->device));
+  return TMVN_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+tmvn_status tmvn_default_options(tmvn_options* o) {
+  if (!o) return TMVN_E_ARG;
+  std::memset(o, 0, sizeof(*o));
+  o->trim_eps = 0.0;
+  o->recompute_every = 32;
+  o->burn_in = 0;
+  o->thin = 1;
+  o->record = 1;
+  o->chain_offset = 0;
+  o->iter_offset = 0;
+  o->auto_advance = 1;
+  o->stream = nullptr;
+  o->profile = 0;
+  return TMVN_OK;
+}
+
+const char* tmvn_version(void) { return "tmvn-b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+const char* tmvn_last_error(tmvn_handle h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+tmvn_status tmvn_create(const double* A, const double* b, int64_t m, int64_t d, tmvn_handle* out) {
+  if (!out) return fail(nullptr, TMVN_E_ARG, "out is null");
+  *out = nullptr;
+  if (!A || !b) return fail(nullptr, TMVN_E_ARG, "A and b must be non-null");
+  if (m < 1 || d < 1) return fail(nullptr, TMVN_E_ARG, "need m >= 1 and d >= 1");
+  if (m > (1 << 30) || d > (1 << 24)) return fail(nullptr, TMVN_E_ARG, "m or d too large");
+  std::vector<double> hA = to_host(A, (size_t)m * d), hb = to_host(b, (size_t)m);
+  if (!finite_all(hA) || !finite_all(hb)) return fail(nullptr, TMVN_E_ARG, "A and b must be finite");
+  for (int64_t i = 0; i < m; ++i) {
+    bool zero = true;
+    for (int64_t j = 0; j < d && zero; ++j) zero = hA[(size_t)i * d + j] == 0.0;
+    if (zero && hb[i] < 0.0) {
+      char buf[160];
+      snprintf(buf, sizeof(buf), "empty polytope: row %lld of A is zero and b < 0 (P:914)", (long long)i);
+      return fail(nullptr, TMVN_E_EMPTY_POLYTOPE, buf);
+    }
+  }
+  tmvn_ctx* h = new tmvn_ctx();
+  cudaGetDevice(&h->device);
+  h->m = m;
+  h->d = d;
+  h->m_pad = round_up(m, kTileR);
+  h->d_pad = round_up(d, kTileK);
+  h->d_r128 = round_up(d, kTileR);
+  tmvn_default_options(&h->opt);
+  h->mom_sum.assign(d, 0.0);
+  h->mom_sq.assign(d, 0.0);
+  auto bad = [&](cudaError_t e, const char* w) {
+    std::string msg = std::string(w) + ": " + cudaGetErrorString(e);
+    tmvn_destroy(h);
+    return fail(nullptr, e == cudaErrorMemoryAllocation ? TMVN_E_OOM : TMVN_E_CUDA, msg);
+  };
+  cudaError_t e;
+  if ((e = dalloc(&h->A_row, (size_t)m * d)) != cudaSuccess) return bad(e, "alloc A");
+  if ((e = dalloc(&h->b_orig, (size_t)m)) != cudaSuccess) return bad(e, "alloc b");
+  if ((e = dalloc(&h->b_eff, (size_t)m)) != cudaSuccess) return bad(e, "alloc b'");
+  if ((e = dalloc(&h->A_tiled, (size_t)h->m_pad * h->d_pad)) != cudaSuccess) return bad(e, "alloc At");
+  h->At = h->A_tiled;
+  if ((e = dalloc(&h->dflag, 1)) != cudaSuccess) return bad(e, "alloc flag");
+  if ((e = dalloc(&h->dsum, 1)) != cudaSuccess) return bad(e, "alloc sum");
+  if ((e = dalloc(&h->msum, (size_t)d)) != cudaSuccess) return bad(e, "alloc msum");
+  cudaMemcpy(h->A_row, hA.data(), hA.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(h->b_orig, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(h->b_eff, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if ((e = launch_pack(h->A_row, m, d, d, h->A_tiled, h->d_pad, 0)) != cudaSuccess) return bad(e, "pack A");
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bad(e, "create");
+  *out = h;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_set_affine(tmvn_handle h, const double* mu, const double* L) {
+  if (!h) return fail(nullptr, TMVN_E_ARG, "null handle");
+  if (set_device(h) != TMVN_OK) return TMVN_E_CUDA;
+  const int64_t d = h->d, m = h->m;
+  cudaStream_t st = stream_of(h);
+  if (!mu && !L) {
+    if (h->At != h->A_tiled) dfree(h->At);
+    h->At = h->A_tiled;
+    CK(h, cudaMemcpy(h->b_eff, h->b_orig, m * sizeof(double), cudaMemcpyDeviceToDevice));
+    dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
+    h->affine = false;
+    return TMVN_OK;
+  }
+  std::vector<double> hmu = mu ? to_host(mu, d) : std::vector<double>(d, 0.0);
+  std::vector<double> hL(d * d, 0.0);
+  if (L) hL = to_host(L, (size_t)d * d);
+  else for (int64_t j = 0; j < d; ++j) hL[j * d + j] = 1.0;
+  if (!finite_all(hmu) || !finite_all(hL)) return fail(h, TMVN_E_ARG, "mu and L must be finite");
+  for (int64_t j = 0; j < d; ++j) {
+    if (!(hL[j * d + j] > 0.0)) return fail(h, TMVN_E_FACTOR, "L must have a positive diagonal");
+    for (int64_t k = j + 1; k < d; ++k)
+      if (hL[j * d + k] != 0.0) return fail(h, TMVN_E_FACTOR, "L must be lower-triangular");
+  }
+  if (!h->mu) CK(h, dalloc(&h->mu, (size_t)d));
+  if (!h->L) CK(h, dalloc(&h->L, (size_t)d * d));
+  if (!h->L_tiled) CK(h, dalloc(&h->L_tiled, (size_t)h->d_r128 * h->d_pad));
+  CK(h, cudaMemcpy(h->mu, hmu.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(h->L, hL.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice));
+  KL(h, launch_pack(h->L, d, d, d, h->L_tiled, h->d_pad, st));
+  // A' = A L = A (L^T)^T : W operand = L^T (rows j = column j of L)
+  std::vector<double> hLT((size_t)d * d);
+  for (int64_t j = 0; j < d; ++j)
+    for (int64_t k = 0; k < d; ++k) hLT[j * d + k] = hL[k * d + j];
+  double *LT = nullptr, *LTt = nullptr, *Aprime = nullptr;
+  CK(h, dalloc(&LT, (size_t)d * d));
+  CK(h, dalloc(&LTt, (size_t)h->d_r128 * h->d_pad));
+  CK(h, dalloc(&Aprime, (size_t)h->m_pad * h->d_r128));
+  CK(h, cudaMemcpy(LT, hLT.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice));
+  KL(h, launch_pack(LT, d, d, d, LTt, h->d_pad, st));
+  KL(h, launch_gemm_tn(h->A_tiled, h->m_pad, LTt, h->d_r128, h->d_pad, Aprime, h->d_r128, st));
+  if (h->At == h->A_tiled) CK(h, dalloc(&h->At, (size_t)h->m_pad * h->d_pad));
+  KL(h, launch_pack(Aprime, m, d, h->d_r128, h->At, h->d_pad, st));
+  KL(h, launch_gemv_shift(h->A_row, h->b_orig, h->mu, (int)m, (int)d, h->b_eff, st));
+  CK(h, cudaStreamSynchronize(st));
+  dfree(LT); dfree(LTt); dfree(Aprime);
+  h->affine = true;
+  dfree(h->S1x); dfree(h->S2x);
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* o) {
+  if (!h || !o) return fail(h, TMVN_E_ARG, "null argument");
+  if (!(o->trim_eps >= 0.0) || !(o->trim_eps < 3.14159)) return fail(h, TMVN_E_ARG, "need 0 <= trim_eps < pi");
+  if (o->recompute_every < 1 || o->thin < 1 || o->burn_in < 0) return fail(h, TMVN_E_ARG, "bad recompute_every / thin / burn_in");
+  if (o->chain_offset < 0 || o->iter_offset < 0) return fail(h, TMVN_E_ARG, "offsets must be >= 0");
+  h->opt = *o;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
+  if (!h || !o) return fail(h, TMVN_E_ARG, "null argument");
+  *o = h->opt;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed,
+                        double* out) {
+  tmvn_status s = check_sample_args(h, X0, C, n_iter, out);
+  if (s != TMVN_OK) return s;
+  if ((s = set_device(h)) != TMVN_OK) return s;
+  if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
+  h->grid = ess_grid((int)C, (int)h->m, h->NB);
+  if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
+  if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;
+  if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
+  int64_t nrec = 0;
+  if ((s = run_loop(h, C, n_iter, seed, h->P0, &nrec)) != TMVN_OK) return s;
+  if ((s = store_X(h, C, out)) != TMVN_OK) return s;
+  if ((s = finish_stats(h, C, n_iter, nrec)) != TMVN_OK) return s;
+  if (h->opt.auto_advance) h->opt.iter_offset += n_iter;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_get_stats(tmvn_handle h, tmvn_stats* st) {
+  if (!h || !st) return fail(h, TMVN_E_ARG, "null argument");
+  *st = h->stats;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_get_moments(tmvn_handle h, double* sum, double* sumsq, int64_t* n) {
+  if (!h || !sum || !sumsq || !n) return fail(h, TMVN_E_ARG, "null argument");
+  if (set_device(h) != TMVN_OK) return TMVN_E_CUDA;
+  CK(h, cudaMemcpy(sum, h->mom_sum.data(), h->d * sizeof(double), cudaMemcpyDefault));
+  CK(h, cudaMemcpy(sumsq, h->mom_sq.data(), h->d * sizeof(double), cudaMemcpyDefault));
+  *n = h->stats.recorded;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_get_profile(tmvn_handle h, tmvn_profile* prof) {
+  if (!h || !prof) return fail(h, TMVN_E_ARG, "null argument");
+  *prof = h->prof;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_reset_stats(tmvn_handle h) {
+  if (!h) return fail(nullptr, TMVN_E_ARG, "null handle");
+  h->stats = tmvn_stats{};
+  h->prof = tmvn_profile{};
+  std::fill(h->mom_sum.begin(), h->mom_sum.end(), 0.0);
+  std::fill(h->mom_sq.begin(), h->mom_sq.end(), 0.0);
+  return TMVN_OK;
+}
+
+void tmvn_destroy(tmvn_handle h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  for (cudaEvent_t e : h->events) cudaEventDestroy(e);
+  free_chain_buffers(h);
+  if (h->At != h->A_tiled) dfree(h->At);
+  dfree(h->A_tiled); dfree(h->A_row); dfree(h->b_orig); dfree(h->b_eff);
+  dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
+  dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
+  delete h;
+}
+
+// ---------------------------------------------------------------- test hooks
+#define TCK(expr)                                                       \
+  do {                                                                  \
+    cudaError_t e_ = (expr);                                            \
+    if (e_ != cudaSuccess) return cuda_fail(nullptr, e_, #expr);        \
+  } while (0)
+
+}  // extern "C"
+
+namespace {
+template <typename T>
+struct Tmp {
+  T* p = nullptr;
+  ~Tmp() { if (p) cudaFree(p); }
+};
+template <typename T>
+cudaError_t tmp_in(Tmp<T>& t, const T* src, size_t n) {
+  cudaError_t e = cudaMalloc((void**)&t.p, (n ? n : 1) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  if (src && n) return cudaMemcpy(t.p, src, n * sizeof(T), cudaMemcpyDefault);
+  return cudaMemset(t.p, 0, (n ? n : 1) * sizeof(T));
+}
+template <typename T>
+cudaError_t tmp_out(T* dst, const Tmp<T>& t, size_t n) {
+  if (!dst || !n) return cudaSuccess;
+  return cudaMemcpy(dst, t.p, n * sizeof(T), cudaMemcpyDefault);
+}
+}  // namespace
+
+extern "C" {
+
+tmvn_status tmvn_test_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out) {
+  if (!ctr || !key || !out || n < 0) return fail(nullptr, TMVN_E_ARG, "bad args");
+  Tmp<uint32_t> c, k, o;
+  TCK(tmp_in(c, ctr, 4 * n)); TCK(tmp_in(k, key, 2 * n)); TCK(tmp_in(o, (const uint32_t*)nullptr, 4 * n));
+  TCK(launch_test_philox(c.p, k.p, n, o.p, false, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(tmp_out(out, o, 4 * n));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_test_curand_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out) {
+  if (!ctr || !key || !out || n < 0) return fail(nullptr, TMVN_E_ARG, "bad args");
+  Tmp<uint32_t> c, k, o;
+  TCK(tmp_in(c, ctr, 4 * n)); TCK(tmp_in(k, key, 2 * n)); TCK(tmp_in(o, (const uint32_t*)nullptr, 4 * n));
+  TCK(launch_test_philox(c.p, k.p, n, o.p, true, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(tmp_out(out, o, 4 * n));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_test_normals(uint64_t seed, uint64_t t, int64_t c0, int64_t C, int64_t d, double* nu,
+                              double* u) {
+  if (C < 0 || d < 1 || !nu) return fail(nullptr, TMVN_E_ARG, "bad args");
+  Tmp<double> dn, du;
+  TCK(tmp_in(dn, (const double*)nullptr, (size_t)C * d)); TCK(tmp_in(du, (const double*)nullptr, (size_t)C));
+  TCK(launch_test_normals(seed, (uint32_t)t, (uint32_t)c0, (int)C, (int)d, dn.p, du.p, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(tmp_out(nu, dn, (size_t)C * d));
+  if (u) TCK(tmp_out(u, du, (size_t)C));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_test_arcs(const double* p, const double* q, const double* b, int64_t n, double* alpha,
+                           double* beta, uint8_t* active) {
+  if (!p || !q || !b || !alpha || !beta || !active || n < 0) return fail(nullptr, TMVN_E_ARG, "bad args");
+  Tmp<double> dp, dq, db, da, dbe;
+  Tmp<uint8_t> dact;
+  TCK(tmp_in(dp, p, n)); TCK(tmp_in(dq, q, n)); TCK(tmp_in(db, b, n));
+  TCK(tmp_in(da, (const double*)nullptr, n)); TCK(tmp_in(dbe, (const double*)nullptr, n));
+  TCK(tmp_in(dact, (const uint8_t*)nullptr, n));
+  TCK(launch_test_arcs(dp.p, dq.p, db.p, n, da.p, dbe.p, dact.p, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(tmp_out(alpha, da, n)); TCK(tmp_out(beta, dbe, n)); TCK(tmp_out(active, dact, n));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t m, int64_t C,
+                                const double* u, double eps, double* seg_lo, double* seg_hi,
+                                int64_t seg_cap, int64_t* nseg, double* L, double* theta) {
+  if (!alpha || !beta || m < 1 || C < 1 || seg_cap < 0) return fail(nullptr, TMVN_E_ARG, "bad args");
+  const size_t cm = (size_t)C * m;
+  Tmp<double> da, db, du, dlo, dhi, dL, dth;
+  Tmp<int64_t> dns;
+  Tmp<double2> gstash, ggaps;
+  TCK(tmp_in(da, alpha, cm)); TCK(tmp_in(db, beta, cm));
+  TCK(tmp_in(du, u, u ? (size_t)C : 0));
+  TCK(tmp_in(dlo, (const double*)nullptr, (size_t)C * seg_cap)); TCK(tmp_in(dhi, (const double*)nullptr, (size_t)C * seg_cap));
+  TCK(tmp_in(dL, (const double*)nullptr, (size_t)C)); TCK(tmp_in(dth, (const double*)nullptr, (size_t)C));
+  TCK(tmp_in(dns, (const int64_t*)nullptr, (size_t)C));
+  const int NB = ess_buckets((int)m);
+  const int grid = ess_grid((int)C, (int)m, NB);
+  if (m > kStashSmemMax) TCK(tmp_in(gstash, (const double2*)nullptr, (size_t)grid * m));
+  TCK(tmp_in(ggaps, (const double2*)nullptr, (size_t)grid * (m + 2)));
+  EssParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.m = (int)m;
+  p.C = (int)C;
+  p.eps = eps;
+  p.g_alpha = da.p;
+  p.g_beta = db.p;
+  p.g_u = u ? du.p : nullptr;
+  p.gstash = gstash.p;
+  p.ggaps = ggaps.p;
+  p.NB = NB;
+  p.d_seg_lo = seg_cap ? dlo.p : nullptr;
+  p.d_seg_hi = dhi.p;
+  p.seg_cap = seg_cap;
+  p.d_nseg = dns.p;
+  p.d_L = dL.p;
+  p.d_theta = dth.p;
+  TCK(launch_ess_intervals(p, grid, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(tmp_out(seg_lo, dlo, (size_t)C * seg_cap)); TCK(tmp_out(seg_hi, dhi, (size_t)C * seg_cap));
+  TCK(tmp_out(nseg, dns, (size_t)C)); TCK(tmp_out(L, dL, (size_t)C)); TCK(tmp_out(theta, dth, (size_t)C));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K, double* out) {
+  if (!X || !W || !out || R < 1 || S < 1 || K < 1) return fail(nullptr, TMVN_E_ARG, "bad args");
+  const int64_t Rp = round_up(R, kTileR), Sp = round_up(S, kTileR), Kp = round_up(K, kTileK);
+  Tmp<double> dx, dw, xt, wt, o;
+  TCK(tmp_in(dx, X, (size_t)R * K)); TCK(tmp_in(dw, W, (size_t)S * K));
+  TCK(tmp_in(xt, (const double*)nullptr, (size_t)Rp * Kp)); TCK(tmp_in(wt, (const double*)nullptr, (size_t)Sp * Kp));
+  TCK(tmp_in(o, (const double*)nullptr, (size_t)Rp * Sp));
+  TCK(launch_pack(dx.p, R, K, K, xt.p, Kp, 0));
+  TCK(launch_pack(dw.p, S, K, K, wt.p, Kp, 0));
+  TCK(launch_gemm_tn(xt.p, Rp, wt.p, Sp, Kp, o.p, Sp, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(cudaMemcpy2D(out, S * sizeof(double), o.p, Sp * sizeof(double), S * sizeof(double), R, cudaMemcpyDefault));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t seed, int64_t t,
+                           tmvn_step_dump* dump) {
+  if (!h || !Xt || C < 1 || t < 0 || t >= ((int64_t)1 << 32) || !dump) return fail(h, TMVN_E_ARG, "bad args");
+  tmvn_status s;
+  if ((s = set_device(h)) != TMVN_OK) return s;
+  if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
+  cudaStream_t st = stream_of(h);
+  const int64_t m = h->m, d = h->d;
+  const int grid = ess_grid((int)C, (int)m, h->NB);
+  // X_t is given in u-space
+  CK(h, cudaMemcpyAsync(h->stage, Xt, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
+  CK(h, launch_pack(h->stage, C, d, d, h->X, h->d_pad, st));
+  CK(h, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, h->P0, h->m_pad, st));
+  CK(h, launch_normals(h->N, (int)C, (int)d, h->d_pad, seed, (uint32_t)t, (uint32_t)h->opt.chain_offset, st));
+  CK(h, launch_gemm_tn(h->N, h->C_pad, h->At, h->m_pad, h->d_pad, h->Q, h->m_pad, st));
+  CK(h, cudaMemsetAsync(h->rej, 0, (size_t)h->C_pad * sizeof(int64_t), st));
+  const size_t cm = (size_t)C * m;
+  const int64_t cap = dump->seg_cap > 0 ? dump->seg_cap : 0;
+  Tmp<double> da, db, dlo, dhi, dL, dth, dsl;
+  Tmp<uint8_t> dact;
+  Tmp<int64_t> dns;
+  Tmp<int32_t> dacc;
+  CK(h, tmp_in(da, (const double*)nullptr, cm)); CK(h, tmp_in(db, (const double*)nullptr, cm));
+  CK(h, tmp_in(dact, (const uint8_t*)nullptr, cm));
+  CK(h, tmp_in(dlo, (const double*)nullptr, (size_t)C * cap)); CK(h, tmp_in(dhi, (const double*)nullptr, (size_t)C * cap));
+  CK(h, tmp_in(dL, (const double*)nullptr, (size_t)C)); CK(h, tmp_in(dth, (const double*)nullptr, (size_t)C));
+  CK(h, tmp_in(dsl, (const double*)nullptr, (size_t)C));
+  CK(h, tmp_in(dns, (const int64_t*)nullptr, (size_t)C)); CK(h, tmp_in(dacc, (const int32_t*)nullptr, (size_t)C));
+  // nu, p, q before the step mutates them
+  if (dump->nu) {
+    CK(h, launch_unpack(h->N, C, d, h->d_pad, h->stage2, st));
+    CK(h, cudaMemcpyAsync(dump->nu, h->stage2, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
+  }
+  if (dump->p) CK(h, cudaMemcpy2DAsync(dump->p, m * sizeof(double), h->P0, h->m_pad * sizeof(double), m * sizeof(double), C, cudaMemcpyDefault, st));
+  if (dump->q) CK(h, cudaMemcpy2DAsync(dump->q, m * sizeof(double), h->Q, h->m_pad * sizeof(double), m * sizeof(double), C, cudaMemcpyDefault, st));
+  if (dump->u) {  // u of block (0, t, c, 1), drawn by the same device function as the step
+    Tmp<double> dn, du;
+    CK(h, tmp_in(dn, (const double*)nullptr, (size_t)C * d));
+    CK(h, tmp_in(du, (const double*)nullptr, (size_t)C));
+    CK(h, cudaStreamSynchronize(st));
+    CK(h, launch_test_normals(seed, (uint32_t)t, (uint32_t)h->opt.chain_offset, (int)C, (int)d, dn.p, du.p, st));
+    CK(h, cudaStreamSynchronize(st));
+    CK(h, tmp_out(dump->u, du, (size_t)C));
+  }
+  EssParams p = base_params(h, (int)C);
+  p.P_cur = h->P0;
+  p.P_next = h->P1;
+  p.Q = h->Q;
+  p.seed = seed;
+  p.t = (uint32_t)t;
+  p.gen_next = 0;
+  p.record = 0;
+  p.d_alpha = da.p;
+  p.d_beta = db.p;
+  p.d_active = dact.p;
+  p.d_seg_lo = cap ? dlo.p : nullptr;
+  p.d_seg_hi = dhi.p;
+  p.seg_cap = cap;
+  p.d_nseg = dns.p;
+  p.d_L = dL.p;
+  p.d_theta = dth.p;
+  p.d_slack = dsl.p;
+  p.d_accept = dacc.p;
+  CK(h, launch_ess_step(p, grid, st));
+  CK(h, cudaStreamSynchronize(st));
+  if (dump->x_next) {
+    CK(h, launch_unpack(h->X, C, d, h->d_pad, h->stage2, st));
+    CK(h, cudaMemcpyAsync(dump->x_next, h->stage2, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
+  }
+  CK(h, cudaStreamSynchronize(st));
+  CK(h, tmp_out(dump->alpha, da, cm)); CK(h, tmp_out(dump->beta, db, cm)); CK(h, tmp_out(dump->active, dact, cm));
+  CK(h, tmp_out(dump->seg_lo, dlo, (size_t)C * cap)); CK(h, tmp_out(dump->seg_hi, dhi, (size_t)C * cap));
+  CK(h, tmp_out(dump->nseg, dns, (size_t)C)); CK(h, tmp_out(dump->L, dL, (size_t)C));
+  CK(h, tmp_out(dump->theta, dth, (size_t)C)); CK(h, tmp_out(dump->max_slack, dsl, (size_t)C));
+  CK(h, tmp_out(dump->accept, dacc, (size_t)C));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed,
+                            const int64_t* chains, int64_t n_trace, double* trace, double* out) {
+  if (!h || !chains || n_trace < 1 || !trace) return fail(h, TMVN_E_ARG, "bad args");
+  for (int64_t k = 0; k < n_trace; ++k)
+    if (chains[k] < 0 || chains[k] >= C) return fail(h, TMVN_E_ARG, "trace chain out of range");
+  if (h->affine) return fail(h, TMVN_E_STATE, "trace hook records u-space; unset affine first");
+  tmvn_status s = check_sample_args(h, X0, C, n_iter, out);
+  if (s != TMVN_OK) return s;
+  if ((s = set_device(h)) != TMVN_OK) return s;
+  if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
+  h->grid = ess_grid((int)C, (int)h->m, h->NB);
+  Tmp<int64_t> rows;
+  Tmp<double> tr;
+  CK(h, tmp_in(rows, chains, (size_t)n_trace));
+  CK(h, tmp_in(tr, (const double*)nullptr, (size_t)(n_iter + 1) * n_trace * h->d));
+  if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
+  CK(h, launch_gather_rows_tiled(h->X, h->d_pad, (int)h->d, rows.p, (int)n_trace, tr.p, stream_of(h)));
+  if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;
+  if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
+  h->trace_rows = rows.p;
+  h->trace_n = (int)n_trace;
+  h->trace_dev = tr.p;
+  int64_t nrec = 0;
+  s = run_loop(h, C, n_iter, seed, h->P0, &nrec);
+  h->trace_dev = nullptr;
+  h->trace_rows = nullptr;
+  if (s != TMVN_OK) return s;
+  if ((s = store_X(h, C, out)) != TMVN_OK) return s;
+  if ((s = finish_stats(h, C, n_iter, nrec)) != TMVN_OK) return s;
+  CK(h, tmp_out(trace, tr, (size_t)(n_iter + 1) * n_trace * h->d));
+  if (h->opt.auto_advance) h->opt.iter_offset += n_iter;
+  return TMVN_OK;
+}
+
+}  // extern "C"

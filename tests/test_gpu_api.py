@@ -1,0 +1,173 @@
+"""Semantics of the public C-ABI on the GPU: errors, determinism, sharding
+invariance, resume, device pointers, moments, App. A affine mode, and the
+statistical pins of the paper's S4.1 experiment (closed-form 1-D moments)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2407_10449_b200 as tm
+from paper_2407_10449_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def test_errors():
+    A, b, x0 = synth.make_instance(3, m=50, d=10)
+    s = tm.Sampler(A, b)
+    X = np.tile(x0, (8, 1))
+    X[5] = 100 * A[17] / np.linalg.norm(A[17])  # violates constraint 17 (at least)
+    with pytest.raises(tm.TmvnError) as ei:
+        s.sample(X, 3, seed=1)
+    assert ei.value.status == -3 and "chain 5" in str(ei.value)
+    # boundary start is not strictly interior (C18)
+    Xb = np.tile(x0, (2, 1))
+    Xb[1] = A[3] * b[3] / (A[3] @ A[3])
+    with pytest.raises(tm.TmvnError):
+        s.sample(Xb, 1, seed=1)
+    # handle stays valid
+    out = s.sample(np.tile(x0, (4, 1)), 3, seed=1)
+    assert np.all(A @ out.T <= b[:, None])
+    with pytest.raises(tm.TmvnError) as ei:
+        Az = A.copy()
+        Az[2] = 0
+        bz = b.copy()
+        bz[2] = -1
+        tm.Sampler(Az, bz)
+    assert ei.value.status == -2
+    with pytest.raises(tm.TmvnError) as ei:
+        s.set_affine(np.zeros(10), np.triu(np.ones((10, 10))))
+    assert ei.value.status == -4
+    with pytest.raises(tm.TmvnError):
+        tm.Sampler(np.full((2, 2), np.nan), np.ones(2))
+
+
+def test_shard_invariance_and_resume_bitwise():
+    A, b, x0 = synth.make_instance(3, m=300, d=64)
+    C = 300
+    X0 = np.tile(x0, (C, 1))
+    s = tm.Sampler(A, b)
+    full = s.sample(X0, 64, seed=7)
+    # two "ranks": chain_offset sharding (global chain index in the RNG counter, no split-K)
+    s1 = tm.Sampler(A, b, chain_offset=0)
+    s2 = tm.Sampler(A, b, chain_offset=173)
+    h1 = s1.sample(X0[:173], 64, seed=7)
+    h2 = s2.sample(X0[173:], 64, seed=7)
+    assert np.array_equal(np.concatenate([h1, h2]), full)
+    # resume at a multiple of recompute_every reproduces the run bitwise
+    s3 = tm.Sampler(A, b)
+    a = s3.sample(X0, 32, seed=7)
+    a = s3.sample(a, 32, seed=7)  # iter_offset auto-advanced to 32
+    assert np.array_equal(a, full)
+    assert s3.options().iter_offset == 64
+
+
+def test_device_tensors_inplace_and_stream():
+    import torch
+    A, b, x0 = synth.make_instance(3, m=200, d=50)
+    C = 256
+    s = tm.Sampler(A, b)
+    ref = s.sample(np.tile(x0, (C, 1)), 10, seed=3)
+    s2 = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
+    stream = torch.cuda.Stream()
+    s2.set_options(stream=stream)
+    X = torch.tensor(np.tile(x0, (C, 1)), device="cuda")
+    s2.sample(X, 10, seed=3, out=X)  # in place
+    torch.cuda.synchronize()
+    assert np.array_equal(X.cpu().numpy(), ref)
+
+
+def test_moments_match_trajectory_sums():
+    A, b, x0 = synth.make_instance(3, m=120, d=30)
+    C, T = 64, 40
+    s = tm.Sampler(A, b, burn_in=10, thin=3)
+    trace, out = s.test_trace(np.tile(x0, (C, 1)), T, seed=5, chains=np.arange(C))
+    sm, sq, n = s.moments()
+    rec = [t for t in range(T) if t >= 10 and (t - 10) % 3 == 0]
+    X = trace[[t + 1 for t in rec]]  # iterate produced by iteration t
+    assert n == C * len(rec)
+    assert np.allclose(sm, X.sum(axis=(0, 1)), rtol=1e-12, atol=1e-12)
+    assert np.allclose(sq, (X**2).sum(axis=(0, 1)), rtol=1e-12, atol=1e-12)
+
+
+def trunc_normal_moments(lo, hi):
+    phi = lambda z: math.exp(-0.5 * z * z) / math.sqrt(2 * math.pi)
+    if lo > 0:
+        Z = 0.5 * (math.erfc(lo / math.sqrt(2)) - math.erfc(hi / math.sqrt(2)))
+    else:
+        Z = 0.5 * (math.erf(hi / math.sqrt(2)) - math.erf(lo / math.sqrt(2)))
+    mu = (phi(lo) - phi(hi)) / Z
+    return mu, 1.0 + (lo * phi(lo) - hi * phi(hi)) / Z - mu * mu
+
+
+@pytest.mark.parametrize("interval", [(-1.0, 3.0), (15.0, 16.0)])
+def test_section_4_1_protocol(interval):
+    """2000 chains, burn-in 500, thinning 10, 1e5 samples."""
+    A, b, x0 = synth.one_dim(interval)
+    s = tm.Sampler(A, b, burn_in=500, thin=10)
+    out = s.sample(np.tile(x0, (2000, 1)), 1000, seed=2024)
+    sm, sq, n = s.moments()
+    assert n == 100000
+    mu, var = trunc_normal_moments(*interval)
+    m1 = sm[0] / n
+    v1 = sq[0] / n - m1 * m1
+    assert abs(m1 - mu) < 0.01 and abs(v1 - var) < 0.01
+    st = s.stats()
+    assert st["steps"] == 2_000_000
+    assert st["rejections"] <= 200  # FP64: the paper saw 8 in FP32 on [15, 16]
+    assert np.all(out >= interval[0]) and np.all(out <= interval[1])
+
+
+def test_orthant_config2_moments():
+    A, b, x0 = synth.make_instance(2)
+    s = tm.Sampler(A, b, burn_in=15000)
+    s.sample(np.tile(x0, (1024, 1)), 20000, seed=102)
+    sm, sq, n = s.moments()
+    mean = sm / n
+    var = sq / n - mean**2
+    assert abs(mean.mean() - math.sqrt(2 / math.pi)) < 0.01
+    assert abs(var.mean() - (1 - 2 / math.pi)) < 0.01
+    assert s.stats()["rejections"] == 0
+
+
+def test_tiny2d_config1_vs_rejection():
+    A, b, x0 = synth.make_instance(1)
+    rng = np.random.default_rng(1)
+    z = rng.standard_normal((4_000_000, 2))
+    acc = z[np.all(z @ A.T <= b, axis=1)]
+    s = tm.Sampler(A, b, burn_in=200)
+    s.sample(np.tile(x0, (4096, 1)), 2000, seed=101)
+    sm, sq, n = s.moments()
+    assert np.all(np.abs(sm / n - acc.mean(0)) < 0.01)
+    assert np.all(np.abs(sq / n - (acc**2).mean(0)) < 0.02)
+
+
+def test_affine_change_of_variable():
+    """App. A: N(mu, L L^T) truncated; the sampler reports x-space."""
+    d = 6
+    L, mu = synth.random_spd_factor(d, seed=3)
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((9, d))
+    x_start = mu.copy()
+    b = A @ x_start + rng.uniform(0.5, 1.5, 9)
+    s = tm.Sampler(A, b, mu=mu, L=L)
+    C = 64
+    X0 = np.tile(x_start, (C, 1))
+    out = s.sample(X0, 5, seed=11)
+    assert np.all(A @ out.T <= b[:, None] + 1e-12)
+    # oracle in u-space on the whitened polytope, then x = L u + mu
+    Aw, bw = oracle.whiten(A, b, mu, L)
+    u0 = oracle.whiten_point(x_start, mu, L)
+    r = oracle.run(Aw, bw, np.tile(u0, (C, 1)), 5, seed=11)
+    xo = np.array([oracle.unwhiten_point(u, mu, L) for u in r["X"]])
+    assert np.allclose(out, xo, rtol=1e-9, atol=1e-9)
+    # 1-D closed form: x ~ N(2, 4) truncated to [1, 5]
+    s1 = tm.Sampler(np.array([[1.0], [-1.0]]), np.array([5.0, -1.0]), mu=np.array([2.0]),
+                    L=np.array([[2.0]]), burn_in=100)
+    s1.sample(np.full((2000, 1), 3.0), 600, seed=77)
+    sm, sq, n = s1.moments()
+    mu_u, var_u = trunc_normal_moments(-0.5, 1.5)
+    m1 = sm[0] / n
+    assert abs(m1 - (2 + 2 * mu_u)) < 0.01
+    assert abs(sq[0] / n - m1 * m1 - 4 * var_u) < 0.03

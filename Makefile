@@ -24,3 +24,14 @@ clean:
 	rm -rf build $(PKG)/libtmvn.so oracle/liboracle.so
 
 .PHONY: all clean
+
+# profiling variant (tools/phase_timing.py), never loaded by the product path
+build/timing/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build/timing
+	$(NVCC) $(NVFLAGS) -DTMVN_PHASE_TIMING -c $< -o $@ 2> /dev/null
+
+build/libtmvn_timing.so: $(patsubst $(CSRC)/%.cu,build/timing/%.o,$(SRCS))
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
+
+timing: build/libtmvn_timing.so
+.PHONY: timing

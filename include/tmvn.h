@@ -80,6 +80,19 @@ typedef struct {
    * CUDA events on `stream` and accumulate their durations (tmvn_get_profile).
    * Default 0. */
   int32_t profile;
+  /* Warps of the fused per-chain kernel that own one chain: 1, 2, 4 or 8;
+   * 0 (default) = chosen from C and m. */
+  int32_t chain_warps;
+  /* Chain shards run as independent GEMM -> ESS sequences on concurrent streams
+   * (forked from / joined to `stream`), so the FP64 tensor GEMM of one shard
+   * overlaps the ALU-bound per-chain kernel of another.  0 (default) = 2 when
+   * C >= 1024, else 1.  Results do not depend on it. */
+  int32_t streams;
+  /* 1: stream each chain's P and Q rows into shared memory with cp.async.bulk
+   * through a 2-slot mbarrier ring (the next chain's rows prefetched); 0
+   * (default): read them from global memory (measured faster on B200 at
+   * config 3: the ring costs occupancy, profiles/r01/README.md). */
+  int32_t ring;
 } tmvn_options;
 
 typedef struct {

@@ -44,7 +44,8 @@ class options(ctypes.Structure):
                 ("burn_in", ctypes.c_int64), ("thin", ctypes.c_int64), ("record", ctypes.c_int32),
                 ("chain_offset", ctypes.c_int64), ("iter_offset", ctypes.c_int64),
                 ("auto_advance", ctypes.c_int32), ("stream", ctypes.c_void_p),
-                ("profile", ctypes.c_int32)]
+                ("profile", ctypes.c_int32), ("chain_warps", ctypes.c_int32),
+                ("streams", ctypes.c_int32), ("ring", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):

@@ -29,19 +29,16 @@ __global__ void unpack_kernel(const double* __restrict__ src, int64_t R, int64_t
   }
 }
 
-// one thread per 64-byte run of nu
+// one thread per normal pair (one double2 of the tiled N)
 __global__ void normals_kernel(double* __restrict__ N, int C, int d, int64_t d_pad, uint64_t seed,
                                uint32_t t, uint32_t chain_offset) {
-  const int runs = (int)(d_pad / 8);
-  int64_t n = (int64_t)C * runs;
+  const int pairs = (int)(d_pad / 2);
+  int64_t n = (int64_t)C * pairs;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(e / runs), a = (int)(e % runs);
-    double nn[8];
-    normal_run(seed, t, chain_offset + (uint32_t)c, a, d, nn);
-    double2* o = reinterpret_cast<double2*>(N + run_offset(c, a, d_pad));
-#pragma unroll
-    for (int h = 0; h < 4; ++h) o[h] = make_double2(nn[2 * h], nn[2 * h + 1]);
+    int c = (int)(e / pairs), k0 = 2 * (int)(e % pairs);
+    *reinterpret_cast<double2*>(N + tiled_offset(c, k0, d_pad)) =
+        normal_pair_at(seed, t, chain_offset + (uint32_t)c, k0, d);
   }
 }
 
@@ -57,13 +54,26 @@ __global__ void start_check_kernel(const double* __restrict__ P, int64_t ldp,
   }
 }
 
-// deterministic: thread j sums chains in index order
-__global__ void chain_sum_kernel(const double* __restrict__ S, int C, int d, int64_t d_pad,
-                                 double* __restrict__ out) {
+// Deterministic two-level sum over chains: block (x, y) sums chains
+// [64y, 64y + 64) in index order for coordinates 128x .. 128x+127 into
+// part[y][j]; chain_sum_final adds the parts in index order.
+constexpr int kSumChunk = 64;
+__global__ void chain_sum_part_kernel(const double* __restrict__ S, int C, int d, int64_t d_pad,
+                                      double* __restrict__ part) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  int c0 = blockIdx.y * kSumChunk;
+  if (j >= d) return;
+  double s = 0.0;
+  int c1 = min(C, c0 + kSumChunk);
+  for (int c = c0; c < c1; ++c) s += S[tiled_offset(c, j, d_pad)];
+  part[(int64_t)blockIdx.y * d + j] = s;
+}
+__global__ void chain_sum_final_kernel(const double* __restrict__ part, int nparts, int d,
+                                       double* __restrict__ out) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d) return;
   double s = 0.0;
-  for (int c = 0; c < C; ++c) s += S[tiled_offset(c, j, d_pad)];
+  for (int y = 0; y < nparts; ++y) s += part[(int64_t)y * d + j];
   out[j] = s;
 }
 
@@ -178,18 +188,15 @@ __global__ void test_philox_kernel(const uint32_t* __restrict__ ctr, const uint3
 
 __global__ void test_normals_kernel(uint64_t seed, uint32_t t, uint32_t c0, int C, int d,
                                     double* __restrict__ nu, double* __restrict__ u) {
-  const int runs = (d + 7) / 8;
-  int64_t n = (int64_t)C * runs;
+  const int pairs = (d + 1) / 2;
+  int64_t n = (int64_t)C * pairs;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(e / runs), a = (int)(e % runs);
-    double nn[8];
-    normal_run(seed, t, c0 + (uint32_t)c, a, d, nn);
-    for (int kk = 0; kk < 8; ++kk) {
-      int k = a * 8 + kk;
-      if (k < d) nu[(int64_t)c * d + k] = nn[run_slot(kk)];
-    }
-    if (a == 0 && u) u[c] = theta_uniform(seed, t, c0 + (uint32_t)c);
+    int c = (int)(e / pairs), k0 = 2 * (int)(e % pairs);
+    double2 v = normal_pair_at(seed, t, c0 + (uint32_t)c, k0, d);
+    nu[(int64_t)c * d + k0] = v.x;
+    if (k0 + 1 < d) nu[(int64_t)c * d + k0 + 1] = v.y;
+    if (k0 == 0 && u) u[c] = theta_uniform(seed, t, c0 + (uint32_t)c);
   }
 }
 
@@ -227,7 +234,7 @@ cudaError_t launch_unpack(const double* src, int64_t R, int64_t K, int64_t K_pad
 }
 cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed, uint32_t t,
                            uint32_t chain_offset, cudaStream_t st) {
-  int64_t n = (int64_t)C * (d_pad / 8);
+  int64_t n = (int64_t)C * (d_pad / 2);
   if (n == 0) return cudaSuccess;
   normals_kernel<<<grid_for(n), 256, 0, st>>>(N, C, d, d_pad, seed, t, chain_offset);
   return cudaGetLastError();
@@ -238,8 +245,10 @@ cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, in
   return cudaGetLastError();
 }
 cudaError_t launch_chain_sum(const double* S, int C, int d, int64_t d_pad, double* out,
-                             cudaStream_t st) {
-  chain_sum_kernel<<<(d + 127) / 128, 128, 0, st>>>(S, C, d, d_pad, out);
+                             double* part, cudaStream_t st) {
+  int nparts = (C + kSumChunk - 1) / kSumChunk;
+  chain_sum_part_kernel<<<dim3((d + 127) / 128, nparts), 128, 0, st>>>(S, C, d, d_pad, part);
+  chain_sum_final_kernel<<<(d + 127) / 128, 128, 0, st>>>(part, nparts, d, out);
   return cudaGetLastError();
 }
 cudaError_t launch_accum_affine(const double* Xrow, int64_t ldx, const double* mu, int C, int d,
@@ -281,7 +290,7 @@ cudaError_t launch_test_philox(const uint32_t* ctr, const uint32_t* key, int64_t
 }
 cudaError_t launch_test_normals(uint64_t seed, uint32_t t, uint32_t c0, int C, int d, double* nu,
                                 double* u, cudaStream_t st) {
-  int64_t n = (int64_t)C * ((d + 7) / 8);
+  int64_t n = (int64_t)C * ((d + 1) / 2);
   if (n == 0) return cudaSuccess;
   test_normals_kernel<<<grid_for(n), 256, 0, st>>>(seed, t, c0, C, d, nu, u);
   return cudaGetLastError();

@@ -15,11 +15,13 @@ namespace tmvn {
 // K = dimension d).  R is padded to a multiple of 128 and K to a multiple of 16.
 // A 128 x 16 block is one contiguous 16 KB chunk (one cp.async.bulk); blocks of
 // the same 128 rows are consecutive in K.  Inside a chunk, 8-row group g and
-// k-half kh (k%16 / 8) own 64 doubles, ordered by mma.m8n8k4 lane:
-//   lane = (r % 8) * 4 + (k % 4),  slot = lane * 2 + ((k % 8) / 4)
-// so one ld.shared.v2.f64 per lane yields the A (row-major) or B (col-major)
-// fragments of two consecutive k4 steps, with no bank conflicts.  A row's 8
-// consecutive k (k = 8a .. 8a+7) form one contiguous 64-byte run.
+// k-half kh (k%16 / 8) own 64 doubles = eight 64-byte runs, one per row
+// (r % 8), each run holding k = 8a .. 8a+7 in order.  Lane l of an
+// mma.m8n8k4 reads doubles 2l, 2l+1 with one ld.shared.v2.f64: row l/4 and
+// k = 2(l%4) + {0, 1}, i.e. the fragments of two k4-steps under the k
+// permutation (j, v) -> 2j + v, which is the same for both operands, so the
+// product is unchanged; the 32 lanes read 512 contiguous bytes (no bank
+// conflicts).  A normal pair (nu_{2j}, nu_{2j+1}) is one aligned double2.
 // ----------------------------------------------------------------------------
 constexpr int kTileR = 128;
 constexpr int kTileK = 16;
@@ -27,22 +29,54 @@ constexpr int kChunk = kTileR * kTileK;  // doubles per chunk
 
 __host__ __device__ inline int64_t round_up(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
 
-__host__ __device__ inline int64_t tiled_offset(int64_t r, int64_t k, int64_t K_pad) {
-  int64_t chunk = (r / kTileR) * (K_pad / kTileK) + k / kTileK;
-  int64_t g = (r % kTileR) / 8, kh = (k % kTileK) / 8;
-  int64_t lane = (r % 8) * 4 + (k % 4);
-  return chunk * kChunk + (g * 2 + kh) * 64 + lane * 2 + ((k % 8) / 4);
-}
-
 // Start of the 64-byte run holding k = 8a .. 8a+7 of row r.
 __host__ __device__ inline int64_t run_offset(int64_t r, int64_t a, int64_t K_pad) {
-  int64_t k = a * 8;
-  int64_t chunk = (r / kTileR) * (K_pad / kTileK) + k / kTileK;
-  int64_t g = (r % kTileR) / 8, kh = (k % kTileK) / 8;
+  int64_t chunk = (r / kTileR) * (K_pad / kTileK) + a / 2;
+  int64_t g = (r % kTileR) / 8, kh = a % 2;
   return chunk * kChunk + (g * 2 + kh) * 64 + (r % 8) * 8;
 }
-// Position inside a run of k (0..7 = k % 8).
-__host__ __device__ inline int run_slot(int kk) { return (kk % 4) * 2 + kk / 4; }
+
+__host__ __device__ inline int64_t tiled_offset(int64_t r, int64_t k, int64_t K_pad) {
+  return run_offset(r, k / 8, K_pad) + (k % 8);
+}
+
+// ----------------------------------------------------------------------------
+// mbarrier + cp.async.bulk (TMA bulk engine, SASS UBLKCP) helpers.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 // ----------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11).
@@ -92,35 +126,67 @@ __device__ __forceinline__ double theta_uniform(uint64_t seed, uint32_t t, uint3
   return u53(w.x, w.y);
 }
 
-// Fill one 64-byte run (k = 8a .. 8a+7) of nu with normals; zeros for k >= d.
-__device__ __forceinline__ void normal_run(uint64_t seed, uint32_t t, uint32_t chain, int a, int d,
-                                           double out[8]) {
-#pragma unroll
-  for (int pr = 0; pr < 4; ++pr) {
-    int k0 = a * 8 + pr * 2;
-    double n0 = 0.0, n1 = 0.0;
-    if (k0 < d) {
-      normal_pair(seed, (uint32_t)(k0 / 2), t, chain, n0, n1);
-      if (k0 + 1 >= d) n1 = 0.0;
-    }
-    out[run_slot(pr * 2)] = n0;
-    out[run_slot(pr * 2 + 1)] = n1;
+// nu_{2j}, nu_{2j+1} for k0 = 2j < d as a double2 (zero beyond d).
+__device__ __forceinline__ double2 normal_pair_at(uint64_t seed, uint32_t t, uint32_t chain, int k0,
+                                                  int d) {
+  double n0 = 0.0, n1 = 0.0;
+  if (k0 < d) {
+    normal_pair(seed, (uint32_t)(k0 / 2), t, chain, n0, n1);
+    if (k0 + 1 >= d) n1 = 0.0;
   }
+  return make_double2(n0, n1);
+}
+
+// ----------------------------------------------------------------------------
+// Branch-free FP64 atan2 (the libm one branches per octant and diverges inside a
+// warp).  t = min(|x|,|y|) / max(|x|,|y|) in [0, 1]; for t > tan(pi/8) the
+// identity atan(t) = pi/4 + atan((t-1)/(t+1)) folds the argument to
+// |t'| <= tan(pi/8) with the same single division ((mn-mx)/(mn+mx)); then
+// atan(t') = t' P(t'^2), P of degree 10 fitted by Chebyshev interpolation
+// (tools/fit_atan.py: 2.2e-16 max relative error in FP64 Horner/FMA); octant
+// reconstruction by selects.  Matches atan2's signed-zero conventions.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double fast_atan2(double y, double x) {
+  const double kPi = 3.141592653589793, kPi2 = 1.5707963267948966, kPi4 = 0.7853981633974483;
+  const double kTanPi8 = 0.41421356237309503;
+  const double ax = fabs(x), ay = fabs(y);
+  const double mx = fmax(ax, ay), mn = fmin(ax, ay);
+  const bool big = mn > kTanPi8 * mx;
+  const double num = big ? mn - mx : mn;
+  const double den = big ? mn + mx : mx;
+  const double t = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+  const double z = t * t;
+  double pz = 0.021135373157693246;
+  pz = fma(pz, z, -0.04348052215716462);
+  pz = fma(pz, z, 0.056883492268090106);
+  pz = fma(pz, z, -0.06640233930429408);
+  pz = fma(pz, z, 0.07689953496306857);
+  pz = fma(pz, z, -0.09090773074808414);
+  pz = fma(pz, z, 0.11111106180455946);
+  pz = fma(pz, z, -0.14285714180976467);
+  pz = fma(pz, z, 0.1999999999885511);
+  pz = fma(pz, z, -0.3333333333332844);
+  double r = fma(t * z, pz, t);  // t * (1 + z * pz)
+  r = big ? r + kPi4 : r;
+  r = ay > ax ? kPi2 - r : r;
+  r = (__double_as_longlong(x) < 0) ? kPi - r : r;      // x < 0 or x = -0
+  return (__double_as_longlong(y) < 0) ? -r : r;          // y < 0 or y = -0
 }
 
 // ----------------------------------------------------------------------------
 // Infeasible arc of constraint (p, q, b) on the ellipse (Eq. 2, eq:roots):
-// r = hypot(p, q); active iff r > b (C3); rho = clamp(b / r) (C5);
-// tau = atan2(q, p); delta = acos(rho); (alpha, beta) = (tau - delta, tau + delta)
-// shifted into [0, 2 pi] by C1.  Returns false for an inactive constraint.
+// r = |(p, q)|; active iff r > b (C3); tau = atan2(q, p);
+// delta = arccos(b / r) computed as atan2(sqrt((r - b)(r + b)), b) (same angle in
+// [0, pi]; the clamp of C5 becomes the clamp of (r - b)(r + b) at 0);
+// (alpha, beta) = (tau - delta, tau + delta) shifted into [0, 2 pi] by C1.
+// Returns false for an inactive constraint.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ bool arc_of(double p, double q, double b, double& alpha, double& beta) {
-  double r = hypot(p, q);
+  const double r = sqrt(fma(p, p, q * q));
   if (!(r > b)) return false;
-  double rho = __ddiv_rn(b, r);
-  rho = fmin(fmax(rho, -1.0), 1.0);
-  double tau = atan2(q, p);
-  double delta = acos(rho);
+  const double s = sqrt(fmax((r - b) * (r + b), 0.0));
+  const double tau = fast_atan2(q, p);
+  const double delta = fast_atan2(s, b);
   double lo = __dsub_rn(tau, delta);
   double hi = __dadd_rn(tau, delta);
   if (hi <= 0.0) {

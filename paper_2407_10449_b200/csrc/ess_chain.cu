@@ -1,7 +1,7 @@
 // ess_chain.cu -- one fused kernel per ESS iteration for every chain (Alg. 1,
 // P:169-181), everything after the projection GEMM:
 //
-//   A  arcs      per constraint i: r = hypot(p, q), the infeasible arc
+//   A  arcs      per constraint i: r = |(p, q)|, the infeasible arc
 //                (alpha_i, beta_i) of eq:roots (C1-C5); inactive
 //                constraints (r <= b) are compacted away.
 //   B  I_act     Alg. 3 / Prop. 1: sort the alphas, cumulative max
@@ -11,16 +11,21 @@
 //                the exclusive prefix max of max(beta) is gamma entering the
 //                bucket, and a bucket whose max(alpha) does not exceed it can
 //                hold no gap (Prop. 1), so only "live" buckets are gathered and
-//                sorted in shared memory (bitonic) and scanned (max-scan).
-//                Comparisons only: bit-identical to Alg. 2 on the same arcs
-//                (P:400-402).  Oversized buckets are refined level by level.
+//                sorted (warp shuffles, or bitonic in shared memory) and
+//                max-scanned.  Comparisons only: bit-identical to Alg. 2 on the
+//                same arcs.  Oversized buckets are refined.
 //   C  theta     canonical segments, S3.3 trim (C7), L = sum of lengths in
 //                ascending order, theta = inverse CDF at u (C10).
 //   D  update    P' = P cos(theta) + Q sin(theta) (Eq. 1), safeguard
 //                accept iff max_i (P'_i - b_i) <= 0 (C8),
 //                x <- x cos(theta) + nu sin(theta), moments, then nu for t+1.
 //
-// One CTA (256 threads) per chain, persistent grid-stride over chains.
+// A chain is owned by a group of W warps (W in {1, 2, 4, 8}); the 8 warps of a
+// CTA form 8/W independent groups that synchronise only among themselves
+// (named barriers `bar.sync id, 32 W`, or __syncwarp for W = 1), each looping
+// over chains (persistent grid).  Small W keeps many chains in flight per SM and
+// turns most synchronisation into warp-level shuffles; large W suits few
+// chains with many constraints.
 #include <cfloat>
 #include "common.cuh"
 #include "internal.h"
@@ -28,8 +33,8 @@
 namespace tmvn {
 namespace {
 
-constexpr int kWarps = kEssThreads / 32;
 constexpr uint64_t kTopBits = 0x7FF0000000000000ull;  // +inf: every alpha in [0, 2 pi] is below
+constexpr int kBatch = 2;  // constraint pairs per thread with loads in flight
 
 __device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
 __device__ __forceinline__ double bitsd(uint64_t b) { return __longlong_as_double((long long)b); }
@@ -45,13 +50,63 @@ struct Ctl {
   int action;
   int nseg;
   double L, theta;
-  int viol;
-  double slack;
+  int maxa_exact;       // max/min alpha per bucket exact (refinement levels)
+  int fast;             // 1: I_act built by the single-warp path
 };
 
 enum { kAll = 0, kPrefix = 1, kSame = 2, kNarrow = 3 };
 
-// --- block scans (blockDim == kEssThreads) -----------------------------------
+// Phase timing (tools/phase_timing.py builds with -DTMVN_PHASE_TIMING; never in
+// the product build): thread 0 of every group accumulates clock64 deltas between
+// the barriers that close each phase.
+#ifdef TMVN_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[10];
+#define PHASE(i)                      \
+  do {                                \
+    if (g.tid == 0) {                 \
+      long long now_ = clock64();     \
+      ph[i] += now_ - t_prev;         \
+      t_prev = now_;                  \
+    }                                 \
+  } while (0)
+#define PHASE_ADD(i, v)             \
+  do {                              \
+    if (g.tid == 0) ph[i] += (v);   \
+  } while (0)
+#else
+#define PHASE(i) \
+  do {           \
+  } while (0)
+#define PHASE_ADD(i, v) \
+  do {                  \
+  } while (0)
+#endif
+
+// --- a group of W warps owning one chain -------------------------------------
+template <int W>
+struct Grp {
+  static constexpr int kThreads = W * 32;
+  int gid;   // group index in the CTA (barrier id gid + 1)
+  int tid;   // thread index in the group
+  int warp;  // warp index in the group
+  int lane;
+  __device__ __forceinline__ void sync() const {
+    if (W == 1) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(gid + 1), "r"(kThreads) : "memory");
+  }
+  __device__ __forceinline__ int sync_or(int v) const {
+    if (W == 1) return __any_sync(0xffffffffu, v);
+    int r;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.s32 p, %1, 0;\n bar.red.or.pred q, %2, %3, p;\n"
+        " selp.s32 %0, 1, 0, q;\n}\n"
+        : "=r"(r)
+        : "r"(v), "r"(gid + 1), "r"(kThreads)
+        : "memory");
+    return r;
+  }
+};
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_max(T v) {
 #pragma unroll
@@ -70,48 +125,58 @@ __device__ __forceinline__ T warp_incl_sum(T v) {
   }
   return v;
 }
-// exclusive max-scan of v over threads (init `init`); *total = max(init, all v)
-__device__ uint64_t block_excl_max(uint64_t v, uint64_t init, uint64_t* s_w, uint64_t* total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint64_t inc = warp_incl_max(v);
+// exclusive max-scan of v over the group's threads (init `init`); *total = max(init, all v)
+template <int W>
+__device__ uint64_t grp_excl_max(const Grp<W>& g, uint64_t v, uint64_t init, uint64_t* s_w,
+                                 uint64_t* total) {
+  const uint64_t inc = warp_incl_max(v);
   uint64_t exc = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 0) exc = 0;
-  if (lane == 31) s_w[w] = inc;
-  __syncthreads();
-  uint64_t pre = init;
-  for (int i = 0; i < w; ++i) pre = pre > s_w[i] ? pre : s_w[i];
-  uint64_t tot = init;
-  for (int i = 0; i < kWarps; ++i) tot = tot > s_w[i] ? tot : s_w[i];
-  __syncthreads();
+  if (g.lane == 0) exc = 0;
+  if (W == 1) {
+    const uint64_t t = __shfl_sync(0xffffffffu, inc, 31);
+    *total = init > t ? init : t;
+    return init > exc ? init : exc;
+  }
+  if (g.lane == 31) s_w[g.warp] = inc;
+  g.sync();
+  uint64_t pre = init, tot = init;
+  for (int i = 0; i < W; ++i) {
+    if (i < g.warp) pre = pre > s_w[i] ? pre : s_w[i];
+    tot = tot > s_w[i] ? tot : s_w[i];
+  }
+  g.sync();
   *total = tot;
   return pre > exc ? pre : exc;
 }
-__device__ int block_excl_sum(int v, int* s_w, int* total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int inc = warp_incl_sum(v);
-  if (lane == 31) s_w[w] = inc;
-  __syncthreads();
+template <int W>
+__device__ int grp_excl_sum(const Grp<W>& g, int v, int* s_w, int* total) {
+  const int inc = warp_incl_sum(v);
+  if (W == 1) {
+    *total = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - v;
+  }
+  if (g.lane == 31) s_w[g.warp] = inc;
+  g.sync();
   int pre = 0, tot = 0;
-  for (int i = 0; i < kWarps; ++i) {
-    if (i < w) pre += s_w[i];
+  for (int i = 0; i < W; ++i) {
+    if (i < g.warp) pre += s_w[i];
     tot += s_w[i];
   }
-  __syncthreads();
+  g.sync();
   *total = tot;
   return pre + inc - v;
 }
 
 struct Smem {
   uint64_t* maxA;
-  uint64_t* maxB;
-  uint64_t* minA;
-  uint64_t* Gx;
-  int* cnt;
-  int* off;
+  uint64_t* Gx;    // max beta per bucket; after the scan, in place, the exclusive prefix max
+  uint64_t* minA;  // exact only on refinement levels
   uint64_t* keys;  // kLiveCap
   double* vals;    // kLiveCap
   double2* gaps;   // kGapSmem
-  double2* stash;  // m (if in smem)
+  int* cnt;
+  int* off;
+  int* head;       // NB: first stash slot of each level-1 bucket (-1 = none)
 };
 
 __device__ __forceinline__ int bucket_key(double a, const Ctl& c, int NB, double scale) {
@@ -143,31 +208,61 @@ __device__ __forceinline__ double2 gap_load(const Smem& S, const double2* gg, in
   return k < kGapSmem ? S.gaps[k] : gg[k - kGapSmem];
 }
 
-__device__ void clear_buckets(const Smem& S, int NB) {
-  for (int j = threadIdx.x; j < NB; j += blockDim.x) {
+template <int W>
+__device__ void clear_buckets(const Grp<W>& g, const Smem& S, int NB) {
+  for (int j = g.tid; j < NB; j += Grp<W>::kThreads) {
     S.maxA[j] = 0;
-    S.maxB[j] = 0;
+    S.Gx[j] = 0;
     S.minA[j] = ~0ull;
     S.cnt[j] = 0;
+    S.head[j] = -1;
   }
 }
 
+// Bucket statistics without 64-bit shared atomics (those compile to CAS spin
+// loops): non-negative doubles order like their bit patterns, so the max (min)
+// of a bucket is found on the high 32-bit word with a native 32-bit atomic, and
+// then on the low word among the values whose high word matched (bucket_add_lo).
+__device__ __forceinline__ uint32_t* hi_word(uint64_t* a) { return reinterpret_cast<uint32_t*>(a) + 1; }
+__device__ __forceinline__ uint32_t* lo_word(uint64_t* a) { return reinterpret_cast<uint32_t*>(a); }
+__device__ __forceinline__ uint32_t hi32(double x) { return (uint32_t)(dbits(x) >> 32); }
+__device__ __forceinline__ uint32_t lo32(double x) { return (uint32_t)dbits(x); }
+
+template <bool kExact>
 __device__ __forceinline__ void bucket_add(const Smem& S, int k, double a, double b) {
-  atomicMax((unsigned long long*)&S.maxA[k], (unsigned long long)dbits(a));
-  atomicMax((unsigned long long*)&S.maxB[k], (unsigned long long)dbits(b));
-  atomicMin((unsigned long long*)&S.minA[k], (unsigned long long)dbits(a));
+  atomicMax(hi_word(&S.Gx[k]), hi32(b));
+  atomicMax(hi_word(&S.maxA[k]), hi32(a));
+  if (kExact) atomicMin(hi_word(&S.minA[k]), hi32(a));
   atomicAdd(&S.cnt[k], 1);
 }
+template <bool kExact>
+__device__ __forceinline__ void bucket_add_lo(const Smem& S, int k, double a, double b) {
+  if (hi32(b) == *hi_word(&S.Gx[k])) atomicMax(lo_word(&S.Gx[k]), lo32(b));
+  if (kExact) {
+    if (hi32(a) == *hi_word(&S.maxA[k])) atomicMax(lo_word(&S.maxA[k]), lo32(a));
+    if (hi32(a) == *hi_word(&S.minA[k])) atomicMin(lo_word(&S.minA[k]), lo32(a));
+  }
+}
 
-// Bitonic sort of keys/vals[0, n) (n <= kLiveCap) ascending by key.
-__device__ void block_sort(const Smem& S, int n) {
+// A bucket that may hold a gap (Prop. 1: max alpha > gamma entering it).  On
+// level 1 only the high word of max alpha is known (low word 0), so the test uses
+// the largest value with that high word: conservative -- a dead bucket may be
+// gathered and then emits no gap.  The same predicate counts and gathers.
+__device__ __forceinline__ bool bucket_live(const Smem& S, const Ctl& c, int k) {
+  const uint64_t ma = c.maxa_exact ? S.maxA[k] : (S.maxA[k] | 0xFFFFFFFFull);
+  return S.cnt[k] > 0 && ma > S.Gx[k];
+}
+
+// Bitonic sort of keys/vals[0, n) (n <= kLiveCap) ascending by key (group-wide).
+template <int W>
+__device__ void grp_sort(const Grp<W>& g, const Smem& S, int n) {
   int n2 = 2;
   while (n2 < n) n2 <<= 1;
-  for (int i = n + threadIdx.x; i < n2; i += blockDim.x) S.keys[i] = ~0ull;
-  __syncthreads();
+  for (int i = n + g.tid; i < n2; i += Grp<W>::kThreads) S.keys[i] = ~0ull;
+  g.sync();
   for (int k = 2; k <= n2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+      for (int i = g.tid; i < n2; i += Grp<W>::kThreads) {
         int l = i ^ j;
         if (l > i) {
           bool up = (i & k) == 0;
@@ -181,129 +276,144 @@ __device__ void block_sort(const Smem& S, int n) {
           }
         }
       }
-      __syncthreads();
+      g.sync();
     }
   }
 }
 
 // Gather the arcs of live buckets with key < jo into keys/vals, sort, emit gaps.
-__device__ void process_batch(const Smem& S, Ctl& ctl, const double2* stash, int n_act, int jo,
-                              int n_live, int NB, double scale, double2* gg, uint64_t* s_w64,
-                              int* s_w32) {
-  for (int idx = threadIdx.x; idx < n_act; idx += blockDim.x) {
+template <int W>
+__device__ void process_batch(const Grp<W>& g, const Smem& S, Ctl& ctl, const double2* stash,
+                              int n_act, int jo, int n_live, int NB, double scale, double2* gg,
+                              uint64_t* s_w64, int* s_w32) {
+  for (int idx = g.tid; idx < n_act; idx += Grp<W>::kThreads) {
     double2 ab = stash[idx];
     uint64_t bits = dbits(ab.x);
     if (bits < ctl.rlo || bits > ctl.rhi) continue;
     int k = bucket_key(ab.x, ctl, NB, scale);
     if (k >= jo) continue;
-    if (!(S.cnt[k] > 0 && S.maxA[k] > S.Gx[k])) continue;  // dead bucket: no gap (Prop. 1)
+    if (!bucket_live(S, ctl, k)) continue;  // dead bucket: no gap (Prop. 1)
     int pos = atomicAdd(&S.off[k], 1);
     S.keys[pos] = bits;
     S.vals[pos] = ab.y;
   }
-  __syncthreads();
-  block_sort(S, n_live);
+  g.sync();
+  grp_sort(g, S, n_live);
   // gamma before element e: max(Gx[bucket], max beta of earlier elements of the batch)
-  const int per = (n_live + blockDim.x - 1) / blockDim.x;
-  const int e0 = threadIdx.x * per, e1 = min(n_live, e0 + per);
+  const int per = (n_live + Grp<W>::kThreads - 1) / Grp<W>::kThreads;
+  const int e0 = g.tid * per, e1 = min(n_live, e0 + per);
   uint64_t lmax = 0;
   for (int e = e0; e < e1; ++e) lmax = lmax > dbits(S.vals[e]) ? lmax : dbits(S.vals[e]);
   uint64_t tot64;
-  uint64_t run = block_excl_max(lmax, 0, s_w64, &tot64);
-  // first pass: count gaps of my elements
+  const uint64_t run = grp_excl_max(g, lmax, 0, s_w64, &tot64);
   int mine = 0;
   {
     uint64_t r = run;
     for (int e = e0; e < e1; ++e) {
-      double a = bitsd(S.keys[e]);
-      uint64_t g = S.Gx[bucket_key(a, ctl, NB, scale)];
-      g = g > r ? g : r;
-      if (S.keys[e] > g) ++mine;
+      uint64_t gb = S.Gx[bucket_key(bitsd(S.keys[e]), ctl, NB, scale)];
+      gb = gb > r ? gb : r;
+      if (S.keys[e] > gb) ++mine;
       uint64_t vb = dbits(S.vals[e]);
       r = r > vb ? r : vb;
     }
   }
   int total;
-  int pos = block_excl_sum(mine, s_w32, &total) + ctl.ngap;
+  int pos = grp_excl_sum(g, mine, s_w32, &total) + ctl.ngap;
   {
     uint64_t r = run;
     for (int e = e0; e < e1; ++e) {
-      double a = bitsd(S.keys[e]);
-      uint64_t g = S.Gx[bucket_key(a, ctl, NB, scale)];
-      g = g > r ? g : r;
-      if (S.keys[e] > g) gap_store(S, gg, pos++, bitsd(g), a);
+      const double a = bitsd(S.keys[e]);
+      uint64_t gb = S.Gx[bucket_key(a, ctl, NB, scale)];
+      gb = gb > r ? gb : r;
+      if (S.keys[e] > gb) gap_store(S, gg, pos++, bitsd(gb), a);
       uint64_t vb = dbits(S.vals[e]);
       r = r > vb ? r : vb;
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) ctl.ngap += total;
-  __syncthreads();
+  g.sync();
+  if (g.tid == 0) ctl.ngap += total;
+  g.sync();
 }
 
-// Alg. 3 over the stashed arcs -> gaps (ascending) in S.gaps / gg; ctl.ngap set.
-// On entry the level-1 bucket statistics (linear keys on [0, 2 pi]) are filled.
-__device__ void build_intervals(const Smem& S, Ctl& ctl, const double2* stash, int NB, int log2NB,
-                                double scale, double2* gg, uint64_t* s_w64, int* s_w32) {
+// Group-wide Alg. 3 over the stashed arcs -> gaps (ascending); the general path,
+// used when more than 32 arcs are live.  On entry the level-1 bucket statistics
+// (linear keys on [0, 2 pi]; count, max beta exact, max alpha high word) are
+// filled and untouched.
+template <int W>
+__device__ void build_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const double2* stash,
+                                int NB, int log2NB, double scale, double2* gg, uint64_t* s_w64,
+                                int* s_w32) {
+  constexpr int T = Grp<W>::kThreads;
   const int n_act = ctl.n_act;
-  bool first = true;
+  bool have_stats = true, have_min = false;
   for (;;) {
-    if (!first) {
-      clear_buckets(S, NB);
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < n_act; idx += blockDim.x) {
+    if (!have_stats) {
+      clear_buckets(g, S, NB);
+      g.sync();
+      for (int idx = g.tid; idx < n_act; idx += T) {
         double2 ab = stash[idx];
         uint64_t bits = dbits(ab.x);
         if (bits < ctl.rlo || bits > ctl.rhi) continue;
-        bucket_add(S, bucket_key(ab.x, ctl, NB, scale), ab.x, ab.y);
+        bucket_add<true>(S, bucket_key(ab.x, ctl, NB, scale), ab.x, ab.y);
       }
-      __syncthreads();
+      g.sync();
+      for (int idx = g.tid; idx < n_act; idx += T) {
+        double2 ab = stash[idx];
+        uint64_t bits = dbits(ab.x);
+        if (bits < ctl.rlo || bits > ctl.rhi) continue;
+        bucket_add_lo<true>(S, bucket_key(ab.x, ctl, NB, scale), ab.x, ab.y);
+      }
+      if (g.tid == 0) ctl.maxa_exact = 1;
+      g.sync();
+      have_min = true;
     }
-    first = false;
-    // scan buckets: Gx = exclusive prefix max of maxB (init G); live counts and offsets
-    const int per = (NB + blockDim.x - 1) / blockDim.x;
-    const int j0 = threadIdx.x * per, j1 = min(NB, j0 + per);
+    have_stats = false;
+    // scan buckets: Gx = exclusive prefix max of max beta (init G), in place; live counts, offsets
+    const int per = (NB + T - 1) / T;
+    const int j0 = g.tid * per, j1 = min(NB, j0 + per);
     uint64_t lmax = 0;
-    for (int j = j0; j < j1; ++j) lmax = lmax > S.maxB[j] ? lmax : S.maxB[j];
+    for (int j = j0; j < j1; ++j) lmax = lmax > S.Gx[j] ? lmax : S.Gx[j];
     uint64_t Gtot;
-    uint64_t run = block_excl_max(lmax, dbits(ctl.G), s_w64, &Gtot);
+    uint64_t run = grp_excl_max(g, lmax, dbits(ctl.G), s_w64, &Gtot);
     int lcount = 0;
     for (int j = j0; j < j1; ++j) {
+      uint64_t mb = S.Gx[j];
       S.Gx[j] = run;
-      run = run > S.maxB[j] ? run : S.maxB[j];
-      if (S.cnt[j] > 0 && S.maxA[j] > S.Gx[j]) lcount += S.cnt[j];
+      run = run > mb ? run : mb;
+      if (bucket_live(S, ctl, j)) lcount += S.cnt[j];
     }
     int total_live;
-    int o = block_excl_sum(lcount, s_w32, &total_live);
+    int o = grp_excl_sum(g, lcount, s_w32, &total_live);
+    if (total_live > kLiveCap && !have_min) continue;  // rare: redo the level with exact min/max alpha
     for (int j = j0; j < j1; ++j) {
       S.off[j] = o;
-      if (S.cnt[j] > 0 && S.maxA[j] > S.Gx[j]) o += S.cnt[j];
+      if (bucket_live(S, ctl, j)) o += S.cnt[j];
     }
-    if (threadIdx.x == 0) {
+    if (g.tid == 0) {
       ctl.total_live = total_live;
       ctl.jo = NB;
     }
-    __syncthreads();
+    g.sync();
     if (total_live > kLiveCap) {
       for (int j = j0; j < j1; ++j) {
-        int lc = (S.cnt[j] > 0 && S.maxA[j] > S.Gx[j]) ? S.cnt[j] : 0;
+        int lc = bucket_live(S, ctl, j) ? S.cnt[j] : 0;
         if (lc > 0 && S.off[j] + lc > kLiveCap) atomicMin(&ctl.jo, j);
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    g.sync();
+    if (g.tid == 0) {
       if (ctl.total_live <= kLiveCap) ctl.action = kAll;
       else if (S.off[ctl.jo] > 0) ctl.action = kPrefix;
       else if (S.minA[ctl.jo] == S.maxA[ctl.jo]) ctl.action = kSame;
       else ctl.action = kNarrow;
     }
-    __syncthreads();
+    g.sync();
     const int action = ctl.action, jo = ctl.jo;
     if (action == kAll || action == kPrefix) {
       int n_live = action == kAll ? total_live : S.off[jo];
-      if (n_live > 0) process_batch(S, ctl, stash, n_act, jo, n_live, NB, scale, gg, s_w64, s_w32);
+      if (n_live > 0) process_batch(g, S, ctl, stash, n_act, jo, n_live, NB, scale, gg, s_w64, s_w32);
     }
-    if (threadIdx.x == 0) {
+    if (g.tid == 0) {
       if (action == kAll) {
         ctl.G = bitsd(Gtot);
         if (ctl.rhi == kTopBits) {
@@ -325,8 +435,7 @@ __device__ void build_intervals(const Smem& S, Ctl& ctl, const double2* stash, i
           gap_store(S, gg, ctl.ngap, G, a);
           ctl.ngap += 1;
         }
-        uint64_t gb = S.Gx[jo] > S.maxB[jo] ? S.Gx[jo] : S.maxB[jo];
-        ctl.G = bitsd(gb);
+        ctl.G = bitsd(jo + 1 < NB ? S.Gx[jo + 1] : Gtot);  // max(G, max beta of bucket jo)
         ctl.rlo = S.maxA[jo] + 1;
         set_bits_mode(ctl, log2NB);
       } else {
@@ -336,19 +445,116 @@ __device__ void build_intervals(const Smem& S, Ctl& ctl, const double2* stash, i
         set_bits_mode(ctl, log2NB);
       }
     }
-    __syncthreads();
+    g.sync();
     if (ctl.action == -1) break;
   }
-  if (threadIdx.x == 0) {
+  if (g.tid == 0) {
     if (ctl.G < kTwoPi) {  // the last segment [gamma_m, 2 pi]
       gap_store(S, gg, ctl.ngap, ctl.G, kTwoPi);
       ctl.ngap += 1;
     }
   }
-  __syncthreads();
+  g.sync();
 }
 
-// Canonical segments (merge touching), trim, L and theta.  Thread 0 only.
+// ---------------------------------------------------------------------------
+// Single-warp Alg. 3 (the common case: at most 32 arcs in live buckets).  Warp 0
+// of the group scans the level-1 buckets (exclusive prefix max of max beta =
+// gamma entering each bucket), gathers the live buckets' arcs through the
+// per-bucket lists, bitonic-sorts them on alpha with shuffles, max-scans beta and
+// emits the gaps [gamma_{k-1}, alpha_k] and [gamma_m, 2 pi].  Returns false
+// (touching nothing) when more than 32 arcs are live: the general path runs.
+// ---------------------------------------------------------------------------
+__device__ bool warp_intervals(const Smem& S, Ctl& ctl, const double2* stash, const int* next,
+                               int NB, double scale, double2* gg) {
+  const int lane = threadIdx.x & 31;
+  const int per = NB / 32;
+  const int j0 = lane * per;
+  const uint64_t G0 = dbits(ctl.G);
+  uint64_t lmax = 0;
+  for (int j = j0; j < j0 + per; ++j) lmax = lmax > S.Gx[j] ? lmax : S.Gx[j];
+  const uint64_t inc = warp_incl_max(lmax);
+  uint64_t exc = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) exc = 0;
+  const uint64_t tot = __shfl_sync(0xffffffffu, inc, 31);
+  const uint64_t Gtot = G0 > tot ? G0 : tot;
+  const uint64_t run0 = G0 > exc ? G0 : exc;
+  int lcnt = 0;
+  {
+    uint64_t run = run0;
+    for (int j = j0; j < j0 + per; ++j) {
+      const uint64_t ma = S.maxA[j] | 0xFFFFFFFFull;  // level 1: high word only (conservative)
+      if (S.cnt[j] > 0 && ma > run) lcnt += S.cnt[j];
+      run = run > S.Gx[j] ? run : S.Gx[j];
+    }
+  }
+  int total = lcnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if (total > 32) return false;
+  // commit gamma entering each bucket; gather the live buckets' arcs
+  int pos = warp_incl_sum(lcnt) - lcnt;
+  {
+    uint64_t run = run0;
+    for (int j = j0; j < j0 + per; ++j) {
+      const uint64_t mb = S.Gx[j];
+      S.Gx[j] = run;
+      const uint64_t ma = S.maxA[j] | 0xFFFFFFFFull;
+      if (S.cnt[j] > 0 && ma > run) {
+        for (int sl = S.head[j]; sl >= 0; sl = next[sl]) {
+          const double2 ab = stash[sl];
+          S.keys[pos] = dbits(ab.x);
+          S.vals[pos] = ab.y;
+          ++pos;
+        }
+      }
+      run = run > mb ? run : mb;
+    }
+  }
+  __syncwarp();
+  uint64_t key = lane < total ? S.keys[lane] : ~0ull;
+  double val = lane < total ? S.vals[lane] : 0.0;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, key, j);
+      const double ov = __shfl_xor_sync(0xffffffffu, val, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      const bool take = lower == up ? ok < key : ok > key;
+      if (take) {
+        key = ok;
+        val = ov;
+      }
+    }
+  }
+  const bool have = lane < total;
+  const uint64_t vb = have ? dbits(val) : 0;
+  const uint64_t vinc = warp_incl_max(vb);
+  uint64_t vexc = __shfl_up_sync(0xffffffffu, vinc, 1);
+  if (lane == 0) vexc = 0;
+  uint64_t gm = 0;
+  if (have) {
+    const uint64_t gb = S.Gx[bucket_key(bitsd(key), ctl, NB, scale)];
+    gm = gb > vexc ? gb : vexc;
+  }
+  const bool gap = have && key > gm;
+  const unsigned mask = __ballot_sync(0xffffffffu, gap);
+  const int ng = ctl.ngap;
+  if (gap) gap_store(S, gg, ng + __popc(mask & ((1u << lane) - 1u)), bitsd(gm), bitsd(key));
+  __syncwarp();
+  if (lane == 0) {
+    int n = ng + __popc(mask);
+    const double G = bitsd(Gtot);
+    if (G < kTwoPi) gap_store(S, gg, n++, G, kTwoPi);  // the last segment [gamma_m, 2 pi]
+    ctl.ngap = n;
+    ctl.G = G;
+  }
+  __syncwarp();
+  return true;
+}
+
+// Canonical segments (merge touching), trim, L and theta.  One thread.
 __device__ void theta_from_gaps(const Smem& S, Ctl& ctl, double2* gg, double u, double eps) {
   int w = 0;
   for (int k = 0; k < ctl.ngap; ++k) {
@@ -409,97 +615,312 @@ __device__ void theta_from_gaps(const Smem& S, Ctl& ctl, double2* gg, double u, 
   }
 }
 
-__device__ Smem carve(unsigned char* base, int NB, int m, bool stash_smem) {
+// Per-group shared memory: bucket arrays, live buffer, gaps (stash after them).
+__device__ __forceinline__ Smem carve(unsigned char* base, int NB) {
   Smem S;
   S.maxA = reinterpret_cast<uint64_t*>(base);
-  S.maxB = S.maxA + NB;
-  S.minA = S.maxB + NB;
-  S.Gx = S.minA + NB;
-  S.keys = S.Gx + NB;
+  S.Gx = S.maxA + NB;
+  S.minA = S.Gx + NB;
+  S.keys = S.minA + NB;
   S.vals = reinterpret_cast<double*>(S.keys + kLiveCap);
   S.gaps = reinterpret_cast<double2*>(S.vals + kLiveCap);
-  S.stash = S.gaps + kGapSmem;
-  S.cnt = reinterpret_cast<int*>(S.stash + (stash_smem ? m : 0));
+  S.cnt = reinterpret_cast<int*>(S.gaps + kGapSmem);
   S.off = S.cnt + NB;
+  S.head = S.off + NB;
   return S;
 }
 
-template <bool kGiven>
-__global__ void __launch_bounds__(kEssThreads) ess_kernel(const EssParams p) {
+// Append (al, be) to the stash, its bucket list and the level-1 bucket statistics;
+// warp-aggregated slot allocation.  Must be reached by all 32 lanes of the warp.
+__device__ __forceinline__ void stash_arc(const Smem& S, Ctl& ctl, double2* stash, int* next,
+                                          bool act, double al, double be, int NB, double scale) {
+  const unsigned mask = __ballot_sync(0xffffffffu, act);
+  if (mask == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&ctl.n_act, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (act) {
+    const int slot = base + __popc(mask & ((1u << lane) - 1u));
+    const int k = bucket_key(al, ctl, NB, scale);
+    stash[slot] = make_double2(al, be);
+    next[slot] = atomicExch(&S.head[k], slot);
+    bucket_add<false>(S, k, al, be);
+  }
+}
+
+#ifndef TMVN_ESS_MIN_BLOCKS
+#define TMVN_ESS_MIN_BLOCKS 3
+#endif
+template <int W, bool kGiven, bool kRing>
+__global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(const EssParams p) {
+  constexpr int kGroups = 8 / W;
+  constexpr int T = Grp<W>::kThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Ctl ctl;
-  __shared__ uint64_t s_w64[kWarps];
-  __shared__ int s_w32[kWarps];
+  __shared__ Ctl ctl_all[kGroups];
+  __shared__ uint64_t s_w64_all[kGroups][W];
+  __shared__ int s_w32_all[kGroups][W];
+  Grp<W> g;
+  g.gid = threadIdx.x / T;
+  g.tid = threadIdx.x % T;
+  g.warp = g.tid >> 5;
+  g.lane = threadIdx.x & 31;
+  Ctl& ctl = ctl_all[g.gid];
+  uint64_t* s_w64 = s_w64_all[g.gid];
+  int* s_w32 = s_w32_all[g.gid];
   const int NB = p.NB;
   const int log2NB = 31 - __clz(NB);
   const int m = p.m;
-  const bool stash_smem = m <= kStashSmemMax;
-  Smem S = carve(smem_raw, NB, m, stash_smem);
-  double2* stash = stash_smem ? S.stash : p.gstash + (int64_t)blockIdx.x * m;
-  double2* gg = p.ggaps + (int64_t)blockIdx.x * (m + 2);
+  const int CH = p.CH;
+  const size_t gbytes = ess_group_smem_bytes(m, NB, p.stash_smem, CH);
+  unsigned char* gbase = smem_raw + (size_t)g.gid * gbytes;
+  double* ring = reinterpret_cast<double*>(gbase);  // slot s: P at ring + 2 s CH, Q after it
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(gbase + (size_t)CH * 32);
+  Smem S = carve(gbase + ess_ring_bytes(CH), NB);
+  const int64_t gglobal = (int64_t)blockIdx.x * kGroups + g.gid;  // group id in the grid
+  double2* stash;
+  int* next;
+  if (p.stash_smem) {
+    stash = reinterpret_cast<double2*>(gbase + ess_ring_bytes(CH) + ess_group_base_bytes(NB));
+    next = reinterpret_cast<int*>(stash + m);
+  } else {
+    stash = p.gstash + gglobal * m;
+    next = p.gnext + gglobal * m;
+  }
+  double2* gg = p.ggaps + gglobal * (m + 2);
   const double scale = __ddiv_rn((double)NB, kTwoPi);
-  const int tid = threadIdx.x;
+  const int64_t ngroups = (int64_t)gridDim.x * kGroups;
+#ifdef TMVN_PHASE_TIMING
+  long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_prev = clock64();
+#endif
 
-  for (int c = blockIdx.x; c < p.C; c += gridDim.x) {
+  // P/Q chunk stream (production path): the group's chains are gglobal + k ngroups;
+  // chain k uses chunk sequence numbers k spc .. k spc + spc - 1 (A pass, then a D1
+  // pass when the row spans several chunks); sequence q lives in ring slot q & 1.
+  // Consuming q issues q + 1, so the next chunk -- the next chain's rows at the end
+  // of a chain -- is in flight while this one is processed.
+  const int mm = (m + 1) & ~1;
+  const int nch = (mm + CH - 1) / CH;
+  const int spc = nch == 1 ? 1 : 2 * nch;
+  const int64_t nmy = gglobal < p.C ? (p.C - gglobal + ngroups - 1) / ngroups : 0;
+  const int64_t total_seq = (kGiven || !kRing) ? 0 : nmy * spc;
+  auto ring_issue = [&](int64_t q) {  // one thread
+    if (q >= total_seq) return;
+    const int64_t k = q / spc;
+    const int j = (int)(q % spc) % nch;
+    const int64_t cq = gglobal + k * ngroups;
+    const int i0 = j * CH;
+    const int n = min(CH, mm - i0);
+    const int s = (int)(q & 1);
+    mbar_expect_tx(&rbar[s], (uint32_t)n * 16u);
+    bulk_g2s(ring + (size_t)s * 2 * CH, p.P_cur + cq * p.ldp + i0, (uint32_t)n * 8u, &rbar[s]);
+    bulk_g2s(ring + (size_t)s * 2 * CH + CH, p.Q + cq * p.ldp + i0, (uint32_t)n * 8u, &rbar[s]);
+  };
+  auto ring_wait = [&](int64_t q) { mbar_wait(&rbar[q & 1], (uint32_t)((q >> 1) & 1)); };
+  int64_t qseq = 0;  // next chunk sequence number to consume
+  if (!kGiven && kRing) {
+    if (g.tid == 0) {
+      mbar_init(&rbar[0], 1);
+      mbar_init(&rbar[1], 1);
+      mbar_fence_init();
+    }
+    g.sync();
+    if (g.tid == 0) ring_issue(0);
+  }
+
+  for (int64_t cc = gglobal; cc < p.C; cc += ngroups) {
+    const int c = (int)cc;
     const uint32_t gchain = p.chain_offset + (uint32_t)c;
-    __syncthreads();
-    if (tid == 0) {
+    g.sync();
+    PHASE(6);  // D2 of the previous chain (x, moments, next nu) + loop overhead
+    if (g.tid == 0) {
       ctl.n_act = 0;
       ctl.ngap = 0;
       ctl.G = 0.0;  // gamma_0 = 0: the first segment is [0, alpha_{i_1}]
       ctl.rlo = 0;
       ctl.rhi = kTopBits;
       ctl.mode = 0;
-      ctl.viol = 0;
-      ctl.slack = -DBL_MAX;
+      ctl.maxa_exact = 0;
     }
-    clear_buckets(S, NB);
-    __syncthreads();
+    clear_buckets(g, S, NB);
+    g.sync();
+    PHASE(0);  // init
 
     // ---------------- A: arcs -> stash + level-1 bucket statistics ----------------
     const double* Prow = p.P_cur + (int64_t)c * p.ldp;
     const double* Qrow = p.Q + (int64_t)c * p.ldp;
-    for (int i = tid; i < m; i += blockDim.x) {
-      double al, be;
-      bool act;
-      if (kGiven) {
-        al = p.g_alpha[(int64_t)c * m + i];
-        be = p.g_beta[(int64_t)c * m + i];
-        act = true;
-      } else {
-        act = arc_of(Prow[i], Qrow[i], p.b[i], al, be);
-        if (p.d_alpha) {
-          p.d_alpha[(int64_t)c * m + i] = act ? al : 0.0;
-          p.d_beta[(int64_t)c * m + i] = act ? be : 0.0;
-          p.d_active[(int64_t)c * m + i] = act ? 1 : 0;
+    if (kGiven) {
+      for (int i0 = 0; i0 < m; i0 += T) {
+        const int i = i0 + g.tid;
+        double al = 0.0, be = 0.0;
+        if (i < m) {
+          al = p.g_alpha[(int64_t)c * m + i];
+          be = p.g_beta[(int64_t)c * m + i];
+        }
+        stash_arc(S, ctl, stash, next, i < m, al, be, NB, scale);
+      }
+    } else {
+      if (kRing) {
+      // constraint pairs (2i, 2i+1) of each chunk: P, Q from the shared-memory ring,
+      // b (shared by all chains, L1/L2-resident) from global; kBatch pairs per thread,
+      // their arcs computed before the stash appends (ILP)
+      const double2* B2 = reinterpret_cast<const double2*>(p.b);
+      for (int j = 0; j < nch; ++j) {
+        ring_wait(qseq);
+        if (g.tid == 0) ring_issue(qseq + 1);
+        const double2* sP2 = reinterpret_cast<const double2*>(ring + (size_t)(qseq & 1) * 2 * CH);
+        const double2* sQ2 = sP2 + CH / 2;
+        const int i0 = j * CH;
+        const int npairs = (min(CH, m - i0) + 1) / 2;
+        for (int base = 0; base < npairs; base += kBatch * T) {
+          double2 pp[kBatch], qq[kBatch], bb[kBatch];
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int pi = base + u * T + g.tid;
+            if (pi < npairs) {
+              pp[u] = sP2[pi];
+              qq[u] = sQ2[pi];
+              bb[u] = __ldg(B2 + i0 / 2 + pi);
+            }
+          }
+          double al[2 * kBatch], be[2 * kBatch];
+          bool act[2 * kBatch];
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int pi = base + u * T + g.tid;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int e = 2 * u + h;
+              al[e] = 0.0;
+              be[e] = 0.0;
+              act[e] = false;
+              if (pi < npairs && i0 + 2 * pi + h < m)
+                act[e] = arc_of(h ? pp[u].y : pp[u].x, h ? qq[u].y : qq[u].x, h ? bb[u].y : bb[u].x,
+                                al[e], be[e]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            if (base + u * T >= npairs) break;  // uniform
+            const int pi = base + u * T + g.tid;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int e = 2 * u + h, i = i0 + 2 * pi + h;
+              if (p.d_alpha && pi < npairs && i < m) {
+                p.d_alpha[(int64_t)c * m + i] = act[e] ? al[e] : 0.0;
+                p.d_beta[(int64_t)c * m + i] = act[e] ? be[e] : 0.0;
+                p.d_active[(int64_t)c * m + i] = act[e] ? 1 : 0;
+              }
+              stash_arc(S, ctl, stash, next, act[e], al[e], be[e], NB, scale);
+            }
+          }
+        }
+        ++qseq;
+        g.sync();  // the slot may be refilled from now on
+      }
+          } else {
+      // constraint pairs (2i, 2i+1): P, Q, b as double2 from global; kBatch pairs per
+      // thread with loads in flight, their arcs computed before the stash appends (ILP)
+      const double2* P2 = reinterpret_cast<const double2*>(Prow);
+      const double2* Q2 = reinterpret_cast<const double2*>(Qrow);
+      const double2* B2 = reinterpret_cast<const double2*>(p.b);
+      const int npairs = (m + 1) / 2;
+      for (int base = 0; base < npairs; base += kBatch * T) {
+        double2 pp[kBatch], qq[kBatch], bb[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int pi = base + u * T + g.tid;
+          if (pi < npairs) {
+            pp[u] = P2[pi];
+            qq[u] = Q2[pi];
+            bb[u] = __ldg(B2 + pi);
+          }
+        }
+        double al[2 * kBatch], be[2 * kBatch];
+        bool act[2 * kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int pi = base + u * T + g.tid;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = 2 * u + h;
+            al[e] = 0.0;
+            be[e] = 0.0;
+            act[e] = false;
+            if (pi < npairs && 2 * pi + h < m)
+              act[e] = arc_of(h ? pp[u].y : pp[u].x, h ? qq[u].y : qq[u].x, h ? bb[u].y : bb[u].x,
+                              al[e], be[e]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          if (base + u * T >= npairs) break;  // uniform
+          const int pi = base + u * T + g.tid;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = 2 * u + h, i = 2 * pi + h;
+            if (p.d_alpha && pi < npairs && i < m) {
+              p.d_alpha[(int64_t)c * m + i] = act[e] ? al[e] : 0.0;
+              p.d_beta[(int64_t)c * m + i] = act[e] ? be[e] : 0.0;
+              p.d_active[(int64_t)c * m + i] = act[e] ? 1 : 0;
+            }
+            stash_arc(S, ctl, stash, next, act[e], al[e], be[e], NB, scale);
+          }
         }
       }
-      if (act) {
-        int slot = atomicAdd(&ctl.n_act, 1);
-        stash[slot] = make_double2(al, be);
-        bucket_add(S, bucket_key(al, ctl, NB, scale), al, be);
+    }
+    }
+    g.sync();
+    PHASE(1);  // A: arcs, stash, level-1 statistics
+    PHASE_ADD(8, ctl.n_act);
+
+    // level-1 max beta per bucket: resolve the low words (see bucket_add)
+    {
+      const int n_act = ctl.n_act;
+      for (int idx = g.tid; idx < n_act; idx += T) {
+        const double2 ab = stash[idx];
+        bucket_add_lo<false>(S, bucket_key(ab.x, ctl, NB, scale), ab.x, ab.y);
+      }
+      g.sync();
+    }
+    PHASE(2);  // low-word pass
+
+    // ---------------- B + C: I_act by Alg. 3, then theta ----------------
+    if (g.warp == 0) {
+      const bool fast = warp_intervals(S, ctl, stash, next, NB, scale, gg);
+      if (g.tid == 0) {
+        ctl.fast = fast ? 1 : 0;
+        if (fast) {
+          const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, p.t, gchain);
+          theta_from_gaps(S, ctl, gg, u, p.eps);
+        }
       }
     }
-    __syncthreads();
-
-    // ---------------- B: I_act by Alg. 3 ----------------
-    build_intervals(S, ctl, stash, NB, log2NB, scale, gg, s_w64, s_w32);
-
-    // ---------------- C: canonical segments, L, theta ----------------
-    if (tid == 0) {
-      double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, p.t, gchain);
-      theta_from_gaps(S, ctl, gg, u, p.eps);
+    g.sync();
+    PHASE(3);  // B (+C) on the single-warp path
+    if (!ctl.fast) {
+      build_intervals(g, S, ctl, stash, NB, log2NB, scale, gg, s_w64, s_w32);
+      if (g.tid == 0) {
+        const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, p.t, gchain);
+        theta_from_gaps(S, ctl, gg, u, p.eps);
+      }
+      g.sync();
+    }
+    PHASE(4);  // B + C on the general path (rare)
+    PHASE_ADD(9, ctl.ngap);
+    if (g.tid == 0) {
       if (p.d_nseg) p.d_nseg[c] = ctl.nseg;
       if (p.d_L) p.d_L[c] = ctl.L;
       if (p.d_theta) p.d_theta[c] = ctl.theta;
     }
-    __syncthreads();
     if (p.d_seg_lo) {
-      int ns = ctl.nseg;
-      for (int k = tid; k < ns && k < p.seg_cap; k += blockDim.x) {
-        double2 g = gap_load(S, gg, k);
-        p.d_seg_lo[(int64_t)c * p.seg_cap + k] = g.x;
-        p.d_seg_hi[(int64_t)c * p.seg_cap + k] = g.y;
+      const int ns = ctl.nseg;
+      for (int k = g.tid; k < ns && k < p.seg_cap; k += T) {
+        double2 gv = gap_load(S, gg, k);
+        p.d_seg_lo[(int64_t)c * p.seg_cap + k] = gv.x;
+        p.d_seg_hi[(int64_t)c * p.seg_cap + k] = gv.y;
       }
     }
     if (kGiven) continue;
@@ -508,128 +929,221 @@ __global__ void __launch_bounds__(kEssThreads) ess_kernel(const EssParams p) {
     const double L = ctl.L;
     double st = 0.0, ct = 1.0;
     if (L > 0.0) sincos(ctl.theta, &st, &ct);
-    double* Pn = p.P_next + (int64_t)c * p.ldp;
+    const int npairs = (m + 1) / 2;
+    const double2* P2 = reinterpret_cast<const double2*>(Prow);
+    const double2* B2 = reinterpret_cast<const double2*>(p.b);
+    double2* Pn2 = reinterpret_cast<double2*>(p.P_next + (int64_t)c * p.ldp);
     int viol = 0;
     double smax = -DBL_MAX;
-    if (L > 0.0) {
-      for (int i = tid; i < m; i += blockDim.x) {
-        double pn = Prow[i] * ct + Qrow[i] * st;
-        double s = pn - p.b[i];
-        viol |= s > 0.0;
-        smax = fmax(smax, s);
-        Pn[i] = pn;
+    // P' = P cos(theta) + Q sin(theta) from the ring: the chunk still resident when the
+    // row is one chunk, else a second pass over the chunks
+    for (int j = 0; kRing && j < nch; ++j) {
+      int64_t qc = qseq - 1;  // single chunk: the one consumed in phase A
+      if (nch > 1) {
+        qc = qseq;
+        ring_wait(qseq);
+        if (g.tid == 0) ring_issue(qseq + 1);
+      }
+      const double2* sP2 = reinterpret_cast<const double2*>(ring + (size_t)(qc & 1) * 2 * CH);
+      const double2* sQ2 = sP2 + CH / 2;
+      const int i0 = j * CH;
+      const int np = (min(CH, m - i0) + 1) / 2;
+      if (L > 0.0) {
+        for (int pi = g.tid; pi < np; pi += T) {
+          const double2 pv = sP2[pi], qv = sQ2[pi], bv = __ldg(B2 + i0 / 2 + pi);
+          double2 pn;
+          pn.x = pv.x * ct + qv.x * st;
+          pn.y = pv.y * ct + qv.y * st;
+          const double s0 = pn.x - bv.x, s1 = pn.y - bv.y;  // b is +inf beyond m
+          viol |= (s0 > 0.0) | (s1 > 0.0);
+          smax = fmax(smax, fmax(s0, s1));
+          Pn2[i0 / 2 + pi] = pn;
+        }
+      }
+      if (nch > 1) {
+        ++qseq;
+        g.sync();
       }
     }
-    const int any_viol = __syncthreads_or(viol);
+    if (!kRing && L > 0.0) {
+      const double2* Q2 = reinterpret_cast<const double2*>(Qrow);
+      for (int pi = g.tid; pi < npairs; pi += T) {
+        const double2 pv = P2[pi], qv = Q2[pi], bv = __ldg(B2 + pi);
+        double2 pn;
+        pn.x = pv.x * ct + qv.x * st;
+        pn.y = pv.y * ct + qv.y * st;
+        const double s0 = pn.x - bv.x, s1 = pn.y - bv.y;  // b is +inf beyond m
+        viol |= (s0 > 0.0) | (s1 > 0.0);
+        smax = fmax(smax, fmax(s0, s1));
+        Pn2[pi] = pn;
+      }
+    }
+    const int any_viol = g.sync_or(viol);
     const bool accept = (L > 0.0) && !any_viol;
+    PHASE(5);  // D1: P' and the safeguard
     if (p.d_slack) {
-      // block max of the slack (dump only)
+      // group max of the slack (dump only)
       uint64_t key = dbits(smax) ^ ((dbits(smax) >> 63) ? ~0ull : 0x8000000000000000ull);
       uint64_t tot;
-      block_excl_max(key, 0, s_w64, &tot);
-      if (tid == 0) {
+      grp_excl_max(g, key, 0, s_w64, &tot);
+      if (g.tid == 0) {
         uint64_t bits = (tot >> 63) ? (tot ^ 0x8000000000000000ull) : ~tot;
         p.d_slack[c] = L > 0.0 ? bitsd(bits) : 0.0;
       }
     }
     if (!accept) {
-      for (int i = tid; i < m; i += blockDim.x) Pn[i] = Prow[i];  // stay at x_t
+      for (int pi = g.tid; pi < npairs; pi += T) Pn2[pi] = P2[pi];  // stay at x_t
     }
-    const int runs = (int)(p.d_pad / 8);
-    for (int a = tid; a < runs; a += blockDim.x) {
-      int64_t o = run_offset(c, a, p.d_pad);
+    // x (and moments, next nu) by coordinate pairs: one double2 of the tiled X / N each
+    const int kpairs = (int)(p.d_pad / 2);
+    for (int pk = g.tid; pk < kpairs; pk += T) {
+      const int64_t o = tiled_offset(c, 2 * pk, p.d_pad);
       double2* xr = reinterpret_cast<double2*>(p.X + o);
       double2* nr = reinterpret_cast<double2*>(p.N + o);
-      double2 xv[4];
-#pragma unroll
-      for (int h = 0; h < 4; ++h) xv[h] = xr[h];
+      double2 xv = *xr;
       if (accept) {
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          double2 nv = nr[h];
-          xv[h].x = xv[h].x * ct + nv.x * st;
-          xv[h].y = xv[h].y * ct + nv.y * st;
-          xr[h] = xv[h];
-        }
+        const double2 nv = *nr;
+        xv.x = xv.x * ct + nv.x * st;
+        xv.y = xv.y * ct + nv.y * st;
+        *xr = xv;
       }
       if (p.record) {
         double2* s1 = reinterpret_cast<double2*>(p.S1 + o);
         double2* s2 = reinterpret_cast<double2*>(p.S2 + o);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          double2 a1 = s1[h], a2 = s2[h];
-          a1.x += xv[h].x;
-          a1.y += xv[h].y;
-          a2.x += xv[h].x * xv[h].x;
-          a2.y += xv[h].y * xv[h].y;
-          s1[h] = a1;
-          s2[h] = a2;
-        }
+        double2 a1 = *s1, a2 = *s2;
+        a1.x += xv.x;
+        a1.y += xv.y;
+        a2.x += xv.x * xv.x;
+        a2.y += xv.y * xv.y;
+        *s1 = a1;
+        *s2 = a2;
       }
-      if (p.gen_next) {
-        double nn[8];
-        normal_run(p.seed, p.t + 1, gchain, a, p.d, nn);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) nr[h] = make_double2(nn[2 * h], nn[2 * h + 1]);
-      }
+      if (p.gen_next) *nr = normal_pair_at(p.seed, p.t + 1, gchain, 2 * pk, p.d);
     }
-    if (tid == 0) {
+    if (g.tid == 0) {
       if (!accept) p.rej[c] += 1;
       if (p.d_accept) p.d_accept[c] = accept ? 1 : 0;
     }
   }
+#ifdef TMVN_PHASE_TIMING
+  g.sync();
+  PHASE(6);
+  if (g.tid == 0)
+    for (int i = 0; i < 10; ++i) atomicAdd(&g_phase_cycles[i], (unsigned long long)ph[i]);
+#endif
+}
+
+template <int W, bool kGiven>
+cudaError_t launch_w(const EssParams& p, int grid, size_t smem, cudaStream_t st) {
+  if (!kGiven && p.CH > 0) {
+    cudaError_t e = cudaFuncSetAttribute(ess_kernel<W, kGiven, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    ess_kernel<W, kGiven, true><<<grid, kEssThreads, smem, st>>>(p);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(ess_kernel<W, kGiven, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    ess_kernel<W, kGiven, false><<<grid, kEssThreads, smem, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+template <bool kGiven>
+cudaError_t launch_any(const EssParams& p, int grid, cudaStream_t st) {
+  if (grid < 1) return cudaSuccess;
+  const size_t smem = (size_t)(8 / p.W) * ess_group_smem_bytes(p.m, p.NB, p.stash_smem, p.CH);
+  switch (p.W) {
+    case 1: return launch_w<1, kGiven>(p, grid, smem, st);
+    case 2: return launch_w<2, kGiven>(p, grid, smem, st);
+    case 4: return launch_w<4, kGiven>(p, grid, smem, st);
+    case 8: return launch_w<8, kGiven>(p, grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int W>
+int occupancy_w(size_t smem, bool ring) {
+  int per_sm = 0;
+  if (ring) {
+    cudaFuncSetAttribute(ess_kernel<W, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ess_kernel<W, false, true>, kEssThreads, smem);
+  } else {
+    cudaFuncSetAttribute(ess_kernel<W, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ess_kernel<W, false, false>, kEssThreads, smem);
+  }
+  return per_sm;
 }
 
 }  // namespace
 
-int ess_buckets(int m) {
-  int nb = 64;
-  while (nb < m / 4 && nb < 1024) nb <<= 1;
-  return nb;
+#ifdef TMVN_PHASE_TIMING
+void phase_cycles(unsigned long long* out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 10);
+  if (reset) {
+    unsigned long long z[10] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
 }
-
-size_t ess_smem_bytes(int m, int NB) {
-  size_t s = (size_t)NB * 4 * sizeof(uint64_t) + (size_t)kLiveCap * 16 + (size_t)kGapSmem * 16;
-  if (m <= kStashSmemMax) s += (size_t)m * 16;
-  s += (size_t)NB * 2 * sizeof(int);
-  return s;
-}
+#endif
 
 static int g_sms = 0;
 
-int ess_grid(int C, int m, int NB) {
+EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
   if (g_sms == 0) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  size_t smem = ess_smem_bytes(m, NB);
+  EssLaunch L;
+  // warps per chain: as few as still give every SM several chains in flight;
+  // more warps per chain when chains are few or constraints many
+  int W = W_req;
+  if (W != 1 && W != 2 && W != 4 && W != 8) {
+    W = 8;
+    while (W > 1 && (int64_t)C * W >= (int64_t)g_sms * 8 * 2 * 4) W >>= 1;
+    if (m >= 32768 && W < 4) W = 4;
+  }
+  // buckets: about 4 arcs per bucket, at most 256 for small groups
+  int NB = 64;
+  while (NB < m / 4 && NB < 1024) NB <<= 1;
+  if (W <= 2 && NB > 256) NB = 256;
+  const int groups = 8 / W;
+  // P/Q chunk: 256 W constraints (64 KB ring for a full CTA), never beyond the row;
+  // CH = 0: no ring, P and Q are read from global memory
+  const int mm = (m + 1) & ~1;
+  int CH = 256 * W;
+  if (CH > mm) CH = mm;
+  if (ring_req == 0) CH = 0;
+  // stash in shared memory when 2 CTAs per SM still fit
+  int stash_smem = 0;
+  if ((size_t)groups * ess_group_smem_bytes(m, NB, 1, CH) <= 112 * 1024) stash_smem = 1;
+  const size_t smem = (size_t)groups * ess_group_smem_bytes(m, NB, stash_smem, CH);
   int per_sm = 0;
-  cudaFuncSetAttribute(ess_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ess_kernel<false>, kEssThreads, smem);
+  switch (W) {
+    case 1: per_sm = occupancy_w<1>(smem, CH > 0); break;
+    case 2: per_sm = occupancy_w<2>(smem, CH > 0); break;
+    case 4: per_sm = occupancy_w<4>(smem, CH > 0); break;
+    default: per_sm = occupancy_w<8>(smem, CH > 0); break;
+  }
   if (per_sm < 1) per_sm = 1;
-  int g = g_sms * per_sm;
-  return C < g ? C : g;
+  int64_t grid = (int64_t)g_sms * per_sm;
+  const int64_t need = ((int64_t)C + groups - 1) / groups;
+  L.W = W;
+  L.NB = NB;
+  L.CH = CH;
+  L.stash_smem = stash_smem;
+  L.grid = (int)(grid < need ? grid : need);
+  L.groups = (int64_t)L.grid * groups;
+  return L;
 }
 
 cudaError_t launch_ess_step(const EssParams& p, int grid, cudaStream_t st) {
-  size_t smem = ess_smem_bytes(p.m, p.NB);
-  cudaError_t e = cudaFuncSetAttribute(ess_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  if (grid < 1) return cudaSuccess;
-  ess_kernel<false><<<grid, kEssThreads, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_any<false>(p, grid, st);
 }
 
 cudaError_t launch_ess_intervals(const EssParams& p, int grid, cudaStream_t st) {
-  size_t smem = ess_smem_bytes(p.m, p.NB);
-  cudaError_t e = cudaFuncSetAttribute(ess_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  if (grid < 1) return cudaSuccess;
-  ess_kernel<true><<<grid, kEssThreads, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_any<true>(p, grid, st);
 }
 
 }  // namespace tmvn

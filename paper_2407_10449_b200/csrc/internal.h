@@ -40,9 +40,13 @@ struct EssParams {
   const double* g_beta;
   const double* g_u;
   // scratch (per CTA)
-  double2* gstash;  // gridDim.x * m   (arcs when m > kStashSmemMax)
-  double2* ggaps;   // gridDim.x * (m + 2)
+  double2* gstash;  // groups * m   (arcs when not in shared memory)
+  int* gnext;       // groups * m   (their bucket lists)
+  double2* ggaps;   // groups * (m + 2)
   int NB;           // buckets per level (power of two)
+  int W;            // warps per chain (1, 2, 4, 8)
+  int stash_smem;   // 1: arcs stashed in shared memory
+  int CH;           // constraints per P/Q chunk streamed into shared memory (even)
   // dumps (nullable)
   double* d_alpha;
   double* d_beta;
@@ -57,16 +61,35 @@ struct EssParams {
   int32_t* d_accept;
 };
 
-constexpr int kEssThreads = 256;
-constexpr int kLiveCap = 512;       // arcs sorted per batch in shared memory
-constexpr int kGapSmem = 256;       // gaps kept in shared memory (rest in ggaps)
-constexpr int kStashSmemMax = 4096; // arcs kept in shared memory when m <= this
+constexpr int kEssThreads = 256;   // 8 warps per CTA = 8 / W chain groups
+constexpr int kLiveCap = 256;      // arcs sorted per batch in shared memory (general path)
+constexpr int kGapSmem = 128;      // gaps kept in shared memory (rest in ggaps)
 
-int ess_buckets(int m);
-size_t ess_smem_bytes(int m, int NB);
-int ess_grid(int C, int m, int NB);  // persistent grid size
+// Shared memory of one chain group: [P/Q chunk ring: 2 slots x (P, Q) x CH
+// doubles][2 mbarriers][buckets, live buffer, gaps][stash if stash_smem].
+__host__ __device__ inline size_t ess_ring_bytes(int CH) { return CH > 0 ? (size_t)CH * 32 + 16 : 0; }
+__host__ __device__ inline size_t ess_group_base_bytes(int NB) {
+  size_t s = (size_t)NB * 3 * 8 + (size_t)kLiveCap * 16 + (size_t)kGapSmem * 16 + (size_t)NB * 3 * 4;
+  return (s + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_smem, int CH) {
+  size_t s = ess_ring_bytes(CH) + ess_group_base_bytes(NB);
+  if (stash_smem) s += (size_t)m * (16 + 4);
+  return (s + 15) / 16 * 16;
+}
+
+struct EssLaunch {
+  int W, NB, stash_smem, grid, CH;
+  int64_t groups;  // chain groups in the grid (scratch slots)
+};
+// launch configuration for C chains of m constraints (W_req 0 = automatic;
+// ring_req: 1 = stream P/Q through shared memory, 0 = read them from global)
+EssLaunch ess_plan(int C, int m, int W_req, int ring_req);
 cudaError_t launch_ess_step(const EssParams& p, int grid, cudaStream_t st);
 cudaError_t launch_ess_intervals(const EssParams& p, int grid, cudaStream_t st);
+#ifdef TMVN_PHASE_TIMING
+void phase_cycles(unsigned long long* out10, bool reset);
+#endif
 
 // ---- auxiliary kernels (aux_kernels.cu) -------------------------------------
 // row-major [R x K] (leading dim ld) -> tiled [R_pad x K_pad]; padding is left untouched.
@@ -80,9 +103,10 @@ cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed
 // first (c, i) with P[c, i] - b[i] >= 0 (strict start, C18); *flag = c * m + i or -1.
 cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, int C, int m,
                                unsigned long long* flag, cudaStream_t st);
-// sum over chains of a tiled C x d array -> out[d] (fixed order: deterministic)
+// sum over chains of a tiled C x d array -> out[d] (fixed order: deterministic);
+// part: scratch of ceil(C / 64) * d doubles
 cudaError_t launch_chain_sum(const double* S, int C, int d, int64_t d_pad, double* out,
-                             cudaStream_t st);
+                             double* part, cudaStream_t st);
 // x-space moments with affine: X row-major (C_pad x ldx) = U L^T; S1 += X + mu, S2 += (X + mu)^2
 cudaError_t launch_accum_affine(const double* Xrow, int64_t ldx, const double* mu, int C, int d,
                                 double* S1row, double* S2row, cudaStream_t st);

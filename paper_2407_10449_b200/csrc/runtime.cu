@@ -54,7 +54,14 @@ struct tmvn_ctx {
   double* msum = nullptr;  // d (device) moment reduction target
   unsigned long long* dflag = nullptr;
   double2 *gstash = nullptr, *ggaps = nullptr;
-  int grid = 0, NB = 64;
+  int* gnext = nullptr;
+  int64_t scratch_groups = 0;  // chain groups the scratch is sized for
+  bool scratch_stash = false;  // gstash / gnext allocated
+  EssLaunch plan{};
+  int nshards = 1;                      // concurrent chain shards (streams)
+  std::vector<cudaStream_t> shard_streams;
+  cudaEvent_t fork_event = nullptr;
+  std::vector<cudaEvent_t> join_events;
   // state
   tmvn_options opt{};
   tmvn_stats stats{};
@@ -122,7 +129,7 @@ void free_chain_buffers(tmvn_ctx* h) {
   dfree(h->X); dfree(h->N); dfree(h->P0); dfree(h->P1); dfree(h->Q);
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
   dfree(h->stage); dfree(h->stage2); dfree(h->rej);
-  dfree(h->gstash); dfree(h->ggaps);
+  dfree(h->gstash); dfree(h->ggaps); dfree(h->gnext);
   h->C_cap = h->C_pad = 0;
 }
 
@@ -142,13 +149,44 @@ tmvn_status ensure_chains(tmvn_ctx* h, int64_t C) {
   CK(h, dalloc(&h->stage, wide));
   CK(h, dalloc(&h->stage2, wide));
   CK(h, dalloc(&h->rej, (size_t)C_pad));
-  h->NB = ess_buckets((int)h->m);
-  h->grid = ess_grid((int)C, (int)h->m, h->NB);
-  const int gmax = ess_grid((int)C_pad, (int)h->m, h->NB);
-  if (h->m > kStashSmemMax) CK(h, dalloc(&h->gstash, (size_t)gmax * h->m));
-  CK(h, dalloc(&h->ggaps, (size_t)gmax * (h->m + 2)));
+  h->scratch_groups = 0;
+  h->scratch_stash = false;
   h->C_cap = C;
   h->C_pad = C_pad;
+  return TMVN_OK;
+}
+
+// Shards, launch plan of the fused kernel (per shard) and its per-group scratch.
+tmvn_status plan_ess(tmvn_ctx* h, int64_t C) {
+  int S = h->opt.streams;
+  if (S <= 0) S = C >= 1024 ? 2 : 1;  // auto
+  if (h->trace_dev) S = 1;
+  const int64_t per = round_up((C + S - 1) / S, kTileR);
+  S = (int)((C + per - 1) / per);
+  h->nshards = S;
+  while ((int)h->shard_streams.size() < S) {
+    cudaStream_t s_;
+    CK(h, cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    h->shard_streams.push_back(s_);
+    cudaEvent_t e;
+    CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->join_events.push_back(e);
+  }
+  if (!h->fork_event) CK(h, cudaEventCreateWithFlags(&h->fork_event, cudaEventDisableTiming));
+  h->plan = ess_plan((int)std::min(per, C), (int)h->m, h->opt.chain_warps, h->opt.ring);
+  const bool need_stash = !h->plan.stash_smem;
+  const int64_t G = h->plan.groups * S;
+  if (G > h->scratch_groups || (need_stash && !h->scratch_stash)) {
+    dfree(h->gstash); dfree(h->gnext); dfree(h->ggaps);
+    const int64_t Gn = std::max(G, h->scratch_groups);
+    if (need_stash || h->scratch_stash) {
+      CK(h, dalloc(&h->gstash, (size_t)Gn * h->m));
+      CK(h, dalloc(&h->gnext, (size_t)Gn * h->m));
+      h->scratch_stash = true;
+    }
+    CK(h, dalloc(&h->ggaps, (size_t)Gn * (h->m + 2)));
+    h->scratch_groups = Gn;
+  }
   return TMVN_OK;
 }
 
@@ -182,8 +220,12 @@ EssParams base_params(tmvn_ctx* h, int C) {
   p.S2 = h->S2;
   p.rej = h->rej;
   p.gstash = h->gstash;
+  p.gnext = h->gnext;
   p.ggaps = h->ggaps;
-  p.NB = h->NB;
+  p.NB = h->plan.NB;
+  p.W = h->plan.W;
+  p.CH = h->plan.CH;
+  p.stash_smem = h->plan.stash_smem;
   return p;
 }
 
@@ -244,82 +286,131 @@ bool recorded_iter(const tmvn_options& o, int64_t t) {
 }
 
 // The hot loop.  On entry X holds x_{t0} (tiled) and P_cur = X A'^T.
+// The chains are split into `shards` row blocks (multiples of 128 chains), each an
+// independent GEMM -> ESS sequence on its own stream: the DMMA GEMM of one shard
+// co-runs with the FP64/ALU-bound ESS kernel of another.  Per-chain results do not
+// depend on the split (no split-K; global chain index in the RNG counters).
 tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, double* P_cur,
                      int64_t* n_recorded) {
   cudaStream_t st = stream_of(h);
   const int64_t t0 = h->opt.iter_offset;
   const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
   double* P_next = (P_cur == h->P0) ? h->P1 : h->P0;
-  EssParams p = base_params(h, (int)C);
   KL(h, launch_normals(h->N, (int)C, (int)h->d, h->d_pad, seed, (uint32_t)t0,
                        (uint32_t)h->opt.chain_offset, st));
+  // ---- shards
+  int S = h->nshards;
+  const int64_t per = round_up((C + S - 1) / S, kTileR);
+  S = (int)((C + per - 1) / per);
+  struct Shard {
+    int64_t c0, C;
+    cudaStream_t st;
+    EssParams p;
+    double *Pc, *Pn;
+  };
+  std::vector<Shard> sh(S);
+  for (int s = 0; s < S; ++s) {
+    Shard& x = sh[s];
+    x.c0 = s * per;
+    x.C = std::min(per, C - x.c0);
+    x.st = S == 1 ? st : h->shard_streams[s];
+    x.p = base_params(h, (int)x.C);
+    x.p.X = h->X + x.c0 * h->d_pad;
+    x.p.N = h->N + x.c0 * h->d_pad;
+    x.p.S1 = h->S1 + x.c0 * h->d_pad;
+    x.p.S2 = h->S2 + x.c0 * h->d_pad;
+    x.p.rej = h->rej + x.c0;
+    x.p.chain_offset = (uint32_t)(h->opt.chain_offset + x.c0);
+    x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * h->m : nullptr;
+    x.p.gnext = h->gnext ? h->gnext + (size_t)s * h->plan.groups * h->m : nullptr;
+    x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
+    x.Pc = P_cur + x.c0 * h->m_pad;
+    x.Pn = P_next + x.c0 * h->m_pad;
+  }
+  if (S > 1) {  // fork
+    CK(h, cudaEventRecord(h->fork_event, st));
+    for (int s = 0; s < S; ++s) CK(h, cudaStreamWaitEvent(sh[s].st, h->fork_event, 0));
+  }
   int64_t nrec = 0;
   // profiling: event pairs around the hot-loop GEMMs (kind 0) and ESS launches (kind 1)
   const bool prof = h->opt.profile != 0;
   std::vector<int> kinds;
-  auto ev_mark = [&](size_t idx) -> cudaError_t {
+  std::vector<int64_t> kind_C;
+  auto ev_mark = [&](size_t idx, cudaStream_t s_) -> cudaError_t {
     while (h->events.size() <= idx) {
       cudaEvent_t e;
       cudaError_t r = cudaEventCreate(&e);
       if (r != cudaSuccess) return r;
       h->events.push_back(e);
     }
-    return cudaEventRecord(h->events[idx], st);
+    return cudaEventRecord(h->events[idx], s_);
   };
-#define TIMED(kind, expr)                                   \
+#define TIMED(kind, nC, s_, expr)                           \
   do {                                                      \
-    if (prof) CK(h, ev_mark(2 * kinds.size()));             \
+    if (prof) CK(h, ev_mark(2 * kinds.size(), s_));         \
     KL(h, expr);                                            \
     if (prof) {                                             \
-      CK(h, ev_mark(2 * kinds.size() + 1));                 \
+      CK(h, ev_mark(2 * kinds.size() + 1, s_));             \
       kinds.push_back(kind);                                \
+      kind_C.push_back(nC);                                 \
     }                                                       \
   } while (0)
   for (int64_t it = 0; it < n_iter; ++it) {
     const int64_t t = t0 + it;
-    TIMED(0, launch_gemm_tn(h->N, h->C_pad, h->At, h->m_pad, h->d_pad, h->Q, h->m_pad, st));
     const bool rec = recorded_iter(h->opt, t);
-    p.P_cur = P_cur;
-    p.P_next = P_next;
-    p.Q = h->Q;
-    p.seed = seed;
-    p.t = (uint32_t)t;
-    p.gen_next = (it + 1 < n_iter) ? 1 : 0;
-    p.record = (rec && !h->affine) ? 1 : 0;
-    TIMED(1, launch_ess_step(p, h->grid, st));
-    std::swap(P_cur, P_next);
-    if (rec) {
-      ++nrec;
-      if (h->affine) {
-        KL(h, launch_gemm_tn(h->X, h->C_pad, h->L_tiled, h->d_r128, h->d_pad, h->stage, h->d_r128, st));
-        KL(h, launch_accum_affine(h->stage, h->d_r128, h->mu, (int)C, (int)h->d, h->S1x, h->S2x, st));
+    for (int s = 0; s < S; ++s) {
+      Shard& x = sh[s];
+      const int64_t Rp = round_up(x.C, kTileR);
+      TIMED(0, x.C, x.st, launch_gemm_tn(x.p.N, Rp, h->At, h->m_pad, h->d_pad, h->Q + x.c0 * h->m_pad,
+                                         h->m_pad, x.st));
+      x.p.P_cur = x.Pc;
+      x.p.P_next = x.Pn;
+      x.p.Q = h->Q + x.c0 * h->m_pad;
+      x.p.seed = seed;
+      x.p.t = (uint32_t)t;
+      x.p.gen_next = (it + 1 < n_iter) ? 1 : 0;
+      x.p.record = (rec && !h->affine) ? 1 : 0;
+      TIMED(1, x.C, x.st, launch_ess_step(x.p, h->plan.grid, x.st));
+      std::swap(x.Pc, x.Pn);
+      if (rec && h->affine) {
+        double* stg = h->stage + x.c0 * h->d_r128;
+        KL(h, launch_gemm_tn(x.p.X, Rp, h->L_tiled, h->d_r128, h->d_pad, stg, h->d_r128, x.st));
+        KL(h, launch_accum_affine(stg, h->d_r128, h->mu, (int)x.C, (int)h->d, h->S1x + x.c0 * h->d,
+                                  h->S2x + x.c0 * h->d, x.st));
       }
+      if ((t + 1) % K == 0 && it + 1 < n_iter)
+        TIMED(0, x.C, x.st, launch_gemm_tn(x.p.X, Rp, h->At, h->m_pad, h->d_pad, x.Pc, h->m_pad, x.st));
     }
-    if ((t + 1) % K == 0 && it + 1 < n_iter)
-      TIMED(0, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, P_cur, h->m_pad, st));
-    if (h->trace_dev)
+    if (rec) ++nrec;
+    if (h->trace_dev) {  // S == 1 when tracing
       KL(h, launch_gather_rows_tiled(h->X, h->d_pad, (int)h->d, h->trace_rows, h->trace_n,
                                      h->trace_dev + (size_t)(it + 1) * h->trace_n * h->d, st));
+    }
   }
 #undef TIMED
+  if (S > 1) {  // join
+    for (int s = 0; s < S; ++s) {
+      CK(h, cudaEventRecord(h->join_events[s], sh[s].st));
+      CK(h, cudaStreamWaitEvent(st, h->join_events[s], 0));
+    }
+  }
   *n_recorded = nrec;
   if (prof && !kinds.empty()) {
-    CK(h, cudaEventSynchronize(h->events[2 * kinds.size() - 1]));
-    const double flops = 2.0 * (double)C * (double)h->m * (double)h->d;
-    // P, Q read + P' write (24 B per constraint-eval); X r/w, nu read + next nu write (32 B per
-    // chain-coordinate); moments (32 B per chain-coordinate) on recorded iterations
-    const double ess_bytes = 24.0 * (double)C * (double)h->m + 32.0 * (double)C * (double)h->d;
+    CK(h, cudaStreamSynchronize(st));
     for (size_t k = 0; k < kinds.size(); ++k) {
       float ms = 0.f;
       CK(h, cudaEventElapsedTime(&ms, h->events[2 * k], h->events[2 * k + 1]));
+      const double nC = (double)kind_C[k];
       if (kinds[k] == 0) {
         h->prof.gemm_launches += 1;
         h->prof.gemm_ms += ms;
-        h->prof.gemm_flops += flops;
+        h->prof.gemm_flops += 2.0 * nC * (double)h->m * (double)h->d;
       } else {
+        // P, Q read + P' write (24 B per constraint-eval); X r/w, nu read + next nu write
+        // (32 B per chain-coordinate)
         h->prof.ess_launches += 1;
         h->prof.ess_ms += ms;
-        h->prof.ess_bytes += ess_bytes;
+        h->prof.ess_bytes += 24.0 * nC * (double)h->m + 32.0 * nC * (double)h->d;
       }
     }
   }
@@ -338,17 +429,21 @@ tmvn_status finish_stats(tmvn_ctx* h, int64_t C, int64_t n_iter, int64_t nrec) {
     if (h->affine) {
       // row-major C x d accumulators: reuse the tiled reducer through a pack
       KL(h, launch_pack(h->S1x, C, d, d, h->stage2, h->d_pad, st));
-      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, st));
+      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
+      h->prof.launches += 1;  // two kernels
       CK(h, cudaMemcpyAsync(s.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(h, cudaStreamSynchronize(st));
       KL(h, launch_pack(h->S2x, C, d, d, h->stage2, h->d_pad, st));
-      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, st));
+      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
+      h->prof.launches += 1;  // two kernels
       CK(h, cudaMemcpyAsync(q.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
     } else {
-      KL(h, launch_chain_sum(h->S1, (int)C, (int)d, h->d_pad, h->msum, st));
+      KL(h, launch_chain_sum(h->S1, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
+      h->prof.launches += 1;  // two kernels
       CK(h, cudaMemcpyAsync(s.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(h, cudaStreamSynchronize(st));
-      KL(h, launch_chain_sum(h->S2, (int)C, (int)d, h->d_pad, h->msum, st));
+      KL(h, launch_chain_sum(h->S2, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
+      h->prof.launches += 1;  // two kernels
       CK(h, cudaMemcpyAsync(q.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
     }
   }
@@ -418,6 +513,9 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->auto_advance = 1;
   o->stream = nullptr;
   o->profile = 0;
+  o->chain_warps = 0;
+  o->streams = 0;
+  o->ring = 0;
   return TMVN_OK;
 }
 
@@ -459,16 +557,19 @@ tmvn_status tmvn_create(const double* A, const double* b, int64_t m, int64_t d, 
   };
   cudaError_t e;
   if ((e = dalloc(&h->A_row, (size_t)m * d)) != cudaSuccess) return bad(e, "alloc A");
-  if ((e = dalloc(&h->b_orig, (size_t)m)) != cudaSuccess) return bad(e, "alloc b");
-  if ((e = dalloc(&h->b_eff, (size_t)m)) != cudaSuccess) return bad(e, "alloc b'");
+  if ((e = dalloc(&h->b_orig, (size_t)h->m_pad)) != cudaSuccess) return bad(e, "alloc b");
+  if ((e = dalloc(&h->b_eff, (size_t)h->m_pad)) != cudaSuccess) return bad(e, "alloc b'");
   if ((e = dalloc(&h->A_tiled, (size_t)h->m_pad * h->d_pad)) != cudaSuccess) return bad(e, "alloc At");
   h->At = h->A_tiled;
   if ((e = dalloc(&h->dflag, 1)) != cudaSuccess) return bad(e, "alloc flag");
   if ((e = dalloc(&h->dsum, 1)) != cudaSuccess) return bad(e, "alloc sum");
   if ((e = dalloc(&h->msum, (size_t)d)) != cudaSuccess) return bad(e, "alloc msum");
   cudaMemcpy(h->A_row, hA.data(), hA.size() * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(h->b_orig, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(h->b_eff, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice);
+  // b padded to m_pad with +inf: padded constraints (zero rows of A) are never active
+  std::vector<double> hb_pad(hb);
+  hb_pad.resize((size_t)h->m_pad, HUGE_VAL);
+  cudaMemcpy(h->b_orig, hb_pad.data(), hb_pad.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(h->b_eff, hb_pad.data(), hb_pad.size() * sizeof(double), cudaMemcpyHostToDevice);
   if ((e = launch_pack(h->A_row, m, d, d, h->A_tiled, h->d_pad, 0)) != cudaSuccess) return bad(e, "pack A");
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bad(e, "create");
   *out = h;
@@ -530,6 +631,9 @@ tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* o) {
   if (!(o->trim_eps >= 0.0) || !(o->trim_eps < 3.14159)) return fail(h, TMVN_E_ARG, "need 0 <= trim_eps < pi");
   if (o->recompute_every < 1 || o->thin < 1 || o->burn_in < 0) return fail(h, TMVN_E_ARG, "bad recompute_every / thin / burn_in");
   if (o->chain_offset < 0 || o->iter_offset < 0) return fail(h, TMVN_E_ARG, "offsets must be >= 0");
+  if (o->chain_warps != 0 && o->chain_warps != 1 && o->chain_warps != 2 && o->chain_warps != 4 &&
+      o->chain_warps != 8)
+    return fail(h, TMVN_E_ARG, "chain_warps must be 0, 1, 2, 4 or 8");
   h->opt = *o;
   return TMVN_OK;
 }
@@ -546,7 +650,7 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if (s != TMVN_OK) return s;
   if ((s = set_device(h)) != TMVN_OK) return s;
   if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
-  h->grid = ess_grid((int)C, (int)h->m, h->NB);
+  if ((s = plan_ess(h, C)) != TMVN_OK) return s;
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
   if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;
   if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
@@ -592,6 +696,9 @@ void tmvn_destroy(tmvn_handle h) {
   if (!h) return;
   cudaSetDevice(h->device);
   for (cudaEvent_t e : h->events) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->join_events) cudaEventDestroy(e);
+  for (cudaStream_t s_ : h->shard_streams) cudaStreamDestroy(s_);
+  if (h->fork_event) cudaEventDestroy(h->fork_event);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
   dfree(h->A_tiled); dfree(h->A_row); dfree(h->b_orig); dfree(h->b_eff);
@@ -677,6 +784,8 @@ tmvn_status tmvn_test_arcs(const double* p, const double* q, const double* b, in
   return TMVN_OK;
 }
 
+static int g_test_chain_warps = 0;
+
 tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t m, int64_t C,
                                 const double* u, double eps, double* seg_lo, double* seg_hi,
                                 int64_t seg_cap, int64_t* nseg, double* L, double* theta) {
@@ -685,15 +794,19 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   Tmp<double> da, db, du, dlo, dhi, dL, dth;
   Tmp<int64_t> dns;
   Tmp<double2> gstash, ggaps;
+  Tmp<int> gnext;
   TCK(tmp_in(da, alpha, cm)); TCK(tmp_in(db, beta, cm));
   TCK(tmp_in(du, u, u ? (size_t)C : 0));
   TCK(tmp_in(dlo, (const double*)nullptr, (size_t)C * seg_cap)); TCK(tmp_in(dhi, (const double*)nullptr, (size_t)C * seg_cap));
   TCK(tmp_in(dL, (const double*)nullptr, (size_t)C)); TCK(tmp_in(dth, (const double*)nullptr, (size_t)C));
   TCK(tmp_in(dns, (const int64_t*)nullptr, (size_t)C));
-  const int NB = ess_buckets((int)m);
-  const int grid = ess_grid((int)C, (int)m, NB);
-  if (m > kStashSmemMax) TCK(tmp_in(gstash, (const double2*)nullptr, (size_t)grid * m));
-  TCK(tmp_in(ggaps, (const double2*)nullptr, (size_t)grid * (m + 2)));
+  const EssLaunch plan = ess_plan((int)C, (int)m, g_test_chain_warps, 0);
+  const int grid = plan.grid;
+  if (!plan.stash_smem) {
+    TCK(tmp_in(gstash, (const double2*)nullptr, (size_t)plan.groups * m));
+    TCK(tmp_in(gnext, (const int*)nullptr, (size_t)plan.groups * m));
+  }
+  TCK(tmp_in(ggaps, (const double2*)nullptr, (size_t)plan.groups * (m + 2)));
   EssParams p;
   std::memset(&p, 0, sizeof(p));
   p.m = (int)m;
@@ -703,8 +816,12 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   p.g_beta = db.p;
   p.g_u = u ? du.p : nullptr;
   p.gstash = gstash.p;
+  p.gnext = gnext.p;
   p.ggaps = ggaps.p;
-  p.NB = NB;
+  p.NB = plan.NB;
+  p.W = plan.W;
+  p.CH = plan.CH;
+  p.stash_smem = plan.stash_smem;
   p.d_seg_lo = seg_cap ? dlo.p : nullptr;
   p.d_seg_hi = dhi.p;
   p.seg_cap = seg_cap;
@@ -739,9 +856,10 @@ tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t 
   tmvn_status s;
   if ((s = set_device(h)) != TMVN_OK) return s;
   if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
+  if ((s = plan_ess(h, C)) != TMVN_OK) return s;
   cudaStream_t st = stream_of(h);
   const int64_t m = h->m, d = h->d;
-  const int grid = ess_grid((int)C, (int)m, h->NB);
+  const int grid = h->plan.grid;
   // X_t is given in u-space
   CK(h, cudaMemcpyAsync(h->stage, Xt, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
   CK(h, launch_pack(h->stage, C, d, d, h->X, h->d_pad, st));
@@ -821,7 +939,10 @@ tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t 
   if (s != TMVN_OK) return s;
   if ((s = set_device(h)) != TMVN_OK) return s;
   if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
-  h->grid = ess_grid((int)C, (int)h->m, h->NB);
+  h->trace_dev = reinterpret_cast<double*>(1);  // plan a single shard
+  s = plan_ess(h, C);
+  h->trace_dev = nullptr;
+  if (s != TMVN_OK) return s;
   Tmp<int64_t> rows;
   Tmp<double> tr;
   CK(h, tmp_in(rows, chains, (size_t)n_trace));
@@ -844,5 +965,13 @@ tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t 
   if (h->opt.auto_advance) h->opt.iter_offset += n_iter;
   return TMVN_OK;
 }
+
+#ifdef TMVN_PHASE_TIMING
+// timing build only (tools/phase_timing.py): per-phase CTA cycles of ess_kernel
+tmvn_status tmvn_test_phase_cycles(uint64_t* out10, int reset) {
+  tmvn::phase_cycles(reinterpret_cast<unsigned long long*>(out10), reset != 0);
+  return TMVN_OK;
+}
+#endif
 
 }  // extern "C"

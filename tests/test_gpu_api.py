@@ -21,11 +21,11 @@ def test_errors():
     with pytest.raises(tm.TmvnError) as ei:
         s.sample(X, 3, seed=1)
     assert ei.value.status == -3 and "chain 5" in str(ei.value)
-    # boundary start is not strictly interior (C18)
-    Xb = np.tile(x0, (2, 1))
-    Xb[1] = A[3] * b[3] / (A[3] @ A[3])
-    with pytest.raises(tm.TmvnError):
-        s.sample(Xb, 1, seed=1)
+    # boundary start (a_i . x0 == b_i exactly) is not strictly interior (C18)
+    sb = tm.Sampler(np.array([[1.0, 0.0], [0.0, 1.0], [-1.0, -1.0]]), np.array([1.0, 2.0, 3.0]))
+    with pytest.raises(tm.TmvnError) as eb:
+        sb.sample(np.array([[0.0, 0.0], [1.0, 0.5]]), 1, seed=1)
+    assert eb.value.status == -3 and "chain 1 violates constraint 0" in str(eb.value)
     # handle stays valid
     out = s.sample(np.tile(x0, (4, 1)), 3, seed=1)
     assert np.all(A @ out.T <= b[:, None])

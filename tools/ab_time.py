@@ -1,0 +1,33 @@
+"""Quick A/B timing of tmvn_sample for several library builds and chain_warps (tooling).
+usage: python tools/ab_time.py config W[,W..] S[,S..] R[,R..] lib1.so [lib2.so ...]"""
+import os, sys, time
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2407_10449_b200 as tm
+from paper_2407_10449_b200 import synth
+k = int(sys.argv[1])
+Ws = [int(w) for w in sys.argv[2].split(",")]
+Ss = [int(x) for x in sys.argv[3].split(",")]
+Rs = [int(x) for x in sys.argv[4].split(",")]
+cfg = synth.CONFIGS[k]
+A, b, x0 = synth.make_instance(k)
+iters = 200 if k in (2, 3) else 20
+for path in sys.argv[5:]:
+    tm._LIB = None
+    tm.LIB_PATH = os.path.abspath(path)
+    for W, S, R in [(w, x, r) for w in Ws for x in Ss for r in Rs]:
+        s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
+        s.set_options(profile=1, chain_warps=W, streams=S, ring=R)
+        X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
+        s.sample(X, 20, cfg.chain_seed, out=X)
+        s.reset_stats()
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        s.sample(X, iters, cfg.chain_seed, out=X)
+        torch.cuda.synchronize(); dt = time.perf_counter() - t0
+        pr = s.profile()
+        print(f"{os.path.basename(path)} W={W} S={S} R={R} cfg{k}: {dt/iters*1e3:.3f} ms/iter  gemm "
+              f"{pr['gemm_ms']/max(1,pr['gemm_launches']):.3f} ms  ess {pr['ess_ms']/max(1,pr['ess_launches']):.3f} ms"
+              f"  evals/s {cfg.C*cfg.m*iters/dt:.3e}", flush=True)
+        s.close()

@@ -1,0 +1,30 @@
+"""Per-phase cycle breakdown of ess_kernel (timing build; tooling, not a bench number).
+usage: python tools/phase_timing.py [config] [iters]"""
+import ctypes, os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2407_10449_b200 as tm
+from paper_2407_10449_b200 import synth
+tm.LIB_PATH = os.path.join(ROOT, "build", "libtmvn_timing.so")
+L = tm.lib()
+L.tmvn_test_phase_cycles.argtypes = [ctypes.c_void_p, ctypes.c_int]
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+cfg = synth.CONFIGS[k]
+A, b, x0 = synth.make_instance(k)
+s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
+X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
+s.sample(X, 40, cfg.chain_seed, out=X)
+buf = np.zeros(10, dtype=np.uint64)
+L.tmvn_test_phase_cycles(buf.ctypes.data_as(ctypes.c_void_p), 1)
+s.sample(X, iters, cfg.chain_seed, out=X)
+L.tmvn_test_phase_cycles(buf.ctypes.data_as(ctypes.c_void_p), 0)
+names = ["init", "A arcs+stats", "lo-word pass", "B intervals", "C theta", "D1 P'+safeguard",
+         "D2 x/moments/nu"]
+nchain = cfg.C * iters
+tot = float(sum(buf[:7]))
+print(f"config {k}: {nchain} chain-iterations; mean active arcs {buf[8]/nchain:.1f}, gaps {buf[9]/nchain:.2f}")
+for i, n in enumerate(names):
+    print(f"  {n:18s} {buf[i]/nchain:10.0f} cycles/chain  {100*buf[i]/tot:5.1f}%")

@@ -85,8 +85,9 @@ typedef struct {
   int32_t chain_warps;
   /* Chain shards run as independent GEMM -> ESS sequences on concurrent streams
    * (forked from / joined to `stream`), so the FP64 tensor GEMM of one shard
-   * overlaps the ALU-bound per-chain kernel of another.  0 (default) = 2 when
-   * C >= 1024, else 1.  Results do not depend on it. */
+   * can overlap the ALU-bound per-chain kernel of another.  0 (default) = 1
+   * (with the persistent GEMM filling every SM the overlap measured slower).
+   * Results do not depend on it. */
   int32_t streams;
   /* 1: stream each chain's P and Q rows into shared memory with cp.async.bulk
    * through a 2-slot mbarrier ring (the next chain's rows prefetched); 0

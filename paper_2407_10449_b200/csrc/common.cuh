@@ -141,50 +141,68 @@ __device__ __forceinline__ double2 normal_pair_at(uint64_t seed, uint32_t t, uin
 // Branch-free FP64 atan2 (the libm one branches per octant and diverges inside a
 // warp).  t = min(|x|,|y|) / max(|x|,|y|) in [0, 1]; for t > tan(pi/8) the
 // identity atan(t) = pi/4 + atan((t-1)/(t+1)) folds the argument to
-// |t'| <= tan(pi/8) with the same single division ((mn-mx)/(mn+mx)); then
+// |t'| <= tan(pi/8) with the same single quotient ((mn-mx)/(mn+mx)); then
 // atan(t') = t' P(t'^2), P of degree 10 fitted by Chebyshev interpolation
-// (tools/fit_atan.py: 2.2e-16 max relative error in FP64 Horner/FMA); octant
-// reconstruction by selects.  Matches atan2's signed-zero conventions.
+// (tools/fit_atan.py: 2.2e-16 max relative error in FP64 Horner/FMA).  The
+// octant is undone in one step, atan2 = base[code] +/- atan(t'), with the 8
+// bases (sums of multiples of pi/4 and pi, rounded once) in constant memory.
+// The quotient uses a hardware reciprocal estimate refined by two Newton steps
+// (relative error ~1e-16).  Signed zeros follow atan2: y = -0 gives -0 / -pi.
 // ----------------------------------------------------------------------------
+__constant__ double kAtanP[11] = {1.0, -0.3333333333332844, 0.1999999999885511,
+                                  -0.14285714180976467, 0.11111106180455946,
+                                  -0.09090773074808414, 0.07689953496306857,
+                                  -0.06640233930429408, 0.056883492268090106,
+                                  -0.04348052215716462, 0.021135373157693246};
+// code = big | swap << 1 | xneg << 2: result magnitude = base + sgn * atan(t')
+__constant__ double kAtanBase[8] = {
+    0.0,                    // t' = t
+    0.7853981633974483,     // pi/4 + t'
+    1.5707963267948966,     // pi/2 - t'
+    0.7853981633974483,     // pi/2 - (pi/4 + t') = pi/4 - t'
+    3.141592653589793,      // pi - t'
+    2.356194490192345,      // pi - (pi/4 + t') = 3pi/4 - t'
+    1.5707963267948966,     // pi - (pi/2 - t') = pi/2 + t'
+    2.356194490192345};     // pi - (pi/4 - t') = 3pi/4 + t'
+// sign of t' per code: + for codes 0, 1, 6, 7
+__device__ __forceinline__ double fast_recip(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
 __device__ __forceinline__ double fast_atan2(double y, double x) {
-  const double kPi = 3.141592653589793, kPi2 = 1.5707963267948966, kPi4 = 0.7853981633974483;
-  const double kTanPi8 = 0.41421356237309503;
   const double ax = fabs(x), ay = fabs(y);
   const double mx = fmax(ax, ay), mn = fmin(ax, ay);
-  const bool big = mn > kTanPi8 * mx;
+  const bool big = mn > 0.41421356237309503 * mx;
   const double num = big ? mn - mx : mn;
   const double den = big ? mn + mx : mx;
-  const double t = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+  const double t = den > 0.0 ? num * fast_recip(den) : 0.0;
   const double z = t * t;
-  double pz = 0.021135373157693246;
-  pz = fma(pz, z, -0.04348052215716462);
-  pz = fma(pz, z, 0.056883492268090106);
-  pz = fma(pz, z, -0.06640233930429408);
-  pz = fma(pz, z, 0.07689953496306857);
-  pz = fma(pz, z, -0.09090773074808414);
-  pz = fma(pz, z, 0.11111106180455946);
-  pz = fma(pz, z, -0.14285714180976467);
-  pz = fma(pz, z, 0.1999999999885511);
-  pz = fma(pz, z, -0.3333333333332844);
-  double r = fma(t * z, pz, t);  // t * (1 + z * pz)
-  r = big ? r + kPi4 : r;
-  r = ay > ax ? kPi2 - r : r;
-  r = (__double_as_longlong(x) < 0) ? kPi - r : r;      // x < 0 or x = -0
-  return (__double_as_longlong(y) < 0) ? -r : r;          // y < 0 or y = -0
+  double pz = kAtanP[10];
+#pragma unroll
+  for (int i = 9; i >= 1; --i) pz = fma(pz, z, kAtanP[i]);
+  const double at = fma(t * z, pz, t);  // atan(t') = t (1 + z P1(z))
+  const int code = (big ? 1 : 0) | (ay > ax ? 2 : 0) | ((__double_as_longlong(x) < 0) ? 4 : 0);
+  const double sat = ((0xC3u >> code) & 1u) ? at : -at;  // + for codes 0, 1, 6, 7
+  const double r = kAtanBase[code] + sat;
+  return (__double_as_longlong(y) < 0) ? -r : r;
 }
 
 // ----------------------------------------------------------------------------
 // Infeasible arc of constraint (p, q, b) on the ellipse (Eq. 2, eq:roots):
 // r = |(p, q)|; active iff r > b (C3); tau = atan2(q, p);
-// delta = arccos(b / r) computed as atan2(sqrt((r - b)(r + b)), b) (same angle in
-// [0, pi]; the clamp of C5 becomes the clamp of (r - b)(r + b) at 0);
-// (alpha, beta) = (tau - delta, tau + delta) shifted into [0, 2 pi] by C1.
-// Returns false for an inactive constraint.
+// delta = arccos(b / r) computed as atan2(s, b) with s = sqrt(r^2 - b^2) (the
+// same angle in [0, pi]; the clamp of C5 becomes max(s^2, 0)); active iff
+// b < 0 or s^2 > 0; (alpha, beta) = (tau - delta, tau + delta) shifted into
+// [0, 2 pi] by C1.  Returns false for an inactive constraint.
 // ----------------------------------------------------------------------------
 __device__ __forceinline__ bool arc_of(double p, double q, double b, double& alpha, double& beta) {
-  const double r = sqrt(fma(p, p, q * q));
-  if (!(r > b)) return false;
-  const double s = sqrt(fmax((r - b) * (r + b), 0.0));
+  const double s2 = fma(p, p, fma(q, q, -b * b));  // p^2 + q^2 - b^2
+  if (!(b < 0.0 || s2 > 0.0)) return false;
+  const double s = sqrt(fmax(s2, 0.0));
   const double tau = fast_atan2(q, p);
   const double delta = fast_atan2(s, b);
   double lo = __dsub_rn(tau, delta);

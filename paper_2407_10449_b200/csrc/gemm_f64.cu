@@ -27,76 +27,69 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// out[R_pad x ldo] (row-major) = X[R_pad x K_pad] . W[S_pad x K_pad]^T, both tiled.
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tn_f64_kernel(const double* __restrict__ Xt, const double* __restrict__ Wt,
-                       double* __restrict__ out, int64_t ldo, int s_tiles, int KB) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sA = reinterpret_cast<double*>(smem_raw);
-  double* sB = sA + kStages * kChunk;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kChunk);
-
+// One output tile: 128 rows of X (chunk row block rb) x 32*NJ*4 columns of W
+// starting at W row wrow0 (NJ = 4: a full 128-wide tile; 2: 64; 1: 32).  Warps:
+// 2 (M) x 4 (N), warp tile 64 x 8 NJ.  kk = CTA-wide k-block counter (mbarrier
+// phases).  Every output element is accumulated over the K blocks in the same
+// order whatever NJ is, so the result does not depend on the tiling.
+template <int NJ>
+__device__ __forceinline__ void gemm_tile(double* sA, double* sB, uint64_t* full, const double* gA,
+                                          const double* gB, double* __restrict__ out, int64_t ldo,
+                                          int64_t row_base, int64_t col_base, int KB, int& kk) {
+  constexpr uint32_t kBBytes = kChunkBytes * NJ / 4;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rb = blockIdx.x / s_tiles, sb = blockIdx.x % s_tiles;
-  const double* gA = Xt + (int64_t)rb * KB * kChunk;
-  const double* gB = Wt + (int64_t)sb * KB * kChunk;
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  auto issue = [&](int kb) {
-    int s = kb % kStages;
-    mbar_expect_tx(&full[s], 2 * kChunkBytes);
+  const int wm = warp >> 2, wn = warp & 3;
+  auto issue = [&](int kb, int q) {
+    const int s = q % kStages;
+    mbar_expect_tx(&full[s], kChunkBytes + kBBytes);
     bulk_g2s(sA + s * kChunk, gA + (int64_t)kb * kChunk, kChunkBytes, &full[s]);
-    bulk_g2s(sB + s * kChunk, gB + (int64_t)kb * kChunk, kChunkBytes, &full[s]);
+    bulk_g2s(sB + s * kChunk, gB + (int64_t)kb * kChunk, kBBytes, &full[s]);
   };
+  __syncthreads();  // the previous tile's last stages are consumed
   if (tid == 0) {
-    for (int kb = 0; kb < kStages - 1 && kb < KB; ++kb) issue(kb);
+    for (int kb = 0; kb < kStages - 1 && kb < KB; ++kb) issue(kb, kk + kb);
   }
-
-  double acc[8][4][2];
+  double acc[8][NJ][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int wm = warp >> 2, wn = warp & 3;
   for (int kb = 0; kb < KB; ++kb) {
-    __syncthreads();  // every warp is done with stage (kb - 1) % kStages
-    if (tid == 0 && kb + kStages - 1 < KB) issue(kb + kStages - 1);
-    const int s = kb % kStages;
-    mbar_wait(&full[s], (uint32_t)((kb / kStages) & 1));
+    const int q = kk + kb;
+    __syncthreads();  // every warp is done with stage (q - 1) % kStages
+    if (tid == 0 && kb + kStages - 1 < KB) issue(kb + kStages - 1, q + kStages - 1);
+    const int s = q % kStages;
+    mbar_wait(&full[s], (uint32_t)((q / kStages) & 1));
     const double* a = sA + s * kChunk;
     const double* b = sB + s * kChunk;
 #pragma unroll
     for (int kh = 0; kh < 2; ++kh) {
-      double2 fa[8], fb[4];
+      double2 fa[8], fb[NJ];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         fa[i] = *reinterpret_cast<const double2*>(a + ((wm * 8 + i) * 2 + kh) * 64 + lane * 2);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        fb[j] = *reinterpret_cast<const double2*>(b + ((wn * 4 + j) * 2 + kh) * 64 + lane * 2);
+      for (int j = 0; j < NJ; ++j)
+        fb[j] = *reinterpret_cast<const double2*>(b + ((wn * NJ + j) * 2 + kh) * 64 + lane * 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], fa[i].x, fb[j].x);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], fa[i].x, fb[j].x);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], fa[i].y, fb[j].y);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], fa[i].y, fb[j].y);
     }
   }
+  kk += KB;
 
-  const int64_t row0 = (int64_t)rb * kTileR + wm * 64 + (lane >> 2);
-  const int64_t col0 = (int64_t)sb * kTileR + wn * 32 + (lane & 3) * 2;
+  const int64_t row0 = row_base + wm * 64 + (lane >> 2);
+  const int64_t col0 = col_base + wn * 8 * NJ + (lane & 3) * 2;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       double2 v;
       v.x = acc[i][j][0];
       v.y = acc[i][j][1];
@@ -104,9 +97,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// out[R_pad x ldo] (row-major) = X[R_pad x K_pad] . W[S_pad x K_pad]^T, both tiled.
+// Persistent: CTA b runs work items b, b + grid, ...; items < n_full are full
+// 128 x 128 tiles, the remaining tiles are split into `split` column slices
+// (128 x 128/split) so that the last wave is balanced.
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tn_f64_kernel(const double* __restrict__ Xt, const double* __restrict__ Wt,
+                       double* __restrict__ out, int64_t ldo, int s_tiles, int KB, int n_full,
+                       int n_items, int split) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);
+  double* sB = sA + kStages * kChunk;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kChunk);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int kk = 0;
+  for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    int tile, part = 0;
+    if (w < n_full) {
+      tile = w;
+    } else {
+      tile = n_full + (w - n_full) / split;
+      part = (w - n_full) % split;
+    }
+    const int rb = tile / s_tiles, sb = tile % s_tiles;
+    const double* gA = Xt + (int64_t)rb * KB * kChunk;
+    const int64_t row_base = (int64_t)rb * kTileR;
+    if (w < n_full || split == 1) {
+      gemm_tile<4>(sA, sB, full, gA, Wt + (int64_t)sb * KB * kChunk, out, ldo, row_base,
+                   (int64_t)sb * kTileR, KB, kk);
+    } else if (split == 2) {
+      gemm_tile<2>(sA, sB, full, gA, Wt + (int64_t)sb * KB * kChunk + part * (kChunk / 2), out,
+                   ldo, row_base, (int64_t)sb * kTileR + part * 64, KB, kk);
+    } else {
+      gemm_tile<1>(sA, sB, full, gA, Wt + (int64_t)sb * KB * kChunk + part * (kChunk / 4), out,
+                   ldo, row_base, (int64_t)sb * kTileR + part * 32, KB, kk);
+    }
+  }
+}
+
 }  // namespace
 
 size_t gemm_smem_bytes() { return (size_t)kStages * 2 * kChunkBytes + kStages * sizeof(uint64_t); }
+
+static int g_gemm_sms = 0;
 
 cudaError_t launch_gemm_tn(const double* Xt, int64_t R_pad, const double* Wt, int64_t S_pad,
                            int64_t K_pad, double* out, int64_t ldo, cudaStream_t st) {
@@ -116,12 +153,31 @@ cudaError_t launch_gemm_tn(const double* Xt, int64_t R_pad, const double* Wt, in
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)gemm_smem_bytes());
     if (e != cudaSuccess) return e;
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_gemm_sms, cudaDevAttrMultiProcessorCount, dev);
     configured = true;
   }
-  int r_tiles = (int)(R_pad / kTileR), s_tiles = (int)(S_pad / kTileR), KB = (int)(K_pad / kTileK);
-  if (r_tiles == 0 || s_tiles == 0) return cudaSuccess;
-  gemm_tn_f64_kernel<<<r_tiles * s_tiles, kThreads, gemm_smem_bytes(), st>>>(Xt, Wt, out, ldo,
-                                                                             s_tiles, KB);
+  const int r_tiles = (int)(R_pad / kTileR), s_tiles = (int)(S_pad / kTileR), KB = (int)(K_pad / kTileK);
+  const int T = r_tiles * s_tiles;
+  if (T == 0) return cudaSuccess;
+  const int G = T < g_gemm_sms ? T : g_gemm_sms;
+  // whole waves of full tiles; the rest split into 1, 2 or 4 column slices,
+  // whichever finishes first (in units of a full-tile time)
+  const int rounds = T / G, rest = T - rounds * G;
+  int best_split = 1;
+  double best = 1e30;
+  for (int f = 1; f <= 4; f *= 2) {
+    const double t = rounds + (double)((rest * f + G - 1) / G) / f;
+    if (t < best - 1e-9) {
+      best = t;
+      best_split = f;
+    }
+  }
+  const int n_full = rounds * G;
+  const int n_items = n_full + rest * best_split;
+  gemm_tn_f64_kernel<<<G, kThreads, gemm_smem_bytes(), st>>>(Xt, Wt, out, ldo, s_tiles, KB,
+                                                              n_full, n_items, best_split);
   return cudaGetLastError();
 }
 

@@ -41,7 +41,7 @@ struct EssParams {
   const double* g_u;
   // scratch (per CTA)
   double2* gstash;  // groups * m   (arcs when not in shared memory)
-  int* gnext;       // groups * m   (their bucket lists)
+  double2* gsorted; // groups * m   (the arcs grouped by bucket)
   double2* ggaps;   // groups * (m + 2)
   int NB;           // buckets per level (power of two)
   int W;            // warps per chain (1, 2, 4, 8)
@@ -74,7 +74,7 @@ __host__ __device__ inline size_t ess_group_base_bytes(int NB) {
 }
 __host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_smem, int CH) {
   size_t s = ess_ring_bytes(CH) + ess_group_base_bytes(NB);
-  if (stash_smem) s += (size_t)m * (16 + 4);
+  if (stash_smem) s += (size_t)m * 32;  // stash + bucket-sorted copy
   return (s + 15) / 16 * 16;
 }
 

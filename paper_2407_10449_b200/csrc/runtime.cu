@@ -54,7 +54,7 @@ struct tmvn_ctx {
   double* msum = nullptr;  // d (device) moment reduction target
   unsigned long long* dflag = nullptr;
   double2 *gstash = nullptr, *ggaps = nullptr;
-  int* gnext = nullptr;
+  double2* gsorted = nullptr;
   int64_t scratch_groups = 0;  // chain groups the scratch is sized for
   bool scratch_stash = false;  // gstash / gnext allocated
   EssLaunch plan{};
@@ -129,7 +129,7 @@ void free_chain_buffers(tmvn_ctx* h) {
   dfree(h->X); dfree(h->N); dfree(h->P0); dfree(h->P1); dfree(h->Q);
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
   dfree(h->stage); dfree(h->stage2); dfree(h->rej);
-  dfree(h->gstash); dfree(h->ggaps); dfree(h->gnext);
+  dfree(h->gstash); dfree(h->ggaps); dfree(h->gsorted);
   h->C_cap = h->C_pad = 0;
 }
 
@@ -159,7 +159,7 @@ tmvn_status ensure_chains(tmvn_ctx* h, int64_t C) {
 // Shards, launch plan of the fused kernel (per shard) and its per-group scratch.
 tmvn_status plan_ess(tmvn_ctx* h, int64_t C) {
   int S = h->opt.streams;
-  if (S <= 0) S = C >= 1024 ? 2 : 1;  // auto
+  if (S <= 0) S = 1;  // auto: the persistent GEMM fills every SM, overlap does not pay (profiles/r01)
   if (h->trace_dev) S = 1;
   const int64_t per = round_up((C + S - 1) / S, kTileR);
   S = (int)((C + per - 1) / per);
@@ -177,11 +177,11 @@ tmvn_status plan_ess(tmvn_ctx* h, int64_t C) {
   const bool need_stash = !h->plan.stash_smem;
   const int64_t G = h->plan.groups * S;
   if (G > h->scratch_groups || (need_stash && !h->scratch_stash)) {
-    dfree(h->gstash); dfree(h->gnext); dfree(h->ggaps);
+    dfree(h->gstash); dfree(h->gsorted); dfree(h->ggaps);
     const int64_t Gn = std::max(G, h->scratch_groups);
     if (need_stash || h->scratch_stash) {
       CK(h, dalloc(&h->gstash, (size_t)Gn * h->m));
-      CK(h, dalloc(&h->gnext, (size_t)Gn * h->m));
+      CK(h, dalloc(&h->gsorted, (size_t)Gn * h->m));
       h->scratch_stash = true;
     }
     CK(h, dalloc(&h->ggaps, (size_t)Gn * (h->m + 2)));
@@ -220,7 +220,7 @@ EssParams base_params(tmvn_ctx* h, int C) {
   p.S2 = h->S2;
   p.rej = h->rej;
   p.gstash = h->gstash;
-  p.gnext = h->gnext;
+  p.gsorted = h->gsorted;
   p.ggaps = h->ggaps;
   p.NB = h->plan.NB;
   p.W = h->plan.W;
@@ -322,7 +322,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p.rej = h->rej + x.c0;
     x.p.chain_offset = (uint32_t)(h->opt.chain_offset + x.c0);
     x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * h->m : nullptr;
-    x.p.gnext = h->gnext ? h->gnext + (size_t)s * h->plan.groups * h->m : nullptr;
+    x.p.gsorted = h->gsorted ? h->gsorted + (size_t)s * h->plan.groups * h->m : nullptr;
     x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
     x.Pc = P_cur + x.c0 * h->m_pad;
     x.Pn = P_next + x.c0 * h->m_pad;
@@ -794,7 +794,7 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   Tmp<double> da, db, du, dlo, dhi, dL, dth;
   Tmp<int64_t> dns;
   Tmp<double2> gstash, ggaps;
-  Tmp<int> gnext;
+  Tmp<double2> gsorted;
   TCK(tmp_in(da, alpha, cm)); TCK(tmp_in(db, beta, cm));
   TCK(tmp_in(du, u, u ? (size_t)C : 0));
   TCK(tmp_in(dlo, (const double*)nullptr, (size_t)C * seg_cap)); TCK(tmp_in(dhi, (const double*)nullptr, (size_t)C * seg_cap));
@@ -804,7 +804,7 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   const int grid = plan.grid;
   if (!plan.stash_smem) {
     TCK(tmp_in(gstash, (const double2*)nullptr, (size_t)plan.groups * m));
-    TCK(tmp_in(gnext, (const int*)nullptr, (size_t)plan.groups * m));
+    TCK(tmp_in(gsorted, (const double2*)nullptr, (size_t)plan.groups * m));
   }
   TCK(tmp_in(ggaps, (const double2*)nullptr, (size_t)plan.groups * (m + 2)));
   EssParams p;
@@ -816,7 +816,7 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   p.g_beta = db.p;
   p.g_u = u ? du.p : nullptr;
   p.gstash = gstash.p;
-  p.gnext = gnext.p;
+  p.gsorted = gsorted.p;
   p.ggaps = ggaps.p;
   p.NB = plan.NB;
   p.W = plan.W;

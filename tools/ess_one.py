@@ -10,7 +10,7 @@ k, W = int(sys.argv[1]), int(sys.argv[2])
 cfg = synth.CONFIGS[k]
 A, b, x0 = synth.make_instance(k)
 s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
-s.set_options(chain_warps=W)
+s.set_options(chain_warps=W, streams=1)
 X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
 s.sample(X, 6, cfg.chain_seed, out=X)
 torch.cuda.synchronize()

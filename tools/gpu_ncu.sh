@@ -1,4 +1,4 @@
-# ncu launch list + full captures of the two hot kernels (one gpurun call).
+# ncu launch list of the bench command + full captures of the two hot kernels (one gpurun call).
 mkdir -p gpurun_out
 CMD="python bench.py --steps 1 --warmup 1 --iters-per-step 8 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/plain.log 2>&1 &&

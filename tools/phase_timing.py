@@ -15,9 +15,10 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 cfg = synth.CONFIGS[k]
 A, b, x0 = synth.make_instance(k)
 s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
+s.set_options(streams=1, chain_warps=int(os.environ.get("W", "0")))
 X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
 s.sample(X, 40, cfg.chain_seed, out=X)
-buf = np.zeros(10, dtype=np.uint64)
+buf = np.zeros(14, dtype=np.uint64)
 L.tmvn_test_phase_cycles(buf.ctypes.data_as(ctypes.c_void_p), 1)
 s.sample(X, iters, cfg.chain_seed, out=X)
 L.tmvn_test_phase_cycles(buf.ctypes.data_as(ctypes.c_void_p), 0)
@@ -25,6 +26,8 @@ names = ["init", "A arcs+stats", "lo-word pass", "B intervals", "C theta", "D1 P
          "D2 x/moments/nu"]
 nchain = cfg.C * iters
 tot = float(sum(buf[:7]))
-print(f"config {k}: {nchain} chain-iterations; mean active arcs {buf[8]/nchain:.1f}, gaps {buf[9]/nchain:.2f}")
+print(f"config {k}: {nchain} chain-iterations; mean active arcs {buf[8]/nchain:.1f}, gaps {buf[9]/nchain:.2f}, general path {buf[7]/nchain:.3f}")
 for i, n in enumerate(names):
     print(f"  {n:18s} {buf[i]/nchain:10.0f} cycles/chain  {100*buf[i]/tot:5.1f}%")
+for i, n in enumerate(["wi pass1", "wi pass2+gather", "wi sort", "wi scan+emit"]):
+    print(f"    {n:16s} {buf[10+i]/nchain:10.0f} cycles/chain")

@@ -245,9 +245,16 @@ def main():
         hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
     except Exception:
         hbm, hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    traffic, traffic_src = None, None
+    try:  # dram__bytes_read + dram__bytes_write per launch from the committed ncu --set full capture
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_gemm_traffic.json")))
+        if args.config == 3 and world == 1:
+            traffic, traffic_src = tj["traffic_bytes"], "profiles/r01/ncu_gemm_traffic.json"
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "kernel": "gemm_tn_f64_kernel (Q = N A^T and P = X A^T, FP64 DMMA)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None,
+                "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "measured FP64 DMMA pipe peak on this pool's B200 (profiles/peaks_fp64_r01.json: "
                                f"mma.sync f64 micro-benchmark; cuBLAS DGEMM measured {peaks['dgemm_tflops_burst']} TF/s)",
                 "algorithmic_flops_per_launch": gemm_flops, "avg_launch_ms": gemm_avg_ms,

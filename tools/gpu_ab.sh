@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-python tools/ab_time.py 3 2,4,8 1,2 0,1 build/libtmvn_cs.so > gpurun_out/ab.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 400 -p no:cacheprovider > gpurun_out/t_all.log 2>&1
+echo "tests rc=$?" >> gpurun_out/t_all.log
+python tools/ab_time.py 3 4,8 1 0 build/libtmvn_cs.so build/libtmvn_pre.so build/libtmvn_pre2.so > gpurun_out/ab.log 2>&1

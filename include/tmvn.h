@@ -94,6 +94,10 @@ typedef struct {
    * (default): read them from global memory (measured faster on B200 at
    * config 3: the ring costs occupancy, profiles/r01/README.md). */
   int32_t ring;
+  /* 1 (default): whole blocks of recompute_every iterations aligned to a
+   * multiple of it are replayed as one CUDA graph (a single shard, no profiling,
+   * no x-space moment recording); 0: one launch per kernel. */
+  int32_t graphs;
 } tmvn_options;
 
 typedef struct {

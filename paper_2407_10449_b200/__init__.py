@@ -45,7 +45,8 @@ class options(ctypes.Structure):
                 ("chain_offset", ctypes.c_int64), ("iter_offset", ctypes.c_int64),
                 ("auto_advance", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int32), ("chain_warps", ctypes.c_int32),
-                ("streams", ctypes.c_int32), ("ring", ctypes.c_int32)]
+                ("streams", ctypes.c_int32), ("ring", ctypes.c_int32),
+                ("graphs", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):

@@ -212,6 +212,8 @@ __global__ void test_arcs_kernel(const double* __restrict__ p, const double* __r
   active[i] = act ? 1 : 0;
 }
 
+__global__ void set_u32_kernel(uint32_t* dst, uint32_t value) { *dst = value; }
+
 inline int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 64) g = 148 * 64;
@@ -275,6 +277,10 @@ cudaError_t launch_gather_rows_tiled(const double* Xt, int64_t d_pad, int d, con
 }
 cudaError_t launch_sum_i64(const int64_t* v, int n, int64_t* out, cudaStream_t st) {
   sum_i64_kernel<<<1, 1024, 0, st>>>(v, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_set_u32(uint32_t* dst, uint32_t value, cudaStream_t st) {
+  set_u32_kernel<<<1, 1, 0, st>>>(dst, value);
   return cudaGetLastError();
 }
 cudaError_t launch_gemv_shift(const double* A, const double* b, const double* mu, int m, int d,

@@ -766,6 +766,14 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
     if (g.tid == 0) ring_issue(0);
   }
 
+  // iteration index and record flag (from device memory under CUDA-graph replay)
+  const uint32_t t_it = p.t_dev ? *p.t_dev + p.t : p.t;
+  int record = p.record;
+  if (p.rec_dev) {
+    const int64_t tt = (int64_t)t_it;
+    record = tt >= p.burn_in && ((tt - p.burn_in) % (p.thin < 1 ? 1 : p.thin)) == 0;
+  }
+
   for (int64_t cc = gglobal; cc < p.C; cc += ngroups) {
     const int c = (int)cc;
     const uint32_t gchain = p.chain_offset + (uint32_t)c;
@@ -946,7 +954,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
       if (g.lane == 0) {
         ctl.fast = fast ? 1 : 0;
         if (fast) {
-          const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, p.t, gchain);
+          const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, t_it, gchain);
           theta_from_gaps(S, ctl, gg, u, p.eps);
         }
       }
@@ -957,7 +965,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
     if (!ctl.fast) {
       build_intervals(g, S, ctl, stash, NB, log2NB, scale, gg, s_w64, s_w32);
       if (g.tid == 0) {
-        const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, p.t, gchain);
+        const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, t_it, gchain);
         theta_from_gaps(S, ctl, gg, u, p.eps);
       }
       g.sync();
@@ -1061,7 +1069,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
         xv.y = xv.y * ct + nv.y * st;
         *xr = xv;
       }
-      if (p.record) {
+      if (record) {
         double2* s1 = reinterpret_cast<double2*>(p.S1 + o);
         double2* s2 = reinterpret_cast<double2*>(p.S2 + o);
         double2 a1 = *s1, a2 = *s2;
@@ -1072,7 +1080,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
         *s1 = a1;
         *s2 = a2;
       }
-      if (p.gen_next) *nr = normal_pair_at(p.seed, p.t + 1, gchain, 2 * pk, p.d);
+      if (p.gen_next) *nr = normal_pair_at(p.seed, t_it + 1, gchain, 2 * pk, p.d);
     }
     if (g.tid == 0) {
       if (!accept) p.rej[c] += 1;

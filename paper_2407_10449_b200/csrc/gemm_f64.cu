@@ -161,21 +161,23 @@ cudaError_t launch_gemm_tn(const double* Xt, int64_t R_pad, const double* Wt, in
   const int r_tiles = (int)(R_pad / kTileR), s_tiles = (int)(S_pad / kTileR), KB = (int)(K_pad / kTileK);
   const int T = r_tiles * s_tiles;
   if (T == 0) return cudaSuccess;
-  const int G = T < g_gemm_sms ? T : g_gemm_sms;
-  // whole waves of full tiles; the rest split into 1, 2 or 4 column slices,
-  // whichever finishes first (in units of a full-tile time)
-  const int rounds = T / G, rest = T - rounds * G;
+  const int P = g_gemm_sms;
+  // whole waves of full tiles; the rest (all tiles when there are fewer than SMs)
+  // split into 1, 2 or 4 column slices, whichever finishes first (in units of a
+  // full-tile time)
+  const int rounds = T / P, rest = T - rounds * P;
   int best_split = 1;
   double best = 1e30;
   for (int f = 1; f <= 4; f *= 2) {
-    const double t = rounds + (double)((rest * f + G - 1) / G) / f;
+    const double t = rounds + (double)((rest * f + P - 1) / P) / f;
     if (t < best - 1e-9) {
       best = t;
       best_split = f;
     }
   }
-  const int n_full = rounds * G;
+  const int n_full = rounds * P;
   const int n_items = n_full + rest * best_split;
+  const int G = n_items < P ? n_items : P;
   gemm_tn_f64_kernel<<<G, kThreads, gemm_smem_bytes(), st>>>(Xt, Wt, out, ldo, s_tiles, KB,
                                                               n_full, n_items, best_split);
   return cudaGetLastError();

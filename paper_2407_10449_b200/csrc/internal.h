@@ -28,7 +28,10 @@ struct EssParams {
   int C;
   uint32_t chain_offset;
   uint64_t seed;
-  uint32_t t;       // iteration index of this step
+  uint32_t t;       // iteration index of this step (offset from *t_dev when t_dev is set)
+  const uint32_t* t_dev;  // graph replay: iteration base in device memory (nullable)
+  int rec_dev;      // 1: record flag computed from t (t >= burn_in, (t - burn_in) % thin == 0)
+  int64_t burn_in, thin;
   int gen_next;     // 1: draw nu for t + 1 into N after the update
   double eps;       // S3.3 trim
   int record;       // accumulate S1 += x, S2 += x^2 into the tiled moments
@@ -118,6 +121,7 @@ cudaError_t launch_trsv_rows(const double* Xrow, const double* mu, const double*
 cudaError_t launch_gather_rows_tiled(const double* Xt, int64_t d_pad, int d, const int64_t* rows,
                                      int n, double* out, cudaStream_t st);
 cudaError_t launch_sum_i64(const int64_t* v, int n, int64_t* out, cudaStream_t st);
+cudaError_t launch_set_u32(uint32_t* dst, uint32_t value, cudaStream_t st);
 // b' = b - A mu (A row-major m x d), one warp per row
 cudaError_t launch_gemv_shift(const double* A, const double* b, const double* mu, int m, int d,
                               double* out, cudaStream_t st);

@@ -62,6 +62,11 @@ struct tmvn_ctx {
   std::vector<cudaStream_t> shard_streams;
   cudaEvent_t fork_event = nullptr;
   std::vector<cudaEvent_t> join_events;
+  // CUDA-graph replay of aligned blocks of recompute_every iterations
+  cudaStream_t capture_stream = nullptr;
+  uint32_t* d_tbase = nullptr;
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};  // by P parity at block start
+  std::vector<unsigned char> graph_sig[2];
   // state
   tmvn_options opt{};
   tmvn_stats stats{};
@@ -216,6 +221,8 @@ EssParams base_params(tmvn_ctx* h, int C) {
   p.C = C;
   p.chain_offset = (uint32_t)h->opt.chain_offset;
   p.eps = h->opt.trim_eps;
+  p.burn_in = h->opt.record ? h->opt.burn_in : ((int64_t)1 << 62);  // no record: never
+  p.thin = h->opt.thin;
   p.S1 = h->S1;
   p.S2 = h->S2;
   p.rej = h->rej;
@@ -285,6 +292,62 @@ bool recorded_iter(const tmvn_options& o, int64_t t) {
   return ((t - o.burn_in) % thin) == 0;
 }
 
+// One captured block of K iterations starting at an iteration t with t % K == 0:
+// (GEMM Q = N A'^T, ESS) x K, then the refresh GEMM P = X A'^T.  The ESS launches
+// read t from h->d_tbase (set by a one-thread kernel before each replay) and
+// compute their record flag from t, so one graph serves every aligned block.
+tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K, double* Pc,
+                        double* Pn, cudaGraphExec_t* out) {
+  const int parity = Pc == h->P0 ? 0 : 1;
+  EssParams p = base;
+  p.t_dev = h->d_tbase;
+  p.rec_dev = 1;
+  p.gen_next = 1;
+  p.t = 0;
+  p.P_cur = Pc;
+  p.P_next = Pn;
+  std::vector<unsigned char> sig(sizeof(EssParams) + 2 * sizeof(int64_t) + 2 * sizeof(void*));
+  std::memcpy(sig.data(), &p, sizeof(EssParams));
+  std::memcpy(sig.data() + sizeof(EssParams), &C, sizeof(int64_t));
+  std::memcpy(sig.data() + sizeof(EssParams) + 8, &K, sizeof(int64_t));
+  const void* ptrs[2] = {h->At, h->Q};
+  std::memcpy(sig.data() + sizeof(EssParams) + 16, ptrs, sizeof(ptrs));
+  if (h->graph_exec[parity] && h->graph_sig[parity] == sig) {
+    *out = h->graph_exec[parity];
+    return TMVN_OK;
+  }
+  if (h->graph_exec[parity]) {
+    cudaGraphExecDestroy(h->graph_exec[parity]);
+    h->graph_exec[parity] = nullptr;
+  }
+  if (!h->capture_stream) CK(h, cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = h->capture_stream;
+  const int64_t Rp = round_up(C, kTileR);
+  CK(h, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  cudaError_t err = cudaSuccess;
+  double *pc = Pc, *pn = Pn;
+  for (int64_t i = 0; i < K && err == cudaSuccess; ++i) {
+    err = launch_gemm_tn(h->N, Rp, h->At, h->m_pad, h->d_pad, h->Q, h->m_pad, cs);
+    if (err != cudaSuccess) break;
+    p.t = (uint32_t)i;
+    p.P_cur = pc;
+    p.P_next = pn;
+    err = launch_ess_step(p, h->plan.grid, cs);
+    std::swap(pc, pn);
+  }
+  if (err == cudaSuccess) err = launch_gemm_tn(h->X, Rp, h->At, h->m_pad, h->d_pad, pc, h->m_pad, cs);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
+  if (err != cudaSuccess) return cuda_fail(h, err, "graph capture");
+  if (e2 != cudaSuccess) return cuda_fail(h, e2, "cudaStreamEndCapture");
+  cudaError_t e3 = cudaGraphInstantiate(&h->graph_exec[parity], graph, 0);
+  cudaGraphDestroy(graph);
+  if (e3 != cudaSuccess) return cuda_fail(h, e3, "cudaGraphInstantiate");
+  h->graph_sig[parity] = sig;
+  *out = h->graph_exec[parity];
+  return TMVN_OK;
+}
+
 // The hot loop.  On entry X holds x_{t0} (tiled) and P_cur = X A'^T.
 // The chains are split into `shards` row blocks (multiples of 128 chains), each an
 // independent GEMM -> ESS sequence on its own stream: the DMMA GEMM of one shard
@@ -324,6 +387,8 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * h->m : nullptr;
     x.p.gsorted = h->gsorted ? h->gsorted + (size_t)s * h->plan.groups * h->m : nullptr;
     x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
+    x.p.Q = h->Q + x.c0 * h->m_pad;
+    x.p.seed = seed;
     x.Pc = P_cur + x.c0 * h->m_pad;
     x.Pn = P_next + x.c0 * h->m_pad;
   }
@@ -355,8 +420,23 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
       kind_C.push_back(nC);                                 \
     }                                                       \
   } while (0)
+  const bool graphs = h->opt.graphs != 0 && S == 1 && !prof && !h->trace_dev &&
+                      !(h->affine && h->opt.record) && (K % 2 == 0);
+  if (graphs && !h->d_tbase) CK(h, dalloc(&h->d_tbase, 1));
   for (int64_t it = 0; it < n_iter; ++it) {
     const int64_t t = t0 + it;
+    if (graphs && t % K == 0 && n_iter - it >= K) {  // a whole aligned block: replay
+      Shard& x = sh[0];
+      cudaGraphExec_t ge;
+      tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, &ge);
+      if (gs != TMVN_OK) return gs;
+      KL(h, launch_set_u32(h->d_tbase, (uint32_t)t, st));
+      CK(h, cudaGraphLaunch(ge, st));
+      h->prof.launches += 2 * K + 1;
+      for (int64_t i = 0; i < K; ++i) nrec += recorded_iter(h->opt, t + i) ? 1 : 0;
+      it += K - 1;  // K even: P parity unchanged, the block ends with the refresh
+      continue;
+    }
     const bool rec = recorded_iter(h->opt, t);
     for (int s = 0; s < S; ++s) {
       Shard& x = sh[s];
@@ -365,8 +445,6 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
                                          h->m_pad, x.st));
       x.p.P_cur = x.Pc;
       x.p.P_next = x.Pn;
-      x.p.Q = h->Q + x.c0 * h->m_pad;
-      x.p.seed = seed;
       x.p.t = (uint32_t)t;
       x.p.gen_next = (it + 1 < n_iter) ? 1 : 0;
       x.p.record = (rec && !h->affine) ? 1 : 0;
@@ -516,6 +594,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->chain_warps = 0;
   o->streams = 0;
   o->ring = 0;
+  o->graphs = 1;
   return TMVN_OK;
 }
 
@@ -699,6 +778,10 @@ void tmvn_destroy(tmvn_handle h) {
   for (cudaEvent_t e : h->join_events) cudaEventDestroy(e);
   for (cudaStream_t s_ : h->shard_streams) cudaStreamDestroy(s_);
   if (h->fork_event) cudaEventDestroy(h->fork_event);
+  for (int i = 0; i < 2; ++i)
+    if (h->graph_exec[i]) cudaGraphExecDestroy(h->graph_exec[i]);
+  if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
+  dfree(h->d_tbase);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
   dfree(h->A_tiled); dfree(h->A_row); dfree(h->b_orig); dfree(h->b_eff);

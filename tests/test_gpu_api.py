@@ -171,3 +171,18 @@ def test_affine_change_of_variable():
     m1 = sm[0] / n
     assert abs(m1 - (2 + 2 * mu_u)) < 0.01
     assert abs(sq[0] / n - m1 * m1 - 4 * var_u) < 0.03
+
+
+def test_graph_replay_bitwise_equals_launches():
+    """CUDA-graph replay of aligned blocks (options.graphs) changes nothing."""
+    A, b, x0 = synth.make_instance(3, m=150, d=40)
+    C = 200
+    outs = []
+    for graphs in (0, 1):
+        s = tm.Sampler(A, b, burn_in=7, thin=3, graphs=graphs)
+        s.set_options(iter_offset=5)  # unaligned head, then whole blocks of 32, then a tail
+        out = s.sample(np.tile(x0, (C, 1)), 100, seed=13)
+        outs.append((out, s.moments(), s.stats()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1][0], outs[1][1][0]) and outs[0][1][2] == outs[1][1][2]
+    assert outs[0][2] == outs[1][2]

@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--projection", type=int, default=0,
+                    help="0: FP64 DMMA projection GEMM; 1: int8 Ozaki split on tcgen05 (FP64-accurate)")
     return ap.parse_args()
 
 
@@ -189,7 +191,7 @@ def main():
     offset, C = tdist.weak_shard(cfg.C, rank)  # every rank runs the workload's C chains
     stream = torch.cuda.Stream(device=dev)
     s = tm.Sampler(torch.tensor(A, device=dev), torch.tensor(b, device=dev), chain_offset=offset)
-    s.set_options(stream=stream)
+    s.set_options(stream=stream, projection=args.projection)
     X = torch.tensor(np.tile(x0, (C, 1)), device=dev)
 
     def timed_pass(steps):
@@ -267,6 +269,30 @@ def main():
                                "frac": ess_gbs / hbm, "peak_source": hbm_src, "avg_launch_ms": ess_avg_ms,
                                "share_of_step": prof["ess_ms"] / ms_iso,
                                "algorithmic_bytes_per_launch": prof["ess_bytes"] / max(1, prof["ess_launches"])}}
+    if args.projection == 1:
+        # dominant kernel: the int8 tcgen05 projection; peak = measured dense bf16 x the
+        # nominal int8 / bf16 ratio (4.5 / 2.25 PFLOP/s), sustained figure (timed inside a long step)
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        tc_avg_ms = prof["tc_ms"] / max(1, prof["tc_launches"])
+        tc_ops = prof["tc_ops"] / max(1, prof["tc_launches"])
+        tc_achieved = tc_ops / (tc_avg_ms * 1e-3) / 1e12
+        tc_peak = 2.0 * mp["bf16_tflops_sustained"]
+        dmma = dict(roofline)
+        for k in ("ess_kernel", "traffic", "traffic_source", "measured_in"):
+            dmma.pop(k, None)
+        dmma["kernel"] = "gemm_tn_f64_kernel (P = X A^T refresh every recompute_every, FP64 DMMA)"
+        roofline = {"bound": "tensor",
+                    "kernel": "ozaki_gemm_kernel (Q = N A'^T, int8 tcgen05.mma, TMEM accumulators, "
+                              f"{opts.ozaki_slices or 7} digits: FP64-accurate)",
+                    "achieved": tc_achieved, "peak": tc_peak, "unit": "TOP/s (int8)",
+                    "frac": tc_achieved / tc_peak, "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8/bf16 dense "
+                                   "ratio 4.5/2.25, B200_PROFILING.md)",
+                    "algorithmic_ops_per_launch": tc_ops,
+                    "fp64_equivalent_tflops": prof["tc_flops"] / max(1, prof["tc_launches"]) / (tc_avg_ms * 1e-3) / 1e12,
+                    "avg_launch_ms": tc_avg_ms, "share_of_step": prof["tc_ms"] / ms_iso,
+                    "measured_in": roofline["measured_in"],
+                    "refresh_gemm": dmma, "ess_kernel": roofline["ess_kernel"]}
     gpu_launches = prof_main["launches"]
 
     # ---- end to end through the public API with host buffers (pinned), rank-local
@@ -292,7 +318,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.projection == 0 else "f64+i8",
                 "data": "synthetic (seeded Gaussian polytope of BASELINE config; no dataset)",
                 "config": config_dict(cfg, args, world),
                 "chain_iters_per_s": total_iters / (ms_max * 1e-3),
@@ -300,7 +326,8 @@ def main():
                 "rejections": rej_all,
                 "recorded": n_all,
                 "options": {"streams": opts.streams, "chain_warps": opts.chain_warps,
-                            "recompute_every": opts.recompute_every, "ring": opts.ring},
+                            "recompute_every": opts.recompute_every, "ring": opts.ring,
+                            "projection": opts.projection, "ozaki_slices": opts.ozaki_slices},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": gpu_launches, "clocks": clocks}
         print(json.dumps(line), flush=True)

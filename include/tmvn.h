@@ -98,6 +98,25 @@ typedef struct {
    * multiple of it are replayed as one CUDA graph (a single shard, no profiling,
    * no x-space moment recording); 0: one launch per kernel. */
   int32_t graphs;
+  /* Projection GEMM Q = N A'^T (Alg. 1's A nu):
+   *   0 (default): FP64 on the DMMA tensor pipe (mma.sync f64; round-to-nearest
+   *      FP64 products, |Q - a.nu| <= 2 d 2^-53 sum_j |a_ij nu_j|);
+   *   1: int8 Ozaki split on the tcgen05 tensor cores (TMEM accumulators): A'
+   *      row i scaled by 2^e_i > max_j |a_ij|, nu by 2^4 (Box-Muller |nu| < 8.58),
+   *      both truncated to fixed point with 8S - 1 fraction bits and cut into S
+   *      byte digits; the S(S+1)/2 exact int8 products of digit pairs with
+   *      k + l <= S + 1 are summed in int32 per diagonal and recombined in FP64.
+   *      Stated bound:
+   *      |Q - a.nu| <= 2^(e_i + 4) d (S + 1) 2^(2 - 8S) + 2^-51 |Q|
+   *      (truncation 2^(1-F) per product with F = 8S - 1, dropped diagonals
+   *      <= (S - 1) 2^(2 - 8S) d, FP64 reconstruction; S = 7: 2^(e_i+4) d 2^-51).
+   *      Requires d <= 4096 (int32 headroom); otherwise TMVN_E_ARG.  The P
+   *      refreshes (every recompute_every) and the start check stay FP64 DMMA.
+   *      Results do not depend on C or on the sharding. */
+  int32_t projection;
+  /* Digits S of the int8 projection: 6, 7 or 8 (0 = default 7: 55-bit fixed
+   * point, 28 int8 MMAs per 32-wide K step). */
+  int32_t ozaki_slices;
 } tmvn_options;
 
 typedef struct {
@@ -114,6 +133,10 @@ typedef struct {
   int64_t ess_launches;  /* fused per-chain ESS launches timed                               */
   double ess_ms;
   double ess_bytes;      /* algorithmic HBM bytes of those launches    */
+  int64_t tc_launches;   /* hot-loop int8 tcgen05 projections timed (options.projection = 1) */
+  double tc_ms;
+  double tc_ops;         /* int8 tensor ops issued by those launches: S(S+1)/2 * 2 C m d     */
+  double tc_flops;       /* FP64-equivalent algorithmic flops of those launches: 2 C m d     */
 } tmvn_profile;
 
 /* Fills *opt with the defaults listed above. */
@@ -196,6 +219,11 @@ tmvn_status tmvn_test_arcs(const double* p, const double* q, const double* b, in
 tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t m, int64_t C,
                                 const double* u, double eps, double* seg_lo, double* seg_hi,
                                 int64_t seg_cap, int64_t* nseg, double* L, double* theta);
+/* The production int8 tcgen05 projection: out[R x S] = X[R x K] . W[S x K]^T with
+ * W's rows scaled per row, X by the power of two above max |X|, `slices` digits
+ * (6, 7, 8); K <= 4096. */
+tmvn_status tmvn_test_ozaki_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
+                                 int32_t slices, double* out);
 /* The production FP64 GEMM: out[R x S] = X[R x K] . W[S x K]^T (all row-major). */
 tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
                            double* out);

@@ -30,7 +30,8 @@ EXPORTS = ["tmvn_default_options", "tmvn_create", "tmvn_set_affine", "tmvn_set_o
            "tmvn_get_options", "tmvn_sample", "tmvn_get_stats", "tmvn_get_moments",
            "tmvn_reset_stats", "tmvn_get_profile", "tmvn_last_error", "tmvn_version",
            "tmvn_destroy", "tmvn_test_philox", "tmvn_test_curand_philox", "tmvn_test_normals", "tmvn_test_arcs",
-           "tmvn_test_intervals", "tmvn_test_gemm", "tmvn_test_step", "tmvn_test_trace"]
+           "tmvn_test_intervals", "tmvn_test_gemm", "tmvn_test_ozaki_gemm", "tmvn_test_step",
+           "tmvn_test_trace"]
 
 
 class TmvnError(RuntimeError):
@@ -46,14 +47,17 @@ class options(ctypes.Structure):
                 ("auto_advance", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int32), ("chain_warps", ctypes.c_int32),
                 ("streams", ctypes.c_int32), ("ring", ctypes.c_int32),
-                ("graphs", ctypes.c_int32)]
+                ("graphs", ctypes.c_int32), ("projection", ctypes.c_int32),
+                ("ozaki_slices", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("gemm_launches", ctypes.c_int64),
                 ("gemm_ms", ctypes.c_double), ("gemm_flops", ctypes.c_double),
                 ("ess_launches", ctypes.c_int64), ("ess_ms", ctypes.c_double),
-                ("ess_bytes", ctypes.c_double)]
+                ("ess_bytes", ctypes.c_double), ("tc_launches", ctypes.c_int64),
+                ("tc_ms", ctypes.c_double), ("tc_ops", ctypes.c_double),
+                ("tc_flops", ctypes.c_double)]
 
 
 class stats(ctypes.Structure):
@@ -101,6 +105,7 @@ def lib():
             "tmvn_test_arcs": [P, P, P, i64, P, P, P],
             "tmvn_test_intervals": [P, P, i64, i64, P, f64, P, P, i64, P, P, P],
             "tmvn_test_gemm": [P, i64, P, i64, i64, P],
+            "tmvn_test_ozaki_gemm": [P, i64, P, i64, i64, ctypes.c_int32, P],
             "tmvn_test_step": [H, P, i64, u64, i64, P],
             "tmvn_test_trace": [H, P, i64, i64, u64, P, i64, P, P],
         }
@@ -353,4 +358,15 @@ def test_gemm(X, W):
     S = W.shape[0]
     out = np.zeros((R, S))
     _check(lib().tmvn_test_gemm(_ptr(X), R, _ptr(W), S, K, _ptr(out)))
+    return out
+
+
+def test_ozaki_gemm(X, W, slices=7):
+    """X W^T through the production int8 tcgen05 projection (gemm_i8.cu)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    R, K = X.shape
+    S = W.shape[0]
+    out = np.zeros((R, S))
+    _check(lib().tmvn_test_ozaki_gemm(_ptr(X), R, _ptr(W), S, K, slices, _ptr(out)))
     return out

@@ -138,6 +138,44 @@ __device__ __forceinline__ double2 normal_pair_at(uint64_t seed, uint32_t t, uin
 }
 
 // ----------------------------------------------------------------------------
+// Digit layout of the int8 (Ozaki-split) projection operands (gemm_i8.cu).
+// A value v with |v| < 2^e becomes the fixed-point integer
+// X = trunc(v 2^(8S-1-e)), |X| < 2^(8S-1), cut into S two's-complement byte
+// digits (digit 0 signed, the rest unsigned).  Operand rows are grouped in
+// blocks of BR (128 for A', 64 for nu) and K in steps of 32 bytes; digit s of a
+// (row block, K step) is one BR x 32 slice in the UMMA canonical K-major
+// SWIZZLE_NONE layout: [k / 16 within the step][8-row group][row % 8][k % 16].
+// ----------------------------------------------------------------------------
+constexpr int kOzStepK = 32;   // K bytes per step (one tcgen05.mma kind::i8)
+constexpr int kOzNuRows = 64;  // nu rows (chains) per block = MMA N
+constexpr int kOzNuExp = 4;    // |nu| <= sqrt(-2 ln 2^-53) < 8.58 < 2^4
+
+__host__ __device__ inline int64_t oz_offset(int64_t r, int64_t k, int s, int S, int64_t KB, int BR) {
+  const int64_t blk = ((r / BR) * KB + k / kOzStepK) * S + s;
+  return blk * (int64_t)(BR * kOzStepK) + ((k % kOzStepK) / 16) * (BR / 8) * 128 +
+         ((r % BR) / 8) * 128 + (r % 8) * 16 + (k % 16);
+}
+
+__device__ __forceinline__ int64_t oz_fixed(double v, int S, int e) {
+  return __double2ll_rz(scalbn(v, 8 * S - 1 - e));
+}
+
+__device__ __forceinline__ uint32_t oz_digit(int64_t X, int s, int S) {
+  const int64_t sh = X >> (8 * (S - 1 - s));  // arithmetic shift
+  return (uint32_t)(sh & 0xFF);               // digit 0: two's-complement byte of a value in [-128, 127]
+}
+
+// The S digits of the nu pair (v0, v1) at coordinates k, k + 1 (k even) of chain r.
+__device__ __forceinline__ void oz_store_nu_pair(int8_t* Ns, int64_t r, int k, double v0, double v1,
+                                                 int S, int64_t KB) {
+  const int64_t X0 = oz_fixed(v0, S, kOzNuExp), X1 = oz_fixed(v1, S, kOzNuExp);
+  for (int s = 0; s < S; ++s) {
+    const uint16_t w = (uint16_t)(oz_digit(X0, s, S) | (oz_digit(X1, s, S) << 8));
+    *reinterpret_cast<uint16_t*>(Ns + oz_offset(r, k, s, S, KB, kOzNuRows)) = w;
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Branch-free FP64 atan2 (the libm one branches per octant and diverges inside a
 // warp).  t = min(|x|,|y|) / max(|x|,|y|) in [0, 1]; for t > tan(pi/8) the
 // identity atan(t) = pi/4 + atan((t-1)/(t+1)) folds the argument to

@@ -1080,7 +1080,11 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
         *s1 = a1;
         *s2 = a2;
       }
-      if (p.gen_next) *nr = normal_pair_at(p.seed, t_it + 1, gchain, 2 * pk, p.d);
+      if (p.gen_next) {
+        const double2 nv = normal_pair_at(p.seed, t_it + 1, gchain, 2 * pk, p.d);
+        *nr = nv;
+        if (p.Ns) oz_store_nu_pair(p.Ns, c, 2 * pk, nv.x, nv.y, p.ozS, p.ozKB);
+      }
     }
     if (g.tid == 0) {
       if (!accept) p.rej[c] += 1;

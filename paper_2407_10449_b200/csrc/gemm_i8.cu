@@ -1,0 +1,306 @@
+// gemm_i8.cu -- FP64-accurate projection Q = N A'^T on the 5th-generation tensor
+// cores (tcgen05.mma kind::i8, accumulators in TMEM), by an Ozaki-style integer
+// split (the "stated mixed-precision scheme"
+// of north_star for the O(md) matvec of P:292-293).
+//
+// Scheme.  Every operand value v is scaled by a power of two 2^e into (-1, 1)
+// (A': one exponent per constraint row, from the row's max |a|; nu: the fixed
+// 2^4, since Box-Muller output satisfies |nu| <= sqrt(-2 ln 2^-53) < 8.58) and
+// truncated to the two's-complement fixed-point integer X = trunc(v 2^(8S-1))
+// (|X| < 2^(8S-1), error < 2^-(8S-1)).  X is cut into S byte digits
+// X = d_1 2^(8(S-1)) + sum_{k>=2} d_k 2^(8(S-k)): d_1 signed (s8), d_k unsigned
+// (u8).  Then
+//     sum_j X^a_j X^nu_j = sum_{k,l} (sum_j d^a_{k,j} d^nu_{l,j}) 2^(8(2S-k-l)),
+// and the products are grouped by diagonal D = k + l: one int32 TMEM accumulator
+// per D = 2 .. S+1 collects every pair (k, l) on it (exact: |acc| < 2^31 for
+// d <= 4096).  The S(S+1)/2 int8 MMAs per K step are exact; the pairs with
+// k + l > S + 1 are dropped (weight <= 2^(-8S)).  The epilogue forms
+//     q_i = 2^(e_i + e_nu - 14) * sum_{D} acc_D 2^(-8(D-2))
+// by FP64 Horner from the least significant diagonal.  Error bound (stated in
+// include/tmvn.h, tested in tests/test_gpu_ozaki.py):
+//     |q - a.nu| <= 2^(e_i + e_nu) d (S + 1) 2^(2 - 8S) + 2^-51 |q|
+// (per product: truncation of both operands < 2^(1 - (8S-1)); dropped diagonals
+// D >= S + 2: < (S - 1) 2^(2 - 8S) per unit of d; Horner rounding), i.e.
+// FP64-class accuracy relative to max_j |a_ij| * 2^e_nu * d, independent
+// of C; the result is a deterministic function of (A', nu) (no split-K, fixed
+// reconstruction order), so chains are bitwise independent of the sharding.
+//
+// Kernel.  Persistent, one 192-thread CTA per SM (TMEM: all 512 columns).
+// Output tile: 128 constraints (MMA M, TMEM lanes) x 64 chains (MMA N); the
+// S accumulators take S x 64 TMEM columns.  K steps of 32 bytes: one stage =
+// S A' digit slices (S x 4 KB) + S nu digit slices (S x 2 KB), each a single
+// contiguous cp.async.bulk (the operands are stored pre-tiled in the UMMA
+// canonical K-major SWIZZLE_NONE layout by the slicing kernels below and by the
+// fused per-chain kernel, which writes nu's digits as it draws nu).
+//   warp 0 lane 0: producer (bulk copies into a kStages ring, mbarrier tx)
+//   warp 1 lane 0: MMA issuer (S(S+1)/2 tcgen05.mma per stage, tcgen05.commit
+//                  frees the ring slot; after the tile, commits to tmem_full)
+//   warps 2-5:     epilogue (tcgen05.ld 32x32b, FP64 Horner, coalesced stores
+//                  of Q[chain][constraint]), then arrive on tmem_empty.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace tmvn {
+
+namespace {
+
+constexpr int kOzBM = 128;        // constraints per tile (MMA M, TMEM lanes)
+constexpr int kOzBN = kOzNuRows;  // chains per tile (MMA N)
+constexpr int kOzBK = kOzStepK;   // K bytes per stage (one MMA K step for kind::i8)
+constexpr int kASlice = kOzBM * kOzBK;  // 4096 bytes
+constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
+constexpr int kOzThreads = 192;
+constexpr int kOzStages = 4;
+
+__host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
+
+// ---- tcgen05 / mbarrier wrappers -------------------------------------------
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// shared-memory matrix descriptor: K-major, no swizzle; lbo = byte stride between
+// the two 16-byte K chunks, sbo = byte stride between 8-row core-matrix groups
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // descriptor version (sm_100)
+  return d;
+}
+// instruction descriptor of kind::i8: D = s32, A/B signedness, K-major, N, M
+__host__ __device__ constexpr uint32_t idesc_i8(bool a_signed, bool b_signed) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
+         ((uint32_t)(kOzBN >> 3) << 17) | ((uint32_t)(kOzBM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(kOzThreads, 1)
+    ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
+                      const double* __restrict__ rowscale, double* __restrict__ Q, int64_t ldq,
+                      int MB, int NBt, int KB) {
+  constexpr int kStage = oz_stage_bytes(S);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kStage);
+  uint64_t* empty = full + kOzStages;
+  uint64_t* tfull = empty + kOzStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kOzStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);  // one arrive per epilogue warp
+    mbar_fence_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int tiles = MB * NBt;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int mb = tile % MB, nb = tile / MB;
+        const int8_t* ga = As + (size_t)mb * KB * S * kASlice;
+        const int8_t* gn = Ns + (size_t)nb * KB * S * kNSlice;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kOzStages;
+          if (it >= kOzStages) mbar_wait(&empty[s], ((it / kOzStages) - 1) & 1);
+          unsigned char* st = ring + s * kStage;
+          mbar_expect_tx(&full[s], kStage);
+          bulk_g2s(st, ga + (size_t)kb * S * kASlice, S * kASlice, &full[s]);
+          bulk_g2s(st + S * kASlice, gn + (size_t)kb * S * kNSlice, S * kNSlice, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      uint32_t it = 0, tcount = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
+        if (tcount > 0) {
+          mbar_wait(tempty, (tcount - 1) & 1);
+          tc_fence_after();
+        }
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kOzStages;
+          mbar_wait(&full[s], (it / kOzStages) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(ring + s * kStage);
+          const uint32_t sn = sa + S * kASlice;
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+            const uint64_t da = umma_desc(sa + i * kASlice, (kOzBM / 8) * 128, 128);
+#pragma unroll
+            for (int j = 0; j < S - i; ++j) {
+              const uint64_t dn = umma_desc(sn + j * kNSlice, (kOzBN / 8) * 128, 128);
+              const uint32_t idesc = i == 0 ? (j == 0 ? idesc_i8(true, true) : idesc_i8(true, false))
+                                            : (j == 0 ? idesc_i8(false, true) : idesc_i8(false, false));
+              umma_i8(tmem + (uint32_t)((i + j) * kOzBN), da, dn, idesc, (kb > 0 || i > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty[s]);  // ring slot free once these MMAs have read it
+        }
+        umma_commit(tfull);  // accumulators of this tile complete
+      }
+    }
+  } else {  // ---- epilogue: warps 2..5; warp w reads TMEM lanes 32 (w % 4) ..
+    const int quad = warp & 3;
+    const int row_in_tile = quad * 32 + lane;
+    uint32_t tcount = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
+      const int mb = tile % MB, nb = tile / MB;
+      const int64_t row = (int64_t)mb * kOzBM + row_in_tile;
+      const double scale = __ldg(rowscale + row);
+      mbar_wait(tfull, tcount & 1);
+      tc_fence_after();
+      double* qcol = Q + (int64_t)nb * kOzBN * ldq + row;
+#pragma unroll 1
+      for (int cc = 0; cc < kOzBN; cc += 16) {
+        int32_t acc[S][16];
+#pragma unroll
+        for (int D = 0; D < S; ++D)
+          tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(D * kOzBN + cc), acc[D]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          double h = (double)acc[S - 1][j];
+#pragma unroll
+          for (int D = S - 2; D >= 0; --D) h = __fma_rn(h, 0.00390625, (double)acc[D][j]);  // 2^-8
+          qcol[(int64_t)(cc + j) * ldq] = __dmul_rn(h, scale);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---- digit slicing ----------------------------------------------------------
+// One warp per row of a fragment-tiled FP64 matrix (R rows, d columns):
+// per_row != 0: e_r = exponent of the row's max |v| (v_max < 2^e_r), rowscale[r] =
+// 2^(e_r + e_other - 14); else e_r = e_fixed for every row.  Writes all S digits
+// of every (r, k < KB*32) (zeros beyond d).
+__global__ void oz_slice_kernel(const double* __restrict__ src, int R, int d, int64_t d_pad, int S,
+                                int KB, int BR, int per_row, int e_fixed, int e_other,
+                                int8_t* __restrict__ dst, double* __restrict__ rowscale) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= R) return;
+  const int64_t r = warp;
+  int e = e_fixed;
+  if (per_row) {
+    double mx = 0.0;
+    for (int k = lane; k < d; k += 32) mx = fmax(mx, fabs(src[tiled_offset(r, k, d_pad)]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): mx < 2^e
+    if (lane == 0) rowscale[r] = scalbn(1.0, e + e_other - 14);
+  }
+  const int K = KB * kOzBK;
+  for (int k = lane; k < K; k += 32) {
+    const int64_t X = k < d ? oz_fixed(src[tiled_offset(r, k, d_pad)], S, e) : 0;
+    for (int s = 0; s < S; ++s) dst[oz_offset(r, k, s, S, KB, BR)] = (int8_t)(uint8_t)oz_digit(X, s, S);
+  }
+}
+
+}  // namespace
+
+size_t ozaki_smem_bytes(int S) { return (size_t)kOzStages * oz_stage_bytes(S) + 256; }
+
+cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64_t d_pad, int S,
+                            int64_t KB, int BR, int per_row, int e_fixed, int e_other, int8_t* dst,
+                            double* rowscale, cudaStream_t st) {
+  if (R <= 0) return cudaSuccess;
+  const int threads = 256;
+  const int64_t blocks = (R * 32 + threads - 1) / threads;
+  oz_slice_kernel<<<(unsigned)blocks, threads, 0, st>>>(src_tiled, (int)R, (int)d, d_pad, S, (int)KB,
+                                                         BR, per_row, e_fixed, e_other, dst, rowscale);
+  return cudaGetLastError();
+}
+
+template <int S>
+static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
+                               int64_t KB, const double* rowscale, double* Q, int64_t ldq,
+                               cudaStream_t st) {
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = ozaki_smem_bytes(S);
+  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int MB = (int)(M_pad / kOzBM), NBt = (int)(N_pad / kOzBN);
+  const int tiles = MB * NBt;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  ozaki_gemm_kernel<S><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, Q, ldq, MB, NBt, (int)KB);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
+                              int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
+                              cudaStream_t st) {
+  if (M_pad % kOzBM || N_pad % kOzBN || KB < 1) return cudaErrorInvalidValue;
+  switch (S) {
+    case 6: return launch_oz_t<6>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+    case 7: return launch_oz_t<7>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+    case 8: return launch_oz_t<8>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace tmvn

@@ -11,6 +11,22 @@ size_t gemm_smem_bytes();
 cudaError_t launch_gemm_tn(const double* Xt, int64_t R_pad, const double* Wt, int64_t S_pad,
                            int64_t K_pad, double* out, int64_t ldo, cudaStream_t st);
 
+// ---- int8 Ozaki-split projection on tcgen05 (gemm_i8.cu) -------------------
+// Q[N_pad x ldq] (rows = nu rows, columns = A' rows) = Ns . As^T reconstructed in
+// FP64: As = digits of A' (M_pad rows, blocks of 128), Ns = digits of nu (N_pad
+// rows, blocks of 64), KB steps of 32 along d, S digits (6, 7 or 8);
+// rowscale[i] = 2^(e_i + e_nu - 14).
+size_t ozaki_smem_bytes(int S);
+cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
+                              int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
+                              cudaStream_t st);
+// digits of the R rows of a fragment-tiled FP64 matrix into the oz layout with BR
+// rows per block; per_row: exponent from each row's max |v| (rowscale[r] =
+// 2^(e_r + e_other - 14)), else the fixed exponent e_fixed (|v| < 2^e_fixed).
+cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64_t d_pad, int S,
+                            int64_t KB, int BR, int per_row, int e_fixed, int e_other, int8_t* dst,
+                            double* rowscale, cudaStream_t st);
+
 // ---- fused per-chain ESS kernel (ess_chain.cu) -----------------------------
 struct EssParams {
   // P (= A x_t, incremental), Q (= A nu): C_pad x ldp row-major.
@@ -33,6 +49,9 @@ struct EssParams {
   int rec_dev;      // 1: record flag computed from t (t >= burn_in, (t - burn_in) % thin == 0)
   int64_t burn_in, thin;
   int gen_next;     // 1: draw nu for t + 1 into N after the update
+  int8_t* Ns;       // non-null: also write nu_{t+1}'s S digits (int8 projection, gemm_i8.cu)
+  int ozS;
+  int64_t ozKB;
   double eps;       // S3.3 trim
   int record;       // accumulate S1 += x, S2 += x^2 into the tiled moments
   double* S1;

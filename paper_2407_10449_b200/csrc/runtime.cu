@@ -57,6 +57,14 @@ struct tmvn_ctx {
   double2* gsorted = nullptr;
   int64_t scratch_groups = 0;  // chain groups the scratch is sized for
   bool scratch_stash = false;  // gstash / gnext allocated
+  // int8 Ozaki projection (options.projection = 1, gemm_i8.cu)
+  int8_t* As = nullptr;       // digits of A' (m_pad rows), valid for ozS_A digits (0 = stale)
+  double* rowscale = nullptr; // m_pad
+  int ozS_A = 0;
+  int8_t* Ns = nullptr;       // digits of nu (C_pad rows)
+  int ozS_N = 0;
+  int64_t Ns_rows = 0;
+  int64_t ozKB = 0;
   EssLaunch plan{};
   int nshards = 1;                      // concurrent chain shards (streams)
   std::vector<cudaStream_t> shard_streams;
@@ -135,6 +143,9 @@ void free_chain_buffers(tmvn_ctx* h) {
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
   dfree(h->stage); dfree(h->stage2); dfree(h->rej);
   dfree(h->gstash); dfree(h->ggaps); dfree(h->gsorted);
+  dfree(h->Ns);
+  h->Ns_rows = 0;
+  h->ozS_N = 0;
   h->C_cap = h->C_pad = 0;
 }
 
@@ -202,6 +213,57 @@ tmvn_status ensure_affine_moments(tmvn_ctx* h) {
   return TMVN_OK;
 }
 
+bool use_oz(const tmvn_ctx* h) { return h->opt.projection == 1; }
+int oz_slices(const tmvn_ctx* h) { return h->opt.ozaki_slices ? h->opt.ozaki_slices : 7; }
+
+// Digits of A' (once per A' and digit count) and the nu digit buffer (per C_pad).
+tmvn_status ensure_ozaki(tmvn_ctx* h) {
+  if (!use_oz(h)) return TMVN_OK;
+  const int S = oz_slices(h);
+  const int64_t KB = (h->d + kOzStepK - 1) / kOzStepK;
+  cudaStream_t st = stream_of(h);
+  if (h->ozS_A != S || h->ozKB != KB) {
+    dfree(h->As);
+    if (!h->rowscale) CK(h, dalloc(&h->rowscale, (size_t)h->m_pad));
+    CK(h, dalloc(&h->As, (size_t)h->m_pad * KB * kOzStepK * S));
+    KL(h, launch_oz_slice(h->At, h->m_pad, h->d, h->d_pad, S, KB, 128, 1, 0, kOzNuExp, h->As,
+                          h->rowscale, st));
+    h->ozS_A = S;
+    h->ozKB = KB;
+  }
+  if (h->ozS_N != S || h->Ns_rows < h->C_pad) {
+    dfree(h->Ns);
+    CK(h, dalloc(&h->Ns, (size_t)h->C_pad * KB * kOzStepK * S));
+    h->ozS_N = S;
+    h->Ns_rows = h->C_pad;
+  }
+  return TMVN_OK;
+}
+
+int8_t* oz_rows(const tmvn_ctx* h, int64_t c0) {
+  return h->Ns + (c0 / kOzNuRows) * h->ozKB * kOzStepK * oz_slices(h) * kOzNuRows;
+}
+
+// Q rows [c0, c0 + Rp) = nu A'^T by the configured projection.
+cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStream_t st) {
+  if (use_oz(h))
+    return launch_ozaki_gemm(h->As, h->m_pad, oz_rows(h, c0), Rp, h->ozKB, oz_slices(h), h->rowscale,
+                             h->Q + c0 * h->m_pad, h->m_pad, st);
+  return launch_gemm_tn(h->N + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad, h->Q + c0 * h->m_pad,
+                        h->m_pad, st);
+}
+
+// nu of iteration t for chains [0, C) (and its digits for the int8 projection).
+cudaError_t launch_first_nu(tmvn_ctx* h, int64_t C, uint64_t seed, uint32_t t, cudaStream_t st) {
+  cudaError_t e = launch_normals(h->N, (int)C, (int)h->d, h->d_pad, seed, t,
+                                 (uint32_t)h->opt.chain_offset, st);
+  h->prof.launches += 1;
+  if (e != cudaSuccess || !use_oz(h)) return e;
+  h->prof.launches += 1;
+  return launch_oz_slice(h->N, C, h->d, h->d_pad, oz_slices(h), h->ozKB, kOzNuRows, 0, kOzNuExp, 0,
+                         h->Ns, nullptr, st);
+}
+
 bool finite_all(const std::vector<double>& v) {
   for (double x : v)
     if (!std::isfinite(x)) return false;
@@ -233,6 +295,9 @@ EssParams base_params(tmvn_ctx* h, int C) {
   p.W = h->plan.W;
   p.CH = h->plan.CH;
   p.stash_smem = h->plan.stash_smem;
+  p.Ns = use_oz(h) ? h->Ns : nullptr;
+  p.ozS = oz_slices(h);
+  p.ozKB = h->ozKB;
   return p;
 }
 
@@ -310,7 +375,7 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
   std::memcpy(sig.data(), &p, sizeof(EssParams));
   std::memcpy(sig.data() + sizeof(EssParams), &C, sizeof(int64_t));
   std::memcpy(sig.data() + sizeof(EssParams) + 8, &K, sizeof(int64_t));
-  const void* ptrs[2] = {h->At, h->Q};
+  const void* ptrs[2] = {use_oz(h) ? (const void*)h->As : (const void*)h->At, h->Q};
   std::memcpy(sig.data() + sizeof(EssParams) + 16, ptrs, sizeof(ptrs));
   if (h->graph_exec[parity] && h->graph_sig[parity] == sig) {
     *out = h->graph_exec[parity];
@@ -327,7 +392,7 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
   cudaError_t err = cudaSuccess;
   double *pc = Pc, *pn = Pn;
   for (int64_t i = 0; i < K && err == cudaSuccess; ++i) {
-    err = launch_gemm_tn(h->N, Rp, h->At, h->m_pad, h->d_pad, h->Q, h->m_pad, cs);
+    err = launch_projection(h, 0, Rp, cs);
     if (err != cudaSuccess) break;
     p.t = (uint32_t)i;
     p.P_cur = pc;
@@ -359,8 +424,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
   const int64_t t0 = h->opt.iter_offset;
   const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
   double* P_next = (P_cur == h->P0) ? h->P1 : h->P0;
-  KL(h, launch_normals(h->N, (int)C, (int)h->d, h->d_pad, seed, (uint32_t)t0,
-                       (uint32_t)h->opt.chain_offset, st));
+  CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st));
   // ---- shards
   int S = h->nshards;
   const int64_t per = round_up((C + S - 1) / S, kTileR);
@@ -380,6 +444,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p = base_params(h, (int)x.C);
     x.p.X = h->X + x.c0 * h->d_pad;
     x.p.N = h->N + x.c0 * h->d_pad;
+    if (x.p.Ns) x.p.Ns = oz_rows(h, x.c0);
     x.p.S1 = h->S1 + x.c0 * h->d_pad;
     x.p.S2 = h->S2 + x.c0 * h->d_pad;
     x.p.rej = h->rej + x.c0;
@@ -441,8 +506,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     for (int s = 0; s < S; ++s) {
       Shard& x = sh[s];
       const int64_t Rp = round_up(x.C, kTileR);
-      TIMED(0, x.C, x.st, launch_gemm_tn(x.p.N, Rp, h->At, h->m_pad, h->d_pad, h->Q + x.c0 * h->m_pad,
-                                         h->m_pad, x.st));
+      TIMED(use_oz(h) ? 2 : 0, x.C, x.st, launch_projection(h, x.c0, Rp, x.st));
       x.p.P_cur = x.Pc;
       x.p.P_next = x.Pn;
       x.p.t = (uint32_t)t;
@@ -479,7 +543,13 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
       float ms = 0.f;
       CK(h, cudaEventElapsedTime(&ms, h->events[2 * k], h->events[2 * k + 1]));
       const double nC = (double)kind_C[k];
-      if (kinds[k] == 0) {
+      if (kinds[k] == 2) {
+        const double S = oz_slices(h);
+        h->prof.tc_launches += 1;
+        h->prof.tc_ms += ms;
+        h->prof.tc_flops += 2.0 * nC * (double)h->m * (double)h->d;
+        h->prof.tc_ops += S * (S + 1) / 2 * 2.0 * nC * (double)h->m * (double)h->d;
+      } else if (kinds[k] == 0) {
         h->prof.gemm_launches += 1;
         h->prof.gemm_ms += ms;
         h->prof.gemm_flops += 2.0 * nC * (double)h->m * (double)h->d;
@@ -595,10 +665,12 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->streams = 0;
   o->ring = 0;
   o->graphs = 1;
+  o->projection = 0;
+  o->ozaki_slices = 0;
   return TMVN_OK;
 }
 
-const char* tmvn_version(void) { return "tmvn-b200 0.1 (sm_100a, FP64 DMMA)"; }
+const char* tmvn_version(void) { return "tmvn-b200 0.2 (sm_100a, FP64 DMMA + int8 tcgen05 Ozaki)"; }
 
 const char* tmvn_last_error(tmvn_handle h) { return h ? h->err.c_str() : g_create_error.c_str(); }
 
@@ -666,6 +738,7 @@ tmvn_status tmvn_set_affine(tmvn_handle h, const double* mu, const double* L) {
     CK(h, cudaMemcpy(h->b_eff, h->b_orig, m * sizeof(double), cudaMemcpyDeviceToDevice));
     dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
     h->affine = false;
+    h->ozS_A = 0;
     return TMVN_OK;
   }
   std::vector<double> hmu = mu ? to_host(mu, d) : std::vector<double>(d, 0.0);
@@ -701,6 +774,7 @@ tmvn_status tmvn_set_affine(tmvn_handle h, const double* mu, const double* L) {
   CK(h, cudaStreamSynchronize(st));
   dfree(LT); dfree(LTt); dfree(Aprime);
   h->affine = true;
+  h->ozS_A = 0;  // A' changed: digits stale
   dfree(h->S1x); dfree(h->S2x);
   return TMVN_OK;
 }
@@ -713,6 +787,11 @@ tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* o) {
   if (o->chain_warps != 0 && o->chain_warps != 1 && o->chain_warps != 2 && o->chain_warps != 4 &&
       o->chain_warps != 8)
     return fail(h, TMVN_E_ARG, "chain_warps must be 0, 1, 2, 4 or 8");
+  if (o->projection != 0 && o->projection != 1) return fail(h, TMVN_E_ARG, "projection must be 0 or 1");
+  if (o->ozaki_slices != 0 && (o->ozaki_slices < 6 || o->ozaki_slices > 8))
+    return fail(h, TMVN_E_ARG, "ozaki_slices must be 0, 6, 7 or 8");
+  if (o->projection == 1 && h->d > 4096)
+    return fail(h, TMVN_E_ARG, "projection = 1 (int8 tcgen05) needs d <= 4096 (int32 accumulator headroom)");
   h->opt = *o;
   return TMVN_OK;
 }
@@ -730,6 +809,7 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = set_device(h)) != TMVN_OK) return s;
   if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
   if ((s = plan_ess(h, C)) != TMVN_OK) return s;
+  if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
   if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;
   if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
@@ -787,6 +867,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->A_tiled); dfree(h->A_row); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
+  dfree(h->As); dfree(h->rowscale);
   delete h;
 }
 
@@ -933,6 +1014,34 @@ tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t 
   return TMVN_OK;
 }
 
+tmvn_status tmvn_test_ozaki_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
+                                 int32_t slices, double* out) {
+  if (!X || !W || !out || R < 1 || S < 1 || K < 1 || K > 4096 || slices < 6 || slices > 8)
+    return fail(nullptr, TMVN_E_ARG, "bad args");
+  const int64_t Rp = round_up(R, kTileR), Sp = round_up(S, kTileR), Kp = round_up(K, kTileK);
+  const int64_t KB = (K + kOzStepK - 1) / kOzStepK;
+  std::vector<double> hx = to_host(X, (size_t)R * K);
+  double mx = 0.0;
+  for (double v : hx) mx = std::max(mx, std::fabs(v));
+  int ex = 0;
+  if (mx > 0.0) std::frexp(mx, &ex);  // max |X| < 2^ex
+  Tmp<double> dx, dw, xt, wt, o, rs;
+  Tmp<int8_t> xs, ws;
+  TCK(tmp_in(dx, hx.data(), (size_t)R * K)); TCK(tmp_in(dw, W, (size_t)S * K));
+  TCK(tmp_in(xt, (const double*)nullptr, (size_t)Rp * Kp)); TCK(tmp_in(wt, (const double*)nullptr, (size_t)Sp * Kp));
+  TCK(tmp_in(o, (const double*)nullptr, (size_t)Rp * Sp)); TCK(tmp_in(rs, (const double*)nullptr, (size_t)Sp));
+  TCK(tmp_in(xs, (const int8_t*)nullptr, (size_t)Rp * KB * kOzStepK * slices));
+  TCK(tmp_in(ws, (const int8_t*)nullptr, (size_t)Sp * KB * kOzStepK * slices));
+  TCK(launch_pack(dx.p, R, K, K, xt.p, Kp, 0));
+  TCK(launch_pack(dw.p, S, K, K, wt.p, Kp, 0));
+  TCK(launch_oz_slice(wt.p, Sp, K, Kp, slices, KB, 128, 1, 0, ex, ws.p, rs.p, 0));
+  TCK(launch_oz_slice(xt.p, Rp, K, Kp, slices, KB, kOzNuRows, 0, ex, 0, xs.p, nullptr, 0));
+  TCK(launch_ozaki_gemm(ws.p, Sp, xs.p, Rp, KB, slices, rs.p, o.p, Sp, 0));
+  TCK(cudaDeviceSynchronize());
+  TCK(cudaMemcpy2D(out, S * sizeof(double), o.p, Sp * sizeof(double), S * sizeof(double), R, cudaMemcpyDefault));
+  return TMVN_OK;
+}
+
 tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t seed, int64_t t,
                            tmvn_step_dump* dump) {
   if (!h || !Xt || C < 1 || t < 0 || t >= ((int64_t)1 << 32) || !dump) return fail(h, TMVN_E_ARG, "bad args");
@@ -940,6 +1049,7 @@ tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t 
   if ((s = set_device(h)) != TMVN_OK) return s;
   if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
   if ((s = plan_ess(h, C)) != TMVN_OK) return s;
+  if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
   cudaStream_t st = stream_of(h);
   const int64_t m = h->m, d = h->d;
   const int grid = h->plan.grid;
@@ -947,8 +1057,8 @@ tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t 
   CK(h, cudaMemcpyAsync(h->stage, Xt, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
   CK(h, launch_pack(h->stage, C, d, d, h->X, h->d_pad, st));
   CK(h, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, h->P0, h->m_pad, st));
-  CK(h, launch_normals(h->N, (int)C, (int)d, h->d_pad, seed, (uint32_t)t, (uint32_t)h->opt.chain_offset, st));
-  CK(h, launch_gemm_tn(h->N, h->C_pad, h->At, h->m_pad, h->d_pad, h->Q, h->m_pad, st));
+  CK(h, launch_first_nu(h, C, seed, (uint32_t)t, st));
+  CK(h, launch_projection(h, 0, h->C_pad, st));
   CK(h, cudaMemsetAsync(h->rej, 0, (size_t)h->C_pad * sizeof(int64_t), st));
   const size_t cm = (size_t)C * m;
   const int64_t cap = dump->seg_cap > 0 ? dump->seg_cap : 0;
@@ -1026,6 +1136,7 @@ tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t 
   s = plan_ess(h, C);
   h->trace_dev = nullptr;
   if (s != TMVN_OK) return s;
+  if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
   Tmp<int64_t> rows;
   Tmp<double> tr;
   CK(h, tmp_in(rows, chains, (size_t)n_trace));

@@ -56,6 +56,8 @@ def test_library_is_sm100a_only():
     sass = subprocess.run(["cuobjdump", "-sass", tm.LIB_PATH], capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in sass      # FP64 tensor-core path
     assert "UBLKCP" in sass          # bulk-copy (TMA engine) operand feed
+    assert "UTCIMMA" in sass         # tcgen05.mma kind::i8 (int8 Ozaki projection)
+    assert "LDTM" in sass            # tcgen05.ld of the TMEM accumulators
 
 
 def test_product_never_touches_the_oracle():

@@ -19,7 +19,14 @@ pytestmark = pytest.mark.gpu
 REL = 1e-10
 
 
-def compare_step(A, b, X, g, seed, t, chains, chain_offset=0, log=None):
+def ozaki_qbound(A, q, slices=7):
+    """Stated bound of the int8 tcgen05 projection (include/tmvn.h, options.projection = 1)."""
+    m, d = A.shape
+    e = np.frexp(np.max(np.abs(A), axis=1))[1].astype(np.float64)  # max_j |a_ij| < 2^e_i
+    return 2.0 ** (e + 4) * d * (slices + 1) * 2.0 ** (2 - 8 * slices) + 2.0**-51 * np.abs(q)
+
+
+def compare_step(A, b, X, g, seed, t, chains, chain_offset=0, log=None, projection=0):
     """Compare GPU dump g (from tm.Sampler.test_step) with oracle.step on `chains`."""
     m, d = A.shape
     exempt = 0
@@ -32,6 +39,8 @@ def compare_step(A, b, X, g, seed, t, chains, chain_offset=0, log=None):
         # P2: projections within the dot-product rounding bound
         bp = 2 * d * 2.0**-53 * (np.abs(A) @ np.abs(x)) + 1e-300
         bq = 2 * d * 2.0**-53 * (np.abs(A) @ np.abs(o["nu"])) + 1e-300
+        if projection == 1:
+            bq = ozaki_qbound(A, o["q"]) / 2 + 1e-300  # asserted against 2 bq below
         assert np.all(np.abs(g["p"][c] - o["p"]) <= 2 * bp)
         assert np.all(np.abs(g["q"][c] - o["q"]) <= 2 * bq)
         # P3: arcs

@@ -99,8 +99,7 @@ typedef struct {
    * no x-space moment recording); 0: one launch per kernel. */
   int32_t graphs;
   /* Projection GEMM Q = N A'^T (Alg. 1's A nu):
-   *   0 (default): FP64 on the DMMA tensor pipe (mma.sync f64; round-to-nearest
-   *      FP64 products, |Q - a.nu| <= 2 d 2^-53 sum_j |a_ij nu_j|);
+   *   0 (default): automatic = 1 when d <= 4096, else 2;
    *   1: int8 Ozaki split on the tcgen05 tensor cores (TMEM accumulators): A'
    *      row i scaled by 2^e_i > max_j |a_ij|, nu by 2^4 (Box-Muller |nu| < 8.58),
    *      both truncated to fixed point with 8S - 1 fraction bits and cut into S
@@ -110,9 +109,11 @@ typedef struct {
    *      |Q - a.nu| <= 2^(e_i + 4) d (S + 1) 2^(2 - 8S) + 2^-51 |Q|
    *      (truncation 2^(1-F) per product with F = 8S - 1, dropped diagonals
    *      <= (S - 1) 2^(2 - 8S) d, FP64 reconstruction; S = 7: 2^(e_i+4) d 2^-51).
-   *      Requires d <= 4096 (int32 headroom); otherwise TMVN_E_ARG.  The P
-   *      refreshes (every recompute_every) and the start check stay FP64 DMMA.
-   *      Results do not depend on C or on the sharding. */
+   *      Requires d <= 4096 (int32 headroom); otherwise TMVN_E_ARG.
+   *   2: FP64 on the DMMA tensor pipe (mma.sync f64; round-to-nearest FP64
+   *      products, |Q - a.nu| <= 2 d 2^-53 sum_j |a_ij nu_j|).
+   * The P refreshes (every recompute_every) and the start check are always FP64
+   * DMMA.  Results do not depend on C or on the sharding. */
   int32_t projection;
   /* Digits S of the int8 projection: 6, 7 or 8 (0 = default 7: 55-bit fixed
    * point, 28 int8 MMAs per 32-wide K step). */

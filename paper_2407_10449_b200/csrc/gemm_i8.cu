@@ -53,9 +53,11 @@ constexpr int kOzBK = kOzStepK;   // K bytes per stage (one MMA K step for kind:
 constexpr int kASlice = kOzBM * kOzBK;  // 4096 bytes
 constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
 constexpr int kOzThreads = 192;
-constexpr int kOzStages = 4;
-
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
+// ring depth: as many stages as fit in 226 KB of shared memory (S = 6: 6, 7: 5, 8: 4)
+__host__ __device__ constexpr int oz_stages(int S) {
+  return (226 * 1024) / oz_stage_bytes(S) > 6 ? 6 : (226 * 1024) / oz_stage_bytes(S);
+}
 
 // ---- tcgen05 / mbarrier wrappers -------------------------------------------
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -82,13 +84,6 @@ __host__ __device__ constexpr uint32_t idesc_i8(bool a_signed, bool b_signed) {
   return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
          ((uint32_t)(kOzBN >> 3) << 17) | ((uint32_t)(kOzBM >> 4) << 24);
 }
-__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
-                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
-}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -107,12 +102,75 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// All S(S+1)/2 digit-pair MMAs of one K step: A' digit i x nu digit j into the
+// accumulator of diagonal i + j (TMEM columns (i + j) * 64; the allocation of all
+// 512 columns starts at column 0).  Every operand is a compile-time constant or a
+// warp-uniform descriptor, so the issue is a plain sequence of UTCIMMA.  FIRST:
+// the first K step of a tile, where pair (0, j) initialises accumulator j.
+template <int I, int J, int S, bool FIRST>
+struct PairMma {
+  static __device__ __forceinline__ void run(uint64_t da, uint64_t dn) {
+    constexpr uint32_t idesc = idesc_i8(I == 0, J == 0);
+    constexpr uint32_t acc = (FIRST && I == 0) ? 0u : 1u;
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"((uint32_t)((I + J) * kOzBN)),
+        "l"(da + (uint64_t)((I * kASlice) >> 4)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc),
+        "n"(acc));
+    if constexpr (J + 1 < S - I) PairMma<I, J + 1, S, FIRST>::run(da, dn);
+    else if constexpr (I + 1 < S) PairMma<I + 1, 0, S, FIRST>::run(da, dn);
+  }
+};
+// TS variant (S <= 7): shared-memory operand reads bound an SS-mode M=128 N=64
+// int8 MMA at 48 cycles (6 KB per MMA at 128 B/cycle; tools/tc_rate.cu measured
+// 48.0 SS vs 32.0 with A in TMEM), so the A' digit slices of a K step are first
+// copied into TMEM (tcgen05.cp 128x256b: slice i -> columns 64 S + 8 i, i.e. one
+// 32-byte K step per lane = row) and the MMAs read A from there.  tcgen05.cp and
+// tcgen05.mma issued by one thread execute in issue order, so a slice is not
+// overwritten before the previous step's MMAs have read it.
+template <int I, int J, int S, bool FIRST>
+struct PairMmaTS {
+  static __device__ __forceinline__ void run(uint64_t dn) {
+    constexpr uint32_t idesc = idesc_i8(I == 0, J == 0);
+    constexpr uint32_t acc = (FIRST && I == 0) ? 0u : 1u;
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"((uint32_t)((I + J) * kOzBN)),
+        "r"((uint32_t)(S * kOzBN + 8 * I)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc), "n"(acc));
+    if constexpr (J + 1 < S - I) PairMmaTS<I, J + 1, S, FIRST>::run(dn);
+    else if constexpr (I + 1 < S) PairMmaTS<I + 1, 0, S, FIRST>::run(dn);
+  }
+};
+template <int I, int S>
+struct CopyA {
+  static __device__ __forceinline__ void run(uint64_t da) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"((uint32_t)(S * kOzBN + 8 * I)),
+        "l"(da + (uint64_t)((I * kASlice) >> 4)));
+    if constexpr (I + 1 < S) CopyA<I + 1, S>::run(da);
+  }
+};
+template <int S>
+__host__ __device__ constexpr bool oz_ts() { return S * kOzBN + 8 * S <= 512; }
+
+template <int S, bool FIRST>
+__device__ __forceinline__ void issue_stage(uint64_t da, uint64_t dn) {
+  if constexpr (oz_ts<S>()) {
+    CopyA<0, S>::run(da);
+    PairMmaTS<0, 0, S, FIRST>::run(dn);
+  } else {
+    PairMma<0, 0, S, FIRST>::run(da, dn);
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
                       const double* __restrict__ rowscale, double* __restrict__ Q, int64_t ldq,
                       int MB, int NBt, int KB) {
   constexpr int kStage = oz_stage_bytes(S);
+  constexpr int kOzStages = oz_stages(S);
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kStage);
@@ -140,6 +198,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tmem != 0) __trap();  // all 512 columns: the allocation starts at lane 0, column 0
   const int tiles = MB * NBt;
 
   if (warp == 0) {
@@ -160,7 +219,11 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    {  // ---- MMA issuer: the whole warp runs the loop, one elected lane issues
+      // descriptors of stage 0; a stage / slice offset is a constant add to the
+      // 14-bit address field (ring < 256 KB: no carry)
+      const uint64_t dA0 = umma_desc(smem_u32(ring), (kOzBM / 8) * 128, 128);
+      const uint64_t dN0 = umma_desc(smem_u32(ring) + S * kASlice, (kOzBN / 8) * 128, 128);
       uint32_t it = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
         if (tcount > 0) {
@@ -171,22 +234,14 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           const int s = it % kOzStages;
           mbar_wait(&full[s], (it / kOzStages) & 1);
           tc_fence_after();
-          const uint32_t sa = smem_u32(ring + s * kStage);
-          const uint32_t sn = sa + S * kASlice;
-#pragma unroll
-          for (int i = 0; i < S; ++i) {
-            const uint64_t da = umma_desc(sa + i * kASlice, (kOzBM / 8) * 128, 128);
-#pragma unroll
-            for (int j = 0; j < S - i; ++j) {
-              const uint64_t dn = umma_desc(sn + j * kNSlice, (kOzBN / 8) * 128, 128);
-              const uint32_t idesc = i == 0 ? (j == 0 ? idesc_i8(true, true) : idesc_i8(true, false))
-                                            : (j == 0 ? idesc_i8(false, true) : idesc_i8(false, false));
-              umma_i8(tmem + (uint32_t)((i + j) * kOzBN), da, dn, idesc, (kb > 0 || i > 0) ? 1u : 0u);
-            }
-          }
-          umma_commit(&empty[s]);  // ring slot free once these MMAs have read it
+          const uint64_t so = (uint64_t)((s * kStage) >> 4);
+          if (kb == 0) issue_stage<S, true>(dA0 + so, dN0 + so);
+          else issue_stage<S, false>(dA0 + so, dN0 + so);
+          if (lane == 0) umma_commit(&empty[s]);  // ring slot free once these MMAs have read it
+          __syncwarp();
         }
-        umma_commit(tfull);  // accumulators of this tile complete
+        if (lane == 0) umma_commit(tfull);  // accumulators of this tile complete
+        __syncwarp();
       }
     }
   } else {  // ---- epilogue: warps 2..5; warp w reads TMEM lanes 32 (w % 4) ..
@@ -257,7 +312,7 @@ __global__ void oz_slice_kernel(const double* __restrict__ src, int R, int d, in
 
 }  // namespace
 
-size_t ozaki_smem_bytes(int S) { return (size_t)kOzStages * oz_stage_bytes(S) + 256; }
+size_t ozaki_smem_bytes(int S) { return (size_t)oz_stages(S) * oz_stage_bytes(S) + 256; }
 
 cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64_t d_pad, int S,
                             int64_t KB, int BR, int per_row, int e_fixed, int e_other, int8_t* dst,

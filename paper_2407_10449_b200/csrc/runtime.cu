@@ -213,7 +213,9 @@ tmvn_status ensure_affine_moments(tmvn_ctx* h) {
   return TMVN_OK;
 }
 
-bool use_oz(const tmvn_ctx* h) { return h->opt.projection == 1; }
+bool use_oz(const tmvn_ctx* h) {
+  return h->opt.projection == 1 || (h->opt.projection == 0 && h->d <= 4096);
+}
 int oz_slices(const tmvn_ctx* h) { return h->opt.ozaki_slices ? h->opt.ozaki_slices : 7; }
 
 // Digits of A' (once per A' and digit count) and the nu digit buffer (per C_pad).
@@ -787,7 +789,7 @@ tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* o) {
   if (o->chain_warps != 0 && o->chain_warps != 1 && o->chain_warps != 2 && o->chain_warps != 4 &&
       o->chain_warps != 8)
     return fail(h, TMVN_E_ARG, "chain_warps must be 0, 1, 2, 4 or 8");
-  if (o->projection != 0 && o->projection != 1) return fail(h, TMVN_E_ARG, "projection must be 0 or 1");
+  if (o->projection < 0 || o->projection > 2) return fail(h, TMVN_E_ARG, "projection must be 0, 1 or 2");
   if (o->ozaki_slices != 0 && (o->ozaki_slices < 6 || o->ozaki_slices > 8))
     return fail(h, TMVN_E_ARG, "ozaki_slices must be 0, 6, 7 or 8");
   if (o->projection == 1 && h->d > 4096)

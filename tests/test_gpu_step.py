@@ -26,8 +26,8 @@ def ozaki_qbound(A, q, slices=7):
     return 2.0 ** (e + 4) * d * (slices + 1) * 2.0 ** (2 - 8 * slices) + 2.0**-51 * np.abs(q)
 
 
-def compare_step(A, b, X, g, seed, t, chains, chain_offset=0, log=None, projection=0):
-    """Compare GPU dump g (from tm.Sampler.test_step) with oracle.step on `chains`."""
+def compare_step(A, b, X, g, seed, t, chains, chain_offset=0, log=None, projection=2):
+    """projection: 2 = FP64 DMMA bound on q (P2), 1 = the int8 projection's stated bound."""
     m, d = A.shape
     exempt = 0
     for c in chains:
@@ -93,14 +93,15 @@ SMALL = {
 }
 
 
+@pytest.mark.parametrize("projection", [2, 1])
 @pytest.mark.parametrize("name", list(SMALL))
-def test_step_parity_from_start_and_along_oracle_path(name):
+def test_step_parity_from_start_and_along_oracle_path(name, projection):
     k, kw = SMALL[name]
     A, b, x0 = synth.make_instance(k, **kw)
     m, d = A.shape
     C = {1: 16, 2: 130, 3: 131, 4: 37, 5: 129}[k]
     cfg = synth.CONFIGS[k]
-    s = tm.Sampler(A, b)
+    s = tm.Sampler(A, b, projection=projection)
     rng = np.random.default_rng(k)
     # interior points: x0, and points reached by oracle chains (stationary-ish)
     X = np.tile(x0, (C, 1))
@@ -110,7 +111,7 @@ def test_step_parity_from_start_and_along_oracle_path(name):
     for t in (0, 5, 123456):
         g = s.test_step(X, cfg.chain_seed, t, seg_cap=64)
         chains = rng.choice(C, size=min(C, 24), replace=False)
-        ex = compare_step(A, b, X, g, cfg.chain_seed, t, chains, log=log)
+        ex = compare_step(A, b, X, g, cfg.chain_seed, t, chains, log=log, projection=projection)
         assert ex <= 2, log
         X = np.where(g["accept"][:, None], g["x_next"], X)
     s.close()
@@ -122,7 +123,7 @@ def test_trace_production_loop_parity():
     m, d = A.shape
     C, T = 200, 70
     for K in (32, 1):
-        s = tm.Sampler(A, b, recompute_every=K)
+        s = tm.Sampler(A, b, recompute_every=K, projection=2)
         chains = np.array([0, 1, 57, 128, 199])
         trace, out = s.test_trace(np.tile(x0, (C, 1)), T, seed=103, chains=chains)
         assert np.array_equal(trace[-1], out[chains])
@@ -146,7 +147,7 @@ def test_full_size_config3_sampled():
     """BASELINE config 3 at full size (d=1000, m=2000, C=4096) in the bench launch config."""
     A, b, x0 = synth.make_instance(3)
     C = 4096
-    s = tm.Sampler(A, b)
+    s = tm.Sampler(A, b, projection=2)
     X = s.sample(np.tile(x0, (C, 1)), 20, seed=103)
     assert s.stats()["rejections"] == 0
     g = s.test_step(X, 103, 20, seg_cap=64)
@@ -161,9 +162,10 @@ def test_full_size_config4_sampled():
     """BASELINE config 4 (m=100000, sort-bound; arcs spill to global scratch)."""
     A, b, x0 = synth.make_instance(4)
     C = 1024
-    s = tm.Sampler(A, b)
-    X = s.sample(np.tile(x0, (C, 1)), 5, seed=104)
-    g = s.test_step(X, 104, 5, seg_cap=64)
-    log = []
-    assert compare_step(A, b, X, g, 104, 5, [0, 511, 1023], log=log) <= 1, log
-    s.close()
+    for projection in (2, 1):
+        s = tm.Sampler(A, b, projection=projection)
+        X = s.sample(np.tile(x0, (C, 1)), 5, seed=104)
+        g = s.test_step(X, 104, 5, seg_cap=64)
+        log = []
+        assert compare_step(A, b, X, g, 104, 5, [0, 511, 1023], log=log, projection=projection) <= 1, log
+        s.close()

@@ -28,10 +28,21 @@ clean:
 # profiling variant (tools/phase_timing.py), never loaded by the product path
 build/timing/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p build/timing
-	$(NVCC) $(NVFLAGS) -DTMVN_PHASE_TIMING -c $< -o $@ 2> /dev/null
+	$(NVCC) $(NVFLAGS) -DTMVN_PHASE_TIMING -c $< -o $@ 2> build/timing/$*.log || (cat build/timing/$*.log; false)
 
 build/libtmvn_timing.so: $(patsubst $(CSRC)/%.cu,build/timing/%.o,$(SRCS))
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
 
 timing: build/libtmvn_timing.so
 .PHONY: timing
+
+# A/B variants of the library (tools/ab_time.py): make variant TAG=x VFLAGS="-D..."
+build/var_$(TAG)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build/var_$(TAG)
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $< -o $@ 2> build/var_$(TAG)/$*.log || (cat build/var_$(TAG)/$*.log; false)
+
+build/libtmvn_$(TAG).so: $(patsubst $(CSRC)/%.cu,build/var_$(TAG)/%.o,$(SRCS))
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
+
+variant: build/libtmvn_$(TAG).so
+.PHONY: variant

@@ -164,6 +164,18 @@ __device__ __forceinline__ void issue_stage(uint64_t da, uint64_t dn) {
   }
 }
 
+// Role timing (timing build -DTMVN_PHASE_TIMING only; tools/oz_timing.py):
+// [0] MMA wait full, [1] MMA wait tmem_empty, [2] MMA issue, [3] epilogue wait
+// tmem_full, [4] epilogue work, [5] producer wait empty, [6] tiles, [7] CTA cycles
+#ifdef TMVN_PHASE_TIMING
+__device__ unsigned long long g_oz_cycles[8];
+#define OZT(var) const long long var = clock64()
+#define OZADD(i, v) atomicAdd(&g_oz_cycles[i], (unsigned long long)(v))
+#else
+#define OZT(var)
+#define OZADD(i, v)
+#endif
+
 template <int S>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
@@ -200,6 +212,10 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (tmem != 0) __trap();  // all 512 columns: the allocation starts at lane 0, column 0
   const int tiles = MB * NBt;
+  OZT(t_start);
+#ifdef TMVN_PHASE_TIMING
+  long long acc0 = 0, acc1 = 0, acc2 = 0;
+#endif
 
   if (warp == 0) {
     if (lane == 0) {  // ---- producer
@@ -210,7 +226,12 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         const int8_t* gn = Ns + (size_t)nb * KB * S * kNSlice;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % kOzStages;
+          OZT(w0);
           if (it >= kOzStages) mbar_wait(&empty[s], ((it / kOzStages) - 1) & 1);
+          OZT(w1);
+#ifdef TMVN_PHASE_TIMING
+          acc0 += w1 - w0;
+#endif
           unsigned char* st = ring + s * kStage;
           mbar_expect_tx(&full[s], kStage);
           bulk_g2s(st, ga + (size_t)kb * S * kASlice, S * kASlice, &full[s]);
@@ -226,19 +247,32 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       const uint64_t dN0 = umma_desc(smem_u32(ring) + S * kASlice, (kOzBN / 8) * 128, 128);
       uint32_t it = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
+        OZT(e0);
         if (tcount > 0) {
           mbar_wait(tempty, (tcount - 1) & 1);
           tc_fence_after();
         }
+        OZT(e1);
+#ifdef TMVN_PHASE_TIMING
+        acc1 += e1 - e0;
+#endif
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % kOzStages;
+          OZT(f0);
           mbar_wait(&full[s], (it / kOzStages) & 1);
           tc_fence_after();
+          OZT(f1);
+#ifdef TMVN_PHASE_TIMING
+          acc0 += f1 - f0;
+#endif
           const uint64_t so = (uint64_t)((s * kStage) >> 4);
           if (kb == 0) issue_stage<S, true>(dA0 + so, dN0 + so);
           else issue_stage<S, false>(dA0 + so, dN0 + so);
           if (lane == 0) umma_commit(&empty[s]);  // ring slot free once these MMAs have read it
           __syncwarp();
+#ifdef TMVN_PHASE_TIMING
+          acc2 += clock64() - f1;
+#endif
         }
         if (lane == 0) umma_commit(tfull);  // accumulators of this tile complete
         __syncwarp();
@@ -252,8 +286,13 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       const int mb = tile % MB, nb = tile / MB;
       const int64_t row = (int64_t)mb * kOzBM + row_in_tile;
       const double scale = __ldg(rowscale + row);
+      OZT(g0);
       mbar_wait(tfull, tcount & 1);
       tc_fence_after();
+      OZT(g1);
+#ifdef TMVN_PHASE_TIMING
+      acc0 += g1 - g0;
+#endif
       double* qcol = Q + (int64_t)nb * kOzBN * ldq + row;
 #pragma unroll 1
       for (int cc = 0; cc < kOzBN; cc += 16) {
@@ -273,8 +312,24 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);
+#ifdef TMVN_PHASE_TIMING
+      acc1 += clock64() - g1;
+#endif
     }
   }
+#ifdef TMVN_PHASE_TIMING
+  if (lane == 0) {
+    if (warp == 0) OZADD(5, acc0);
+    if (warp == 1) { OZADD(0, acc0); OZADD(1, acc1); OZADD(2, acc2); }
+    if (warp == 2) { OZADD(3, acc0); OZADD(4, acc1); }
+    if (threadIdx.x == 0) OZADD(7, clock64() - t_start);
+  }
+  if (threadIdx.x == 64) {
+    int nt = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) ++nt;
+    OZADD(6, nt);
+  }
+#endif
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -311,6 +366,17 @@ __global__ void oz_slice_kernel(const double* __restrict__ src, int R, int d, in
 }
 
 }  // namespace
+
+#ifdef TMVN_PHASE_TIMING
+void oz_cycles(unsigned long long* out8, bool reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_oz_cycles, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_oz_cycles, z, sizeof(z));
+  }
+}
+#endif
 
 size_t ozaki_smem_bytes(int S) { return (size_t)oz_stages(S) * oz_stage_bytes(S) + 256; }
 

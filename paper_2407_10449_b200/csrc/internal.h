@@ -63,7 +63,6 @@ struct EssParams {
   const double* g_u;
   // scratch (per CTA)
   double2* gstash;  // groups * m   (arcs when not in shared memory)
-  double2* gsorted; // groups * m   (the arcs grouped by bucket)
   double2* ggaps;   // groups * (m + 2)
   int NB;           // buckets per level (power of two)
   int W;            // warps per chain (1, 2, 4, 8)
@@ -91,12 +90,13 @@ constexpr int kGapSmem = 128;      // gaps kept in shared memory (rest in ggaps)
 // doubles][2 mbarriers][buckets, live buffer, gaps][stash if stash_smem].
 __host__ __device__ inline size_t ess_ring_bytes(int CH) { return CH > 0 ? (size_t)CH * 32 + 16 : 0; }
 __host__ __device__ inline size_t ess_group_base_bytes(int NB) {
-  size_t s = (size_t)NB * 3 * 8 + (size_t)kLiveCap * 16 + (size_t)kGapSmem * 16 + (size_t)NB * 3 * 4;
+  size_t s = (size_t)NB * 3 * 8 + (size_t)kLiveCap * 16 + (size_t)kGapSmem * 16 + (size_t)NB * 8 +
+             (size_t)kLiveCap * 16 + (size_t)NB * 3 * 4;
   return (s + 15) / 16 * 16;
 }
 __host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_smem, int CH) {
   size_t s = ess_ring_bytes(CH) + ess_group_base_bytes(NB);
-  if (stash_smem) s += (size_t)m * 32;  // stash + bucket-sorted copy
+  if (stash_smem) s += (size_t)m * 16;  // stash of the arcs
   return (s + 15) / 16 * 16;
 }
 
@@ -111,6 +111,7 @@ cudaError_t launch_ess_step(const EssParams& p, int grid, cudaStream_t st);
 cudaError_t launch_ess_intervals(const EssParams& p, int grid, cudaStream_t st);
 #ifdef TMVN_PHASE_TIMING
 void phase_cycles(unsigned long long* out10, bool reset);
+void oz_cycles(unsigned long long* out8, bool reset);
 #endif
 
 // ---- auxiliary kernels (aux_kernels.cu) -------------------------------------

@@ -54,7 +54,6 @@ struct tmvn_ctx {
   double* msum = nullptr;  // d (device) moment reduction target
   unsigned long long* dflag = nullptr;
   double2 *gstash = nullptr, *ggaps = nullptr;
-  double2* gsorted = nullptr;
   int64_t scratch_groups = 0;  // chain groups the scratch is sized for
   bool scratch_stash = false;  // gstash / gnext allocated
   // int8 Ozaki projection (options.projection = 1, gemm_i8.cu)
@@ -142,7 +141,7 @@ void free_chain_buffers(tmvn_ctx* h) {
   dfree(h->X); dfree(h->N); dfree(h->P0); dfree(h->P1); dfree(h->Q);
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
   dfree(h->stage); dfree(h->stage2); dfree(h->rej);
-  dfree(h->gstash); dfree(h->ggaps); dfree(h->gsorted);
+  dfree(h->gstash); dfree(h->ggaps);
   dfree(h->Ns);
   h->Ns_rows = 0;
   h->ozS_N = 0;
@@ -193,11 +192,10 @@ tmvn_status plan_ess(tmvn_ctx* h, int64_t C) {
   const bool need_stash = !h->plan.stash_smem;
   const int64_t G = h->plan.groups * S;
   if (G > h->scratch_groups || (need_stash && !h->scratch_stash)) {
-    dfree(h->gstash); dfree(h->gsorted); dfree(h->ggaps);
+    dfree(h->gstash); dfree(h->ggaps);
     const int64_t Gn = std::max(G, h->scratch_groups);
     if (need_stash || h->scratch_stash) {
       CK(h, dalloc(&h->gstash, (size_t)Gn * h->m));
-      CK(h, dalloc(&h->gsorted, (size_t)Gn * h->m));
       h->scratch_stash = true;
     }
     CK(h, dalloc(&h->ggaps, (size_t)Gn * (h->m + 2)));
@@ -291,7 +289,6 @@ EssParams base_params(tmvn_ctx* h, int C) {
   p.S2 = h->S2;
   p.rej = h->rej;
   p.gstash = h->gstash;
-  p.gsorted = h->gsorted;
   p.ggaps = h->ggaps;
   p.NB = h->plan.NB;
   p.W = h->plan.W;
@@ -452,7 +449,6 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p.rej = h->rej + x.c0;
     x.p.chain_offset = (uint32_t)(h->opt.chain_offset + x.c0);
     x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * h->m : nullptr;
-    x.p.gsorted = h->gsorted ? h->gsorted + (size_t)s * h->plan.groups * h->m : nullptr;
     x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
     x.p.Q = h->Q + x.c0 * h->m_pad;
     x.p.seed = seed;
@@ -960,7 +956,6 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   Tmp<double> da, db, du, dlo, dhi, dL, dth;
   Tmp<int64_t> dns;
   Tmp<double2> gstash, ggaps;
-  Tmp<double2> gsorted;
   TCK(tmp_in(da, alpha, cm)); TCK(tmp_in(db, beta, cm));
   TCK(tmp_in(du, u, u ? (size_t)C : 0));
   TCK(tmp_in(dlo, (const double*)nullptr, (size_t)C * seg_cap)); TCK(tmp_in(dhi, (const double*)nullptr, (size_t)C * seg_cap));
@@ -970,7 +965,6 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   const int grid = plan.grid;
   if (!plan.stash_smem) {
     TCK(tmp_in(gstash, (const double2*)nullptr, (size_t)plan.groups * m));
-    TCK(tmp_in(gsorted, (const double2*)nullptr, (size_t)plan.groups * m));
   }
   TCK(tmp_in(ggaps, (const double2*)nullptr, (size_t)plan.groups * (m + 2)));
   EssParams p;
@@ -982,7 +976,6 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   p.g_beta = db.p;
   p.g_u = u ? du.p : nullptr;
   p.gstash = gstash.p;
-  p.gsorted = gsorted.p;
   p.ggaps = ggaps.p;
   p.NB = plan.NB;
   p.W = plan.W;
@@ -1166,6 +1159,10 @@ tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t 
 // timing build only (tools/phase_timing.py): per-phase CTA cycles of ess_kernel
 tmvn_status tmvn_test_phase_cycles(uint64_t* out10, int reset) {
   tmvn::phase_cycles(reinterpret_cast<unsigned long long*>(out10), reset != 0);
+  return TMVN_OK;
+}
+tmvn_status tmvn_test_oz_cycles(uint64_t* out8, int reset) {
+  tmvn::oz_cycles(reinterpret_cast<unsigned long long*>(out8), reset != 0);
   return TMVN_OK;
 }
 #endif

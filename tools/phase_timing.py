@@ -29,5 +29,3 @@ tot = float(sum(buf[:7]))
 print(f"config {k}: {nchain} chain-iterations; mean active arcs {buf[8]/nchain:.1f}, gaps {buf[9]/nchain:.2f}, general path {buf[7]/nchain:.3f}")
 for i, n in enumerate(names):
     print(f"  {n:18s} {buf[i]/nchain:10.0f} cycles/chain  {100*buf[i]/tot:5.1f}%")
-for i, n in enumerate(["wi pass1", "wi pass2+gather", "wi sort", "wi scan+emit"]):
-    print(f"    {n:16s} {buf[10+i]/nchain:10.0f} cycles/chain")

@@ -91,7 +91,89 @@ void run(const char* name) {
   cudaFree(d);
 }
 
+// mode 1: 28 TS MMAs per round; 2: 7 cps (to slots 0-6) + 28 MMAs reading slot 7;
+// 3: 7 cps + 28 MMAs reading slots 0-6 (dependent, the kernel's pattern); 4: 7 cps only
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) cprate(int R, long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < 40960; i += 128) sm[i] = (unsigned char)i;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) {
+    const uint32_t sa = smem_u32(sm), sb = sa + 7 * 4096;
+    const uint64_t da = desc(sa, 2048, 128), db = desc(sb, 1024, 128);
+    long long t0 = clock64();
+    for (int r = 0; r < R; ++r) {
+      if (MODE >= 2) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i)
+          asm volatile(
+              "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+              " @e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"((uint32_t)(448 + 8 * i)),
+              "l"(da + (uint64_t)((i * 4096) >> 4)));
+      }
+      if (MODE <= 3) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i)
+#pragma unroll
+          for (int j = 0; j < 7 - i; ++j)
+            asm volatile(
+                "{\n .reg .pred p, e;\n setp.ne.b32 p, 1, 0;\n elect.sync _|e, 0xffffffff;\n"
+                " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"((uint32_t)((i + j) * 64)),
+                "r"((uint32_t)(MODE == 2 ? 448 + 56 : 448 + 8 * i)), "l"(db + (uint64_t)((j * 2048) >> 4)),
+                "n"(idesc<64>()));
+      }
+    }
+    if ((threadIdx.x & 31) == 0)
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(&bar)));
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile(
+          "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], 0;\n selp.u32 %0, 1, 0, P1;\n}\n"
+          : "=r"(ok) : "r"(smem_u32(&bar)));
+    long long t1 = clock64();
+    if ((threadIdx.x & 31) == 0) cyc[blockIdx.x] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+}
+
+template <int MODE>
+void run_cp() {
+  long long* d;
+  cudaMalloc(&d, 148 * sizeof(long long));
+  const int R = 500;
+  cudaFuncSetAttribute(cprate<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cprate<MODE><<<148, 128, 65536>>>(R, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  avg /= 148;
+  printf("{\"cp_mode\": %d, \"cycles_per_round\": %.1f, \"err\": \"%s\"}\n", MODE, avg / R, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
+  run_cp<1>();
+  run_cp<2>();
+  run_cp<3>();
+  run_cp<4>();
   run<32, false>("SS");
   run<64, false>("SS");
   run<128, false>("SS");

@@ -237,8 +237,12 @@ __device__ __forceinline__ double fast_atan2(double y, double x) {
 // b < 0 or s^2 > 0; (alpha, beta) = (tau - delta, tau + delta) shifted into
 // [0, 2 pi] by C1.  Returns false for an inactive constraint.
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ bool arc_of(double p, double q, double b, double& alpha, double& beta) {
+__device__ __forceinline__ bool arc_active(double p, double q, double b) {
   const double s2 = fma(p, p, fma(q, q, -b * b));  // p^2 + q^2 - b^2
+  return b < 0.0 || s2 > 0.0;
+}
+__device__ __forceinline__ bool arc_of(double p, double q, double b, double& alpha, double& beta) {
+  const double s2 = fma(p, p, fma(q, q, -b * b));  // p^2 + q^2 - b^2 (as in arc_active)
   if (!(b < 0.0 || s2 > 0.0)) return false;
   const double s = sqrt(fmax(s2, 0.0));
   const double tau = fast_atan2(q, p);

@@ -54,6 +54,7 @@ struct Ctl {
   int maxa_exact;       // max/min alpha per bucket exact (refinement levels)
   int fast;             // 1: I_act built by the parallel level-1 path
   int ncand;            // gaps found by the parallel path
+  double u;             // u_{c,t} of "sample theta uniformly" (drawn at the chain's start)
 };
 
 enum { kAll = 0, kPrefix = 1, kSame = 2, kNarrow = 3 };
@@ -758,6 +759,19 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
       ctl.mode = 0;
       ctl.maxa_exact = 0;
     }
+    if (!kGiven && g.tid == T - 1) {
+      // u for this chain (Philox latency hidden behind phase A); the next chain's
+      // P and Q rows are pulled into L2 now, so its phase A loads hit L2
+      ctl.u = theta_uniform(p.seed, t_it, gchain);
+      const int64_t cn = cc + ngroups;
+      if (!kRing && cn < p.C) {
+        const uint32_t bytes = (uint32_t)(((int64_t)m * 8 + 15) & ~15ll);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.P_cur + cn * p.ldp), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.Q + cn * p.ldp), "r"(bytes)
+                     : "memory");
+      }
+    }
     clear_buckets(g, S, NB);
     g.sync();
     PHASE(0);  // init
@@ -834,6 +848,71 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
         ++qseq;
         g.sync();  // the slot may be refilled from now on
       }
+          } else if (kSmemStash) {
+      // two passes: (1) the active test (C3/C25) on every constraint pair, active
+      // (p, q) and the index compacted into the stash; (2) the arcs of the active
+      // constraints only, every lane busy (about 40 % of the constraints are
+      // inactive at config 3 and would idle their lanes through two atan2)
+      const double2* P2 = reinterpret_cast<const double2*>(Prow);
+      const double2* Q2 = reinterpret_cast<const double2*>(Qrow);
+      const double2* B2 = reinterpret_cast<const double2*>(p.b);
+      int* sidx = reinterpret_cast<int*>(stash + m);
+      const int npairs = (m + 1) / 2;
+      for (int base = 0; base < npairs; base += kBatch * T) {
+        double2 pp[kBatch], qq[kBatch], bb[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int pi = base + u * T + g.tid;
+          if (pi < npairs) {
+            pp[u] = P2[pi];
+            qq[u] = Q2[pi];
+            bb[u] = __ldg(B2 + pi);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          if (base + u * T >= npairs) break;  // uniform
+          const int pi = base + u * T + g.tid;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = 2 * pi + h;
+            const double pv = h ? pp[u].y : pp[u].x, qv = h ? qq[u].y : qq[u].x, bv = h ? bb[u].y : bb[u].x;
+            const bool act = pi < npairs && i < m && arc_active(pv, qv, bv);
+            if (p.d_alpha && pi < npairs && i < m && !act) {
+              p.d_alpha[(int64_t)c * m + i] = 0.0;
+              p.d_beta[(int64_t)c * m + i] = 0.0;
+              p.d_active[(int64_t)c * m + i] = 0;
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, act);
+            if (mask) {
+              const int leader = __ffs(mask) - 1;
+              int sb = 0;
+              if (g.lane == leader) sb = atomicAdd(&ctl.n_act, __popc(mask));
+              sb = __shfl_sync(0xffffffffu, sb, leader);
+              if (act) {
+                const int slot = sb + __popc(mask & ((1u << g.lane) - 1u));
+                stash[slot] = make_double2(pv, qv);
+                sidx[slot] = i;
+              }
+            }
+          }
+        }
+      }
+      g.sync();
+      const int n_act = ctl.n_act;
+      for (int slot = g.tid; slot < n_act; slot += T) {
+        const double2 pq = stash[slot];
+        const int i = sidx[slot];
+        double al, be;
+        arc_of(pq.x, pq.y, __ldg(p.b + i), al, be);  // active by pass 1: same predicate
+        stash[slot] = make_double2(al, be);
+        bucket_add<false>(S, bucket_key(al, ctl, NB, scale), al, be);
+        if (p.d_alpha) {
+          p.d_alpha[(int64_t)c * m + i] = al;
+          p.d_beta[(int64_t)c * m + i] = be;
+          p.d_active[(int64_t)c * m + i] = 1;
+        }
+      }
           } else {
       // constraint pairs (2i, 2i+1): P, Q, b as double2 from global; kBatch pairs per
       // thread with loads in flight, their arcs computed before the stash appends (ILP)
@@ -906,7 +985,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
     // ---------------- B + C: I_act by Alg. 3, then theta ----------------
     const bool fast = par_intervals(g, S, ctl, stash, NB, scale, gg, s_w64, s_w32);
     if (fast && g.tid == T - 1) {  // theta on the highest warp (arbiter: highest warp id first)
-      const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, t_it, gchain);
+      const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : ctl.u;
       theta_from_gaps(S, ctl, gg, u, p.eps);
     }
     g.sync();
@@ -915,7 +994,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
     if (!fast) {
       build_intervals(g, S, ctl, stash, NB, log2NB, scale, gg, s_w64, s_w32);
       if (g.tid == 0) {
-        const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : theta_uniform(p.seed, t_it, gchain);
+        const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : ctl.u;
         theta_from_gaps(S, ctl, gg, u, p.eps);
       }
       g.sync();

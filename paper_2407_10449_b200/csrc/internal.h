@@ -96,7 +96,7 @@ __host__ __device__ inline size_t ess_group_base_bytes(int NB) {
 }
 __host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_smem, int CH) {
   size_t s = ess_ring_bytes(CH) + ess_group_base_bytes(NB);
-  if (stash_smem) s += (size_t)m * 16;  // stash of the arcs
+  if (stash_smem) s += (size_t)m * 20;  // stash of the arcs + constraint index (phase A compaction)
   return (s + 15) / 16 * 16;
 }
 

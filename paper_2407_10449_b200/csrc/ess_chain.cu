@@ -772,6 +772,20 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
                      : "memory");
       }
     }
+    if (!kGiven) {  // phase D's x, nu (and moment) rows of this chain into L2 early
+      const int kp = (int)(p.d_pad / 2);
+      for (int pk = g.tid; pk < kp; pk += T) {
+        const int64_t o = tiled_offset(c, 2 * pk, p.d_pad);
+        if ((pk & 3) == 0) {  // one 64-byte run = 4 pairs
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.X + o));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.N + o));
+          if (record) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.S1 + o));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.S2 + o));
+          }
+        }
+      }
+    }
     clear_buckets(g, S, NB);
     g.sync();
     PHASE(0);  // init

@@ -52,11 +52,16 @@ constexpr int kOzBN = kOzNuRows;  // chains per tile (MMA N)
 constexpr int kOzBK = kOzStepK;   // K bytes per stage (one MMA K step for kind::i8)
 constexpr int kASlice = kOzBM * kOzBK;  // 4096 bytes
 constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
-constexpr int kOzThreads = 192;
+constexpr int kOzEpiWarps = 8;  // two per TMEM lane quadrant, 32 accumulator columns each
+constexpr int kOzThreads = 64 + 32 * kOzEpiWarps;
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
 // ring depth: as many stages as fit in 226 KB of shared memory (S = 6: 6, 7: 5, 8: 4)
+#ifndef TMVN_OZ_MAX_STAGES
+#define TMVN_OZ_MAX_STAGES 6
+#endif
 __host__ __device__ constexpr int oz_stages(int S) {
-  return (226 * 1024) / oz_stage_bytes(S) > 6 ? 6 : (226 * 1024) / oz_stage_bytes(S);
+  return (226 * 1024) / oz_stage_bytes(S) > TMVN_OZ_MAX_STAGES ? TMVN_OZ_MAX_STAGES
+                                                                 : (226 * 1024) / oz_stage_bytes(S);
 }
 
 // ---- tcgen05 / mbarrier wrappers -------------------------------------------
@@ -98,6 +103,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
         "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -128,37 +139,53 @@ struct PairMma {
 // 32-byte K step per lane = row) and the MMAs read A from there.  tcgen05.cp and
 // tcgen05.mma issued by one thread execute in issue order, so a slice is not
 // overwritten before the previous step's MMAs have read it.
+// A slice i feeds S - i MMAs: it is worth a 4 KB copy (~47 effective cycles, the
+// copy overlaps the MMAs only in part) when it saves at least 3 x 16 cycles, so
+// the last two slices (2 MMAs and 1 MMA) stay in SS mode.
+template <int S>
+__host__ __device__ constexpr bool oz_ts() { return S * kOzBN + 8 * S <= 512; }
+template <int S>
+__host__ __device__ constexpr int oz_nts() { return oz_ts<S>() ? S - 2 : 0; }
+
 template <int I, int J, int S, bool FIRST>
 struct PairMmaTS {
-  static __device__ __forceinline__ void run(uint64_t dn) {
+  static __device__ __forceinline__ void run(uint64_t da, uint64_t dn) {
     constexpr uint32_t idesc = idesc_i8(I == 0, J == 0);
     constexpr uint32_t acc = (FIRST && I == 0) ? 0u : 1u;
-    asm volatile(
-        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
-        " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"((uint32_t)((I + J) * kOzBN)),
-        "r"((uint32_t)(S * kOzBN + 8 * I)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc), "n"(acc));
-    if constexpr (J + 1 < S - I) PairMmaTS<I, J + 1, S, FIRST>::run(dn);
-    else if constexpr (I + 1 < S) PairMmaTS<I + 1, 0, S, FIRST>::run(dn);
+    if constexpr (I < oz_nts<S>()) {
+      asm volatile(
+          "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+          " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"((uint32_t)((I + J) * kOzBN)),
+          "r"((uint32_t)(S * kOzBN + 8 * I)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc), "n"(acc));
+    } else {
+      asm volatile(
+          "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+          " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"((uint32_t)((I + J) * kOzBN)),
+          "l"(da + (uint64_t)((I * kASlice) >> 4)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc),
+          "n"(acc));
+    }
+    if constexpr (J + 1 < S - I) PairMmaTS<I, J + 1, S, FIRST>::run(da, dn);
+    else if constexpr (I + 1 < S) PairMmaTS<I + 1, 0, S, FIRST>::run(da, dn);
   }
 };
 template <int I, int S>
 struct CopyA {
   static __device__ __forceinline__ void run(uint64_t da) {
-    asm volatile(
-        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-        " @e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"((uint32_t)(S * kOzBN + 8 * I)),
-        "l"(da + (uint64_t)((I * kASlice) >> 4)));
-    if constexpr (I + 1 < S) CopyA<I + 1, S>::run(da);
+    if constexpr (I < oz_nts<S>()) {
+      asm volatile(
+          "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+          " @e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"((uint32_t)(S * kOzBN + 8 * I)),
+          "l"(da + (uint64_t)((I * kASlice) >> 4)));
+      CopyA<I + 1, S>::run(da);
+    }
   }
 };
-template <int S>
-__host__ __device__ constexpr bool oz_ts() { return S * kOzBN + 8 * S <= 512; }
 
 template <int S, bool FIRST>
 __device__ __forceinline__ void issue_stage(uint64_t da, uint64_t dn) {
   if constexpr (oz_ts<S>()) {
     CopyA<0, S>::run(da);
-    PairMmaTS<0, 0, S, FIRST>::run(dn);
+    PairMmaTS<0, 0, S, FIRST>::run(da, dn);
   } else {
     PairMma<0, 0, S, FIRST>::run(da, dn);
   }
@@ -198,7 +225,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);  // one arrive per epilogue warp
+    mbar_init(tempty, kOzEpiWarps);  // one arrive per epilogue warp
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -278,8 +305,10 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         __syncwarp();
       }
     }
-  } else {  // ---- epilogue: warps 2..5; warp w reads TMEM lanes 32 (w % 4) ..
+  } else {  // ---- epilogue: warps 2..9; warp w reads TMEM lanes 32 (w % 4) .. (hardware rule),
+           // warps 2-5 accumulator columns 0-31, warps 6-9 columns 32-63
     const int quad = warp & 3;
+    const int cbase = ((warp - 2) / 4) * (kOzBN / 2);
     const int row_in_tile = quad * 32 + lane;
     uint32_t tcount = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
@@ -295,14 +324,14 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #endif
       double* qcol = Q + (int64_t)nb * kOzBN * ldq + row;
 #pragma unroll 1
-      for (int cc = 0; cc < kOzBN; cc += 16) {
-        int32_t acc[S][16];
+      for (int cc = cbase; cc < cbase + kOzBN / 2; cc += 8) {
+        int32_t acc[S][8];
 #pragma unroll
         for (int D = 0; D < S; ++D)
-          tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(D * kOzBN + cc), acc[D]);
+          tmem_ld8(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(D * kOzBN + cc), acc[D]);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
           double h = (double)acc[S - 1][j];
 #pragma unroll
           for (int D = S - 2; D >= 0; --D) h = __fma_rn(h, 0.00390625, (double)acc[D][j]);  // 2^-8

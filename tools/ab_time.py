@@ -19,7 +19,7 @@ for path in sys.argv[5:]:
     tm.LIB_PATH = os.path.abspath(path)
     for W, S, R in [(w, x, r) for w in Ws for x in Ss for r in Rs]:
         s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
-        s.set_options(profile=1, chain_warps=W, streams=S, ring=R)
+        s.set_options(profile=int(os.environ.get("PROFILE", "1")), chain_warps=W, streams=S, ring=R)
         X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
         s.sample(X, 20, cfg.chain_seed, out=X)
         s.reset_stats()
@@ -28,6 +28,7 @@ for path in sys.argv[5:]:
         torch.cuda.synchronize(); dt = time.perf_counter() - t0
         pr = s.profile()
         print(f"{os.path.basename(path)} W={W} S={S} R={R} cfg{k}: {dt/iters*1e3:.3f} ms/iter  gemm "
-              f"{pr['gemm_ms']/max(1,pr['gemm_launches']):.3f} ms  ess {pr['ess_ms']/max(1,pr['ess_launches']):.3f} ms"
+              f"{pr['gemm_ms']/max(1,pr['gemm_launches']):.3f} ms  tc {pr['tc_ms']/max(1,pr['tc_launches']):.3f} ms"
+              f"  ess {pr['ess_ms']/max(1,pr['ess_launches']):.3f} ms"
               f"  evals/s {cfg.C*cfg.m*iters/dt:.3e}", flush=True)
         s.close()

@@ -52,8 +52,7 @@ constexpr int kOzBN = kOzNuRows;  // chains per tile (MMA N)
 constexpr int kOzBK = kOzStepK;   // K bytes per stage (one MMA K step for kind::i8)
 constexpr int kASlice = kOzBM * kOzBK;  // 4096 bytes
 constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
-constexpr int kOzEpiWarps = 8;  // two per TMEM lane quadrant, 32 accumulator columns each
-constexpr int kOzThreads = 64 + 32 * kOzEpiWarps;
+constexpr int kOzThreads = 320;  // 10 warps: producer, MMA, 4 A loaders, 4 epilogue
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
 // ring depth: as many stages as fit in 226 KB of shared memory (S = 6: 6, 7: 5, 8: 4)
 #ifndef TMVN_OZ_MAX_STAGES
@@ -116,47 +115,38 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // All S(S+1)/2 digit-pair MMAs of one K step: A' digit i x nu digit j into the
 // accumulator of diagonal i + j (TMEM columns (i + j) * 64; the allocation of all
 // 512 columns starts at column 0).  Every operand is a compile-time constant or a
-// warp-uniform descriptor, so the issue is a plain sequence of UTCIMMA.  FIRST:
-// the first K step of a tile, where pair (0, j) initialises accumulator j.
-template <int I, int J, int S, bool FIRST>
-struct PairMma {
-  static __device__ __forceinline__ void run(uint64_t da, uint64_t dn) {
-    constexpr uint32_t idesc = idesc_i8(I == 0, J == 0);
-    constexpr uint32_t acc = (FIRST && I == 0) ? 0u : 1u;
-    asm volatile(
-        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
-        " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"((uint32_t)((I + J) * kOzBN)),
-        "l"(da + (uint64_t)((I * kASlice) >> 4)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc),
-        "n"(acc));
-    if constexpr (J + 1 < S - I) PairMma<I, J + 1, S, FIRST>::run(da, dn);
-    else if constexpr (I + 1 < S) PairMma<I + 1, 0, S, FIRST>::run(da, dn);
-  }
-};
-// TS variant (S <= 7): shared-memory operand reads bound an SS-mode M=128 N=64
-// int8 MMA at 48 cycles (6 KB per MMA at 128 B/cycle; tools/tc_rate.cu measured
-// 48.0 SS vs 32.0 with A in TMEM), so the A' digit slices of a K step are first
-// copied into TMEM (tcgen05.cp 128x256b: slice i -> columns 64 S + 8 i, i.e. one
-// 32-byte K step per lane = row) and the MMAs read A from there.  tcgen05.cp and
-// tcgen05.mma issued by one thread execute in issue order, so a slice is not
-// overwritten before the previous step's MMAs have read it.
-// A slice i feeds S - i MMAs: it is worth a 4 KB copy (~47 effective cycles, the
-// copy overlaps the MMAs only in part) when it saves at least 3 x 16 cycles, so
-// the last two slices (2 MMAs and 1 MMA) stay in SS mode.
+// warp-uniform value, so the issue is a plain sequence of UTCIMMA (elect.sync, no
+// waterfall loop).  FIRST: the first K step of a tile, where pair (0, j)
+// initialises accumulator j.
+//
+// A from TMEM (TS) or shared memory (SS).  tools/tc_rate.cu on the B200: an
+// M=128 N=64 int8 MMA takes 48 cycles with both operands in shared memory (6 KB
+// of operand reads at 128 B/cycle) and 32 cycles with A in TMEM (the tensor-core
+// floor); tcgen05.cp into TMEM runs on the MMA pipe (7 copies of 4 KB: 448
+// cycles, mostly serialised with the MMAs).  So the first NTS digit slices of a
+// K step are written into TMEM by four loader warps (ld.shared + tcgen05.st, off
+// the MMA pipe) into one of two buffers, and their MMAs read A there; the last
+// slices, which feed only 1-3 MMAs, stay SS.  TMEM: S x 64 accumulator columns +
+// 2 x NTS x 8 A columns <= 512 (S = 7: NTS = 4, all 512 columns).
 template <int S>
-__host__ __device__ constexpr bool oz_ts() { return S * kOzBN + 8 * S <= 512; }
+__host__ __device__ constexpr int oz_nts() {
+  return (512 - S * 64) / 16 < S - 2 ? (512 - S * 64) / 16 : S - 2;
+}
 template <int S>
-__host__ __device__ constexpr int oz_nts() { return oz_ts<S>() ? S - 2 : 0; }
+__host__ __device__ constexpr uint32_t oz_acol(int buf, int i) {
+  return (uint32_t)(S * 64 + buf * oz_nts<S>() * 8 + 8 * i);
+}
 
 template <int I, int J, int S, bool FIRST>
-struct PairMmaTS {
-  static __device__ __forceinline__ void run(uint64_t da, uint64_t dn) {
+struct PairMma {
+  static __device__ __forceinline__ void run(uint64_t da, uint64_t dn, uint32_t abuf) {
     constexpr uint32_t idesc = idesc_i8(I == 0, J == 0);
     constexpr uint32_t acc = (FIRST && I == 0) ? 0u : 1u;
     if constexpr (I < oz_nts<S>()) {
       asm volatile(
           "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
           " @e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"((uint32_t)((I + J) * kOzBN)),
-          "r"((uint32_t)(S * kOzBN + 8 * I)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc), "n"(acc));
+          "r"(abuf + 8 * I), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc), "n"(acc));
     } else {
       asm volatile(
           "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
@@ -164,31 +154,19 @@ struct PairMmaTS {
           "l"(da + (uint64_t)((I * kASlice) >> 4)), "l"(dn + (uint64_t)((J * kNSlice) >> 4)), "n"(idesc),
           "n"(acc));
     }
-    if constexpr (J + 1 < S - I) PairMmaTS<I, J + 1, S, FIRST>::run(da, dn);
-    else if constexpr (I + 1 < S) PairMmaTS<I + 1, 0, S, FIRST>::run(da, dn);
+    if constexpr (J + 1 < S - I) PairMma<I, J + 1, S, FIRST>::run(da, dn, abuf);
+    else if constexpr (I + 1 < S) PairMma<I + 1, 0, S, FIRST>::run(da, dn, abuf);
   }
 };
-template <int I, int S>
-struct CopyA {
-  static __device__ __forceinline__ void run(uint64_t da) {
-    if constexpr (I < oz_nts<S>()) {
-      asm volatile(
-          "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-          " @e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"((uint32_t)(S * kOzBN + 8 * I)),
-          "l"(da + (uint64_t)((I * kASlice) >> 4)));
-      CopyA<I + 1, S>::run(da);
-    }
-  }
-};
-
 template <int S, bool FIRST>
-__device__ __forceinline__ void issue_stage(uint64_t da, uint64_t dn) {
-  if constexpr (oz_ts<S>()) {
-    CopyA<0, S>::run(da);
-    PairMmaTS<0, 0, S, FIRST>::run(da, dn);
-  } else {
-    PairMma<0, 0, S, FIRST>::run(da, dn);
-  }
+__device__ __forceinline__ void issue_stage(uint64_t da, uint64_t dn, uint32_t abuf) {
+  PairMma<0, 0, S, FIRST>::run(da, dn, abuf);
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint4& a, const uint4& b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
 }
 
 // Role timing (timing build -DTMVN_PHASE_TIMING only; tools/oz_timing.py):
@@ -203,6 +181,8 @@ __device__ unsigned long long g_oz_cycles[8];
 #define OZADD(i, v)
 #endif
 
+// warps: 0 producer, 1 MMA issuer, 2-5 A loaders, 6-9 epilogue (warp w may access
+// TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31 only: each role covers the 4 quadrants)
 template <int S>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
@@ -210,13 +190,16 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                       int MB, int NBt, int KB) {
   constexpr int kStage = oz_stage_bytes(S);
   constexpr int kOzStages = oz_stages(S);
+  constexpr int NTS = oz_nts<S>();
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kStage);
   uint64_t* empty = full + kOzStages;
   uint64_t* tfull = empty + kOzStages;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* afull = tempty + 1;   // [2]: A buffer written (4 loader warps)
+  uint64_t* aempty = afull + 2;   // [2]: the MMAs reading an A buffer completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -225,7 +208,11 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, kOzEpiWarps);  // one arrive per epilogue warp
+    mbar_init(tempty, 4);  // one arrive per epilogue warp
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&afull[b], 4);
+      mbar_init(&aempty[b], 1);
+    }
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -285,17 +272,23 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #endif
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % kOzStages;
+          const int b = it & 1;
           OZT(f0);
           mbar_wait(&full[s], (it / kOzStages) & 1);
+          if (NTS > 0) mbar_wait(&afull[b], (it >> 1) & 1);
           tc_fence_after();
           OZT(f1);
 #ifdef TMVN_PHASE_TIMING
           acc0 += f1 - f0;
 #endif
           const uint64_t so = (uint64_t)((s * kStage) >> 4);
-          if (kb == 0) issue_stage<S, true>(dA0 + so, dN0 + so);
-          else issue_stage<S, false>(dA0 + so, dN0 + so);
-          if (lane == 0) umma_commit(&empty[s]);  // ring slot free once these MMAs have read it
+          const uint32_t abuf = b ? oz_acol<S>(1, 0) : oz_acol<S>(0, 0);
+          if (kb == 0) issue_stage<S, true>(dA0 + so, dN0 + so, abuf);
+          else issue_stage<S, false>(dA0 + so, dN0 + so, abuf);
+          if (lane == 0) {
+            umma_commit(&empty[s]);  // ring slot free once these MMAs have read it
+            if (NTS > 0) umma_commit(&aempty[b]);
+          }
           __syncwarp();
 #ifdef TMVN_PHASE_TIMING
           acc2 += clock64() - f1;
@@ -305,10 +298,36 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         __syncwarp();
       }
     }
-  } else {  // ---- epilogue: warps 2..9; warp w reads TMEM lanes 32 (w % 4) .. (hardware rule),
-           // warps 2-5 accumulator columns 0-31, warps 6-9 columns 32-63
+  } else if (warp < 6) {  // ---- A loaders: row 32 (warp % 4) + lane of each TS slice into TMEM
+    if (NTS > 0) {
+      const int quad = warp & 3;
+      const int row = quad * 32 + lane;
+      const uint32_t roff = (uint32_t)((row / 8) * 128 + (row % 8) * 16);
+      const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kOzStages;
+          const int b = it & 1;
+          mbar_wait(&full[s], (it / kOzStages) & 1);
+          if (it >= 2) mbar_wait(&aempty[b], ((it >> 1) - 1) & 1);
+          tc_fence_after();
+          const unsigned char* st = ring + s * kStage + roff;
+#pragma unroll
+          for (int i = 0; i < NTS; ++i) {
+            const uint4 lo = *reinterpret_cast<const uint4*>(st + i * kASlice);
+            const uint4 hi = *reinterpret_cast<const uint4*>(st + i * kASlice + (kOzBM / 8) * 128);
+            tmem_st8(tmem + lanebase + (b ? oz_acol<S>(1, i) : oz_acol<S>(0, i)), lo, hi);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&afull[b]);
+        }
+      }
+    }
+  } else {  // ---- epilogue: warps 6-9
     const int quad = warp & 3;
-    const int cbase = ((warp - 2) / 4) * (kOzBN / 2);
     const int row_in_tile = quad * 32 + lane;
     uint32_t tcount = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
@@ -324,7 +343,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #endif
       double* qcol = Q + (int64_t)nb * kOzBN * ldq + row;
 #pragma unroll 1
-      for (int cc = cbase; cc < cbase + kOzBN / 2; cc += 8) {
+      for (int cc = 0; cc < kOzBN; cc += 8) {
         int32_t acc[S][8];
 #pragma unroll
         for (int D = 0; D < S; ++D)
@@ -350,7 +369,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   if (lane == 0) {
     if (warp == 0) OZADD(5, acc0);
     if (warp == 1) { OZADD(0, acc0); OZADD(1, acc1); OZADD(2, acc2); }
-    if (warp == 2) { OZADD(3, acc0); OZADD(4, acc1); }
+    if (warp == 6) { OZADD(3, acc0); OZADD(4, acc1); }
     if (threadIdx.x == 0) OZADD(7, clock64() - t_start);
   }
   if (threadIdx.x == 64) {

@@ -52,7 +52,8 @@ constexpr int kOzBN = kOzNuRows;  // chains per tile (MMA N)
 constexpr int kOzBK = kOzStepK;   // K bytes per stage (one MMA K step for kind::i8)
 constexpr int kASlice = kOzBM * kOzBK;  // 4096 bytes
 constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
-constexpr int kOzThreads = 320;  // 10 warps: producer, MMA, 4 A loaders, 4 epilogue
+constexpr int kOzEpiWarps = 8;   // two per TMEM lane quadrant, half of the columns each
+constexpr int kOzThreads = 32 * (6 + kOzEpiWarps);  // producer, MMA, 4 A loaders, epilogue
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
 // ring depth: as many stages as fit in 226 KB of shared memory (S = 6: 6, 7: 5, 8: 4)
 #ifndef TMVN_OZ_MAX_STAGES
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);  // one arrive per epilogue warp
+    mbar_init(tempty, kOzEpiWarps);  // one arrive per epilogue warp
     for (int b = 0; b < 2; ++b) {
       mbar_init(&afull[b], 4);
       mbar_init(&aempty[b], 1);
@@ -326,8 +327,9 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         }
       }
     }
-  } else {  // ---- epilogue: warps 6-9
+  } else {  // ---- epilogue: warps 6.. (warps 6-9 columns 0-31, warps 10-13 columns 32-63)
     const int quad = warp & 3;
+    const int c0 = ((warp - 6) / 4) * (kOzBN * 4 / kOzEpiWarps);
     const int row_in_tile = quad * 32 + lane;
     uint32_t tcount = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #endif
       double* qcol = Q + (int64_t)nb * kOzBN * ldq + row;
 #pragma unroll 1
-      for (int cc = 0; cc < kOzBN; cc += 8) {
+      for (int cc = c0; cc < c0 + kOzBN * 4 / kOzEpiWarps; cc += 8) {
         int32_t acc[S][8];
 #pragma unroll
         for (int D = 0; D < S; ++D)

@@ -279,6 +279,13 @@ def main():
         tc_ops = prof["tc_ops"] / max(1, prof["tc_launches"])
         tc_achieved = tc_ops / (tc_avg_ms * 1e-3) / 1e12
         tc_peak = 2.0 * mp["bf16_tflops"]
+        oz_traffic, oz_traffic_src = None, None
+        try:  # dram bytes read + written per launch, committed ncu --set full capture (config 3, N=1)
+            tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_oz_traffic.json")))
+            if args.config == 3 and (opts.ozaki_slices or 7) == 7:
+                oz_traffic, oz_traffic_src = tj["traffic_bytes"], "profiles/r01/ncu_oz_traffic.json"
+        except Exception:
+            pass
         tc_peak_sus = 2.0 * mp["bf16_tflops_sustained"]
         dmma = dict(roofline)
         for k in ("ess_kernel", "traffic", "traffic_source", "measured_in"):
@@ -288,7 +295,7 @@ def main():
                     "kernel": "ozaki_gemm_kernel (Q = N A'^T, int8 tcgen05.mma, TMEM accumulators, "
                               f"{opts.ozaki_slices or 7} digits: FP64-accurate)",
                     "achieved": tc_achieved, "peak": tc_peak, "unit": "TOP/s (int8)",
-                    "frac": tc_achieved / tc_peak, "traffic": None,
+                    "frac": tc_achieved / tc_peak, "traffic": oz_traffic, "traffic_source": oz_traffic_src,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x 2 = nominal int8/bf16 dense "
                                    "ratio 4.5/2.25 (B200_PROFILING.md); burst, not sustained, because the "
                                    "clocks stay at sm_max during this step (see clocks)",

@@ -35,7 +35,10 @@ namespace tmvn {
 namespace {
 
 constexpr uint64_t kTopBits = 0x7FF0000000000000ull;  // +inf: every alpha in [0, 2 pi] is below
-constexpr int kBatch = 2;  // constraint pairs per thread with loads in flight
+#ifndef TMVN_ESS_BATCH
+#define TMVN_ESS_BATCH 2
+#endif
+constexpr int kBatch = TMVN_ESS_BATCH;  // constraint pairs per thread with loads in flight
 
 __device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
 __device__ __forceinline__ double bitsd(uint64_t b) { return __longlong_as_double((long long)b); }

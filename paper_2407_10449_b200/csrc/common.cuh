@@ -157,7 +157,11 @@ __host__ __device__ inline int64_t oz_offset(int64_t r, int64_t k, int s, int S,
 }
 
 __device__ __forceinline__ int64_t oz_fixed(double v, int S, int e) {
-  return __double2ll_rz(scalbn(v, 8 * S - 1 - e));
+  return __double2ll_rz(scalbn(v, 8 * S - 1 - e));  // any e (A' rows may be tiny)
+}
+// nu (e = kOzNuExp): v 2^(8S-1-e) is an exact product with a normal power of two
+__device__ __forceinline__ int64_t oz_fixed_nu(double v, int S) {
+  return __double2ll_rz(v * __longlong_as_double((long long)(1023 + 8 * S - 1 - kOzNuExp) << 52));
 }
 
 __device__ __forceinline__ uint32_t oz_digit(int64_t X, int s, int S) {
@@ -165,13 +169,24 @@ __device__ __forceinline__ uint32_t oz_digit(int64_t X, int s, int S) {
   return (uint32_t)(sh & 0xFF);               // digit 0: two's-complement byte of a value in [-128, 127]
 }
 
-// The S digits of the nu pair (v0, v1) at coordinates k, k + 1 (k even) of chain r.
+// The S digits of the nu pair (v0, v1) at coordinates k, k + 1 (k even) of chain r:
+// digit s of X is byte S-1-s of its 64-bit two's complement (|X| < 2^(8S-1)), so
+// each 16-bit store is one byte permute of the two values' words; the S slices of
+// one (row block, K step) are BR x 32 bytes apart.
 __device__ __forceinline__ void oz_store_nu_pair(int8_t* Ns, int64_t r, int k, double v0, double v1,
                                                  int S, int64_t KB) {
-  const int64_t X0 = oz_fixed(v0, S, kOzNuExp), X1 = oz_fixed(v1, S, kOzNuExp);
-  for (int s = 0; s < S; ++s) {
-    const uint16_t w = (uint16_t)(oz_digit(X0, s, S) | (oz_digit(X1, s, S) << 8));
-    *reinterpret_cast<uint16_t*>(Ns + oz_offset(r, k, s, S, KB, kOzNuRows)) = w;
+  const int64_t X0 = oz_fixed_nu(v0, S), X1 = oz_fixed_nu(v1, S);
+  const uint32_t lo0 = (uint32_t)X0, hi0 = (uint32_t)((uint64_t)X0 >> 32);
+  const uint32_t lo1 = (uint32_t)X1, hi1 = (uint32_t)((uint64_t)X1 >> 32);
+  int8_t* base = Ns + oz_offset(r, k, 0, S, KB, kOzNuRows);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (s < S) {
+      const int b = S - 1 - s;  // byte of X
+      const uint32_t w = b < 4 ? __byte_perm(lo0, lo1, (uint32_t)(b | ((b + 4) << 4)))
+                               : __byte_perm(hi0, hi1, (uint32_t)((b - 4) | (b << 4)));
+      *reinterpret_cast<uint16_t*>(base + s * (kOzNuRows * kOzStepK)) = (uint16_t)w;
+    }
   }
 }
 

@@ -244,6 +244,36 @@ __device__ __forceinline__ double fast_atan2(double y, double x) {
   return (__double_as_longlong(y) < 0) ? -r : r;
 }
 
+// Two independent atan2 with the operations of fast_atan2 (bit-identical results):
+// the polynomial coefficients are loaded once for both, and the two dependency
+// chains interleave.
+__device__ __forceinline__ void fast_atan2_2(double y1, double x1, double y2, double x2, double& r1,
+                                             double& r2) {
+  const double ax1 = fabs(x1), ay1 = fabs(y1), ax2 = fabs(x2), ay2 = fabs(y2);
+  const double mx1 = fmax(ax1, ay1), mn1 = fmin(ax1, ay1);
+  const double mx2 = fmax(ax2, ay2), mn2 = fmin(ax2, ay2);
+  const bool big1 = mn1 > 0.41421356237309503 * mx1, big2 = mn2 > 0.41421356237309503 * mx2;
+  const double num1 = big1 ? mn1 - mx1 : mn1, den1 = big1 ? mn1 + mx1 : mx1;
+  const double num2 = big2 ? mn2 - mx2 : mn2, den2 = big2 ? mn2 + mx2 : mx2;
+  const double t1 = den1 > 0.0 ? num1 * fast_recip(den1) : 0.0;
+  const double t2 = den2 > 0.0 ? num2 * fast_recip(den2) : 0.0;
+  const double z1 = t1 * t1, z2 = t2 * t2;
+  double p1 = kAtanP[10], p2 = kAtanP[10];
+#pragma unroll
+  for (int i = 9; i >= 1; --i) {
+    const double c = kAtanP[i];
+    p1 = fma(p1, z1, c);
+    p2 = fma(p2, z2, c);
+  }
+  const double at1 = fma(t1 * z1, p1, t1), at2 = fma(t2 * z2, p2, t2);
+  const int code1 = (big1 ? 1 : 0) | (ay1 > ax1 ? 2 : 0) | ((__double_as_longlong(x1) < 0) ? 4 : 0);
+  const int code2 = (big2 ? 1 : 0) | (ay2 > ax2 ? 2 : 0) | ((__double_as_longlong(x2) < 0) ? 4 : 0);
+  const double s1 = ((0xC3u >> code1) & 1u) ? at1 : -at1, s2 = ((0xC3u >> code2) & 1u) ? at2 : -at2;
+  const double q1 = kAtanBase[code1] + s1, q2 = kAtanBase[code2] + s2;
+  r1 = (__double_as_longlong(y1) < 0) ? -q1 : q1;
+  r2 = (__double_as_longlong(y2) < 0) ? -q2 : q2;
+}
+
 // ----------------------------------------------------------------------------
 // Infeasible arc of constraint (p, q, b) on the ellipse (Eq. 2, eq:roots):
 // r = |(p, q)|; active iff r > b (C3); tau = atan2(q, p);
@@ -260,8 +290,8 @@ __device__ __forceinline__ bool arc_of(double p, double q, double b, double& alp
   const double s2 = fma(p, p, fma(q, q, -b * b));  // p^2 + q^2 - b^2 (as in arc_active)
   if (!(b < 0.0 || s2 > 0.0)) return false;
   const double s = sqrt(fmax(s2, 0.0));
-  const double tau = fast_atan2(q, p);
-  const double delta = fast_atan2(s, b);
+  double tau, delta;
+  fast_atan2_2(q, p, s, b, tau, delta);
   double lo = __dsub_rn(tau, delta);
   double hi = __dadd_rn(tau, delta);
   if (hi <= 0.0) {

@@ -305,6 +305,25 @@ def main():
                     "avg_launch_ms": tc_avg_ms, "share_of_step": prof["tc_ms"] / ms_iso,
                     "measured_in": roofline["measured_in"],
                     "refresh_gemm": dmma, "ess_kernel": roofline["ess_kernel"]}
+    # the contract's roofline is the DOMINANT kernel's: when the fused per-chain kernel
+    # takes the larger share of the step it moves to the top level (HBM roofline of its
+    # algorithmic bytes), the projection GEMM nested beside it
+    if roofline["ess_kernel"]["share_of_step"] > roofline["share_of_step"]:
+        ess = dict(roofline.pop("ess_kernel"))
+        ess["kernel"] = "ess_kernel (arcs, Alg. 3 intervals, theta, P', safeguard, x update, moments, next nu)"
+        ess["traffic"], ess["traffic_source"] = None, None
+        try:
+            sj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_full_int8_summary.json")))
+            e = sj["ess_kernel<8>"]
+            if args.config == 3 and world == 1:
+                ess["traffic"] = (float(e["dram__bytes_read.sum"]["value"]) +
+                                  float(e["dram__bytes_write.sum"]["value"])) * 1e6
+                ess["traffic_source"] = "profiles/r01/ncu_full_int8_summary.json"
+        except Exception:
+            pass
+        ess["measured_in"] = roofline["measured_in"]
+        ess["projection_gemm"] = roofline
+        roofline = ess
     gpu_launches = prof_main["launches"]
 
     # ---- end to end through the public API with host buffers (pinned), rank-local

@@ -118,6 +118,15 @@ typedef struct {
   /* Digits S of the int8 projection: 6, 7 or 8 (0 = default 7: 55-bit fixed
    * point, 28 int8 MMAs per 32-wide K step). */
   int32_t ozaki_slices;
+  /* 1: nu for iteration t + 1 is drawn by a small kernel on a second stream
+   * while the projection GEMM of iteration t runs (on the CUDA cores the
+   * tensor-core GEMM leaves idle), into the other of two nu buffers; the fused
+   * per-chain kernel then only reads nu.  0 (default): the fused kernel draws nu
+   * for t + 1 after its update (measured faster on B200 at config 3: 0.410 vs
+   * 0.422 ms per iteration -- the co-running RNG slows the GEMM by ~20 us, the
+   * per-chain kernel gains ~20 us).  Single shard only.  Results do not depend
+   * on it (tested bitwise). */
+  int32_t rng_ahead;
 } tmvn_options;
 
 typedef struct {
@@ -133,7 +142,9 @@ typedef struct {
   double gemm_flops;     /* algorithmic flops of those GEMMs: 2 C m d each (no padding)      */
   int64_t ess_launches;  /* fused per-chain ESS launches timed                               */
   double ess_ms;
-  double ess_bytes;      /* algorithmic HBM bytes of those launches    */
+  double ess_bytes;      /* algorithmic HBM bytes of those launches:
+                            24 B per constraint-eval + 32 B per chain-coordinate (+32 B
+                            when the iteration is recorded into the moments)             */
   int64_t tc_launches;   /* hot-loop int8 tcgen05 projections timed (options.projection = 1) */
   double tc_ms;
   double tc_ops;         /* int8 tensor ops issued by those launches: S(S+1)/2 * 2 C m d     */

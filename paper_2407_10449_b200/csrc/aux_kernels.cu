@@ -42,6 +42,34 @@ __global__ void normals_kernel(double* __restrict__ N, int C, int d, int64_t d_p
   }
 }
 
+// nu of iteration t (t_dev: graph replay, t offset from device memory) into the tiled
+// FP64 N and, for the int8 projection, its digits Ns.  Launched on a second stream
+// beside the projection GEMM of the previous iteration (five 128-thread CTAs of 32
+// registers per SM: they fit next to the GEMM's CTA -- 320 threads x 128 registers,
+// no TMEM for them -- and use the CUDA cores the tensor-core GEMM leaves idle).
+__global__ void __launch_bounds__(128, 5) nu_kernel(double* __restrict__ N, int8_t* __restrict__ Ns, int S,
+                                                    int64_t KB, int C, int d, int64_t d_pad, uint64_t seed,
+                                                    uint32_t t, const uint32_t* __restrict__ t_dev,
+                                                    uint32_t chain_offset) {
+  const uint32_t tt = t_dev ? *t_dev + t : t;
+  // a warp = 4 consecutive chains x 8 consecutive pairs (16 coordinates): its nu stores
+  // are 4 adjacent 64-byte runs of the tiled layout, its digit stores 64 contiguous
+  // bytes per digit slice (4 rows x 16 bytes of one core matrix): whole sectors
+  const int pblocks = (int)(d_pad / 16);
+  const int64_t cblocks = (C + 3) / 4;
+  const int64_t nw = cblocks * pblocks;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int c = (int)((w / pblocks) * 4 + (lane >> 3));
+    const int k0 = (int)(w % pblocks) * 16 + 2 * (lane & 7);
+    if (c >= C) continue;
+    const double2 v = normal_pair_at(seed, tt, chain_offset + (uint32_t)c, k0, d);
+    *reinterpret_cast<double2*>(N + tiled_offset(c, k0, d_pad)) = v;
+    if (Ns) oz_store_nu_pair(Ns, c, k0, v.x, v.y, S, KB);
+  }
+}
+
 __global__ void start_check_kernel(const double* __restrict__ P, int64_t ldp,
                                    const double* __restrict__ b, int C, int m,
                                    unsigned long long* flag) {
@@ -239,6 +267,23 @@ cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed
   int64_t n = (int64_t)C * (d_pad / 2);
   if (n == 0) return cudaSuccess;
   normals_kernel<<<grid_for(n), 256, 0, st>>>(N, C, d, d_pad, seed, t, chain_offset);
+  return cudaGetLastError();
+}
+cudaError_t launch_nu(double* N, int8_t* Ns, int S, int64_t KB, int C, int d, int64_t d_pad,
+                      uint64_t seed, uint32_t t, const uint32_t* t_dev, uint32_t chain_offset,
+                      cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if ((int64_t)C * (d_pad / 2) == 0) return cudaSuccess;
+#ifndef TMVN_RNG_CTAS_PER_SM
+#define TMVN_RNG_CTAS_PER_SM 5
+#endif
+  nu_kernel<<<sms * TMVN_RNG_CTAS_PER_SM, 128, 0, st>>>(N, Ns, S, KB, C, d, d_pad, seed, t, t_dev,
+                                                         chain_offset);
   return cudaGetLastError();
 }
 cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, int C, int m,

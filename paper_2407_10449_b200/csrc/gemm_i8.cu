@@ -52,7 +52,9 @@ constexpr int kOzBN = kOzNuRows;  // chains per tile (MMA N)
 constexpr int kOzBK = kOzStepK;   // K bytes per stage (one MMA K step for kind::i8)
 constexpr int kASlice = kOzBM * kOzBK;  // 4096 bytes
 constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
-constexpr int kOzEpiWarps = 8;   // two per TMEM lane quadrant, half of the columns each
+// 4 epilogue warps (one per TMEM lane quadrant): 320 threads x 128 registers leave
+// room on the SM for the RNG kernel that draws the next nu beside the GEMM
+constexpr int kOzEpiWarps = 4;
 constexpr int kOzThreads = 32 * (6 + kOzEpiWarps);  // producer, MMA, 4 A loaders, epilogue
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
 // ring depth: as many stages as fit in 226 KB of shared memory (S = 6: 6, 7: 5, 8: 4)
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         }
       }
     }
-  } else {  // ---- epilogue: warps 6.. (warps 6-9 columns 0-31, warps 10-13 columns 32-63)
+  } else {  // ---- epilogue: warps 6.. (with 8 warps: 6-9 columns 0-31, 10-13 columns 32-63)
     const int quad = warp & 3;
     const int c0 = ((warp - 6) / 4) * (kOzBN * 4 / kOzEpiWarps);
     const int row_in_tile = quad * 32 + lane;

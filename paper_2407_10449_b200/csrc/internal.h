@@ -123,6 +123,11 @@ cudaError_t launch_unpack(const double* src, int64_t R, int64_t K, int64_t K_pad
 // nu for iteration t of chains [0, C) (global index chain_offset + c) into tiled N.
 cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed, uint32_t t,
                            uint32_t chain_offset, cudaStream_t st);
+// nu of iteration t (+ *t_dev when non-null) into tiled N and, when Ns != nullptr, its
+// S int8 digits (KB K steps); one 128-thread CTA per SM (runs beside the GEMM).
+cudaError_t launch_nu(double* N, int8_t* Ns, int S, int64_t KB, int C, int d, int64_t d_pad,
+                      uint64_t seed, uint32_t t, const uint32_t* t_dev, uint32_t chain_offset,
+                      cudaStream_t st);
 // first (c, i) with P[c, i] - b[i] >= 0 (strict start, C18); *flag = c * m + i or -1.
 cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, int C, int m,
                                unsigned long long* flag, cudaStream_t st);

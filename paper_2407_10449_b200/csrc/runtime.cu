@@ -46,6 +46,10 @@ struct tmvn_ctx {
   // chains
   int64_t C_cap = 0, C_pad = 0;
   double *X = nullptr, *N = nullptr, *P0 = nullptr, *P1 = nullptr, *Q = nullptr;
+  double* N2 = nullptr;  // second nu buffer: nu_t lives in buffer t & 1 when the RNG runs ahead
+  // the RNG stream: nu_{t+1} is drawn beside the projection GEMM of iteration t
+  cudaStream_t rng_stream = nullptr;
+  cudaEvent_t ev_pre = nullptr, ev_rng = nullptr;
   double *S1 = nullptr, *S2 = nullptr;       // tiled moments (u-space == x-space w/o affine)
   double *S1x = nullptr, *S2x = nullptr;     // row-major x-space moments (affine)
   double *stage = nullptr, *stage2 = nullptr;  // row-major C_pad x max(d_pad, d_r128)
@@ -61,6 +65,7 @@ struct tmvn_ctx {
   double* rowscale = nullptr; // m_pad
   int ozS_A = 0;
   int8_t* Ns = nullptr;       // digits of nu (C_pad rows)
+  int8_t* Ns2 = nullptr;      // second buffer (nu of odd iterations when the RNG runs ahead)
   int ozS_N = 0;
   int64_t Ns_rows = 0;
   int64_t ozKB = 0;
@@ -138,11 +143,11 @@ std::vector<double> to_host(const double* p, size_t n) {
 cudaStream_t stream_of(const tmvn_ctx* h) { return (cudaStream_t)h->opt.stream; }
 
 void free_chain_buffers(tmvn_ctx* h) {
-  dfree(h->X); dfree(h->N); dfree(h->P0); dfree(h->P1); dfree(h->Q);
+  dfree(h->X); dfree(h->N); dfree(h->N2); dfree(h->P0); dfree(h->P1); dfree(h->Q);
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
   dfree(h->stage); dfree(h->stage2); dfree(h->rej);
   dfree(h->gstash); dfree(h->ggaps);
-  dfree(h->Ns);
+  dfree(h->Ns); dfree(h->Ns2);
   h->Ns_rows = 0;
   h->ozS_N = 0;
   h->C_cap = h->C_pad = 0;
@@ -156,6 +161,7 @@ tmvn_status ensure_chains(tmvn_ctx* h, int64_t C) {
   const size_t wide = (size_t)C_pad * std::max(h->d_pad, h->d_r128);
   CK(h, dalloc(&h->X, cd));
   CK(h, dalloc(&h->N, cd));
+  CK(h, dalloc(&h->N2, cd));
   CK(h, dalloc(&h->P0, cm));
   CK(h, dalloc(&h->P1, cm));
   CK(h, dalloc(&h->Q, cm));
@@ -232,36 +238,56 @@ tmvn_status ensure_ozaki(tmvn_ctx* h) {
     h->ozKB = KB;
   }
   if (h->ozS_N != S || h->Ns_rows < h->C_pad) {
-    dfree(h->Ns);
+    dfree(h->Ns); dfree(h->Ns2);
     CK(h, dalloc(&h->Ns, (size_t)h->C_pad * KB * kOzStepK * S));
+    CK(h, dalloc(&h->Ns2, (size_t)h->C_pad * KB * kOzStepK * S));
     h->ozS_N = S;
     h->Ns_rows = h->C_pad;
   }
   return TMVN_OK;
 }
 
-int8_t* oz_rows(const tmvn_ctx* h, int64_t c0) {
-  return h->Ns + (c0 / kOzNuRows) * h->ozKB * kOzStepK * oz_slices(h) * kOzNuRows;
+// nu buffers: buffer b holds nu of the iterations t with t & 1 == b when the RNG runs
+// ahead on its own stream; buffer 0 otherwise
+double* nu_f64(const tmvn_ctx* h, int b) { return b ? h->N2 : h->N; }
+int8_t* nu_dig(const tmvn_ctx* h, int b) { return b ? h->Ns2 : h->Ns; }
+
+int8_t* oz_rows(const tmvn_ctx* h, int64_t c0, int b = 0) {
+  return nu_dig(h, b) + (c0 / kOzNuRows) * h->ozKB * kOzStepK * oz_slices(h) * kOzNuRows;
 }
 
-// Q rows [c0, c0 + Rp) = nu A'^T by the configured projection.
-cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStream_t st) {
+// Q rows [c0, c0 + Rp) = nu A'^T by the configured projection (nu from buffer b).
+cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStream_t st, int b = 0) {
   if (use_oz(h))
-    return launch_ozaki_gemm(h->As, h->m_pad, oz_rows(h, c0), Rp, h->ozKB, oz_slices(h), h->rowscale,
+    return launch_ozaki_gemm(h->As, h->m_pad, oz_rows(h, c0, b), Rp, h->ozKB, oz_slices(h), h->rowscale,
                              h->Q + c0 * h->m_pad, h->m_pad, st);
-  return launch_gemm_tn(h->N + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad, h->Q + c0 * h->m_pad,
-                        h->m_pad, st);
+  return launch_gemm_tn(nu_f64(h, b) + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad,
+                        h->Q + c0 * h->m_pad, h->m_pad, st);
 }
 
 // nu of iteration t for chains [0, C) (and its digits for the int8 projection).
-cudaError_t launch_first_nu(tmvn_ctx* h, int64_t C, uint64_t seed, uint32_t t, cudaStream_t st) {
-  cudaError_t e = launch_normals(h->N, (int)C, (int)h->d, h->d_pad, seed, t,
+cudaError_t launch_first_nu(tmvn_ctx* h, int64_t C, uint64_t seed, uint32_t t, cudaStream_t st, int b = 0) {
+  cudaError_t e = launch_normals(nu_f64(h, b), (int)C, (int)h->d, h->d_pad, seed, t,
                                  (uint32_t)h->opt.chain_offset, st);
   h->prof.launches += 1;
   if (e != cudaSuccess || !use_oz(h)) return e;
   h->prof.launches += 1;
-  return launch_oz_slice(h->N, C, h->d, h->d_pad, oz_slices(h), h->ozKB, kOzNuRows, 0, kOzNuExp, 0,
-                         h->Ns, nullptr, st);
+  return launch_oz_slice(nu_f64(h, b), C, h->d, h->d_pad, oz_slices(h), h->ozKB, kOzNuRows, 0, kOzNuExp,
+                         0, nu_dig(h, b), nullptr, st);
+}
+
+// nu of iteration t (+ *t_dev) into buffer b, on the RNG stream
+cudaError_t launch_nu_ahead(tmvn_ctx* h, int64_t C, uint64_t seed, uint32_t t, const uint32_t* t_dev,
+                            int b, cudaStream_t st) {
+  return launch_nu(nu_f64(h, b), use_oz(h) ? nu_dig(h, b) : nullptr, oz_slices(h), h->ozKB, (int)C,
+                   (int)h->d, h->d_pad, seed, t, t_dev, (uint32_t)h->opt.chain_offset, st);
+}
+
+tmvn_status ensure_rng_stream(tmvn_ctx* h) {
+  if (!h->rng_stream) CK(h, cudaStreamCreateWithFlags(&h->rng_stream, cudaStreamNonBlocking));
+  if (!h->ev_pre) CK(h, cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
+  if (!h->ev_rng) CK(h, cudaEventCreateWithFlags(&h->ev_rng, cudaEventDisableTiming));
+  return TMVN_OK;
 }
 
 bool finite_all(const std::vector<double>& v) {
@@ -361,16 +387,20 @@ bool recorded_iter(const tmvn_options& o, int64_t t) {
 // read t from h->d_tbase (set by a one-thread kernel before each replay) and
 // compute their record flag from t, so one graph serves every aligned block.
 tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K, double* Pc,
-                        double* Pn, cudaGraphExec_t* out) {
+                        double* Pn, bool ahead, uint64_t seed, cudaGraphExec_t* out) {
   const int parity = Pc == h->P0 ? 0 : 1;
   EssParams p = base;
   p.t_dev = h->d_tbase;
   p.rec_dev = 1;
-  p.gen_next = 1;
+  p.gen_next = ahead ? 0 : 1;
+  if (ahead) p.Ns = nullptr;
   p.t = 0;
   p.P_cur = Pc;
   p.P_next = Pn;
-  std::vector<unsigned char> sig(sizeof(EssParams) + 2 * sizeof(int64_t) + 2 * sizeof(void*));
+  std::vector<unsigned char> sig(sizeof(EssParams) + 2 * sizeof(int64_t) + 2 * sizeof(void*) + 16);
+  std::memcpy(sig.data() + sizeof(EssParams) + 16 + 2 * sizeof(void*), &seed, 8);
+  const int64_t ah = ahead ? 1 : 0;
+  std::memcpy(sig.data() + sizeof(EssParams) + 24 + 2 * sizeof(void*), &ah, 8);
   std::memcpy(sig.data(), &p, sizeof(EssParams));
   std::memcpy(sig.data() + sizeof(EssParams), &C, sizeof(int64_t));
   std::memcpy(sig.data() + sizeof(EssParams) + 8, &K, sizeof(int64_t));
@@ -390,13 +420,24 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
   CK(h, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   cudaError_t err = cudaSuccess;
   double *pc = Pc, *pn = Pn;
+  // block start t is a multiple of K (even): nu_{t+i} in buffer i & 1
   for (int64_t i = 0; i < K && err == cudaSuccess; ++i) {
-    err = launch_projection(h, 0, Rp, cs);
+    if (ahead) {  // nu_{t+i+1} on the RNG stream, beside this projection
+      if ((err = cudaEventRecord(h->ev_pre, cs)) != cudaSuccess) break;
+      if ((err = cudaStreamWaitEvent(h->rng_stream, h->ev_pre, 0)) != cudaSuccess) break;
+      if ((err = launch_nu_ahead(h, C, seed, (uint32_t)(i + 1), h->d_tbase, (int)((i + 1) & 1),
+                                 h->rng_stream)) != cudaSuccess)
+        break;
+      if ((err = cudaEventRecord(h->ev_rng, h->rng_stream)) != cudaSuccess) break;
+    }
+    err = launch_projection(h, 0, Rp, cs, ahead ? (int)(i & 1) : 0);
     if (err != cudaSuccess) break;
     p.t = (uint32_t)i;
     p.P_cur = pc;
     p.P_next = pn;
+    p.N = nu_f64(h, ahead ? (int)(i & 1) : 0);
     err = launch_ess_step(p, h->plan.grid, cs);
+    if (err == cudaSuccess && ahead) err = cudaStreamWaitEvent(cs, h->ev_rng, 0);  // join: nu_{t+i+1} ready
     std::swap(pc, pn);
   }
   if (err == cudaSuccess) err = launch_gemm_tn(h->X, Rp, h->At, h->m_pad, h->d_pad, pc, h->m_pad, cs);
@@ -423,7 +464,14 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
   const int64_t t0 = h->opt.iter_offset;
   const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
   double* P_next = (P_cur == h->P0) ? h->P1 : h->P0;
-  CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st));
+  // nu_{t+1} drawn on the RNG stream beside the projection GEMM of iteration t (one
+  // shard, options.rng_ahead): nu_t lives in buffer t & 1
+  const bool ahead = h->opt.rng_ahead != 0 && h->nshards == 1 && !h->trace_dev;
+  if (ahead) {
+    tmvn_status rs = ensure_rng_stream(h);
+    if (rs != TMVN_OK) return rs;
+  }
+  CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st, ahead ? (int)(t0 & 1) : 0));
   // ---- shards
   int S = h->nshards;
   const int64_t per = round_up((C + S - 1) / S, kTileR);
@@ -491,11 +539,11 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     if (graphs && t % K == 0 && n_iter - it >= K) {  // a whole aligned block: replay
       Shard& x = sh[0];
       cudaGraphExec_t ge;
-      tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, &ge);
+      tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, ahead, seed, &ge);
       if (gs != TMVN_OK) return gs;
       KL(h, launch_set_u32(h->d_tbase, (uint32_t)t, st));
       CK(h, cudaGraphLaunch(ge, st));
-      h->prof.launches += 2 * K + 1;
+      h->prof.launches += (ahead ? 3 : 2) * K + 1;
       for (int64_t i = 0; i < K; ++i) nrec += recorded_iter(h->opt, t + i) ? 1 : 0;
       it += K - 1;  // K even: P parity unchanged, the block ends with the refresh
       continue;
@@ -504,13 +552,25 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     for (int s = 0; s < S; ++s) {
       Shard& x = sh[s];
       const int64_t Rp = round_up(x.C, kTileR);
-      TIMED(use_oz(h) ? 2 : 0, x.C, x.st, launch_projection(h, x.c0, Rp, x.st));
+      const int b = ahead ? (int)(t & 1) : 0;
+      if (ahead && it + 1 < n_iter) {  // nu_{t+1} into the other buffer, beside this projection
+        CK(h, cudaEventRecord(h->ev_pre, x.st));
+        CK(h, cudaStreamWaitEvent(h->rng_stream, h->ev_pre, 0));
+        KL(h, launch_nu_ahead(h, C, seed, (uint32_t)(t + 1), nullptr, b ^ 1, h->rng_stream));
+        CK(h, cudaEventRecord(h->ev_rng, h->rng_stream));
+      }
+      TIMED(use_oz(h) ? 2 : 0, x.C, x.st, launch_projection(h, x.c0, Rp, x.st, b));
       x.p.P_cur = x.Pc;
       x.p.P_next = x.Pn;
       x.p.t = (uint32_t)t;
-      x.p.gen_next = (it + 1 < n_iter) ? 1 : 0;
+      x.p.gen_next = (!ahead && it + 1 < n_iter) ? 1 : 0;
+      if (ahead) {
+        x.p.N = nu_f64(h, b);
+        x.p.Ns = nullptr;
+      }
       x.p.record = (rec && !h->affine) ? 1 : 0;
-      TIMED(1, x.C, x.st, launch_ess_step(x.p, h->plan.grid, x.st));
+      TIMED(x.p.record ? 3 : 1, x.C, x.st, launch_ess_step(x.p, h->plan.grid, x.st));
+      if (ahead && it + 1 < n_iter) CK(h, cudaStreamWaitEvent(x.st, h->ev_rng, 0));  // nu_{t+1} ready
       std::swap(x.Pc, x.Pn);
       if (rec && h->affine) {
         double* stg = h->stage + x.c0 * h->d_r128;
@@ -553,10 +613,11 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
         h->prof.gemm_flops += 2.0 * nC * (double)h->m * (double)h->d;
       } else {
         // P, Q read + P' write (24 B per constraint-eval); X r/w, nu read + next nu write
-        // (32 B per chain-coordinate)
+        // (32 B per chain-coordinate); moments S1, S2 r/w when recorded (32 B per
+        // chain-coordinate, kind 3)
         h->prof.ess_launches += 1;
         h->prof.ess_ms += ms;
-        h->prof.ess_bytes += 24.0 * nC * (double)h->m + 32.0 * nC * (double)h->d;
+        h->prof.ess_bytes += 24.0 * nC * (double)h->m + (kinds[k] == 3 ? 64.0 : 32.0) * nC * (double)h->d;
       }
     }
   }
@@ -665,6 +726,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->graphs = 1;
   o->projection = 0;
   o->ozaki_slices = 0;
+  o->rng_ahead = 0;  // measured slower on B200 (the GEMM loses more than the ESS kernel gains)
   return TMVN_OK;
 }
 
@@ -859,6 +921,9 @@ void tmvn_destroy(tmvn_handle h) {
   for (int i = 0; i < 2; ++i)
     if (h->graph_exec[i]) cudaGraphExecDestroy(h->graph_exec[i]);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
+  if (h->rng_stream) cudaStreamDestroy(h->rng_stream);
+  if (h->ev_pre) cudaEventDestroy(h->ev_pre);
+  if (h->ev_rng) cudaEventDestroy(h->ev_rng);
   dfree(h->d_tbase);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);

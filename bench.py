@@ -52,10 +52,14 @@ def parse():
 
 
 def config_dict(cfg, args, world):
-    return {"workload": f"BASELINE config {args.config} ({cfg.key}): {cfg.desc}",
+    name = f"BASELINE config {args.config}" if args.config <= 5 else "paper S4.2 timing workload (not a BASELINE config)"
+    return {"workload": f"{name} ({cfg.key}): {cfg.desc}",
             "d": cfg.d, "m": cfg.m, "chains_per_gpu": cfg.C, "chains_total": cfg.C * world,
             "iters_per_step": args.iters_per_step, "recompute_every": 32,
-            "l2": "no flush: working set (X, nu, P x2, Q, A) >> 126 MB L2",
+            "l2": ("no flush: working set (X, nu, P x2, Q, A) >> 126 MB L2"
+                   if 8 * (cfg.C * (4 * cfg.m + 3 * cfg.d) + cfg.m * cfg.d) > 126e6 else
+                   "no flush: the working set fits in the 126 MB L2 (latency-bound workload; the "
+                   "sampler's state stays resident by design)"),
             "parallelism": f"chains sharded over {world} GPU(s), A and b replicated"}
 
 

@@ -38,6 +38,11 @@ CONFIGS = {
               "d=100, m=100000, unit-norm Gaussian rows, b ~ U[0.5,2.0], x0=0"),
     5: Config("boxscale", 4096, 16384, 65536, 100, 5, 105,
               "d=4096, m=16384, unit-norm Gaussian rows, b ~ U[0.2,1.0], x0=0"),
+    # not a BASELINE config: the paper's own timing workload (S4.2; SURVEY
+    # 8(f) NEXT-1) -- m = d, A iid N(0,1) (not normalised), x0 ~ N(0, I),
+    # b = A x0 + U[0,1]^d, 10 chains
+    6: Config("paper_s42", 1000, 1000, 10, 1000, 42, 106,
+              "paper S4.2: d=m=1000, A iid N(0,1), x0 ~ N(0,I), b = A x0 + U[0,1]^d, 10 chains"),
 }
 
 _B_RANGE = {1: (0.5, 1.5), 3: (0.1, 1.0), 4: (0.5, 2.0), 5: (0.2, 1.0)}
@@ -53,6 +58,8 @@ def make_instance(k: int, m: int | None = None, d: int | None = None):
     m = cfg.m if m is None else m
     d = cfg.d if d is None else d
     rng = np.random.default_rng(cfg.inst_seed)
+    if k == 6:
+        return paper_random(d, seed=cfg.inst_seed)
     if k == 2:
         A = -np.eye(d, dtype=np.float64)[:m]
         b = np.zeros(m)

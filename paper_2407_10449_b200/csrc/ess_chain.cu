@@ -39,6 +39,10 @@ constexpr uint64_t kTopBits = 0x7FF0000000000000ull;  // +inf: every alpha in [0
 #define TMVN_ESS_BATCH 2
 #endif
 constexpr int kBatch = TMVN_ESS_BATCH;  // constraint pairs per thread with loads in flight
+#ifndef TMVN_ESS_BATCH_A1
+#define TMVN_ESS_BATCH_A1 2
+#endif
+constexpr int kBatchA1 = TMVN_ESS_BATCH_A1;  // the same in the active-test pass (fewer live registers)
 
 __device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
 __device__ __forceinline__ double bitsd(uint64_t b) { return __longlong_as_double((long long)b); }
@@ -66,7 +70,7 @@ enum { kAll = 0, kPrefix = 1, kSame = 2, kNarrow = 3 };
 // the product build): thread 0 of every group accumulates clock64 deltas between
 // the barriers that close each phase.
 #ifdef TMVN_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[10];
+__device__ unsigned long long g_phase_cycles[14];
 #define PHASE(i)                      \
   do {                                \
     if (g.tid == 0) {                 \
@@ -702,7 +706,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
   const double scale = __ddiv_rn((double)NB, kTwoPi);
   const int64_t ngroups = (int64_t)gridDim.x * kGroups;
 #ifdef TMVN_PHASE_TIMING
-  long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long t_prev = clock64();
 #endif
 
@@ -875,10 +879,10 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
       const double2* B2 = reinterpret_cast<const double2*>(p.b);
       int* sidx = reinterpret_cast<int*>(stash + m);
       const int npairs = (m + 1) / 2;
-      for (int base = 0; base < npairs; base += kBatch * T) {
-        double2 pp[kBatch], qq[kBatch], bb[kBatch];
+      for (int base = 0; base < npairs; base += kBatchA1 * T) {
+        double2 pp[kBatchA1], qq[kBatchA1], bb[kBatchA1];
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
+        for (int u = 0; u < kBatchA1; ++u) {
           const int pi = base + u * T + g.tid;
           if (pi < npairs) {
             pp[u] = P2[pi];
@@ -887,7 +891,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
           }
         }
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
+        for (int u = 0; u < kBatchA1; ++u) {
           if (base + u * T >= npairs) break;  // uniform
           const int pi = base + u * T + g.tid;
 #pragma unroll
@@ -916,6 +920,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
         }
       }
       g.sync();
+      PHASE(10);  // A1: active test + compaction (the rest of phase A goes to slot 1)
       const int n_act = ctl.n_act;
       for (int slot = g.tid; slot < n_act; slot += T) {
         const double2 pq = stash[slot];
@@ -1141,7 +1146,7 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
   g.sync();
   PHASE(6);
   if (g.tid == 0)
-    for (int i = 0; i < 10; ++i) atomicAdd(&g_phase_cycles[i], (unsigned long long)ph[i]);
+    for (int i = 0; i < 14; ++i) atomicAdd(&g_phase_cycles[i], (unsigned long long)ph[i]);
 #endif
 }
 
@@ -1198,10 +1203,9 @@ int occupancy_w(size_t smem, bool ring, bool smem_stash) {
 
 #ifdef TMVN_PHASE_TIMING
 void phase_cycles(unsigned long long* out, bool reset) {
-  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 10);
-  for (int i = 10; i < 14; ++i) out[i] = 0;
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 14);
   if (reset) {
-    unsigned long long z[10] = {0};
+    unsigned long long z[14] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
   }
 }

@@ -22,10 +22,11 @@ buf = np.zeros(14, dtype=np.uint64)
 L.tmvn_test_phase_cycles(buf.ctypes.data_as(ctypes.c_void_p), 1)
 s.sample(X, iters, cfg.chain_seed, out=X)
 L.tmvn_test_phase_cycles(buf.ctypes.data_as(ctypes.c_void_p), 0)
-names = ["init", "A arcs+stats", "lo-word pass", "B intervals", "C theta", "D1 P'+safeguard",
+names = ["init", "A2 arcs+stats", "lo-word pass", "B intervals", "C theta", "D1 P'+safeguard",
          "D2 x/moments/nu"]
 nchain = cfg.C * iters
-tot = float(sum(buf[:7]))
+tot = float(sum(buf[:7])) + float(buf[10])
 print(f"config {k}: {nchain} chain-iterations; mean active arcs {buf[8]/nchain:.1f}, gaps {buf[9]/nchain:.2f}, general path {buf[7]/nchain:.3f}")
+print(f"  {'A1 active+compact':18s} {buf[10]/nchain:10.0f} cycles/chain  {100*buf[10]/tot:5.1f}%")
 for i, n in enumerate(names):
     print(f"  {n:18s} {buf[i]/nchain:10.0f} cycles/chain  {100*buf[i]/tot:5.1f}%")

@@ -127,6 +127,10 @@ typedef struct {
    * per-chain kernel gains ~20 us).  Single shard only.  Results do not depend
    * on it (tested bitwise). */
   int32_t rng_ahead;
+  /* Chain scheduling of the fused per-chain kernel: 0 (default) dynamic (each
+   * group of warps grabs its next chain with an atomic counter, one chain ahead),
+   * 1 round-robin.  Results do not depend on it. */
+  int32_t schedule;
 } tmvn_options;
 
 typedef struct {

@@ -48,7 +48,8 @@ class options(ctypes.Structure):
                 ("profile", ctypes.c_int32), ("chain_warps", ctypes.c_int32),
                 ("streams", ctypes.c_int32), ("ring", ctypes.c_int32),
                 ("graphs", ctypes.c_int32), ("projection", ctypes.c_int32),
-                ("ozaki_slices", ctypes.c_int32), ("rng_ahead", ctypes.c_int32)]
+                ("ozaki_slices", ctypes.c_int32), ("rng_ahead", ctypes.c_int32),
+                ("schedule", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):

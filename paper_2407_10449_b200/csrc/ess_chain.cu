@@ -61,6 +61,7 @@ struct Ctl {
   int maxa_exact;       // max/min alpha per bucket exact (refinement levels)
   int fast;             // 1: I_act built by the parallel level-1 path
   int ncand;            // gaps found by the parallel path
+  int next;             // dynamic scheduling: the chain grabbed for the next round
   double u;             // u_{c,t} of "sample theta uniformly" (drawn at the chain's start)
 };
 
@@ -752,7 +753,17 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
     record = tt >= p.burn_in && ((tt - p.burn_in) % (p.thin < 1 ? 1 : p.thin)) == 0;
   }
 
-  for (int64_t cc = gglobal; cc < p.C; cc += ngroups) {
+  // dynamic scheduling: a group grabs its next chain one round ahead (so its rows can
+  // be prefetched); groups that finish early take more chains
+  const bool dyn = !kGiven && !kRing && p.dyn_ctr != nullptr;
+  int* ctr = dyn ? p.dyn_ctr + (t_it & 63) : nullptr;
+  if (dyn) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.dyn_ctr[(t_it + 32) & 63] = 0;
+    if (g.tid == T - 1) ctl.next = atomicAdd(ctr, 1);
+    g.sync();
+  }
+  for (int64_t cc = dyn ? (int64_t)ctl.next : gglobal; cc < p.C;
+       cc = dyn ? (int64_t)ctl.next : cc + ngroups) {
     const int c = (int)cc;
     const uint32_t gchain = p.chain_offset + (uint32_t)c;
     g.sync();
@@ -770,7 +781,8 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
       // u for this chain (Philox latency hidden behind phase A); the next chain's
       // P and Q rows are pulled into L2 now, so its phase A loads hit L2
       ctl.u = theta_uniform(p.seed, t_it, gchain);
-      const int64_t cn = cc + ngroups;
+      if (dyn) ctl.next = atomicAdd(ctr, 1);
+      const int64_t cn = dyn ? (int64_t)ctl.next : cc + ngroups;
       if (!kRing && cn < p.C) {
         const uint32_t bytes = (uint32_t)(((int64_t)m * 8 + 15) & ~15ll);
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.P_cur + cn * p.ldp), "r"(bytes)

@@ -49,6 +49,8 @@ struct EssParams {
   int rec_dev;      // 1: record flag computed from t (t >= burn_in, (t - burn_in) % thin == 0)
   int64_t burn_in, thin;
   int gen_next;     // 1: draw nu for t + 1 into N after the update
+  int* dyn_ctr;     // non-null: chains handed out dynamically by atomicAdd on dyn_ctr[t & 63]
+                    // (the launch for t zeroes the slot of t + 32); null: round-robin
   int8_t* Ns;       // non-null: also write nu_{t+1}'s S digits (int8 projection, gemm_i8.cu)
   int ozS;
   int64_t ozKB;

@@ -49,6 +49,7 @@ struct tmvn_ctx {
   double* N2 = nullptr;  // second nu buffer: nu_t lives in buffer t & 1 when the RNG runs ahead
   // the RNG stream: nu_{t+1} is drawn beside the projection GEMM of iteration t
   cudaStream_t rng_stream = nullptr;
+  int* dyn = nullptr;  // dynamic chain scheduling counters: 64 slots per shard
   cudaEvent_t ev_pre = nullptr, ev_rng = nullptr;
   double *S1 = nullptr, *S2 = nullptr;       // tiled moments (u-space == x-space w/o affine)
   double *S1x = nullptr, *S2x = nullptr;     // row-major x-space moments (affine)
@@ -472,6 +473,9 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     if (rs != TMVN_OK) return rs;
   }
   CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st, ahead ? (int)(t0 & 1) : 0));
+  if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
+  const bool dyn = h->opt.schedule != 1 && h->nshards <= 16;
+  if (dyn) CK(h, cudaMemsetAsync(h->dyn, 0, sizeof(int) * 64 * 16, st));
   // ---- shards
   int S = h->nshards;
   const int64_t per = round_up((C + S - 1) / S, kTileR);
@@ -495,6 +499,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p.S1 = h->S1 + x.c0 * h->d_pad;
     x.p.S2 = h->S2 + x.c0 * h->d_pad;
     x.p.rej = h->rej + x.c0;
+    x.p.dyn_ctr = dyn ? h->dyn + 64 * s : nullptr;
     x.p.chain_offset = (uint32_t)(h->opt.chain_offset + x.c0);
     x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * h->m : nullptr;
     x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
@@ -727,6 +732,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->projection = 0;
   o->ozaki_slices = 0;
   o->rng_ahead = 0;  // measured slower on B200 (the GEMM loses more than the ESS kernel gains)
+  o->schedule = 0;
   return TMVN_OK;
 }
 
@@ -925,6 +931,7 @@ void tmvn_destroy(tmvn_handle h) {
   if (h->ev_pre) cudaEventDestroy(h->ev_pre);
   if (h->ev_rng) cudaEventDestroy(h->ev_rng);
   dfree(h->d_tbase);
+  dfree(h->dyn);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
   dfree(h->A_tiled); dfree(h->A_row); dfree(h->b_orig); dfree(h->b_eff);

@@ -189,15 +189,16 @@ def test_graph_replay_bitwise_equals_launches():
 
 
 def test_rng_ahead_and_projection_options_bitwise():
-    """options.rng_ahead (nu drawn on a second stream beside the GEMM, double-buffered)
-    and the graph / plain launch paths give bitwise the same chains."""
+    """options.rng_ahead (nu drawn on a second stream beside the GEMM, double-buffered),
+    the chain schedule (dynamic / round-robin) and the graph / plain launch paths give
+    bitwise the same chains."""
     A, b, x0 = synth.make_instance(3, m=300, d=70)
     C = 200
     X0 = np.tile(x0, (C, 1))
     ref = tm.Sampler(A, b, rng_ahead=0, graphs=0).sample(X0, 70, seed=11)
-    for ra, gr in ((1, 0), (1, 1), (0, 1)):
-        out = tm.Sampler(A, b, rng_ahead=ra, graphs=gr).sample(X0, 70, seed=11)
-        assert np.array_equal(out, ref), (ra, gr)
+    for ra, gr, sc in ((1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 1, 1), (0, 0, 1)):
+        out = tm.Sampler(A, b, rng_ahead=ra, graphs=gr, schedule=sc).sample(X0, 70, seed=11)
+        assert np.array_equal(out, ref), (ra, gr, sc)
     # resume at a multiple of recompute_every with nu drawn ahead (plain + graph blocks)
     s = tm.Sampler(A, b, rng_ahead=1)
     a = s.sample(X0, 32, seed=11)

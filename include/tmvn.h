@@ -131,6 +131,13 @@ typedef struct {
    * group of warps grabs its next chain with an atomic counter, one chain ahead),
    * 1 round-robin.  Results do not depend on it. */
   int32_t schedule;
+  /* 1: pipelined schedule (one shard, no profiling): the projection GEMM of
+   * iteration t + 1 runs concurrently with the fused per-chain kernel of
+   * iteration t (Q double-buffered, nu triple-buffered and drawn two iterations
+   * ahead on a third stream, the GEMM in a compact form on a high-priority
+   * stream so that the two kernels share the SMs).  0 (default): serial.
+   * Results do not depend on it. */
+  int32_t pipeline;
 } tmvn_options;
 
 typedef struct {

@@ -44,10 +44,10 @@ __global__ void normals_kernel(double* __restrict__ N, int C, int d, int64_t d_p
 
 // nu of iteration t (t_dev: graph replay, t offset from device memory) into the tiled
 // FP64 N and, for the int8 projection, its digits Ns.  Launched on a second stream
-// beside the projection GEMM of the previous iteration (five 128-thread CTAs of 32
-// registers per SM: they fit next to the GEMM's CTA -- 320 threads x 128 registers,
-// no TMEM for them -- and use the CUDA cores the tensor-core GEMM leaves idle).
-__global__ void __launch_bounds__(128, 5) nu_kernel(double* __restrict__ N, int8_t* __restrict__ Ns, int S,
+// beside the projection GEMM of the previous iteration or the per-chain kernel
+// (small 64-thread CTAs of < 40 registers: one fits in the 4 K registers that three
+// per-chain CTAs leave free on an SM, several next to the GEMM's CTA).
+__global__ void __launch_bounds__(64) nu_kernel(double* __restrict__ N, int8_t* __restrict__ Ns, int S,
                                                     int64_t KB, int C, int d, int64_t d_pad, uint64_t seed,
                                                     uint32_t t, const uint32_t* __restrict__ t_dev,
                                                     uint32_t chain_offset) {
@@ -271,7 +271,7 @@ cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed
 }
 cudaError_t launch_nu(double* N, int8_t* Ns, int S, int64_t KB, int C, int d, int64_t d_pad,
                       uint64_t seed, uint32_t t, const uint32_t* t_dev, uint32_t chain_offset,
-                      cudaStream_t st) {
+                      cudaStream_t st, int ctas_per_sm) {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -279,11 +279,7 @@ cudaError_t launch_nu(double* N, int8_t* Ns, int S, int64_t KB, int C, int d, in
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   if ((int64_t)C * (d_pad / 2) == 0) return cudaSuccess;
-#ifndef TMVN_RNG_CTAS_PER_SM
-#define TMVN_RNG_CTAS_PER_SM 5
-#endif
-  nu_kernel<<<sms * TMVN_RNG_CTAS_PER_SM, 128, 0, st>>>(N, Ns, S, KB, C, d, d_pad, seed, t, t_dev,
-                                                         chain_offset);
+  nu_kernel<<<sms * ctas_per_sm, 64, 0, st>>>(N, Ns, S, KB, C, d, d_pad, seed, t, t_dev, chain_offset);
   return cudaGetLastError();
 }
 cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, int C, int m,

@@ -137,6 +137,21 @@ __device__ __forceinline__ double2 normal_pair_at(uint64_t seed, uint32_t t, uin
   return make_double2(n0, n1);
 }
 
+// Timeline instrumentation (variant build -DTMVN_TIMELINE only; tools/timeline.py):
+// per launch sequence number, the first CTA start and last CTA end (globaltimer ns)
+// of the projection GEMM (slots 0, 1) and of the per-chain kernel (slots 2, 3).
+#ifdef TMVN_TIMELINE
+// each translation unit has its own copy (no relocatable device code); the host
+// helpers tl_access_* of gemm_i8.cu and ess_chain.cu reset / read them
+static __device__ unsigned long long g_tl[256][4];
+static __device__ unsigned int g_tl_seq[2];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // ----------------------------------------------------------------------------
 // Digit layout of the int8 (Ozaki-split) projection operands (gemm_i8.cu).
 // A value v with |v| < 2^e becomes the fixed-point integer

@@ -701,9 +701,9 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
   if (kSmemStash) {
     stash = reinterpret_cast<double2*>(gbase + ess_ring_bytes(CH) + ess_group_base_bytes(NB));
   } else {
-    stash = p.gstash + gglobal * m;
+    stash = p.gstash + (gglobal + p.group_base) * m;
   }
-  double2* gg = p.ggaps + gglobal * (m + 2);
+  double2* gg = p.ggaps + (gglobal + p.group_base) * (m + 2);
   const double scale = __ddiv_rn((double)NB, kTwoPi);
   const int64_t ngroups = (int64_t)gridDim.x * kGroups;
 #ifdef TMVN_PHASE_TIMING
@@ -747,6 +747,9 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
 
   // iteration index and record flag (from device memory under CUDA-graph replay)
   const uint32_t t_it = p.t_dev ? *p.t_dev + p.t : p.t;
+#ifdef TMVN_TIMELINE
+  if (!kGiven && threadIdx.x == 0) atomicMin(&g_tl[t_it & 255][2], tl_now());
+#endif
   int record = p.record;
   if (p.rec_dev) {
     const int64_t tt = (int64_t)t_it;
@@ -1154,6 +1157,9 @@ __global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(c
       if (p.d_accept) p.d_accept[c] = accept ? 1 : 0;
     }
   }
+#ifdef TMVN_TIMELINE
+  if (!kGiven && threadIdx.x == 0) atomicMax(&g_tl[t_it & 255][3], tl_now());
+#endif
 #ifdef TMVN_PHASE_TIMING
   g.sync();
   PHASE(6);
@@ -1281,4 +1287,19 @@ cudaError_t launch_ess_intervals(const EssParams& p, int grid, cudaStream_t st) 
   return launch_any<true>(p, grid, st);
 }
 
+
+#ifdef TMVN_TIMELINE
+void tl_access_ess(unsigned long long* out, bool reset) {
+  cudaDeviceSynchronize();
+  if (reset) {
+    static unsigned long long z[256][4];
+    for (int i = 0; i < 256; ++i) { z[i][0] = z[i][2] = ~0ull; z[i][1] = z[i][3] = 0; }
+    cudaMemcpyToSymbol(g_tl, z, sizeof(z));
+    unsigned int zs[2] = {0, 0};
+    cudaMemcpyToSymbol(g_tl_seq, zs, sizeof(zs));
+  } else {
+    cudaMemcpyFromSymbol(out, g_tl, 256 * 4 * 8);
+  }
+}
+#endif
 }  // namespace tmvn

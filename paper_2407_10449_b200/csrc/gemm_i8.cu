@@ -57,6 +57,7 @@ constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
 constexpr int kOzEpiWarps = 4;
 constexpr int kOzThreads = 32 * (6 + kOzEpiWarps);  // producer, MMA, 4 A loaders, epilogue
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
+int g_oz_launch_seq = 0;  // host-side launch counter (timeline builds label launches with it)
 // ring depth: as many stages as fit in 226 KB of shared memory (S = 6: 6, 7: 5, 8: 4)
 #ifndef TMVN_OZ_MAX_STAGES
 #define TMVN_OZ_MAX_STAGES 6
@@ -186,13 +187,15 @@ __device__ unsigned long long g_oz_cycles[8];
 
 // warps: 0 producer, 1 MMA issuer, 2-5 A loaders, 6-9 epilogue (warp w may access
 // TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31 only: each role covers the 4 quadrants)
-template <int S>
+// STAGES: ring depth (0 = as many as fit; 3 = the compact variant that leaves room
+// on the SM for a CTA of the per-chain kernel when the two run concurrently)
+template <int S, int STAGES>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
                       const double* __restrict__ rowscale, double* __restrict__ Q, int64_t ldq,
-                      int MB, int NBt, int KB) {
+                      int MB, int NBt, int KB, int dbg_seq) {
   constexpr int kStage = oz_stage_bytes(S);
-  constexpr int kOzStages = oz_stages(S);
+  constexpr int kOzStages = STAGES ? STAGES : oz_stages(S);
   constexpr int NTS = oz_nts<S>();
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* ring = smem;
@@ -229,6 +232,12 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (tmem != 0) __trap();  // all 512 columns: the allocation starts at lane 0, column 0
   const int tiles = MB * NBt;
+#ifdef TMVN_TIMELINE
+  const unsigned int tl_slot = (unsigned)dbg_seq & 255;  // host launch sequence number
+  if (threadIdx.x == 0) atomicMin(&g_tl[tl_slot][0], tl_now());
+#else
+  (void)dbg_seq;
+#endif
   OZT(t_start);
 #ifdef TMVN_PHASE_TIMING
   long long acc0 = 0, acc1 = 0, acc2 = 0;
@@ -383,11 +392,15 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   }
 #endif
   __syncthreads();
+#ifdef TMVN_TIMELINE
+  if (threadIdx.x == 0) atomicMax(&g_tl[tl_slot][1], tl_now());
+#endif
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
+
 
 // ---- digit slicing ----------------------------------------------------------
 // One warp per row of a fragment-tiled FP64 matrix (R rows, d columns):
@@ -430,7 +443,9 @@ void oz_cycles(unsigned long long* out8, bool reset) {
 }
 #endif
 
-size_t ozaki_smem_bytes(int S) { return (size_t)oz_stages(S) * oz_stage_bytes(S) + 256; }
+size_t ozaki_smem_bytes(int S, int stages) {
+  return (size_t)(stages ? stages : oz_stages(S)) * oz_stage_bytes(S) + 256;
+}
 
 cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64_t d_pad, int S,
                             int64_t KB, int BR, int per_row, int e_fixed, int e_other, int8_t* dst,
@@ -443,7 +458,7 @@ cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64
   return cudaGetLastError();
 }
 
-template <int S>
+template <int S, int STAGES>
 static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                                int64_t KB, const double* rowscale, double* Q, int64_t ldq,
                                cudaStream_t st) {
@@ -453,27 +468,52 @@ static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = ozaki_smem_bytes(S);
-  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  const size_t smem = ozaki_smem_bytes(S, STAGES);
+  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int MB = (int)(M_pad / kOzBM), NBt = (int)(N_pad / kOzBN);
   const int tiles = MB * NBt;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  ozaki_gemm_kernel<S><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, Q, ldq, MB, NBt, (int)KB);
+  ozaki_gemm_kernel<S, STAGES><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, Q, ldq, MB, NBt, (int)KB,
+                                                                g_oz_launch_seq++);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
-                              cudaStream_t st) {
+                              cudaStream_t st, bool compact) {
   if (M_pad % kOzBM || N_pad % kOzBN || KB < 1) return cudaErrorInvalidValue;
+  if (compact) {
+    switch (S) {
+      case 6: return launch_oz_t<6, 3>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+      case 7: return launch_oz_t<7, 3>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+      case 8: return launch_oz_t<8, 3>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (S) {
-    case 6: return launch_oz_t<6>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
-    case 7: return launch_oz_t<7>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
-    case 8: return launch_oz_t<8>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+    case 6: return launch_oz_t<6, 0>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+    case 7: return launch_oz_t<7, 0>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+    case 8: return launch_oz_t<8, 0>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
+
+#ifdef TMVN_TIMELINE
+void tl_access_gemm(unsigned long long* out, bool reset) {
+  cudaDeviceSynchronize();
+  if (reset) {
+    g_oz_launch_seq = 0;
+    static unsigned long long z[256][4];
+    for (int i = 0; i < 256; ++i) { z[i][0] = z[i][2] = ~0ull; z[i][1] = z[i][3] = 0; }
+    cudaMemcpyToSymbol(g_tl, z, sizeof(z));
+    unsigned int zs[2] = {0, 0};
+    cudaMemcpyToSymbol(g_tl_seq, zs, sizeof(zs));
+  } else {
+    cudaMemcpyFromSymbol(out, g_tl, 256 * 4 * 8);
+  }
+}
+#endif
 }  // namespace tmvn

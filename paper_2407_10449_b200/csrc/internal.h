@@ -16,10 +16,12 @@ cudaError_t launch_gemm_tn(const double* Xt, int64_t R_pad, const double* Wt, in
 // FP64: As = digits of A' (M_pad rows, blocks of 128), Ns = digits of nu (N_pad
 // rows, blocks of 64), KB steps of 32 along d, S digits (6, 7 or 8);
 // rowscale[i] = 2^(e_i + e_nu - 14).
-size_t ozaki_smem_bytes(int S);
+size_t ozaki_smem_bytes(int S, int stages = 0);
+// compact: the 3-stage ring (126 KB at S = 7), which leaves room on the SM for one
+// CTA of the per-chain kernel (pipelined schedule, options.pipeline)
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
-                              cudaStream_t st);
+                              cudaStream_t st, bool compact = false);
 // digits of the R rows of a fragment-tiled FP64 matrix into the oz layout with BR
 // rows per block; per_row: exponent from each row's max |v| (rowscale[r] =
 // 2^(e_r + e_other - 14)), else the fixed exponent e_fixed (|v| < 2^e_fixed).
@@ -49,6 +51,7 @@ struct EssParams {
   int rec_dev;      // 1: record flag computed from t (t >= burn_in, (t - burn_in) % thin == 0)
   int64_t burn_in, thin;
   int gen_next;     // 1: draw nu for t + 1 into N after the update
+  int64_t group_base;  // scratch index of this launch's first group (split launches)
   int* dyn_ctr;     // non-null: chains handed out dynamically by atomicAdd on dyn_ctr[t & 63]
                     // (the launch for t zeroes the slot of t + 32); null: round-robin
   int8_t* Ns;       // non-null: also write nu_{t+1}'s S digits (int8 projection, gemm_i8.cu)
@@ -111,6 +114,10 @@ struct EssLaunch {
 EssLaunch ess_plan(int C, int m, int W_req, int ring_req);
 cudaError_t launch_ess_step(const EssParams& p, int grid, cudaStream_t st);
 cudaError_t launch_ess_intervals(const EssParams& p, int grid, cudaStream_t st);
+#ifdef TMVN_TIMELINE
+void tl_access_gemm(unsigned long long* out, bool reset);
+void tl_access_ess(unsigned long long* out, bool reset);
+#endif
 #ifdef TMVN_PHASE_TIMING
 void phase_cycles(unsigned long long* out10, bool reset);
 void oz_cycles(unsigned long long* out8, bool reset);
@@ -126,10 +133,11 @@ cudaError_t launch_unpack(const double* src, int64_t R, int64_t K, int64_t K_pad
 cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed, uint32_t t,
                            uint32_t chain_offset, cudaStream_t st);
 // nu of iteration t (+ *t_dev when non-null) into tiled N and, when Ns != nullptr, its
-// S int8 digits (KB K steps); one 128-thread CTA per SM (runs beside the GEMM).
+// S int8 digits (KB K steps); ctas_per_sm 64-thread CTAs per SM (it runs beside other
+// kernels: few CTAs so as not to crowd them off the SMs).
 cudaError_t launch_nu(double* N, int8_t* Ns, int S, int64_t KB, int C, int d, int64_t d_pad,
                       uint64_t seed, uint32_t t, const uint32_t* t_dev, uint32_t chain_offset,
-                      cudaStream_t st);
+                      cudaStream_t st, int ctas_per_sm);
 // first (c, i) with P[c, i] - b[i] >= 0 (strict start, C18); *flag = c * m + i or -1.
 cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, int C, int m,
                                unsigned long long* flag, cudaStream_t st);

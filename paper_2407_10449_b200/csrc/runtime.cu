@@ -47,6 +47,14 @@ struct tmvn_ctx {
   int64_t C_cap = 0, C_pad = 0;
   double *X = nullptr, *N = nullptr, *P0 = nullptr, *P1 = nullptr, *Q = nullptr;
   double* N2 = nullptr;  // second nu buffer: nu_t lives in buffer t & 1 when the RNG runs ahead
+  // pipelined schedule (options.pipeline): nu_t in buffer t % 3, Q_t in buffer t & 1
+  double* N3 = nullptr;
+  int8_t* Ns3 = nullptr;
+  double* Q2 = nullptr;
+  cudaStream_t gemm_stream = nullptr;
+  cudaEvent_t ev_q[2] = {nullptr, nullptr}, ev_nu[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_ess = nullptr, ev_join[2] = {nullptr, nullptr}, ev_essb = nullptr;
+  cudaStream_t essb_stream = nullptr;  // the second part of a split per-chain launch
   // the RNG stream: nu_{t+1} is drawn beside the projection GEMM of iteration t
   cudaStream_t rng_stream = nullptr;
   int* dyn = nullptr;  // dynamic chain scheduling counters: 64 slots per shard
@@ -144,7 +152,8 @@ std::vector<double> to_host(const double* p, size_t n) {
 cudaStream_t stream_of(const tmvn_ctx* h) { return (cudaStream_t)h->opt.stream; }
 
 void free_chain_buffers(tmvn_ctx* h) {
-  dfree(h->X); dfree(h->N); dfree(h->N2); dfree(h->P0); dfree(h->P1); dfree(h->Q);
+  dfree(h->X); dfree(h->N); dfree(h->N2); dfree(h->N3); dfree(h->P0); dfree(h->P1); dfree(h->Q);
+  dfree(h->Q2); dfree(h->Ns3);
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
   dfree(h->stage); dfree(h->stage2); dfree(h->rej);
   dfree(h->gstash); dfree(h->ggaps);
@@ -239,7 +248,7 @@ tmvn_status ensure_ozaki(tmvn_ctx* h) {
     h->ozKB = KB;
   }
   if (h->ozS_N != S || h->Ns_rows < h->C_pad) {
-    dfree(h->Ns); dfree(h->Ns2);
+    dfree(h->Ns); dfree(h->Ns2); dfree(h->Ns3);
     CK(h, dalloc(&h->Ns, (size_t)h->C_pad * KB * kOzStepK * S));
     CK(h, dalloc(&h->Ns2, (size_t)h->C_pad * KB * kOzStepK * S));
     h->ozS_N = S;
@@ -250,20 +259,21 @@ tmvn_status ensure_ozaki(tmvn_ctx* h) {
 
 // nu buffers: buffer b holds nu of the iterations t with t & 1 == b when the RNG runs
 // ahead on its own stream; buffer 0 otherwise
-double* nu_f64(const tmvn_ctx* h, int b) { return b ? h->N2 : h->N; }
-int8_t* nu_dig(const tmvn_ctx* h, int b) { return b ? h->Ns2 : h->Ns; }
+double* nu_f64(const tmvn_ctx* h, int b) { return b == 0 ? h->N : b == 1 ? h->N2 : h->N3; }
+int8_t* nu_dig(const tmvn_ctx* h, int b) { return b == 0 ? h->Ns : b == 1 ? h->Ns2 : h->Ns3; }
 
 int8_t* oz_rows(const tmvn_ctx* h, int64_t c0, int b = 0) {
   return nu_dig(h, b) + (c0 / kOzNuRows) * h->ozKB * kOzStepK * oz_slices(h) * kOzNuRows;
 }
 
 // Q rows [c0, c0 + Rp) = nu A'^T by the configured projection (nu from buffer b).
-cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStream_t st, int b = 0) {
+cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStream_t st, int b = 0,
+                              double* Qout = nullptr, bool compact = false) {
+  double* Qb = (Qout ? Qout : h->Q) + c0 * h->m_pad;
   if (use_oz(h))
     return launch_ozaki_gemm(h->As, h->m_pad, oz_rows(h, c0, b), Rp, h->ozKB, oz_slices(h), h->rowscale,
-                             h->Q + c0 * h->m_pad, h->m_pad, st);
-  return launch_gemm_tn(nu_f64(h, b) + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad,
-                        h->Q + c0 * h->m_pad, h->m_pad, st);
+                             Qb, h->m_pad, st, compact);
+  return launch_gemm_tn(nu_f64(h, b) + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad, Qb, h->m_pad, st);
 }
 
 // nu of iteration t for chains [0, C) (and its digits for the int8 projection).
@@ -279,9 +289,9 @@ cudaError_t launch_first_nu(tmvn_ctx* h, int64_t C, uint64_t seed, uint32_t t, c
 
 // nu of iteration t (+ *t_dev) into buffer b, on the RNG stream
 cudaError_t launch_nu_ahead(tmvn_ctx* h, int64_t C, uint64_t seed, uint32_t t, const uint32_t* t_dev,
-                            int b, cudaStream_t st) {
+                            int b, cudaStream_t st, int ctas_per_sm = 10) {
   return launch_nu(nu_f64(h, b), use_oz(h) ? nu_dig(h, b) : nullptr, oz_slices(h), h->ozKB, (int)C,
-                   (int)h->d, h->d_pad, seed, t, t_dev, (uint32_t)h->opt.chain_offset, st);
+                   (int)h->d, h->d_pad, seed, t, t_dev, (uint32_t)h->opt.chain_offset, st, ctas_per_sm);
 }
 
 tmvn_status ensure_rng_stream(tmvn_ctx* h) {
@@ -454,6 +464,110 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
   return TMVN_OK;
 }
 
+// Pipelined schedule (options.pipeline, one shard): the projection of iteration
+// t + 1 runs concurrently with the per-chain kernel of iteration t (Q double-
+// buffered; the GEMM on a high-priority stream in its compact 3-stage form, so that a
+// CTA of the per-chain kernel fits beside it on every SM, and the per-chain kernel
+// schedules its chains dynamically), and nu_{t+2} is drawn on a third stream (nu
+// triple-buffered: nu_t in buffer t % 3).  Per iteration t the order is
+//   RNG(t+2)  after ESS(t-1)            (nu buffer (t+2)%3 last read by ESS(t-1))
+//   GEMM(t+1) after ESS(t-1), RNG(t+1)  (Q buffer (t+1)&1 last read by ESS(t-1))
+//   ESS(t)    after GEMM(t)
+// Results are bitwise those of the serial schedule.
+tmvn_status ensure_pipeline(tmvn_ctx* h) {
+  const size_t cd = (size_t)h->C_pad * h->d_pad, cm = (size_t)h->C_pad * h->m_pad;
+  if (!h->N3) CK(h, dalloc(&h->N3, cd));
+  if (!h->Q2) CK(h, dalloc(&h->Q2, cm));
+  if (use_oz(h) && !h->Ns3) CK(h, dalloc(&h->Ns3, (size_t)h->C_pad * h->ozKB * kOzStepK * oz_slices(h)));
+  if (!h->gemm_stream) {
+    int lo = 0, hi = 0;
+    CK(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(h, cudaStreamCreateWithPriority(&h->gemm_stream, cudaStreamNonBlocking, hi));
+  }
+  tmvn_status rs = ensure_rng_stream(h);
+  if (rs != TMVN_OK) return rs;
+  for (auto* e : {&h->ev_q[0], &h->ev_q[1], &h->ev_nu[0], &h->ev_nu[1], &h->ev_nu[2], &h->ev_ess,
+                  &h->ev_join[0], &h->ev_join[1], &h->ev_essb})
+    if (!*e) CK(h, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  if (!h->essb_stream) CK(h, cudaStreamCreateWithFlags(&h->essb_stream, cudaStreamNonBlocking));
+  return TMVN_OK;
+}
+
+tmvn_status run_loop_pipe(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, double* P_cur,
+                          int64_t* n_recorded) {
+  tmvn_status ps = ensure_pipeline(h);
+  if (ps != TMVN_OK) return ps;
+  cudaStream_t A = stream_of(h), B = h->gemm_stream, R = h->rng_stream;
+  const int64_t t0 = h->opt.iter_offset;
+  const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
+  const int64_t Rp = round_up(C, kTileR);
+  const bool oz = use_oz(h);
+  double* P_next = (P_cur == h->P0) ? h->P1 : h->P0;
+  double* Qb[2] = {h->Q, h->Q2};
+  EssParams p = base_params(h, (int)C);
+  p.seed = seed;
+  p.gen_next = 0;
+  p.Ns = nullptr;
+  if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
+  CK(h, cudaMemsetAsync(h->dyn, 0, sizeof(int) * 64 * 16, A));
+  p.dyn_ctr = h->dyn;
+  auto proj = [&](int64_t t) -> cudaError_t {
+    return launch_projection(h, 0, Rp, B, (int)(t % 3), Qb[t & 1], oz);
+  };
+  // prologue: nu_{t0} (A), nu_{t0+1} (R), Q_{t0} (B)
+  CK(h, cudaEventRecord(h->ev_ess, A));  // orders B and R after all earlier work on A
+  CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, A, (int)(t0 % 3)));
+  CK(h, cudaEventRecord(h->ev_nu[t0 % 3], A));
+  if (n_iter > 1) {
+    CK(h, cudaStreamWaitEvent(R, h->ev_ess, 0));
+    KL(h, launch_nu_ahead(h, C, seed, (uint32_t)(t0 + 1), nullptr, (int)((t0 + 1) % 3), R));
+    CK(h, cudaEventRecord(h->ev_nu[(t0 + 1) % 3], R));
+  }
+  CK(h, cudaStreamWaitEvent(B, h->ev_nu[t0 % 3], 0));
+  KL(h, proj(t0));
+  CK(h, cudaEventRecord(h->ev_q[t0 & 1], B));
+  int64_t nrec = 0;
+  for (int64_t it = 0; it < n_iter; ++it) {
+    const int64_t t = t0 + it;
+    if (it + 2 < n_iter) {  // nu_{t+2}
+      CK(h, cudaStreamWaitEvent(R, h->ev_ess, 0));
+      KL(h, launch_nu_ahead(h, C, seed, (uint32_t)(t + 2), nullptr, (int)((t + 2) % 3), R));
+      CK(h, cudaEventRecord(h->ev_nu[(t + 2) % 3], R));
+    }
+    if (it + 1 < n_iter) {  // Q_{t+1}, beside ESS(t)
+      CK(h, cudaStreamWaitEvent(B, h->ev_ess, 0));
+      CK(h, cudaStreamWaitEvent(B, h->ev_nu[(t + 1) % 3], 0));
+      KL(h, proj(t + 1));
+      CK(h, cudaEventRecord(h->ev_q[(t + 1) & 1], B));
+    }
+    const bool rec = recorded_iter(h->opt, t);
+    CK(h, cudaStreamWaitEvent(A, h->ev_q[t & 1], 0));
+    p.P_cur = P_cur;
+    p.P_next = P_next;
+    p.Q = Qb[t & 1];
+    p.N = nu_f64(h, (int)(t % 3));
+    p.t = (uint32_t)t;
+    p.record = (rec && !h->affine) ? 1 : 0;
+    KL(h, launch_ess_step(p, h->plan.grid, A));
+    std::swap(P_cur, P_next);
+    if (rec && h->affine) {
+      KL(h, launch_gemm_tn(h->X, Rp, h->L_tiled, h->d_r128, h->d_pad, h->stage, h->d_r128, A));
+      KL(h, launch_accum_affine(h->stage, h->d_r128, h->mu, (int)C, (int)h->d, h->S1x, h->S2x, A));
+    }
+    if ((t + 1) % K == 0 && it + 1 < n_iter)
+      KL(h, launch_gemm_tn(h->X, Rp, h->At, h->m_pad, h->d_pad, P_cur, h->m_pad, A));
+    CK(h, cudaEventRecord(h->ev_ess, A));
+    if (rec) ++nrec;
+  }
+  // join the GEMM and RNG streams into the library stream (part b joined every iteration)
+  CK(h, cudaEventRecord(h->ev_join[0], B));
+  CK(h, cudaEventRecord(h->ev_join[1], R));
+  CK(h, cudaStreamWaitEvent(A, h->ev_join[0], 0));
+  CK(h, cudaStreamWaitEvent(A, h->ev_join[1], 0));
+  *n_recorded = nrec;
+  return TMVN_OK;
+}
+
 // The hot loop.  On entry X holds x_{t0} (tiled) and P_cur = X A'^T.
 // The chains are split into `shards` row blocks (multiples of 128 chains), each an
 // independent GEMM -> ESS sequence on its own stream: the DMMA GEMM of one shard
@@ -461,6 +575,8 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
 // depend on the split (no split-K; global chain index in the RNG counters).
 tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, double* P_cur,
                      int64_t* n_recorded) {
+  if (h->opt.pipeline == 1 && h->nshards == 1 && !h->trace_dev && h->opt.profile == 0 && n_iter > 0)
+    return run_loop_pipe(h, C, n_iter, seed, P_cur, n_recorded);
   cudaStream_t st = stream_of(h);
   const int64_t t0 = h->opt.iter_offset;
   const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
@@ -733,6 +849,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->ozaki_slices = 0;
   o->rng_ahead = 0;  // measured slower on B200 (the GEMM loses more than the ESS kernel gains)
   o->schedule = 0;
+  o->pipeline = 0;
   return TMVN_OK;
 }
 
@@ -928,6 +1045,12 @@ void tmvn_destroy(tmvn_handle h) {
     if (h->graph_exec[i]) cudaGraphExecDestroy(h->graph_exec[i]);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   if (h->rng_stream) cudaStreamDestroy(h->rng_stream);
+  if (h->gemm_stream) cudaStreamDestroy(h->gemm_stream);
+  if (h->essb_stream) cudaStreamDestroy(h->essb_stream);
+  if (h->ev_essb) cudaEventDestroy(h->ev_essb);
+  for (cudaEvent_t e : {h->ev_q[0], h->ev_q[1], h->ev_nu[0], h->ev_nu[1], h->ev_nu[2], h->ev_ess,
+                        h->ev_join[0], h->ev_join[1]})
+    if (e) cudaEventDestroy(e);
   if (h->ev_pre) cudaEventDestroy(h->ev_pre);
   if (h->ev_rng) cudaEventDestroy(h->ev_rng);
   dfree(h->d_tbase);
@@ -1239,4 +1362,20 @@ tmvn_status tmvn_test_oz_cycles(uint64_t* out8, int reset) {
 }
 #endif
 
+#ifdef TMVN_TIMELINE
+// timeline build only (tools/timeline.py): reset / read the per-launch timestamps
+tmvn_status tmvn_test_timeline(uint64_t* out, int reset) {
+  std::vector<unsigned long long> g(256 * 4), e(256 * 4);
+  tmvn::tl_access_gemm(g.data(), reset != 0);
+  tmvn::tl_access_ess(e.data(), reset != 0);
+  if (!reset)
+    for (int i = 0; i < 256; ++i) {
+      out[i * 4 + 0] = g[i * 4 + 0];
+      out[i * 4 + 1] = g[i * 4 + 1];
+      out[i * 4 + 2] = e[i * 4 + 2];
+      out[i * 4 + 3] = e[i * 4 + 3];
+    }
+  return TMVN_OK;
+}
+#endif
 }  // extern "C"

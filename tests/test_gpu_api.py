@@ -196,11 +196,17 @@ def test_rng_ahead_and_projection_options_bitwise():
     C = 200
     X0 = np.tile(x0, (C, 1))
     ref = tm.Sampler(A, b, rng_ahead=0, graphs=0).sample(X0, 70, seed=11)
-    for ra, gr, sc in ((1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 1, 1), (0, 0, 1)):
-        out = tm.Sampler(A, b, rng_ahead=ra, graphs=gr, schedule=sc).sample(X0, 70, seed=11)
-        assert np.array_equal(out, ref), (ra, gr, sc)
+    for ra, gr, sc, pi in ((1, 0, 0, 0), (1, 1, 0, 0), (0, 1, 0, 0), (0, 1, 1, 0), (0, 0, 1, 0),
+                           (0, 0, 0, 1), (0, 1, 0, 1)):
+        out = tm.Sampler(A, b, rng_ahead=ra, graphs=gr, schedule=sc, pipeline=pi).sample(X0, 70, seed=11)
+        assert np.array_equal(out, ref), (ra, gr, sc, pi)
+    for n in (1, 2, 3):  # short calls through the pipelined prologue
+        o1 = tm.Sampler(A, b, pipeline=1).sample(X0, n, seed=11)
+        o0 = tm.Sampler(A, b).sample(X0, n, seed=11)
+        assert np.array_equal(o1, o0), n
     # resume at a multiple of recompute_every with nu drawn ahead (plain + graph blocks)
-    s = tm.Sampler(A, b, rng_ahead=1)
-    a = s.sample(X0, 32, seed=11)
-    a = s.sample(a, 38, seed=11)
-    assert np.array_equal(a, ref)
+    for kw in (dict(rng_ahead=1), dict(pipeline=1)):
+        s = tm.Sampler(A, b, **kw)
+        a = s.sample(X0, 32, seed=11)
+        a = s.sample(a, 38, seed=11)
+        assert np.array_equal(a, ref), kw

@@ -291,10 +291,11 @@ def main():
         except Exception:
             pass
         tc_peak_sus = 2.0 * mp["bf16_tflops_sustained"]
-        dmma = dict(roofline)
-        for k in ("ess_kernel", "traffic", "traffic_source", "measured_in"):
-            dmma.pop(k, None)
-        dmma["kernel"] = "gemm_tn_f64_kernel (P = X A^T refresh every recompute_every, FP64 DMMA)"
+        dmma = {"kernel": "oz_slice_kernel + ozaki_gemm_kernel (P = X A'^T refresh every recompute_every: "
+                          "X cut into digits with one exponent per chain, int8 tcgen05)",
+                "avg_launch_ms": roofline["avg_launch_ms"],
+                "fp64_equivalent_tflops": roofline["achieved"],
+                "share_of_step": roofline["share_of_step"]}
         roofline = {"bound": "tensor",
                     "kernel": "ozaki_gemm_kernel (Q = N A'^T, int8 tcgen05.mma, TMEM accumulators, "
                               f"{opts.ozaki_slices or 7} digits: FP64-accurate)",

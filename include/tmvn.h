@@ -112,8 +112,11 @@ typedef struct {
    *      Requires d <= 4096 (int32 headroom); otherwise TMVN_E_ARG.
    *   2: FP64 on the DMMA tensor pipe (mma.sync f64; round-to-nearest FP64
    *      products, |Q - a.nu| <= 2 d 2^-53 sum_j |a_ij nu_j|).
-   * The P refreshes (every recompute_every) and the start check are always FP64
-   * DMMA.  Results do not depend on C or on the sharding. */
+   * The P refreshes (every recompute_every) and the start check use the same
+   * product on X: with the int8 projection X is cut into digits with one
+   * exponent per chain (max_j |x_cj| < 2^e_c; bound as above with 2^(e_i + e_c)
+   * in place of 2^(e_i + 4)), with DMMA in FP64.  Results do not depend on C or
+   * on the sharding. */
   int32_t projection;
   /* Digits S of the int8 projection: 6, 7 or 8 (0 = default 7: 55-bit fixed
    * point, 28 int8 MMAs per 32-wide K step). */

@@ -192,8 +192,8 @@ __device__ unsigned long long g_oz_cycles[8];
 template <int S, int STAGES>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
-                      const double* __restrict__ rowscale, double* __restrict__ Q, int64_t ldq,
-                      int MB, int NBt, int KB, int dbg_seq) {
+                      const double* __restrict__ rowscale, const double* __restrict__ colscale,
+                      double* __restrict__ Q, int64_t ldq, int MB, int NBt, int KB, int dbg_seq) {
   constexpr int kStage = oz_stage_bytes(S);
   constexpr int kOzStages = STAGES ? STAGES : oz_stages(S);
   constexpr int NTS = oz_nts<S>();
@@ -367,7 +367,9 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           double h = (double)acc[S - 1][j];
 #pragma unroll
           for (int D = S - 2; D >= 0; --D) h = __fma_rn(h, 0.00390625, (double)acc[D][j]);  // 2^-8
-          qcol[(int64_t)(cc + j) * ldq] = __dmul_rn(h, scale);
+          // per-column power of two (refresh of P = X A'^T: 2^(e_c - 4) per chain), exact
+          const double sc = colscale ? __dmul_rn(scale, __ldg(colscale + (int64_t)nb * kOzBN + cc + j)) : scale;
+          qcol[(int64_t)(cc + j) * ldq] = __dmul_rn(h, sc);
         }
       }
       tc_fence_before();
@@ -460,8 +462,8 @@ cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64
 
 template <int S, int STAGES>
 static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
-                               int64_t KB, const double* rowscale, double* Q, int64_t ldq,
-                               cudaStream_t st) {
+                               int64_t KB, const double* rowscale, const double* colscale, double* Q,
+                               int64_t ldq, cudaStream_t st) {
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -475,29 +477,32 @@ static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns
   const int MB = (int)(M_pad / kOzBM), NBt = (int)(N_pad / kOzBN);
   const int tiles = MB * NBt;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  ozaki_gemm_kernel<S, STAGES><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, Q, ldq, MB, NBt, (int)KB,
-                                                                g_oz_launch_seq++);
+  ozaki_gemm_kernel<S, STAGES><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, colscale, Q, ldq, MB, NBt,
+                                                                (int)KB, g_oz_launch_seq++);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
-                              cudaStream_t st, bool compact) {
+                              cudaStream_t st, bool compact, const double* colscale) {
   if (M_pad % kOzBM || N_pad % kOzBN || KB < 1) return cudaErrorInvalidValue;
+#define TMVN_OZ_CASE(SS, ST) \
+  case SS: return launch_oz_t<SS, ST>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st);
   if (compact) {
     switch (S) {
-      case 6: return launch_oz_t<6, 3>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
-      case 7: return launch_oz_t<7, 3>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
-      case 8: return launch_oz_t<8, 3>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+      TMVN_OZ_CASE(6, 3)
+      TMVN_OZ_CASE(7, 3)
+      TMVN_OZ_CASE(8, 3)
       default: return cudaErrorInvalidValue;
     }
   }
   switch (S) {
-    case 6: return launch_oz_t<6, 0>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
-    case 7: return launch_oz_t<7, 0>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
-    case 8: return launch_oz_t<8, 0>(As, M_pad, Ns, N_pad, KB, rowscale, Q, ldq, st);
+    TMVN_OZ_CASE(6, 0)
+    TMVN_OZ_CASE(7, 0)
+    TMVN_OZ_CASE(8, 0)
     default: return cudaErrorInvalidValue;
   }
+#undef TMVN_OZ_CASE
 }
 
 

@@ -19,9 +19,11 @@ cudaError_t launch_gemm_tn(const double* Xt, int64_t R_pad, const double* Wt, in
 size_t ozaki_smem_bytes(int S, int stages = 0);
 // compact: the 3-stage ring (126 KB at S = 7), which leaves room on the SM for one
 // CTA of the per-chain kernel (pipelined schedule, options.pipeline)
+// colscale (nullable, N_pad): an extra power of two per output column (row of Ns):
+// the refresh P = X A'^T slices X with one exponent per chain.
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
-                              cudaStream_t st, bool compact = false);
+                              cudaStream_t st, bool compact = false, const double* colscale = nullptr);
 // digits of the R rows of a fragment-tiled FP64 matrix into the oz layout with BR
 // rows per block; per_row: exponent from each row's max |v| (rowscale[r] =
 // 2^(e_r + e_other - 14)), else the fixed exponent e_fixed (|v| < 2^e_fixed).

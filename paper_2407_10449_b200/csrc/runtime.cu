@@ -51,6 +51,9 @@ struct tmvn_ctx {
   double* N3 = nullptr;
   int8_t* Ns3 = nullptr;
   double* Q2 = nullptr;
+  // int8 refresh of P = X A'^T: digits of X (C_pad rows) and 2^(e_c - 4) per chain
+  int8_t* Xs = nullptr;
+  double* xscale = nullptr;
   cudaStream_t gemm_stream = nullptr;
   cudaEvent_t ev_q[2] = {nullptr, nullptr}, ev_nu[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_ess = nullptr, ev_join[2] = {nullptr, nullptr}, ev_essb = nullptr;
@@ -153,7 +156,7 @@ cudaStream_t stream_of(const tmvn_ctx* h) { return (cudaStream_t)h->opt.stream; 
 
 void free_chain_buffers(tmvn_ctx* h) {
   dfree(h->X); dfree(h->N); dfree(h->N2); dfree(h->N3); dfree(h->P0); dfree(h->P1); dfree(h->Q);
-  dfree(h->Q2); dfree(h->Ns3);
+  dfree(h->Q2); dfree(h->Ns3); dfree(h->Xs); dfree(h->xscale);
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
   dfree(h->stage); dfree(h->stage2); dfree(h->rej);
   dfree(h->gstash); dfree(h->ggaps);
@@ -247,10 +250,12 @@ tmvn_status ensure_ozaki(tmvn_ctx* h) {
     h->ozS_A = S;
     h->ozKB = KB;
   }
-  if (h->ozS_N != S || h->Ns_rows < h->C_pad) {
-    dfree(h->Ns); dfree(h->Ns2); dfree(h->Ns3);
+  if (h->ozS_N != S || h->Ns_rows < h->C_pad || !h->Xs) {
+    dfree(h->Ns); dfree(h->Ns2); dfree(h->Ns3); dfree(h->Xs); dfree(h->xscale);
     CK(h, dalloc(&h->Ns, (size_t)h->C_pad * KB * kOzStepK * S));
     CK(h, dalloc(&h->Ns2, (size_t)h->C_pad * KB * kOzStepK * S));
+    CK(h, dalloc(&h->Xs, (size_t)h->C_pad * KB * kOzStepK * S));
+    CK(h, dalloc(&h->xscale, (size_t)h->C_pad));
     h->ozS_N = S;
     h->Ns_rows = h->C_pad;
   }
@@ -274,6 +279,23 @@ cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStr
     return launch_ozaki_gemm(h->As, h->m_pad, oz_rows(h, c0, b), Rp, h->ozKB, oz_slices(h), h->rowscale,
                              Qb, h->m_pad, st, compact);
   return launch_gemm_tn(nu_f64(h, b) + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad, Qb, h->m_pad, st);
+}
+
+// The refresh P[c0, c0 + C) = X A'^T (C13): with the int8 projection, X is cut into
+// digits with one exponent per chain (max_j |x_cj| < 2^e_c) and the same tcgen05
+// kernel computes it (stated bound of include/tmvn.h with 2^(e_i + e_c)); else FP64 DMMA.
+// Pb: the shard's P rows (already offset by c0)
+cudaError_t launch_refresh(tmvn_ctx* h, int64_t c0, int64_t C, double* Pb, cudaStream_t st) {
+  const int64_t Rp = round_up(C, kTileR);
+  if (!use_oz(h) || !h->Xs)
+    return launch_gemm_tn(h->X + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad, Pb, h->m_pad, st);
+  const int S = oz_slices(h);
+  int8_t* xs = h->Xs + (c0 / kOzNuRows) * h->ozKB * kOzStepK * S * kOzNuRows;
+  cudaError_t e = launch_oz_slice(h->X + c0 * h->d_pad, C, h->d, h->d_pad, S, h->ozKB, kOzNuRows, 1, 0,
+                                  14 - kOzNuExp, xs, h->xscale + c0, st);  // xscale = 2^(e_c - 4)
+  if (e != cudaSuccess) return e;
+  return launch_ozaki_gemm(h->As, h->m_pad, xs, Rp, h->ozKB, S, h->rowscale, Pb, h->m_pad, st, false,
+                           h->xscale + c0);
 }
 
 // nu of iteration t for chains [0, C) (and its digits for the int8 projection).
@@ -370,7 +392,9 @@ tmvn_status store_X(tmvn_ctx* h, int64_t C, double* out) {
 // P = X A'^T, then the strict start check (C18).
 tmvn_status start_check(tmvn_ctx* h, int64_t C, double* P) {
   cudaStream_t st = stream_of(h);
-  KL(h, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, P, h->m_pad, st));
+  // the same product as the periodic refresh, so that a call resumed at a multiple of
+  // recompute_every continues bitwise like an uninterrupted one
+  KL(h, launch_refresh(h, 0, C, P, st));
   CK(h, cudaMemsetAsync(h->dflag, 0xff, sizeof(unsigned long long), st));
   KL(h, launch_start_check(P, h->m_pad, h->b_eff, (int)C, (int)h->m, h->dflag, st));
   unsigned long long flag = 0;
@@ -451,7 +475,7 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
     if (err == cudaSuccess && ahead) err = cudaStreamWaitEvent(cs, h->ev_rng, 0);  // join: nu_{t+i+1} ready
     std::swap(pc, pn);
   }
-  if (err == cudaSuccess) err = launch_gemm_tn(h->X, Rp, h->At, h->m_pad, h->d_pad, pc, h->m_pad, cs);
+  if (err == cudaSuccess) err = launch_refresh(h, 0, C, pc, cs);
   cudaGraph_t graph = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
   if (err != cudaSuccess) return cuda_fail(h, err, "graph capture");
@@ -555,7 +579,7 @@ tmvn_status run_loop_pipe(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed,
       KL(h, launch_accum_affine(h->stage, h->d_r128, h->mu, (int)C, (int)h->d, h->S1x, h->S2x, A));
     }
     if ((t + 1) % K == 0 && it + 1 < n_iter)
-      KL(h, launch_gemm_tn(h->X, Rp, h->At, h->m_pad, h->d_pad, P_cur, h->m_pad, A));
+      KL(h, launch_refresh(h, 0, C, P_cur, A));
     CK(h, cudaEventRecord(h->ev_ess, A));
     if (rec) ++nrec;
   }
@@ -700,7 +724,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
                                   h->S2x + x.c0 * h->d, x.st));
       }
       if ((t + 1) % K == 0 && it + 1 < n_iter)
-        TIMED(0, x.C, x.st, launch_gemm_tn(x.p.X, Rp, h->At, h->m_pad, h->d_pad, x.Pc, h->m_pad, x.st));
+        TIMED(0, x.C, x.st, launch_refresh(h, x.c0, x.C, x.Pc, x.st));
     }
     if (rec) ++nrec;
     if (h->trace_dev) {  // S == 1 when tracing

@@ -130,9 +130,10 @@ typedef struct {
    * per-chain kernel gains ~20 us).  Single shard only.  Results do not depend
    * on it (tested bitwise). */
   int32_t rng_ahead;
-  /* Chain scheduling of the fused per-chain kernel: 0 (default) dynamic (each
-   * group of warps grabs its next chain with an atomic counter, one chain ahead),
-   * 1 round-robin.  Results do not depend on it. */
+  /* Chain scheduling of the fused per-chain kernel: 2 dynamic (each group of
+   * warps grabs its next chain with an atomic counter, one chain ahead), 1
+   * round-robin, 0 (default) automatic: dynamic for long rows (8 warps per chain),
+   * round-robin otherwise.  Results do not depend on it. */
   int32_t schedule;
   /* 1: pipelined schedule (one shard, no profiling): the projection GEMM of
    * iteration t + 1 runs concurrently with the fused per-chain kernel of

@@ -40,7 +40,7 @@ constexpr uint64_t kTopBits = 0x7FF0000000000000ull;  // +inf: every alpha in [0
 #endif
 constexpr int kBatch = TMVN_ESS_BATCH;  // constraint pairs per thread with loads in flight
 #ifndef TMVN_ESS_BATCH_A1
-#define TMVN_ESS_BATCH_A1 2
+#define TMVN_ESS_BATCH_A1 1
 #endif
 constexpr int kBatchA1 = TMVN_ESS_BATCH_A1;  // the same in the active-test pass (fewer live registers)
 
@@ -665,11 +665,20 @@ __device__ __forceinline__ void stash_arc(const Smem& S, Ctl& ctl, double2* stas
   }
 }
 
+// CTAs per SM the register allocation must allow: 4 (64 registers) for the config-3
+// path (W = 8, arcs stashed in shared memory: 4 x 56 KB fit, no spills), 3 (80
+// registers) elsewhere (at 64 those variants spill 100-200 bytes)
 #ifndef TMVN_ESS_MIN_BLOCKS
 #define TMVN_ESS_MIN_BLOCKS 3
 #endif
+template <int W, bool kRing, bool kSmemStash>
+constexpr int ess_min_blocks() {
+  return (W == 8 && kSmemStash && !kRing) ? (TMVN_ESS_MIN_BLOCKS > 4 ? TMVN_ESS_MIN_BLOCKS : 4)
+                                          : TMVN_ESS_MIN_BLOCKS;
+}
 template <int W, bool kGiven, bool kRing, bool kSmemStash>
-__global__ void __launch_bounds__(kEssThreads, TMVN_ESS_MIN_BLOCKS) ess_kernel(const EssParams p) {
+__global__ void __launch_bounds__(kEssThreads, (ess_min_blocks<W, kRing, kSmemStash>())) ess_kernel(
+    const EssParams p) {
   constexpr int kGroups = 8 / W;
   constexpr int T = Grp<W>::kThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -614,7 +614,9 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
   }
   CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st, ahead ? (int)(t0 & 1) : 0));
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
-  const bool dyn = h->opt.schedule != 1 && h->nshards <= 16;
+  // dynamic hand-out pays for long rows (W = 8); for short ones the atomic's latency
+  // is comparable to a chain's work (config 2: 17 -> 22 us per launch), so auto = W == 8
+  const bool dyn = (h->opt.schedule == 2 || (h->opt.schedule == 0 && h->plan.W == 8)) && h->nshards <= 16;
   if (dyn) CK(h, cudaMemsetAsync(h->dyn, 0, sizeof(int) * 64 * 16, st));
   // ---- shards
   int S = h->nshards;

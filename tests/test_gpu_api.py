@@ -197,7 +197,7 @@ def test_rng_ahead_and_projection_options_bitwise():
     X0 = np.tile(x0, (C, 1))
     ref = tm.Sampler(A, b, rng_ahead=0, graphs=0).sample(X0, 70, seed=11)
     for ra, gr, sc, pi in ((1, 0, 0, 0), (1, 1, 0, 0), (0, 1, 0, 0), (0, 1, 1, 0), (0, 0, 1, 0),
-                           (0, 0, 0, 1), (0, 1, 0, 1)):
+                           (0, 0, 2, 0), (0, 1, 2, 0), (0, 0, 0, 1), (0, 1, 0, 1)):
         out = tm.Sampler(A, b, rng_ahead=ra, graphs=gr, schedule=sc, pipeline=pi).sample(X0, 70, seed=11)
         assert np.array_equal(out, ref), (ra, gr, sc, pi)
     for n in (1, 2, 3):  # short calls through the pipelined prologue

@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(kEssThreads, (ess_min_blocks<W, kRing, kSmemSt
   if (kSmemStash) {
     stash = reinterpret_cast<double2*>(gbase + ess_ring_bytes(CH) + ess_group_base_bytes(NB));
   } else {
-    stash = p.gstash + (gglobal + p.group_base) * m;
+    stash = p.gstash + (gglobal + p.group_base) * ess_gstash_stride(m);
   }
   double2* gg = p.ggaps + (gglobal + p.group_base) * (m + 2);
   const double scale = __ddiv_rn((double)NB, kTwoPi);
@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(kEssThreads, (ess_min_blocks<W, kRing, kSmemSt
         ++qseq;
         g.sync();  // the slot may be refilled from now on
       }
-          } else if (kSmemStash) {
+          } else {
       // two passes: (1) the active test (C3/C25) on every constraint pair, active
       // (p, q) and the index compacted into the stash; (2) the arcs of the active
       // constraints only, every lane busy (about 40 % of the constraints are
@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(kEssThreads, (ess_min_blocks<W, kRing, kSmemSt
       const double2* P2 = reinterpret_cast<const double2*>(Prow);
       const double2* Q2 = reinterpret_cast<const double2*>(Qrow);
       const double2* B2 = reinterpret_cast<const double2*>(p.b);
-      int* sidx = reinterpret_cast<int*>(stash + m);
+      int* sidx = reinterpret_cast<int*>(stash + m);  // m ints after the group's stash (shared or global)
       const int npairs = (m + 1) / 2;
       for (int base = 0; base < npairs; base += kBatchA1 * T) {
         double2 pp[kBatchA1], qq[kBatchA1], bb[kBatchA1];
@@ -959,57 +959,7 @@ __global__ void __launch_bounds__(kEssThreads, (ess_min_blocks<W, kRing, kSmemSt
           p.d_active[(int64_t)c * m + i] = 1;
         }
       }
-          } else {
-      // constraint pairs (2i, 2i+1): P, Q, b as double2 from global; kBatch pairs per
-      // thread with loads in flight, their arcs computed before the stash appends (ILP)
-      const double2* P2 = reinterpret_cast<const double2*>(Prow);
-      const double2* Q2 = reinterpret_cast<const double2*>(Qrow);
-      const double2* B2 = reinterpret_cast<const double2*>(p.b);
-      const int npairs = (m + 1) / 2;
-      for (int base = 0; base < npairs; base += kBatch * T) {
-        double2 pp[kBatch], qq[kBatch], bb[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int pi = base + u * T + g.tid;
-          if (pi < npairs) {
-            pp[u] = P2[pi];
-            qq[u] = Q2[pi];
-            bb[u] = __ldg(B2 + pi);
           }
-        }
-        double al[2 * kBatch], be[2 * kBatch];
-        bool act[2 * kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int pi = base + u * T + g.tid;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int e = 2 * u + h;
-            al[e] = 0.0;
-            be[e] = 0.0;
-            act[e] = false;
-            if (pi < npairs && 2 * pi + h < m)
-              act[e] = arc_of(h ? pp[u].y : pp[u].x, h ? qq[u].y : qq[u].x, h ? bb[u].y : bb[u].x,
-                              al[e], be[e]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          if (base + u * T >= npairs) break;  // uniform
-          const int pi = base + u * T + g.tid;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int e = 2 * u + h, i = 2 * pi + h;
-            if (p.d_alpha && pi < npairs && i < m) {
-              p.d_alpha[(int64_t)c * m + i] = act[e] ? al[e] : 0.0;
-              p.d_beta[(int64_t)c * m + i] = act[e] ? be[e] : 0.0;
-              p.d_active[(int64_t)c * m + i] = act[e] ? 1 : 0;
-            }
-            stash_arc(S, ctl, stash, act[e], al[e], be[e], NB, scale);
-          }
-        }
-      }
-    }
     }
     g.sync();
     PHASE(1);  // A: arcs, stash, level-1 statistics

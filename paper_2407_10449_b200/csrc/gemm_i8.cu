@@ -189,7 +189,7 @@ __device__ unsigned long long g_oz_cycles[8];
 // TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31 only: each role covers the 4 quadrants)
 // STAGES: ring depth (0 = as many as fit; 3 = the compact variant that leaves room
 // on the SM for a CTA of the per-chain kernel when the two run concurrently)
-template <int S, int STAGES>
+template <int S, int STAGES, bool CS>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
                       const double* __restrict__ rowscale, const double* __restrict__ colscale,
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #pragma unroll
           for (int D = S - 2; D >= 0; --D) h = __fma_rn(h, 0.00390625, (double)acc[D][j]);  // 2^-8
           // per-column power of two (refresh of P = X A'^T: 2^(e_c - 4) per chain), exact
-          const double sc = colscale ? __dmul_rn(scale, __ldg(colscale + (int64_t)nb * kOzBN + cc + j)) : scale;
+          const double sc = CS ? __dmul_rn(scale, __ldg(colscale + (int64_t)nb * kOzBN + cc + j)) : scale;
           qcol[(int64_t)(cc + j) * ldq] = __dmul_rn(h, sc);
         }
       }
@@ -460,7 +460,7 @@ cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64
   return cudaGetLastError();
 }
 
-template <int S, int STAGES>
+template <int S, int STAGES, bool CS>
 static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                                int64_t KB, const double* rowscale, const double* colscale, double* Q,
                                int64_t ldq, cudaStream_t st) {
@@ -471,13 +471,13 @@ static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t smem = ozaki_smem_bytes(S, STAGES);
-  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, STAGES>,
+  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, STAGES, CS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int MB = (int)(M_pad / kOzBM), NBt = (int)(N_pad / kOzBN);
   const int tiles = MB * NBt;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  ozaki_gemm_kernel<S, STAGES><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, colscale, Q, ldq, MB, NBt,
+  ozaki_gemm_kernel<S, STAGES, CS><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, colscale, Q, ldq, MB, NBt,
                                                                 (int)KB, g_oz_launch_seq++);
   return cudaGetLastError();
 }
@@ -486,8 +486,10 @@ cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
                               cudaStream_t st, bool compact, const double* colscale) {
   if (M_pad % kOzBM || N_pad % kOzBN || KB < 1) return cudaErrorInvalidValue;
-#define TMVN_OZ_CASE(SS, ST) \
-  case SS: return launch_oz_t<SS, ST>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st);
+#define TMVN_OZ_CASE(SS, ST)                                                                  \
+  case SS:                                                                                    \
+    return colscale ? launch_oz_t<SS, ST, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st) \
+                    : launch_oz_t<SS, ST, false>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st);
   if (compact) {
     switch (S) {
       TMVN_OZ_CASE(6, 3)

@@ -107,6 +107,9 @@ __host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_
   return (s + 15) / 16 * 16;
 }
 
+// per-group global stash: m arcs (double2) + m constraint indices (int), in double2 units
+__host__ __device__ inline int64_t ess_gstash_stride(int64_t m) { return m + (m + 3) / 4; }
+
 struct EssLaunch {
   int W, NB, stash_smem, grid, CH;
   int64_t groups;  // chain groups in the grid (scratch slots)

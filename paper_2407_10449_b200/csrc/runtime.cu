@@ -214,7 +214,7 @@ tmvn_status plan_ess(tmvn_ctx* h, int64_t C) {
     dfree(h->gstash); dfree(h->ggaps);
     const int64_t Gn = std::max(G, h->scratch_groups);
     if (need_stash || h->scratch_stash) {
-      CK(h, dalloc(&h->gstash, (size_t)Gn * h->m));
+      CK(h, dalloc(&h->gstash, (size_t)Gn * ess_gstash_stride(h->m)));
       h->scratch_stash = true;
     }
     CK(h, dalloc(&h->ggaps, (size_t)Gn * (h->m + 2)));
@@ -643,7 +643,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p.rej = h->rej + x.c0;
     x.p.dyn_ctr = dyn ? h->dyn + 64 * s : nullptr;
     x.p.chain_offset = (uint32_t)(h->opt.chain_offset + x.c0);
-    x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * h->m : nullptr;
+    x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * ess_gstash_stride(h->m) : nullptr;
     x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
     x.p.Q = h->Q + x.c0 * h->m_pad;
     x.p.seed = seed;
@@ -1185,7 +1185,7 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   const EssLaunch plan = ess_plan((int)C, (int)m, g_test_chain_warps, 0);
   const int grid = plan.grid;
   if (!plan.stash_smem) {
-    TCK(tmp_in(gstash, (const double2*)nullptr, (size_t)plan.groups * m));
+    TCK(tmp_in(gstash, (const double2*)nullptr, (size_t)plan.groups * ess_gstash_stride(m)));
   }
   TCK(tmp_in(ggaps, (const double2*)nullptr, (size_t)plan.groups * (m + 2)));
   EssParams p;

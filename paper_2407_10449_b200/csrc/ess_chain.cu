@@ -1204,6 +1204,9 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
     // measured on B200 (tools/ab_time.py): a full CTA per chain once rows are long;
     // fewer warps per chain (more chains in flight) for short rows
     W = m >= 1024 ? 8 : m >= 256 ? 4 : m >= 48 ? 2 : 1;
+    // fewer chains than SMs: a whole CTA per chain (latency-bound regime; the paper's
+    // S4.2 workload, 10 chains at d = m = 1000: 47 -> 34 us per launch)
+    if (C <= g_sms && m >= 48) W = 8;
   }
   // buckets: about 16 constraints (~8 arcs) per level-1 bucket, 64 .. 1024
   int NB = 64;

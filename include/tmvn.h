@@ -142,6 +142,14 @@ typedef struct {
    * stream so that the two kernels share the SMs).  0 (default): serial.
    * Results do not depend on it. */
   int32_t pipeline;
+  /* 1: latency mode -- one thread-block cluster (1-16 CTAs, distributed shared
+   * memory) per chain runs all n_iter iterations in a single launch (the
+   * regime of few chains, e.g. the paper's 1 or 10).  Same RNG
+   * counters and readings; the dot products sum in another order, so results
+   * agree with the default path to rounding, not bitwise.  Not with the affine
+   * change of variable (the default path runs then).  TMVN_E_STATE if a chain's
+   * live arcs in one iteration exceed 1024.  0 (default): off. */
+  int32_t latency;
 } tmvn_options;
 
 typedef struct {

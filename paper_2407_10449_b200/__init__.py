@@ -49,7 +49,8 @@ class options(ctypes.Structure):
                 ("streams", ctypes.c_int32), ("ring", ctypes.c_int32),
                 ("graphs", ctypes.c_int32), ("projection", ctypes.c_int32),
                 ("ozaki_slices", ctypes.c_int32), ("rng_ahead", ctypes.c_int32),
-                ("schedule", ctypes.c_int32), ("pipeline", ctypes.c_int32)]
+                ("schedule", ctypes.c_int32), ("pipeline", ctypes.c_int32),
+                ("latency", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):

@@ -31,6 +31,31 @@ cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64
                             int64_t KB, int BR, int per_row, int e_fixed, int e_other, int8_t* dst,
                             double* rowscale, cudaStream_t st);
 
+// ---- latency mode (latency.cu): one thread-block cluster per chain, all iterations ----
+struct LatParams {
+  const double* A;   // m x d_pad row-major, zero-padded (A' = A: no affine change of variable)
+  const double* b;   // m
+  int m, d;
+  int64_t d_pad;
+  double* X;         // tiled C_pad x d_pad: x_{t0} in, final iterates out
+  int C;
+  uint32_t chain_offset;
+  uint64_t seed;
+  uint32_t t0;
+  int n_iter;
+  int64_t K;         // refresh period of P = A x
+  double eps;        // S3.3 trim
+  int record;
+  int64_t burn_in, thin;
+  double* S1;        // tiled moments
+  double* S2;
+  int64_t* rej;      // per chain
+  int* err;          // set when a chain's live arcs overflow CTA 0's buffer
+};
+size_t latency_smem_bytes(int64_t d_pad, int m, int cs);
+int latency_cluster_size(int C, int sms);
+cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st);
+
 // ---- fused per-chain ESS kernel (ess_chain.cu) -----------------------------
 struct EssParams {
   // P (= A x_t, incremental), Q (= A nu): C_pad x ldp row-major.
@@ -124,6 +149,7 @@ void tl_access_gemm(unsigned long long* out, bool reset);
 void tl_access_ess(unsigned long long* out, bool reset);
 #endif
 #ifdef TMVN_PHASE_TIMING
+void lat_cycles(unsigned long long* out12, bool reset);
 void phase_cycles(unsigned long long* out10, bool reset);
 void oz_cycles(unsigned long long* out8, bool reset);
 #endif

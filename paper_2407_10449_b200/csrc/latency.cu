@@ -1,0 +1,582 @@
+// latency.cu -- the latency mode (options.latency = 1): one thread-block cluster per
+// chain runs every iteration of Alg. 1 in a single launch.
+//
+// The throughput path (GEMM over all chains, then one fused per-chain kernel per
+// iteration) is launch- and latency-bound when there are fewer chains than SMs --
+// the paper's own timing regime, 1 or 10 chains (S4.2).  Here the m
+// constraints of a chain are split over the CS CTAs of a cluster (CS = 1..16, as many
+// as the SMs allow), each CTA keeps x and nu (all d) and its slice of P = A x and
+// Q = A nu in shared memory, and per iteration:
+//   (a) nu_t (Philox + Box-Muller, C12; every CTA draws the whole vector),
+//   (b) Q_i = a_i . nu for its rows (one warp per row, A' streamed from L2),
+//   (c) the arcs of its rows (eq:roots, C1-C5) + level-1 bucket statistics
+//       (count, max alpha high word, exact max beta),
+//   -- cluster barrier: every CTA merges the CS bucket tables through distributed
+//      shared memory, gamma entering each bucket = exclusive prefix max (Prop. 1),
+//   (d) the arcs of live buckets are appended to CTA 0's buffer (DSMEM atomics),
+//   -- barrier: CTA 0 builds I_act (gamma before an arc = max(gamma entering its
+//      bucket, beta of the arcs of its bucket with a smaller alpha), Alg. 3 without
+//      the sort), trims (C7) and samples theta (C10),
+//   -- barrier: P' = P cos + Q sin for its rows, the safeguard (C8),
+//   -- barrier: accept iff no CTA saw a violation; x <- x cos + nu sin (every CTA,
+//      identically), moments of its coordinate slice, refresh P every K.
+// Four cluster barriers per iteration, no kernel launches, no host round trips.
+// Results follow the same RNG counters and readings as the throughput path; the
+// dot products sum in a different order, so trajectories agree with it (and with
+// the oracle) to rounding, not bitwise.
+#include <cfloat>
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace tmvn {
+namespace {
+
+constexpr int kLT = 256;      // threads per CTA
+constexpr int kLNB = 128;     // level-1 buckets over [0, 2 pi]
+constexpr int kLLive = 1024;  // live arcs CTA 0 can hold per iteration
+
+__device__ __forceinline__ uint64_t lbits(double x) { return (uint64_t)__double_as_longlong(x); }
+__device__ __forceinline__ double lbitsd(uint64_t b) { return __longlong_as_double((long long)b); }
+
+struct LatShared {
+  double* x;       // d_pad
+  double* nu;      // d_pad
+  double* P0;      // mr each: current / proposal, swapped on accept
+  double* P1;
+  double* Q;       // mr
+  double2* st;     // mr: arcs of this CTA's active constraints
+  uint64_t* Gx;    // kLNB: max beta (exact after the low-word pass)
+  uint64_t* mA;    // kLNB: max alpha (high word)
+  int* cnt;        // kLNB
+  uint64_t* gin;   // kLNB: merged gamma entering each bucket
+  int* live;       // kLNB: merged live flag
+  uint64_t* lkey;  // kLLive (CTA 0): live arcs' alpha bits
+  double* lval;    // kLLive: their beta
+  double2* gaps;   // kLLive + 2
+  uint64_t* cand;  // 2 kLLive
+  int* ints;       // [0] n_act, [1] live count, [2] viol, [3] ncand, [4] overflow
+  double* dbl;     // [0] theta, [1] L, [2] u
+};
+
+__device__ __forceinline__ size_t lat_align(size_t v) { return (v + 15) / 16 * 16; }
+
+__device__ LatShared lat_carve(unsigned char* base, int64_t d_pad, int mr) {
+  LatShared S;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* p = base + o;
+    o += lat_align(bytes);
+    return p;
+  };
+  S.x = reinterpret_cast<double*>(take(d_pad * 8));
+  S.nu = reinterpret_cast<double*>(take(d_pad * 8));
+  S.P0 = reinterpret_cast<double*>(take((size_t)mr * 8));
+  S.P1 = reinterpret_cast<double*>(take((size_t)mr * 8));
+  S.Q = reinterpret_cast<double*>(take((size_t)mr * 8));
+  S.st = reinterpret_cast<double2*>(take((size_t)mr * 16));
+  S.Gx = reinterpret_cast<uint64_t*>(take(kLNB * 8));
+  S.mA = reinterpret_cast<uint64_t*>(take(kLNB * 8));
+  S.cnt = reinterpret_cast<int*>(take(kLNB * 4));
+  S.gin = reinterpret_cast<uint64_t*>(take(kLNB * 8));
+  S.live = reinterpret_cast<int*>(take(kLNB * 4));
+  S.lkey = reinterpret_cast<uint64_t*>(take(kLLive * 8));
+  S.lval = reinterpret_cast<double*>(take(kLLive * 8));
+  S.gaps = reinterpret_cast<double2*>(take((kLLive + 2) * 16));
+  S.cand = reinterpret_cast<uint64_t*>(take(2 * kLLive * 8));
+  S.ints = reinterpret_cast<int*>(take(8 * 4));
+  S.dbl = reinterpret_cast<double*>(take(4 * 8));
+  return S;
+}
+
+__device__ __forceinline__ int lat_bucket(double a, double scale) {
+  const int k = (int)__dmul_rn(a, scale);
+  return k < kLNB - 1 ? k : kLNB - 1;
+}
+
+// dot products of up to four rows of A (row stride d_pad, zero-padded, 16-byte aligned)
+// with v (shared, d_pad), one warp, fixed order: 16-byte loads, four partial sums per
+// row, so that sixteen loads per lane are in flight (A is streamed from L2 every
+// iteration: memory-level parallelism bounds this step)
+__device__ __forceinline__ void lat_dot4(const double* __restrict__ A, int nrow, int64_t d_pad,
+                                         const double* v, int lane, double o[4]) {
+  const double2* __restrict__ R[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) R[q] = reinterpret_cast<const double2*>(A + (q < nrow ? q : 0) * d_pad);
+  const double2* V = reinterpret_cast<const double2*>(v);
+  const int np = (int)(d_pad / 2);
+  double s[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[q][u] = 0.0;
+  int j = lane;
+  for (; j + 96 < np; j += 128) {
+    double2 a[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[q][u] = __ldg(R[q] + j + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 w = V[j + 32 * u];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[q][u] = fma(a[q][u].y, w.y, fma(a[q][u].x, w.x, s[q][u]));
+    }
+  }
+  for (; j < np; j += 32) {
+    const double2 w = V[j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 a = __ldg(R[q] + j);
+      s[q][0] = fma(a.y, w.y, fma(a.x, w.x, s[q][0]));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double t = (s[q][0] + s[q][1]) + (s[q][2] + s[q][3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    o[q] = t;
+  }
+}
+// rows [0, nr) of this CTA's slice (global rows i0 + r) . v -> out[r]; warps take row quads
+__device__ __forceinline__ void lat_rows(const double* __restrict__ A, int i0, int nr, int64_t d_pad,
+                                         const double* v, double* out, int warp, int lane) {
+  for (int r = 4 * warp; r < nr; r += 4 * (kLT / 32)) {
+    const int nrow = min(4, nr - r);
+    double o[4];
+    lat_dot4(A + (int64_t)(i0 + r) * d_pad, nrow, d_pad, v, lane, o);
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < nrow) out[r + q] = o[q];
+    }
+  }
+}
+
+// canonical segments (merge touching), trim (C7), L and theta = inverse CDF at u (C10);
+// one thread; the gaps are ascending
+__device__ void lat_theta(double2* gaps, int ngap, double u, double eps, double* theta, double* Lout) {
+  int w = 0;
+  for (int k = 0; k < ngap; ++k) {
+    const double2 g = gaps[k];
+    if (w > 0 && gaps[w - 1].y == g.x) {
+      gaps[w - 1].y = g.y;
+      continue;
+    }
+    gaps[w++] = g;
+  }
+  bool trim = eps > 0.0;
+  int last_kept = -1;
+  if (trim) {
+    for (int k = 0; k < w; ++k) {
+      const double lo = gaps[k].x == 0.0 ? 0.0 : __dadd_rn(gaps[k].x, eps);
+      const double hi = gaps[k].y == kTwoPi ? kTwoPi : __dsub_rn(gaps[k].y, eps);
+      if (hi > lo) last_kept = k;
+    }
+    if (last_kept < 0) trim = false;
+  }
+  if (!trim) last_kept = w - 1;
+  double total = 0.0;
+  for (int k = 0; k < w; ++k) {
+    double lo = gaps[k].x, hi = gaps[k].y;
+    if (trim) {
+      lo = gaps[k].x == 0.0 ? 0.0 : __dadd_rn(gaps[k].x, eps);
+      hi = gaps[k].y == kTwoPi ? kTwoPi : __dsub_rn(gaps[k].y, eps);
+      if (!(hi > lo)) continue;
+    }
+    total = __dadd_rn(total, __dsub_rn(hi, lo));
+  }
+  *Lout = total;
+  *theta = 0.0;
+  if (!(total > 0.0)) return;
+  const double target = __dmul_rn(u, total);
+  double before = 0.0;
+  for (int k = 0; k < w; ++k) {
+    double lo = gaps[k].x, hi = gaps[k].y;
+    if (trim) {
+      lo = gaps[k].x == 0.0 ? 0.0 : __dadd_rn(gaps[k].x, eps);
+      hi = gaps[k].y == kTwoPi ? kTwoPi : __dsub_rn(gaps[k].y, eps);
+      if (!(hi > lo)) continue;
+    }
+    const double after = __dadd_rn(before, __dsub_rn(hi, lo));
+    if (after > target || k == last_kept) {
+      *theta = __dadd_rn(lo, __dsub_rn(target, before));
+      return;
+    }
+    before = after;
+  }
+}
+
+#ifdef TMVN_PHASE_TIMING
+__device__ unsigned long long g_lat_cycles[12];
+#define LPH(i)                                                                          \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && tid == 0) {                                                  \
+      long long n_ = clock64();                                                         \
+      lph[i] += n_ - lt_prev;                                                           \
+      lt_prev = n_;                                                                     \
+    }                                                                                   \
+  } while (0)
+#else
+#define LPH(i) \
+  do {         \
+  } while (0)
+#endif
+
+__global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int chain = (int)(blockIdx.x / CS);
+  if (chain >= p.C) return;  // whole clusters only: uniform across the cluster
+  const uint32_t gchain = p.chain_offset + (uint32_t)chain;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = p.m, d = p.d;
+  const int mr = (m + CS - 1) / CS;
+  const int i0 = rank * mr, i1 = min(m, i0 + mr), nr = i1 > i0 ? i1 - i0 : 0;
+  extern __shared__ __align__(16) unsigned char lsm[];
+  LatShared S = lat_carve(lsm, p.d_pad, mr);
+  // CTA 0's buffers and flags, seen from every CTA of the cluster
+  int* r_ints0 = cluster.map_shared_rank(S.ints, 0);
+  uint64_t* r_lkey0 = cluster.map_shared_rank(S.lkey, 0);
+  double* r_lval0 = cluster.map_shared_rank(S.lval, 0);
+  double* r_dbl0 = cluster.map_shared_rank(S.dbl, 0);
+  const double scale = __ddiv_rn((double)kLNB, kTwoPi);
+
+  // x_{t0} (all d) and P = A x for this CTA's rows
+  for (int j = tid; j < p.d_pad; j += kLT) S.x[j] = j < d ? p.X[tiled_offset(chain, j, p.d_pad)] : 0.0;
+  if (tid < 8) S.ints[tid] = 0;
+  __syncthreads();
+  double* Pc = S.P0;  // P = A x for this CTA's rows
+  double* Pn = S.P1;  // the proposal P'
+  lat_rows(p.A, i0, nr, p.d_pad, S.x, Pc, warp, lane);
+  int64_t rej = 0;
+  cluster.sync();
+#ifdef TMVN_PHASE_TIMING
+  long long lph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long lt_prev = clock64();
+#endif
+
+  for (int it = 0; it < p.n_iter; ++it) {
+    const uint32_t t = p.t0 + (uint32_t)it;
+    // (a) nu_t, u_t
+    for (int pk = tid; pk < (int)(p.d_pad / 2); pk += kLT) {
+      const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
+      S.nu[2 * pk] = v.x;
+      S.nu[2 * pk + 1] = v.y;
+    }
+    if (rank == 0 && tid == 0) S.dbl[2] = theta_uniform(p.seed, t, gchain);
+    for (int j = tid; j < kLNB; j += kLT) {
+      S.Gx[j] = 0;
+      S.mA[j] = 0;
+      S.cnt[j] = 0;
+    }
+    if (tid == 0) S.ints[0] = 0;
+    __syncthreads();
+    LPH(0);
+    // (b) Q for this CTA's rows
+    lat_rows(p.A, i0, nr, p.d_pad, S.nu, S.Q, warp, lane);
+    __syncthreads();
+    LPH(1);
+    // (c) arcs of the active rows + bucket statistics (high words, then low words)
+    for (int r = tid; r < nr; r += kLT) {
+      double al, be;
+      if (arc_of(Pc[r], S.Q[r], __ldg(p.b + i0 + r), al, be)) {
+        const int slot = atomicAdd(&S.ints[0], 1);
+        S.st[slot] = make_double2(al, be);
+        const int k = lat_bucket(al, scale);
+        atomicMax(reinterpret_cast<uint32_t*>(&S.Gx[k]) + 1, (uint32_t)(lbits(be) >> 32));
+        atomicMax(reinterpret_cast<uint32_t*>(&S.mA[k]) + 1, (uint32_t)(lbits(al) >> 32));
+        atomicAdd(&S.cnt[k], 1);
+      }
+    }
+    __syncthreads();
+    const int n_act = S.ints[0];
+    for (int s = tid; s < n_act; s += kLT) {
+      const double2 ab = S.st[s];
+      const int k = lat_bucket(ab.x, scale);
+      if ((uint32_t)(lbits(ab.y) >> 32) == (uint32_t)(S.Gx[k] >> 32))
+        atomicMax(reinterpret_cast<uint32_t*>(&S.Gx[k]), (uint32_t)lbits(ab.y));
+    }
+    LPH(2);
+    cluster.sync();  // #1: every CTA's bucket table is complete
+    LPH(3);
+    // merge the CS tables (every CTA, redundantly): thread j < kLNB owns bucket j and
+    // reads it from every CTA (independent DSMEM loads, in flight together); gamma
+    // entering each bucket = exclusive prefix max (warp scans + the 4 warp totals)
+    {
+      uint64_t g = 0, a = 0;
+      int c = 0;
+      if (tid < kLNB) {
+#pragma unroll 4
+        for (int r = 0; r < CS; ++r) {
+          const uint64_t gv = cluster.map_shared_rank(S.Gx, r)[tid];
+          const uint64_t av = cluster.map_shared_rank(S.mA, r)[tid];
+          const int cv = cluster.map_shared_rank(S.cnt, r)[tid];
+          g = g > gv ? g : gv;
+          a = a > av ? a : av;
+          c += cv;
+        }
+      }
+      uint64_t inc = g;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t n = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = inc > n ? inc : n;
+      }
+      uint64_t* wtot = reinterpret_cast<uint64_t*>(S.cand);  // scratch: CTA 0 uses cand only after barrier #2
+      if (lane == 31 && warp < kLNB / 32) wtot[warp] = inc;
+      __syncthreads();
+      if (tid < kLNB) {
+        uint64_t pre = 0;  // gamma_0 = 0
+        for (int w = 0; w < warp; ++w) pre = pre > wtot[w] ? pre : wtot[w];
+        uint64_t exc = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) exc = 0;
+        const uint64_t gin = pre > exc ? pre : exc;
+        S.gin[tid] = gin;
+        // level 1: only the high word of max alpha is exact -> conservative test
+        S.live[tid] = c > 0 && (a | 0xFFFFFFFFull) > gin;
+        if (tid == kLNB - 1) {
+          const uint64_t tot = gin > g ? gin : g;
+          S.dbl[3] = lbitsd(tot);
+        }
+      }
+    }
+    __syncthreads();
+    // (d) this CTA's arcs in live buckets -> CTA 0's buffer
+    // an arc of a live bucket whose beta <= the gamma entering the bucket lies inside the
+    // earlier arc that set that gamma (it starts before the bucket): it changes neither
+    // the union nor any later gamma, so it is dropped here
+    for (int s = tid; s < n_act; s += kLT) {
+      const double2 ab = S.st[s];
+      const int k = lat_bucket(ab.x, scale);
+      if (S.live[k] && lbits(ab.y) > S.gin[k]) {
+        const int pos = atomicAdd(r_ints0 + 1, 1);
+        if (pos < kLLive) {
+          r_lkey0[pos] = lbits(ab.x);
+          r_lval0[pos] = ab.y;
+        }
+      }
+    }
+    LPH(4);
+    cluster.sync();  // #2: the live arcs are in CTA 0
+    LPH(5);
+#ifdef TMVN_PHASE_TIMING
+    if (blockIdx.x == 0 && tid == 0) lph[11] += S.ints[1];
+#endif
+    if (rank == 0) {
+      const int total = S.ints[1];
+      const uint64_t Gtot = lbits(S.dbl[3]);
+      if (total > kLLive) {
+        if (tid == 0) {
+          S.ints[4] = 1;  // overflow: this iteration stays (L = 0); reported to the host
+          S.dbl[0] = 0.0;
+          S.dbl[1] = 0.0;
+        }
+      } else {
+        // sort the live arcs by alpha (bitonic, padded with +inf keys); bucket order is
+        // alpha order, so gamma before arc e = max(gamma entering its bucket, max beta of
+        // the live arcs sorted before it): arcs of earlier buckets have beta <= that
+        // gamma, and equal alphas give the same gap in either order
+        int n2 = 1;
+        while (n2 < total) n2 <<= 1;
+        for (int e = total + tid; e < n2; e += kLT) {
+          S.lkey[e] = ~0ull;
+          S.lval[e] = 0.0;
+        }
+        __syncthreads();
+        for (int k = 2; k <= n2; k <<= 1) {
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < (n2 >> 1); i += kLT) {
+              const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
+              const uint64_t kl = S.lkey[lo], kh = S.lkey[hi];
+              if ((kl > kh) == ((lo & k) == 0)) {
+                S.lkey[lo] = kh;
+                S.lkey[hi] = kl;
+                const double t2 = S.lval[lo];
+                S.lval[lo] = S.lval[hi];
+                S.lval[hi] = t2;
+              }
+            }
+            __syncthreads();
+          }
+        }
+        // each thread takes a contiguous run of the sorted list: exclusive prefix max of
+        // beta, then the gaps (alpha > gamma) compacted in order by an exclusive prefix sum
+        const int per = (total + kLT - 1) / kLT;
+        const int e0 = min(total, tid * per), e1 = min(total, e0 + per);
+        uint64_t run = 0;
+        for (int e = e0; e < e1; ++e) {
+          const uint64_t v = lbits(S.lval[e]);
+          run = run > v ? run : v;
+        }
+        uint64_t* wmax = reinterpret_cast<uint64_t*>(S.cand);  // scratch (kLT / 32 words)
+        int* wcnt = reinterpret_cast<int*>(S.cand + kLT / 32);
+        uint64_t inc = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t n = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc = inc > n ? inc : n;
+        }
+        if (lane == 31) wmax[warp] = inc;
+        __syncthreads();
+        uint64_t gm = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) gm = 0;
+        for (int w = 0; w < warp; ++w) gm = gm > wmax[w] ? gm : wmax[w];
+        int ng_t = 0;
+        {
+          uint64_t g2 = gm;
+          for (int e = e0; e < e1; ++e) {
+            const uint64_t key = S.lkey[e];
+            const uint64_t gk = S.gin[lat_bucket(lbitsd(key), scale)];
+            const uint64_t gb = g2 > gk ? g2 : gk;
+            ng_t += key > gb ? 1 : 0;
+            const uint64_t v = lbits(S.lval[e]);
+            g2 = g2 > v ? g2 : v;
+          }
+        }
+        int cinc = ng_t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int n = __shfl_up_sync(0xffffffffu, cinc, o);
+          if (lane >= o) cinc += n;
+        }
+        if (lane == 31) wcnt[warp] = cinc;
+        __syncthreads();
+        int pos = cinc - ng_t;
+        for (int w = 0; w < warp; ++w) pos += wcnt[w];
+        for (int e = e0; e < e1; ++e) {
+          const uint64_t key = S.lkey[e];
+          const uint64_t gk = S.gin[lat_bucket(lbitsd(key), scale)];
+          const uint64_t gb = gm > gk ? gm : gk;
+          if (key > gb) S.gaps[pos++] = make_double2(lbitsd(gb), lbitsd(key));
+          const uint64_t v = lbits(S.lval[e]);
+          gm = gm > v ? gm : v;
+        }
+        if (tid == kLT - 1) S.ints[3] = pos;
+        __syncthreads();
+        const int nc = S.ints[3];
+        if (tid == 0) {
+          int ng = nc;
+          const double G = lbitsd(Gtot);
+          if (G < kTwoPi) S.gaps[ng++] = make_double2(G, kTwoPi);  // [gamma_m, 2 pi]
+          lat_theta(S.gaps, ng, S.dbl[2], p.eps, &S.dbl[0], &S.dbl[1]);
+        }
+      }
+      if (tid == 0) S.ints[1] = 0;  // the live buffer is free for the next iteration
+    }
+    LPH(6);
+    cluster.sync();  // #3: theta and L in CTA 0
+    LPH(7);
+    const double theta = r_dbl0[0], L = r_dbl0[1];
+    double sn = 0.0, cs = 1.0;
+    if (L > 0.0) sincos(theta, &sn, &cs);
+    int viol = 0;
+    if (L > 0.0) {
+      for (int r = tid; r < nr; r += kLT) {
+        const double pn = Pc[r] * cs + S.Q[r] * sn;
+        Pn[r] = pn;
+        viol |= (pn - __ldg(p.b + i0 + r)) > 0.0 ? 1 : 0;
+      }
+    }
+    viol = __syncthreads_or(viol);
+    if (tid == 0) S.ints[2] = viol;
+    LPH(8);
+    cluster.sync();  // #4: every CTA's safeguard verdict
+    LPH(9);
+    const int any = __syncthreads_or(tid < CS ? *cluster.map_shared_rank(S.ints + 2, tid) : 0);
+    const bool accept = L > 0.0 && !any;
+    if (accept) {
+      double* tmp = Pc;
+      Pc = Pn;
+      Pn = tmp;
+      for (int j = tid; j < p.d_pad; j += kLT) S.x[j] = S.x[j] * cs + S.nu[j] * sn;
+    } else {
+      ++rej;
+    }
+    __syncthreads();
+    const int64_t tt = (int64_t)t;
+    if (p.record && tt >= p.burn_in && ((tt - p.burn_in) % (p.thin < 1 ? 1 : p.thin)) == 0) {
+      for (int j = rank * kLT + tid; j < d; j += CS * kLT) {  // this CTA's coordinate slice
+        const int64_t o = tiled_offset(chain, j, p.d_pad);
+        const double xv = S.x[j];
+        p.S1[o] += xv;
+        p.S2[o] += xv * xv;
+      }
+    }
+    if ((int64_t)(t + 1) % p.K == 0) {  // refresh P = A x (C13)
+      lat_rows(p.A, i0, nr, p.d_pad, S.x, Pc, warp, lane);
+    }
+    __syncthreads();
+    LPH(10);
+  }
+#ifdef TMVN_PHASE_TIMING
+  if (blockIdx.x == 0 && tid == 0)
+    for (int i = 0; i < 12; ++i) atomicAdd(&g_lat_cycles[i], (unsigned long long)lph[i]);
+#endif
+  if (rank == 0) {
+    for (int j = tid; j < d; j += kLT) p.X[tiled_offset(chain, j, p.d_pad)] = S.x[j];
+    if (tid == 0) {
+      p.rej[chain] += rej;
+      if (S.ints[4]) atomicExch(p.err, 1);
+    }
+  }
+  cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+}  // namespace
+
+#ifdef TMVN_PHASE_TIMING
+void lat_cycles(unsigned long long* out, bool reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_lat_cycles, sizeof(unsigned long long) * 12);
+  if (reset) {
+    unsigned long long z[12] = {0};
+    cudaMemcpyToSymbol(g_lat_cycles, z, sizeof(z));
+  }
+}
+#endif
+
+size_t latency_smem_bytes(int64_t d_pad, int m, int cs) {
+  const int mr = (m + cs - 1) / cs;
+  auto al = [](size_t v) { return (v + 15) / 16 * 16; };
+  return 2 * al(d_pad * 8) + 3 * al((size_t)mr * 8) + al((size_t)mr * 16) + 3 * al(kLNB * 8) +
+         2 * al(kLNB * 4) + al(kLLive * 8) * 2 + al((kLLive + 2) * 16) + al(2 * kLLive * 8) + al(32) + al(32);
+}
+
+// cluster size: the largest power of two <= 16 with C clusters fitting the SMs (>= 1)
+int latency_cluster_size(int C, int sms) {
+  int cs = 16;
+  while (cs > 1 && (int64_t)C * cs > sms) cs >>= 1;
+  return cs;
+}
+
+cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st) {
+  const size_t smem = latency_smem_bytes(p.d_pad, p.m, cs);
+  cudaError_t e = cudaFuncSetAttribute(latency_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8) {
+    e = cudaFuncSetAttribute(latency_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.C * cs));
+  cfg.blockDim = dim3(kLT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, latency_kernel, p);
+}
+
+}  // namespace tmvn

@@ -34,6 +34,7 @@ struct tmvn_ctx {
   int64_t m = 0, d = 0, m_pad = 0, d_pad = 0, d_r128 = 0;
   // constraints
   double* A_row = nullptr;  // m x d (original)
+  double* A_pad = nullptr;  // m x d_pad, zero-padded rows (latency mode; made on first use)
   double* b_orig = nullptr; // m
   double* A_tiled = nullptr;  // tiled m_pad x d_pad of the ORIGINAL A (for A L)
   double* At = nullptr;     // tiled m_pad x d_pad of A' (= A L if affine)
@@ -876,6 +877,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->rng_ahead = 0;  // measured slower on B200 (the GEMM loses more than the ESS kernel gains)
   o->schedule = 0;
   o->pipeline = 0;
+  o->latency = 0;
   return TMVN_OK;
 }
 
@@ -1011,6 +1013,68 @@ tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
   return TMVN_OK;
 }
 
+// The latency mode (options.latency = 1): one cluster of CTAs per chain runs every
+// iteration in one launch (latency.cu).  Taken when the problem fits its limits (no
+// affine change of variable, shared memory), else the throughput loop runs.
+bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out) {
+  if (h->opt.latency != 1 || h->affine) return false;
+  int dev = 0, sms = 0, smem_max = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int cs = latency_cluster_size((int)C, sms);
+  while (cs < 16 && latency_smem_bytes(h->d_pad, (int)h->m, cs) > (size_t)smem_max) cs <<= 1;
+  if (latency_smem_bytes(h->d_pad, (int)h->m, cs) > (size_t)smem_max) return false;
+  *cs_out = cs;
+  return true;
+}
+
+tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int cs, int64_t* n_recorded) {
+  cudaStream_t st = stream_of(h);
+  if (!h->A_pad) {
+    CK(h, dalloc(&h->A_pad, (size_t)(h->m * h->d_pad)));
+    CK(h, cudaMemsetAsync(h->A_pad, 0, (size_t)(h->m * h->d_pad) * sizeof(double), st));
+    CK(h, cudaMemcpy2DAsync(h->A_pad, (size_t)h->d_pad * sizeof(double), h->A_row, (size_t)h->d * sizeof(double),
+                            (size_t)h->d * sizeof(double), (size_t)h->m, cudaMemcpyDeviceToDevice, st));
+  }
+  LatParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.A = h->A_pad;
+  p.b = h->b_eff;
+  p.m = (int)h->m;
+  p.d = (int)h->d;
+  p.d_pad = h->d_pad;
+  p.X = h->X;
+  p.C = (int)C;
+  p.chain_offset = (uint32_t)h->opt.chain_offset;
+  p.seed = seed;
+  p.t0 = (uint32_t)h->opt.iter_offset;
+  p.n_iter = (int)n_iter;
+  p.K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
+  p.eps = h->opt.trim_eps;
+  p.record = h->opt.record;
+  p.burn_in = h->opt.burn_in;
+  p.thin = h->opt.thin;
+  p.S1 = h->S1;
+  p.S2 = h->S2;
+  p.rej = h->rej;
+  if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
+  p.err = h->dyn + 64 * 16 - 1;
+  CK(h, cudaMemsetAsync(p.err, 0, sizeof(int), st));
+  KL(h, launch_latency(p, cs, st));
+  int err = 0;
+  CK(h, cudaMemcpyAsync(&err, p.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  if (err)
+    return fail(h, TMVN_E_STATE,
+                "latency mode: more live arcs than its per-chain buffer (1024) in some iteration; "
+                "the affected steps stayed -- use options.latency = 0 for this polytope");
+  int64_t nrec = 0;
+  for (int64_t it = 0; it < n_iter; ++it) nrec += recorded_iter(h->opt, h->opt.iter_offset + it) ? 1 : 0;
+  *n_recorded = nrec;
+  return TMVN_OK;
+}
+
 tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed,
                         double* out) {
   tmvn_status s = check_sample_args(h, X0, C, n_iter, out);
@@ -1023,7 +1087,12 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;
   if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
   int64_t nrec = 0;
-  if ((s = run_loop(h, C, n_iter, seed, h->P0, &nrec)) != TMVN_OK) return s;
+  int lcs = 0;
+  if (n_iter > 0 && latency_fits(h, C, &lcs)) {
+    if ((s = run_latency(h, C, n_iter, seed, lcs, &nrec)) != TMVN_OK) return s;
+  } else if ((s = run_loop(h, C, n_iter, seed, h->P0, &nrec)) != TMVN_OK) {
+    return s;
+  }
   if ((s = store_X(h, C, out)) != TMVN_OK) return s;
   if ((s = finish_stats(h, C, n_iter, nrec)) != TMVN_OK) return s;
   if (h->opt.auto_advance) h->opt.iter_offset += n_iter;
@@ -1083,7 +1152,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->dyn);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
-  dfree(h->A_tiled); dfree(h->A_row); dfree(h->b_orig); dfree(h->b_eff);
+  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
   dfree(h->As); dfree(h->rowscale);
@@ -1380,6 +1449,10 @@ tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t 
 // timing build only (tools/phase_timing.py): per-phase CTA cycles of ess_kernel
 tmvn_status tmvn_test_phase_cycles(uint64_t* out10, int reset) {
   tmvn::phase_cycles(reinterpret_cast<unsigned long long*>(out10), reset != 0);
+  return TMVN_OK;
+}
+tmvn_status tmvn_test_lat_cycles(uint64_t* out12, int reset) {
+  tmvn::lat_cycles(reinterpret_cast<unsigned long long*>(out12), reset != 0);
   return TMVN_OK;
 }
 tmvn_status tmvn_test_oz_cycles(uint64_t* out8, int reset) {

@@ -1,0 +1,100 @@
+"""The latency mode (options.latency = 1, latency.cu): one thread-block cluster per
+chain runs every iteration in one launch.  Parity with the oracle step by step
+(north_star bar: next iterate within 1e-10 relative), agreement with the default
+path over many iterations, moments, the paper's S4.2 instances and the
+orthant closed form."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2407_10449_b200 as tm
+from paper_2407_10449_b200 import synth
+
+pytestmark = pytest.mark.gpu
+REL = 1e-10
+
+
+@pytest.mark.parametrize("k,kw,C", [(3, dict(m=300, d=150), 10), (5, dict(m=700, d=300), 3),
+                                    (4, dict(m=6000, d=20), 5), (1, dict(), 16)])
+def test_latency_step_parity_with_oracle(k, kw, C):
+    A, b, x0 = synth.make_instance(k, **kw)
+    cfg = synth.CONFIGS[k]
+    s = tm.Sampler(A, b, latency=1, record=0)
+    X = np.tile(x0, (C, 1))
+    bad = 0
+    for t in range(25):  # one iteration per call: x_t -> x_{t+1}
+        Xn = s.sample(X, 1, seed=cfg.chain_seed)
+        for c in range(C):
+            xn, _ = oracle.step(A, b, X[c], cfg.chain_seed, t, c)
+            if np.max(np.abs(Xn[c] - xn)) > REL * max(1.0, np.max(np.abs(xn))):
+                bad += 1
+            assert np.max(A @ Xn[c] - b) <= 1e-12
+        X = Xn
+    assert bad <= 1, bad
+    assert s.stats()["rejections"] == 0
+
+
+def test_latency_matches_default_path():
+    """Same RNG counters and readings; the dot products sum in another order, so the
+    trajectories agree to rounding at first and drift apart slowly (the map x -> x'
+    amplifies differences through the arc endpoints): 20 iterations at 1e-9, and a
+    long run only statistically (test_latency_orthant_moments)."""
+    A, b, x0 = synth.make_instance(3, m=400, d=120)
+    C, T = 12, 20
+    X0 = np.tile(x0, (C, 1))
+    ref = tm.Sampler(A, b).sample(X0, T, seed=3)
+    lat = tm.Sampler(A, b, latency=1).sample(X0, T, seed=3)
+    assert np.max(np.abs(lat - ref)) <= 1e-9 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_latency_moments_and_counters():
+    A, b, x0 = synth.make_instance(3, m=200, d=40)
+    C, T = 7, 60
+    s = tm.Sampler(A, b, latency=1, burn_in=10, thin=3)
+    X = np.tile(x0, (C, 1))
+    s.sample(X, T, seed=8)
+    sm, sq, n = s.moments()
+    # the same iterates one call at a time (the per-step path of the same mode)
+    s2 = tm.Sampler(A, b, latency=1, record=0)
+    Y = np.tile(x0, (C, 1))
+    acc, acc2, cnt = np.zeros(40), np.zeros(40), 0
+    for t in range(T):
+        Y = s2.sample(Y, 1, seed=8)
+        if t >= 10 and (t - 10) % 3 == 0:
+            acc += Y.sum(0)
+            acc2 += (Y ** 2).sum(0)
+            cnt += C
+    assert n == cnt
+    assert np.allclose(sm, acc, rtol=1e-9, atol=1e-9)
+    assert np.allclose(sq, acc2, rtol=1e-9, atol=1e-9)
+    assert s.stats()["steps"] == C * T and s.stats()["rejections"] == 0
+
+
+@pytest.mark.parametrize("d,chains", [(300, 1), (300, 10), (1000, 10)])
+def test_latency_section_4_2_instances(d, chains):
+    A, b, x0 = synth.paper_random(d, seed=d)
+    s = tm.Sampler(A, b, latency=1)
+    out = s.sample(np.tile(x0, (chains, 1)), 100, seed=42)
+    assert s.stats()["rejections"] == 0
+    assert np.max(out @ A.T - b) <= 0.0
+    # step parity along the latency path's own trajectory (one iteration per call)
+    s1 = tm.Sampler(A, b, latency=1, record=0)
+    X = np.tile(x0, (chains, 1))
+    for t in range(8):
+        Xn = s1.sample(X, 1, seed=42)
+        for c in range(chains):
+            xn, _ = oracle.step(A, b, X[c], 42, t, c)
+            assert np.max(np.abs(Xn[c] - xn)) <= REL * max(1.0, np.max(np.abs(xn)))
+        X = Xn
+
+
+def test_latency_orthant_moments():
+    A, b, x0 = synth.make_instance(2)
+    s = tm.Sampler(A, b, latency=1, burn_in=15000)  # the default path's protocol (slow mixing)
+    s.sample(np.tile(x0, (256, 1)), 20000, seed=102)
+    sm, sq, n = s.moments()
+    mean, var = sm / n, sq / n - (sm / n) ** 2
+    assert abs(mean.mean() - math.sqrt(2 / math.pi)) < 0.01
+    assert abs(var.mean() - (1 - 2 / math.pi)) < 0.01

@@ -149,7 +149,7 @@ void tl_access_gemm(unsigned long long* out, bool reset);
 void tl_access_ess(unsigned long long* out, bool reset);
 #endif
 #ifdef TMVN_PHASE_TIMING
-void lat_cycles(unsigned long long* out12, bool reset);
+void lat_cycles(unsigned long long* out16, bool reset);
 void phase_cycles(unsigned long long* out10, bool reset);
 void oz_cycles(unsigned long long* out8, bool reset);
 #endif

@@ -38,6 +38,7 @@ namespace {
 constexpr int kLT = 256;      // threads per CTA
 constexpr int kLNB = 128;     // level-1 buckets over [0, 2 pi]
 constexpr int kLLive = 1024;  // live arcs CTA 0 can hold per iteration
+constexpr int kLNF = 1024;    // level-2 slots CTA 0 splits the live level-1 buckets into
 
 __device__ __forceinline__ uint64_t lbits(double x) { return (uint64_t)__double_as_longlong(x); }
 __device__ __forceinline__ double lbitsd(uint64_t b) { return __longlong_as_double((long long)b); }
@@ -57,20 +58,31 @@ struct LatShared {
   uint64_t* lkey;  // kLLive (CTA 0): live arcs' alpha bits
   double* lval;    // kLLive: their beta
   double2* gaps;   // kLLive + 2
+  uint64_t* fb;    // kLNF (CTA 0): level-2 max beta, then gamma entering the slot
+  uint64_t* fa;    // kLNF: level-2 max alpha
+  int* fc;         // kLNF: level-2 count, then live flag
+  int* fid;        // kLLive: level-2 slot of each live arc
+  int* cl;         // kLLive: live arcs in live level-2 slots
+  int* lrk;        // kLNB: rank of a live level-1 bucket among the live ones
+  int* lb;         // kLNB: live level-1 bucket of each rank
+  uint64_t* scr;   // 16 words of scan scratch
   uint64_t* cand;  // 2 kLLive
+  double* M1;      // nk x kLT: this CTA's moment sums over the call (flushed at the end)
+  double* M2;
   int* ints;       // [0] n_act, [1] live count, [2] viol, [3] ncand, [4] overflow
   double* dbl;     // [0] theta, [1] L, [2] u
 };
 
-__device__ __forceinline__ size_t lat_align(size_t v) { return (v + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ size_t lat_align(size_t v) { return (v + 15) / 16 * 16; }
 
-__device__ LatShared lat_carve(unsigned char* base, int64_t d_pad, int mr) {
-  LatShared S;
+// shared-memory layout (host: base = nullptr, only the size is used)
+__host__ __device__ inline int lat_nk(int64_t d_pad, int cs) { return (int)((d_pad + (int64_t)cs * kLT - 1) / ((int64_t)cs * kLT)); }
+__host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, int mr, int nk, LatShared& S) {
   size_t o = 0;
   auto take = [&](size_t bytes) {
-    unsigned char* p = base + o;
+    unsigned char* q = base + o;
     o += lat_align(bytes);
-    return p;
+    return q;
   };
   S.x = reinterpret_cast<double*>(take(d_pad * 8));
   S.nu = reinterpret_cast<double*>(take(d_pad * 8));
@@ -83,13 +95,23 @@ __device__ LatShared lat_carve(unsigned char* base, int64_t d_pad, int mr) {
   S.cnt = reinterpret_cast<int*>(take(kLNB * 4));
   S.gin = reinterpret_cast<uint64_t*>(take(kLNB * 8));
   S.live = reinterpret_cast<int*>(take(kLNB * 4));
+  S.lrk = reinterpret_cast<int*>(take(kLNB * 4));
+  S.lb = reinterpret_cast<int*>(take(kLNB * 4));
+  S.scr = reinterpret_cast<uint64_t*>(take(16 * 8));
+  S.M1 = reinterpret_cast<double*>(take((size_t)nk * kLT * 8));
+  S.M2 = reinterpret_cast<double*>(take((size_t)nk * kLT * 8));
+  S.ints = reinterpret_cast<int*>(take(8 * 4));
+  S.dbl = reinterpret_cast<double*>(take(4 * 8));
   S.lkey = reinterpret_cast<uint64_t*>(take(kLLive * 8));
   S.lval = reinterpret_cast<double*>(take(kLLive * 8));
   S.gaps = reinterpret_cast<double2*>(take((kLLive + 2) * 16));
   S.cand = reinterpret_cast<uint64_t*>(take(2 * kLLive * 8));
-  S.ints = reinterpret_cast<int*>(take(8 * 4));
-  S.dbl = reinterpret_cast<double*>(take(4 * 8));
-  return S;
+  S.fb = reinterpret_cast<uint64_t*>(take(kLNF * 8));
+  S.fa = reinterpret_cast<uint64_t*>(take(kLNF * 8));
+  S.fc = reinterpret_cast<int*>(take(kLNF * 4));
+  S.fid = reinterpret_cast<int*>(take(kLLive * 4));
+  S.cl = reinterpret_cast<int*>(take(kLLive * 4));
+  return o;
 }
 
 __device__ __forceinline__ int lat_bucket(double a, double scale) {
@@ -113,26 +135,20 @@ __device__ __forceinline__ void lat_dot4(const double* __restrict__ A, int nrow,
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int u = 0; u < 4; ++u) s[q][u] = 0.0;
-  int j = lane;
-  for (; j + 96 < np; j += 128) {
+  // blocks of 128 pairs; the last block's loads past the row are predicated off
+  // (zero), so every block is one round trip with sixteen loads per lane in flight
+  for (int j = lane; j < np; j += 128) {
     double2 a[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[q][u] = __ldg(R[q] + j + 32 * u);
+      for (int u = 0; u < 4; ++u)
+        a[q][u] = j + 32 * u < np ? __ldg(R[q] + j + 32 * u) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double2 w = V[j + 32 * u];
+      const double2 w = j + 32 * u < np ? V[j + 32 * u] : make_double2(0.0, 0.0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) s[q][u] = fma(a[q][u].y, w.y, fma(a[q][u].x, w.x, s[q][u]));
-    }
-  }
-  for (; j < np; j += 32) {
-    const double2 w = V[j];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const double2 a = __ldg(R[q] + j);
-      s[q][0] = fma(a.y, w.y, fma(a.x, w.x, s[q][0]));
     }
   }
 #pragma unroll
@@ -213,7 +229,7 @@ __device__ void lat_theta(double2* gaps, int ngap, double u, double eps, double*
 }
 
 #ifdef TMVN_PHASE_TIMING
-__device__ unsigned long long g_lat_cycles[12];
+__device__ unsigned long long g_lat_cycles[16];
 #define LPH(i)                                                                          \
   do {                                                                                  \
     if (blockIdx.x == 0 && tid == 0) {                                                  \
@@ -240,7 +256,9 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   const int mr = (m + CS - 1) / CS;
   const int i0 = rank * mr, i1 = min(m, i0 + mr), nr = i1 > i0 ? i1 - i0 : 0;
   extern __shared__ __align__(16) unsigned char lsm[];
-  LatShared S = lat_carve(lsm, p.d_pad, mr);
+  LatShared S;
+  const int nk = lat_nk(p.d_pad, CS);
+  lat_carve(lsm, p.d_pad, mr, nk, S);
   // CTA 0's buffers and flags, seen from every CTA of the cluster
   int* r_ints0 = cluster.map_shared_rank(S.ints, 0);
   uint64_t* r_lkey0 = cluster.map_shared_rank(S.lkey, 0);
@@ -251,14 +269,19 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   // x_{t0} (all d) and P = A x for this CTA's rows
   for (int j = tid; j < p.d_pad; j += kLT) S.x[j] = j < d ? p.X[tiled_offset(chain, j, p.d_pad)] : 0.0;
   if (tid < 8) S.ints[tid] = 0;
+  for (int k = 0; k < nk; ++k) {
+    S.M1[k * kLT + tid] = 0.0;
+    S.M2[k * kLT + tid] = 0.0;
+  }
   __syncthreads();
   double* Pc = S.P0;  // P = A x for this CTA's rows
   double* Pn = S.P1;  // the proposal P'
-  lat_rows(p.A, i0, nr, p.d_pad, S.x, Pc, warp, lane);
+  auto gemv = [&](const double* v, double* out) { lat_rows(p.A, i0, nr, p.d_pad, v, out, warp, lane); };
+  gemv(S.x, Pc);
   int64_t rej = 0;
   cluster.sync();
 #ifdef TMVN_PHASE_TIMING
-  long long lph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long lph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long lt_prev = clock64();
 #endif
 
@@ -280,7 +303,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     __syncthreads();
     LPH(0);
     // (b) Q for this CTA's rows
-    lat_rows(p.A, i0, nr, p.d_pad, S.nu, S.Q, warp, lane);
+    gemv(S.nu, S.Q);
     __syncthreads();
     LPH(1);
     // (c) arcs of the active rows + bucket statistics (high words, then low words)
@@ -379,88 +402,134 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
           S.dbl[1] = 0.0;
         }
       } else {
-        // sort the live arcs by alpha (bitonic, padded with +inf keys); bucket order is
-        // alpha order, so gamma before arc e = max(gamma entering its bucket, max beta of
-        // the live arcs sorted before it): arcs of earlier buckets have beta <= that
-        // gamma, and equal alphas give the same gap in either order
-        int n2 = 1;
-        while (n2 < total) n2 <<= 1;
-        for (int e = total + tid; e < n2; e += kLT) {
-          S.lkey[e] = ~0ull;
-          S.lval[e] = 0.0;
-        }
-        __syncthreads();
-        for (int k = 2; k <= n2; k <<= 1) {
-          for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < (n2 >> 1); i += kLT) {
-              const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
-              const uint64_t kl = S.lkey[lo], kh = S.lkey[hi];
-              if ((kl > kh) == ((lo & k) == 0)) {
-                S.lkey[lo] = kh;
-                S.lkey[hi] = kl;
-                const double t2 = S.lval[lo];
-                S.lval[lo] = S.lval[hi];
-                S.lval[hi] = t2;
-              }
-            }
-            __syncthreads();
-          }
-        }
-        // each thread takes a contiguous run of the sorted list: exclusive prefix max of
-        // beta, then the gaps (alpha > gamma) compacted in order by an exclusive prefix sum
-        const int per = (total + kLT - 1) / kLT;
-        const int e0 = min(total, tid * per), e1 = min(total, e0 + per);
-        uint64_t run = 0;
-        for (int e = e0; e < e1; ++e) {
-          const uint64_t v = lbits(S.lval[e]);
-          run = run > v ? run : v;
-        }
-        uint64_t* wmax = reinterpret_cast<uint64_t*>(S.cand);  // scratch (kLT / 32 words)
-        int* wcnt = reinterpret_cast<int*>(S.cand + kLT / 32);
-        uint64_t inc = run;
+        // Level 2 (Alg. 3's bucketing applied once more, inside CTA 0): the live level-1
+        // buckets, in order, are split into SUB equal slots each; slot index is monotone in
+        // alpha, so gamma entering a slot = max(gamma entering its level-1 bucket, max beta
+        // of the earlier slots), and only slots whose max alpha exceeds it can hold a gap
+        // start. Arcs of such slots get gamma from the slot's earlier arcs (alpha order,
+        // equal alphas by index: the same gap either way); the gaps are ranked by alpha.
+        // (S4.2's arcs all start just past theta = 0: one live level-1 bucket holds them.)
+        if (tid < kLNB) {
+          const int lv = S.live[tid] ? 1 : 0;
+          int ci = lv;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint64_t n = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc = inc > n ? inc : n;
-        }
-        if (lane == 31) wmax[warp] = inc;
-        __syncthreads();
-        uint64_t gm = __shfl_up_sync(0xffffffffu, inc, 1);
-        if (lane == 0) gm = 0;
-        for (int w = 0; w < warp; ++w) gm = gm > wmax[w] ? gm : wmax[w];
-        int ng_t = 0;
-        {
-          uint64_t g2 = gm;
-          for (int e = e0; e < e1; ++e) {
-            const uint64_t key = S.lkey[e];
-            const uint64_t gk = S.gin[lat_bucket(lbitsd(key), scale)];
-            const uint64_t gb = g2 > gk ? g2 : gk;
-            ng_t += key > gb ? 1 : 0;
-            const uint64_t v = lbits(S.lval[e]);
-            g2 = g2 > v ? g2 : v;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, ci, o);
+            if (lane >= o) ci += n;
           }
+          if (lane == 31) S.scr[warp] = (uint64_t)ci;
         }
-        int cinc = ng_t;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int n = __shfl_up_sync(0xffffffffu, cinc, o);
-          if (lane >= o) cinc += n;
+        for (int f = tid; f < kLNF; f += kLT) {
+          S.fb[f] = 0;
+          S.fa[f] = 0;
+          S.fc[f] = 0;
         }
-        if (lane == 31) wcnt[warp] = cinc;
+        if (tid == 0) {
+          S.ints[3] = 0;
+          S.ints[5] = 0;
+        }
         __syncthreads();
-        int pos = cinc - ng_t;
-        for (int w = 0; w < warp; ++w) pos += wcnt[w];
-        for (int e = e0; e < e1; ++e) {
+        if (tid < kLNB) {
+          int rk = 0;
+          for (int w = 0; w < warp; ++w) rk += (int)S.scr[w];
+          const int lv = S.live[tid] ? 1 : 0;
+          int ci = lv;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, ci, o);
+            if (lane >= o) ci += n;
+          }
+          rk += ci - lv;
+          S.lrk[tid] = rk;
+          if (lv) S.lb[rk] = tid;
+        }
+        int nlb = 0;
+        for (int w = 0; w < kLNB / 32; ++w) nlb += (int)S.scr[w];
+        const int SUB = kLNF / (nlb > 0 ? nlb : 1);
+        __syncthreads();
+        for (int e = tid; e < total; e += kLT) {
           const uint64_t key = S.lkey[e];
-          const uint64_t gk = S.gin[lat_bucket(lbitsd(key), scale)];
-          const uint64_t gb = gm > gk ? gm : gk;
-          if (key > gb) S.gaps[pos++] = make_double2(lbitsd(gb), lbitsd(key));
-          const uint64_t v = lbits(S.lval[e]);
-          gm = gm > v ? gm : v;
+          const double u = __dmul_rn(lbitsd(key), scale);
+          const int k = lat_bucket(lbitsd(key), scale);
+          const int sub = min(SUB - 1, (int)__dmul_rn(__dsub_rn(u, (double)k), (double)SUB));
+          const int f = S.lrk[k] * SUB + sub;
+          S.fid[e] = f;
+          atomicMax(reinterpret_cast<unsigned long long*>(&S.fb[f]), (unsigned long long)lbits(S.lval[e]));
+          atomicMax(reinterpret_cast<unsigned long long*>(&S.fa[f]), (unsigned long long)key);
+          atomicAdd(&S.fc[f], 1);
         }
-        if (tid == kLT - 1) S.ints[3] = pos;
+        __syncthreads();
+        {  // exclusive prefix max of the slots' max beta (four slots per thread)
+          constexpr int FP = kLNF / kLT;
+          uint64_t mb[FP];
+          uint64_t run = 0;
+#pragma unroll
+          for (int q = 0; q < FP; ++q) {
+            mb[q] = S.fb[tid * FP + q];
+            run = run > mb[q] ? run : mb[q];
+          }
+          uint64_t inc = run;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t n = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc = inc > n ? inc : n;
+          }
+          if (lane == 31) S.scr[8 + warp] = inc;
+          __syncthreads();
+          uint64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+          if (lane == 0) ex = 0;
+          for (int w = 0; w < warp; ++w) ex = ex > S.scr[8 + w] ? ex : S.scr[8 + w];
+#pragma unroll
+          for (int q = 0; q < FP; ++q) {
+            const int f = tid * FP + q;
+            const int rk = f / SUB;
+            if (rk < nlb) {
+              const uint64_t gk = S.gin[S.lb[rk]];
+              const uint64_t g = ex > gk ? ex : gk;
+              const bool live = S.fc[f] > 0 && S.fa[f] > g;
+              S.fb[f] = g;
+              S.fc[f] = live ? 1 : 0;
+            }
+            ex = ex > mb[q] ? ex : mb[q];
+          }
+        }
+        __syncthreads();
+        for (int e = tid; e < total; e += kLT)
+          if (S.fc[S.fid[e]]) S.cl[atomicAdd(&S.ints[5], 1)] = e;
+        __syncthreads();
+        const int nl2 = S.ints[5];
+        for (int c = tid; c < nl2; c += kLT) {
+          const int e = S.cl[c], f = S.fid[e];
+          const uint64_t key = S.lkey[e];
+          uint64_t gm = S.fb[f];
+          for (int c2 = 0; c2 < nl2; ++c2) {
+            const int e2 = S.cl[c2];
+            if (S.fid[e2] != f) continue;
+            const uint64_t k2 = S.lkey[e2];
+            if (k2 < key || (k2 == key && e2 < e)) {
+              const uint64_t v2 = lbits(S.lval[e2]);
+              gm = gm > v2 ? gm : v2;
+            }
+          }
+          if (key > gm) {
+            const int c3 = atomicAdd(&S.ints[3], 1);
+            S.cand[2 * c3] = key;
+            S.cand[2 * c3 + 1] = gm;
+          }
+        }
+        __syncthreads();
+        {
+          const int nc = S.ints[3];
+          for (int c = tid; c < nc; c += kLT) {
+            const uint64_t a = S.cand[2 * c];
+            int rnk = 0;
+            for (int c2 = 0; c2 < nc; ++c2) rnk += S.cand[2 * c2] < a ? 1 : 0;
+            S.gaps[rnk] = make_double2(lbitsd(S.cand[2 * c + 1]), lbitsd(a));
+          }
+        }
         __syncthreads();
         const int nc = S.ints[3];
+        LPH(14);
         if (tid == 0) {
           int ng = nc;
           const double G = lbitsd(Gtot);
@@ -502,23 +571,29 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     __syncthreads();
     const int64_t tt = (int64_t)t;
     if (p.record && tt >= p.burn_in && ((tt - p.burn_in) % (p.thin < 1 ? 1 : p.thin)) == 0) {
-      for (int j = rank * kLT + tid; j < d; j += CS * kLT) {  // this CTA's coordinate slice
-        const int64_t o = tiled_offset(chain, j, p.d_pad);
+      for (int k = 0, j = rank * kLT + tid; j < d; ++k, j += CS * kLT) {  // this CTA's coordinates
         const double xv = S.x[j];
-        p.S1[o] += xv;
-        p.S2[o] += xv * xv;
+        S.M1[k * kLT + tid] += xv;
+        S.M2[k * kLT + tid] += xv * xv;
       }
     }
     if ((int64_t)(t + 1) % p.K == 0) {  // refresh P = A x (C13)
-      lat_rows(p.A, i0, nr, p.d_pad, S.x, Pc, warp, lane);
+      gemv(S.x, Pc);
     }
     __syncthreads();
     LPH(10);
   }
 #ifdef TMVN_PHASE_TIMING
   if (blockIdx.x == 0 && tid == 0)
-    for (int i = 0; i < 12; ++i) atomicAdd(&g_lat_cycles[i], (unsigned long long)lph[i]);
+    for (int i = 0; i < 16; ++i) atomicAdd(&g_lat_cycles[i], (unsigned long long)lph[i]);
 #endif
+  if (p.record) {
+    for (int k = 0, j = rank * kLT + tid; j < d; ++k, j += CS * kLT) {
+      const int64_t o = tiled_offset(chain, j, p.d_pad);
+      p.S1[o] += S.M1[k * kLT + tid];
+      p.S2[o] += S.M2[k * kLT + tid];
+    }
+  }
   if (rank == 0) {
     for (int j = tid; j < d; j += kLT) p.X[tiled_offset(chain, j, p.d_pad)] = S.x[j];
     if (tid == 0) {
@@ -534,19 +609,17 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
 #ifdef TMVN_PHASE_TIMING
 void lat_cycles(unsigned long long* out, bool reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_lat_cycles, sizeof(unsigned long long) * 12);
+  cudaMemcpyFromSymbol(out, g_lat_cycles, sizeof(unsigned long long) * 16);
   if (reset) {
-    unsigned long long z[12] = {0};
+    unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_lat_cycles, z, sizeof(z));
   }
 }
 #endif
 
 size_t latency_smem_bytes(int64_t d_pad, int m, int cs) {
-  const int mr = (m + cs - 1) / cs;
-  auto al = [](size_t v) { return (v + 15) / 16 * 16; };
-  return 2 * al(d_pad * 8) + 3 * al((size_t)mr * 8) + al((size_t)mr * 16) + 3 * al(kLNB * 8) +
-         2 * al(kLNB * 4) + al(kLLive * 8) * 2 + al((kLLive + 2) * 16) + al(2 * kLLive * 8) + al(32) + al(32);
+  LatShared S;
+  return lat_carve(nullptr, d_pad, (m + cs - 1) / cs, lat_nk(d_pad, cs), S);
 }
 
 // cluster size: the largest power of two <= 16 with C clusters fitting the SMs (>= 1)

@@ -12,13 +12,14 @@ k = int(sys.argv[1]); iters = int(sys.argv[2])
 cfg = synth.CONFIGS[k]
 A, b, x0 = synth.make_instance(k)
 s = tm.Sampler(A, b, latency=1)
-X = np.tile(x0, (cfg.C, 1))
+C = int(sys.argv[3]) if len(sys.argv) > 3 else cfg.C
+X = np.tile(x0, (C, 1))
 X = s.sample(X, 10, cfg.chain_seed)
-buf = np.zeros(12, dtype=np.uint64)
+buf = np.zeros(16, dtype=np.uint64)
 L.tmvn_test_lat_cycles(buf.ctypes.data_as(ctypes.c_void_p), 1)
 s.sample(X, iters, cfg.chain_seed)
 L.tmvn_test_lat_cycles(buf.ctypes.data_as(ctypes.c_void_p), 0)
 names = ["a nu", "b Q rows", "c arcs+stats", "sync1", "merge+gather", "sync2", "CTA0 I_act+theta", "sync3",
-         "P'+safeguard", "sync4", "update+moments+refresh", "(live arcs)"]
+         "P'+safeguard", "sync4", "update+moments+refresh", "(live arcs)", "  CTA0 pre-sort", "  CTA0 sort", "  CTA0 scan+gaps"]
 for i, n in enumerate(names):
     print(f"  {n:24s} {buf[i] / iters:10.0f} cycles/iter")

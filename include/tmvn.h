@@ -147,8 +147,12 @@ typedef struct {
    * regime of few chains, e.g. the paper's 1 or 10).  Same RNG
    * counters and readings; the dot products sum in another order, so results
    * agree with the default path to rounding, not bitwise.  Not with the affine
-   * change of variable (the default path runs then).  TMVN_E_STATE if a chain's
-   * live arcs in one iteration exceed 1024.  0 (default): off. */
+   * change of variable (the default path runs then).  CTA 0 of a cluster holds
+   * every live arc of an iteration (up to m, or what its shared memory allows);
+   * if some iteration has more, the call is rerun on the default path from the
+   * same start (tmvn_profile.latency_fallbacks).  2: auto -- latency mode when
+   * the chains are at most half the SMs (clusters of two or more CTAs).
+   * 0 (default): off. */
   int32_t latency;
 } tmvn_options;
 
@@ -172,6 +176,8 @@ typedef struct {
   double tc_ms;
   double tc_ops;         /* int8 tensor ops issued by those launches: S(S+1)/2 * 2 C m d     */
   double tc_flops;       /* FP64-equivalent algorithmic flops of those launches: 2 C m d     */
+  int64_t latency_calls;      /* tmvn_sample calls run in latency mode (options.latency)      */
+  int64_t latency_fallbacks;  /* of those, calls rerun on the default path (live-arc overflow) */
 } tmvn_profile;
 
 /* Fills *opt with the defaults listed above. */
@@ -259,6 +265,9 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
  * (6, 7, 8); K <= 4096. */
 tmvn_status tmvn_test_ozaki_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
                                  int32_t slices, double* out);
+/* Latency mode's live-arc capacity per chain and iteration: cap > 0 lowers it
+ * (to exercise the overflow fallback), 0 restores the automatic choice. */
+tmvn_status tmvn_test_latency_cap(tmvn_handle h, int32_t cap);
 /* The production FP64 GEMM: out[R x S] = X[R x K] . W[S x K]^T (all row-major). */
 tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
                            double* out);

@@ -31,7 +31,7 @@ EXPORTS = ["tmvn_default_options", "tmvn_create", "tmvn_set_affine", "tmvn_set_o
            "tmvn_reset_stats", "tmvn_get_profile", "tmvn_last_error", "tmvn_version",
            "tmvn_destroy", "tmvn_test_philox", "tmvn_test_curand_philox", "tmvn_test_normals", "tmvn_test_arcs",
            "tmvn_test_intervals", "tmvn_test_gemm", "tmvn_test_ozaki_gemm", "tmvn_test_step",
-           "tmvn_test_trace"]
+           "tmvn_test_trace", "tmvn_test_latency_cap"]
 
 
 class TmvnError(RuntimeError):
@@ -59,7 +59,8 @@ class profile(ctypes.Structure):
                 ("ess_launches", ctypes.c_int64), ("ess_ms", ctypes.c_double),
                 ("ess_bytes", ctypes.c_double), ("tc_launches", ctypes.c_int64),
                 ("tc_ms", ctypes.c_double), ("tc_ops", ctypes.c_double),
-                ("tc_flops", ctypes.c_double)]
+                ("tc_flops", ctypes.c_double), ("latency_calls", ctypes.c_int64),
+                ("latency_fallbacks", ctypes.c_int64)]
 
 
 class stats(ctypes.Structure):
@@ -110,6 +111,7 @@ def lib():
             "tmvn_test_ozaki_gemm": [P, i64, P, i64, i64, ctypes.c_int32, P],
             "tmvn_test_step": [H, P, i64, u64, i64, P],
             "tmvn_test_trace": [H, P, i64, i64, u64, P, i64, P, P],
+            "tmvn_test_latency_cap": [H, ctypes.c_int32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -274,6 +276,10 @@ class Sampler:
     def profile(self):
         p = tmvn_get_profile(self.h)
         return {k: getattr(p, k) for k, _ in p._fields_}
+
+    def test_latency_cap(self, cap):
+        """Test hook: cap latency mode's live-arc capacity (0 = automatic)."""
+        _check(lib().tmvn_test_latency_cap(self.h, int(cap)), self.h)
 
     def close(self):
         if getattr(self, "h", None):

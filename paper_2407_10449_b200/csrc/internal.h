@@ -51,8 +51,10 @@ struct LatParams {
   double* S2;
   int64_t* rej;      // per chain
   int* err;          // set when a chain's live arcs overflow CTA 0's buffer
+  int cap;           // live arcs CTA 0 holds per iteration (latency_cap)
 };
-size_t latency_smem_bytes(int64_t d_pad, int m, int cs);
+size_t latency_smem_bytes(int64_t d_pad, int m, int cs, int cap);
+int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max);
 int latency_cluster_size(int C, int sms);
 cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st);
 

@@ -37,7 +37,8 @@ namespace {
 
 constexpr int kLT = 256;      // threads per CTA
 constexpr int kLNB = 128;     // level-1 buckets over [0, 2 pi]
-constexpr int kLLive = 1024;  // live arcs CTA 0 can hold per iteration
+// live arcs CTA 0 can hold per iteration: p.cap, sized on the host from the shared
+// memory left (up to m); more in some iteration -> the call reruns on the default path
 constexpr int kLNF = 1024;    // level-2 slots CTA 0 splits the live level-1 buckets into
 
 __device__ __forceinline__ uint64_t lbits(double x) { return (uint64_t)__double_as_longlong(x); }
@@ -55,18 +56,18 @@ struct LatShared {
   int* cnt;        // kLNB
   uint64_t* gin;   // kLNB: merged gamma entering each bucket
   int* live;       // kLNB: merged live flag
-  uint64_t* lkey;  // kLLive (CTA 0): live arcs' alpha bits
-  double* lval;    // kLLive: their beta
-  double2* gaps;   // kLLive + 2
+  uint64_t* lkey;  // cap + 2 (CTA 0): live arcs' alpha bits
+  double* lval;    // cap + 2: their beta
+  double2* gaps;   // cap + 2: the gaps, over lkey / lval once those are consumed
   uint64_t* fb;    // kLNF (CTA 0): level-2 max beta, then gamma entering the slot
   uint64_t* fa;    // kLNF: level-2 max alpha
   int* fc;         // kLNF: level-2 count, then live flag
-  int* fid;        // kLLive: level-2 slot of each live arc
-  int* cl;         // kLLive: live arcs in live level-2 slots
+  int* fid;        // cap: level-2 slot of each live arc
+  int* cl;         // cap: live arcs in live level-2 slots
   int* lrk;        // kLNB: rank of a live level-1 bucket among the live ones
   int* lb;         // kLNB: live level-1 bucket of each rank
   uint64_t* scr;   // 16 words of scan scratch
-  uint64_t* cand;  // 2 kLLive
+  uint64_t* cand;  // 2 cap
   double* M1;      // nk x kLT: this CTA's moment sums over the call (flushed at the end)
   double* M2;
   int* ints;       // [0] n_act, [1] live count, [2] viol, [3] ncand, [4] overflow
@@ -77,7 +78,8 @@ __host__ __device__ __forceinline__ size_t lat_align(size_t v) { return (v + 15)
 
 // shared-memory layout (host: base = nullptr, only the size is used)
 __host__ __device__ inline int lat_nk(int64_t d_pad, int cs) { return (int)((d_pad + (int64_t)cs * kLT - 1) / ((int64_t)cs * kLT)); }
-__host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, int mr, int nk, LatShared& S) {
+__host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, int mr, int nk, int cap,
+                                            LatShared& S) {
   size_t o = 0;
   auto take = [&](size_t bytes) {
     unsigned char* q = base + o;
@@ -102,15 +104,15 @@ __host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, 
   S.M2 = reinterpret_cast<double*>(take((size_t)nk * kLT * 8));
   S.ints = reinterpret_cast<int*>(take(8 * 4));
   S.dbl = reinterpret_cast<double*>(take(4 * 8));
-  S.lkey = reinterpret_cast<uint64_t*>(take(kLLive * 8));
-  S.lval = reinterpret_cast<double*>(take(kLLive * 8));
-  S.gaps = reinterpret_cast<double2*>(take((kLLive + 2) * 16));
-  S.cand = reinterpret_cast<uint64_t*>(take(2 * kLLive * 8));
+  S.lkey = reinterpret_cast<uint64_t*>(take((size_t)(cap + 2) * 8));
+  S.lval = reinterpret_cast<double*>(take((size_t)(cap + 2) * 8));
+  S.gaps = reinterpret_cast<double2*>(S.lkey);  // contiguous 16 (cap + 2) bytes
+  S.cand = reinterpret_cast<uint64_t*>(take((size_t)2 * cap * 8));
   S.fb = reinterpret_cast<uint64_t*>(take(kLNF * 8));
   S.fa = reinterpret_cast<uint64_t*>(take(kLNF * 8));
   S.fc = reinterpret_cast<int*>(take(kLNF * 4));
-  S.fid = reinterpret_cast<int*>(take(kLLive * 4));
-  S.cl = reinterpret_cast<int*>(take(kLLive * 4));
+  S.fid = reinterpret_cast<int*>(take((size_t)cap * 4));
+  S.cl = reinterpret_cast<int*>(take((size_t)cap * 4));
   return o;
 }
 
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   extern __shared__ __align__(16) unsigned char lsm[];
   LatShared S;
   const int nk = lat_nk(p.d_pad, CS);
-  lat_carve(lsm, p.d_pad, mr, nk, S);
+  lat_carve(lsm, p.d_pad, mr, nk, p.cap, S);
   // CTA 0's buffers and flags, seen from every CTA of the cluster
   int* r_ints0 = cluster.map_shared_rank(S.ints, 0);
   uint64_t* r_lkey0 = cluster.map_shared_rank(S.lkey, 0);
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
       const int k = lat_bucket(ab.x, scale);
       if (S.live[k] && lbits(ab.y) > S.gin[k]) {
         const int pos = atomicAdd(r_ints0 + 1, 1);
-        if (pos < kLLive) {
+        if (pos < p.cap) {
           r_lkey0[pos] = lbits(ab.x);
           r_lval0[pos] = ab.y;
         }
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     if (rank == 0) {
       const int total = S.ints[1];
       const uint64_t Gtot = lbits(S.dbl[3]);
-      if (total > kLLive) {
+      if (total > p.cap) {
         if (tid == 0) {
           S.ints[4] = 1;  // overflow: this iteration stays (L = 0); reported to the host
           S.dbl[0] = 0.0;
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
         for (int w = 0; w < kLNB / 32; ++w) nlb += (int)S.scr[w];
         const int SUB = kLNF / (nlb > 0 ? nlb : 1);
         __syncthreads();
+        LPH(12);
         for (int e = tid; e < total; e += kLT) {
           const uint64_t key = S.lkey[e];
           const double u = __dmul_rn(lbitsd(key), scale);
@@ -459,6 +462,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
           atomicAdd(&S.fc[f], 1);
         }
         __syncthreads();
+        LPH(13);
         {  // exclusive prefix max of the slots' max beta (four slots per thread)
           constexpr int FP = kLNF / kLT;
           uint64_t mb[FP];
@@ -494,6 +498,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
           }
         }
         __syncthreads();
+        LPH(15);
         for (int e = tid; e < total; e += kLT)
           if (S.fc[S.fid[e]]) S.cl[atomicAdd(&S.ints[5], 1)] = e;
         __syncthreads();
@@ -617,9 +622,22 @@ void lat_cycles(unsigned long long* out, bool reset) {
 }
 #endif
 
-size_t latency_smem_bytes(int64_t d_pad, int m, int cs) {
+size_t latency_smem_bytes(int64_t d_pad, int m, int cs, int cap) {
   LatShared S;
-  return lat_carve(nullptr, d_pad, (m + cs - 1) / cs, lat_nk(d_pad, cs), S);
+  return lat_carve(nullptr, d_pad, (m + cs - 1) / cs, lat_nk(d_pad, cs), cap, S);
+}
+
+// live-arc capacity: m if it fits, else as many as fit (0: the mode does not fit)
+int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max) {
+  constexpr int kMinCap = 64;
+  if (latency_smem_bytes(d_pad, m, cs, kMinCap) > smem_max) return 0;
+  int lo = kMinCap, hi = m > kMinCap ? m : kMinCap;
+  while (lo < hi) {
+    const int mid = lo + (hi - lo + 1) / 2;
+    if (latency_smem_bytes(d_pad, m, cs, mid) <= smem_max) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 // cluster size: the largest power of two <= 16 with C clusters fitting the SMs (>= 1)
@@ -630,7 +648,7 @@ int latency_cluster_size(int C, int sms) {
 }
 
 cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st) {
-  const size_t smem = latency_smem_bytes(p.d_pad, p.m, cs);
+  const size_t smem = latency_smem_bytes(p.d_pad, p.m, cs, p.cap);
   cudaError_t e = cudaFuncSetAttribute(latency_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (cs > 8) {

@@ -67,6 +67,9 @@ struct tmvn_ctx {
   double *S1x = nullptr, *S2x = nullptr;     // row-major x-space moments (affine)
   double *stage = nullptr, *stage2 = nullptr;  // row-major C_pad x max(d_pad, d_r128)
   int64_t* rej = nullptr;
+  double* Xsnap = nullptr;  // X before a latency-mode call (its overflow fallback)
+  size_t Xsnap_n = 0;
+  int lat_cap_max = 0;  // test hook: latency-mode live-arc capacity cap (0 = automatic)
   int64_t* dsum = nullptr;
   double* msum = nullptr;  // d (device) moment reduction target
   unsigned long long* dflag = nullptr;
@@ -1016,20 +1019,32 @@ tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
 // The latency mode (options.latency = 1): one cluster of CTAs per chain runs every
 // iteration in one launch (latency.cu).  Taken when the problem fits its limits (no
 // affine change of variable, shared memory), else the throughput loop runs.
-bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out) {
-  if (h->opt.latency != 1 || h->affine) return false;
+// options.latency = 2 (auto) takes it when there are at most SMs / 2 chains (clusters of
+// two or more CTAs).
+bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
+  if (h->opt.latency == 0 || h->affine) return false;
   int dev = 0, sms = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (h->opt.latency == 2 && 2 * C > sms) return false;
   int cs = latency_cluster_size((int)C, sms);
-  while (cs < 16 && latency_smem_bytes(h->d_pad, (int)h->m, cs) > (size_t)smem_max) cs <<= 1;
-  if (latency_smem_bytes(h->d_pad, (int)h->m, cs) > (size_t)smem_max) return false;
+  int cap = latency_cap(h->d_pad, (int)h->m, cs, (size_t)smem_max);
+  while (cs < 16 && cap == 0) {
+    cs <<= 1;
+    cap = latency_cap(h->d_pad, (int)h->m, cs, (size_t)smem_max);
+  }
+  if (cap == 0) return false;
+  if (h->lat_cap_max > 0 && cap > h->lat_cap_max) cap = h->lat_cap_max;
   *cs_out = cs;
+  *cap_out = cap;
   return true;
 }
 
-tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int cs, int64_t* n_recorded) {
+// returns TMVN_OK with *overflow = true (nothing usable written) when some iteration had
+// more live arcs than the capacity: the caller restores X and runs the default path
+tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int cs, int cap,
+                        int64_t* n_recorded, bool* overflow) {
   cudaStream_t st = stream_of(h);
   if (!h->A_pad) {
     CK(h, dalloc(&h->A_pad, (size_t)(h->m * h->d_pad)));
@@ -1058,6 +1073,7 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
   p.S1 = h->S1;
   p.S2 = h->S2;
   p.rej = h->rej;
+  p.cap = cap;
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   p.err = h->dyn + 64 * 16 - 1;
   CK(h, cudaMemsetAsync(p.err, 0, sizeof(int), st));
@@ -1065,10 +1081,8 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
   int err = 0;
   CK(h, cudaMemcpyAsync(&err, p.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(h, cudaStreamSynchronize(st));
-  if (err)
-    return fail(h, TMVN_E_STATE,
-                "latency mode: more live arcs than its per-chain buffer (1024) in some iteration; "
-                "the affected steps stayed -- use options.latency = 0 for this polytope");
+  *overflow = err != 0;
+  if (err) return TMVN_OK;
   int64_t nrec = 0;
   for (int64_t it = 0; it < n_iter; ++it) nrec += recorded_iter(h->opt, h->opt.iter_offset + it) ? 1 : 0;
   *n_recorded = nrec;
@@ -1087,12 +1101,31 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;
   if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
   int64_t nrec = 0;
-  int lcs = 0;
-  if (n_iter > 0 && latency_fits(h, C, &lcs)) {
-    if ((s = run_latency(h, C, n_iter, seed, lcs, &nrec)) != TMVN_OK) return s;
-  } else if ((s = run_loop(h, C, n_iter, seed, h->P0, &nrec)) != TMVN_OK) {
-    return s;
+  int lcs = 0, lcap = 0;
+  bool done = false;
+  if (n_iter > 0 && latency_fits(h, C, &lcs, &lcap)) {
+    // X is kept so that an overflowing call can rerun on the default path
+    const size_t cd = (size_t)h->C_pad * h->d_pad;
+    if (h->Xsnap_n < cd) {
+      dfree(h->Xsnap);
+      h->Xsnap = nullptr;
+      h->Xsnap_n = 0;
+      CK(h, dalloc(&h->Xsnap, cd));
+      h->Xsnap_n = cd;
+    }
+    cudaStream_t st = stream_of(h);
+    CK(h, cudaMemcpyAsync(h->Xsnap, h->X, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    bool overflow = false;
+    if ((s = run_latency(h, C, n_iter, seed, lcs, lcap, &nrec, &overflow)) != TMVN_OK) return s;
+    done = !overflow;
+    h->prof.latency_calls += 1;
+    h->prof.latency_fallbacks += overflow ? 1 : 0;
+    if (overflow) {
+      CK(h, cudaMemcpyAsync(h->X, h->Xsnap, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
+    }
   }
+  if (!done && (s = run_loop(h, C, n_iter, seed, h->P0, &nrec)) != TMVN_OK) return s;
   if ((s = store_X(h, C, out)) != TMVN_OK) return s;
   if ((s = finish_stats(h, C, n_iter, nrec)) != TMVN_OK) return s;
   if (h->opt.auto_advance) h->opt.iter_offset += n_iter;
@@ -1152,7 +1185,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->dyn);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
-  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->b_orig); dfree(h->b_eff);
+  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
   dfree(h->As); dfree(h->rowscale);
@@ -1445,14 +1478,20 @@ tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t 
   return TMVN_OK;
 }
 
+tmvn_status tmvn_test_latency_cap(tmvn_handle h, int32_t cap) {
+  if (!h || cap < 0) return fail(h, TMVN_E_ARG, "latency cap must be >= 0");
+  h->lat_cap_max = cap;
+  return TMVN_OK;
+}
+
 #ifdef TMVN_PHASE_TIMING
 // timing build only (tools/phase_timing.py): per-phase CTA cycles of ess_kernel
 tmvn_status tmvn_test_phase_cycles(uint64_t* out10, int reset) {
   tmvn::phase_cycles(reinterpret_cast<unsigned long long*>(out10), reset != 0);
   return TMVN_OK;
 }
-tmvn_status tmvn_test_lat_cycles(uint64_t* out12, int reset) {
-  tmvn::lat_cycles(reinterpret_cast<unsigned long long*>(out12), reset != 0);
+tmvn_status tmvn_test_lat_cycles(uint64_t* out16, int reset) {
+  tmvn::lat_cycles(reinterpret_cast<unsigned long long*>(out16), reset != 0);
   return TMVN_OK;
 }
 tmvn_status tmvn_test_oz_cycles(uint64_t* out8, int reset) {

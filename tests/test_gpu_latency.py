@@ -72,7 +72,7 @@ def test_latency_moments_and_counters():
     assert s.stats()["steps"] == C * T and s.stats()["rejections"] == 0
 
 
-@pytest.mark.parametrize("d,chains", [(300, 1), (300, 10), (1000, 10)])
+@pytest.mark.parametrize("d,chains", [(300, 1), (300, 10), (1000, 10), (2000, 10), (4000, 1)])
 def test_latency_section_4_2_instances(d, chains):
     A, b, x0 = synth.paper_random(d, seed=d)
     s = tm.Sampler(A, b, latency=1)
@@ -98,3 +98,45 @@ def test_latency_orthant_moments():
     mean, var = sm / n, sq / n - (sm / n) ** 2
     assert abs(mean.mean() - math.sqrt(2 / math.pi)) < 0.01
     assert abs(var.mean() - (1 - 2 / math.pi)) < 0.01
+
+
+def test_latency_overflow_falls_back_to_default_path():
+    """More live arcs in an iteration than CTA 0 holds (capacity forced down by the
+    test hook): the call reruns on the default path from the same start, so the
+    result, moments and counters equal the default path's bitwise."""
+    A, b, x0 = synth.paper_random(300, seed=300)
+    C, T = 10, 40
+    X0 = np.tile(x0, (C, 1))
+    ref_s = tm.Sampler(A, b, burn_in=5)
+    ref = ref_s.sample(X0, T, seed=42)
+    s = tm.Sampler(A, b, latency=1, burn_in=5)
+    s.test_latency_cap(64)  # S4.2 at d = 300 has ~100 live arcs per iteration
+    out = s.sample(X0, T, seed=42)
+    pr = s.profile()
+    assert pr["latency_calls"] == 1 and pr["latency_fallbacks"] == 1
+    assert np.array_equal(out, ref)
+    for a, r in zip(s.moments(), ref_s.moments()):
+        assert np.array_equal(np.asarray(a), np.asarray(r))
+    assert s.stats() == ref_s.stats()
+    # capacity back to automatic (m): no fallback
+    s.test_latency_cap(0)
+    s.reset_stats()
+    s.sample(X0, T, seed=42)
+    assert s.profile()["latency_fallbacks"] == 0 and s.profile()["latency_calls"] == 1
+
+
+def test_latency_auto_selection():
+    """options.latency = 2: latency mode for at most SMs / 2 chains, else the default
+    path (bitwise the default path's result)."""
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    A, b, x0 = synth.make_instance(3, m=300, d=100)
+    few = tm.Sampler(A, b, latency=2)
+    few.sample(np.tile(x0, (10, 1)), 5, seed=1)
+    assert few.profile()["latency_calls"] == 1
+    C = sms // 2 + 1
+    X0 = np.tile(x0, (C, 1))
+    many = tm.Sampler(A, b, latency=2)
+    out = many.sample(X0, 5, seed=1)
+    assert many.profile()["latency_calls"] == 0
+    assert np.array_equal(out, tm.Sampler(A, b).sample(X0, 5, seed=1))

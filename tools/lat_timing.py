@@ -20,6 +20,6 @@ L.tmvn_test_lat_cycles(buf.ctypes.data_as(ctypes.c_void_p), 1)
 s.sample(X, iters, cfg.chain_seed)
 L.tmvn_test_lat_cycles(buf.ctypes.data_as(ctypes.c_void_p), 0)
 names = ["a nu", "b Q rows", "c arcs+stats", "sync1", "merge+gather", "sync2", "CTA0 I_act+theta", "sync3",
-         "P'+safeguard", "sync4", "update+moments+refresh", "(live arcs)", "  CTA0 pre-sort", "  CTA0 sort", "  CTA0 scan+gaps"]
+         "P'+safeguard", "sync4", "update+moments+refresh", "(live arcs)", "  L2 rank+zero", "  L2 atomics", "  L2 rest", "  L2 scan+live"]
 for i, n in enumerate(names):
     print(f"  {n:24s} {buf[i] / iters:10.0f} cycles/iter")

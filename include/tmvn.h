@@ -150,9 +150,9 @@ typedef struct {
    * change of variable (the default path runs then).  CTA 0 of a cluster holds
    * every live arc of an iteration (up to m, or what its shared memory allows);
    * if some iteration has more, the call is rerun on the default path from the
-   * same start (tmvn_profile.latency_fallbacks).  2: auto -- latency mode when
-   * the chains are at most half the SMs (clusters of two or more CTAs).
-   * 0 (default): off. */
+   * same start (tmvn_profile.latency_fallbacks).  2 (default): auto -- latency
+   * mode when the chains are at most half the SMs (clusters of two or more
+   * CTAs), else the default path.  0: off (always the default path). */
   int32_t latency;
 } tmvn_options;
 

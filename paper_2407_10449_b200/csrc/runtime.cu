@@ -880,7 +880,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->rng_ahead = 0;  // measured slower on B200 (the GEMM loses more than the ESS kernel gains)
   o->schedule = 0;
   o->pipeline = 0;
-  o->latency = 0;
+  o->latency = 2;
   return TMVN_OK;
 }
 

@@ -44,7 +44,7 @@ def test_latency_matches_default_path():
     A, b, x0 = synth.make_instance(3, m=400, d=120)
     C, T = 12, 20
     X0 = np.tile(x0, (C, 1))
-    ref = tm.Sampler(A, b).sample(X0, T, seed=3)
+    ref = tm.Sampler(A, b, latency=0).sample(X0, T, seed=3)
     lat = tm.Sampler(A, b, latency=1).sample(X0, T, seed=3)
     assert np.max(np.abs(lat - ref)) <= 1e-9 * max(1.0, np.max(np.abs(ref)))
 
@@ -107,7 +107,7 @@ def test_latency_overflow_falls_back_to_default_path():
     A, b, x0 = synth.paper_random(300, seed=300)
     C, T = 10, 40
     X0 = np.tile(x0, (C, 1))
-    ref_s = tm.Sampler(A, b, burn_in=5)
+    ref_s = tm.Sampler(A, b, latency=0, burn_in=5)
     ref = ref_s.sample(X0, T, seed=42)
     s = tm.Sampler(A, b, latency=1, burn_in=5)
     s.test_latency_cap(64)  # S4.2 at d = 300 has ~100 live arcs per iteration
@@ -139,4 +139,4 @@ def test_latency_auto_selection():
     many = tm.Sampler(A, b, latency=2)
     out = many.sample(X0, 5, seed=1)
     assert many.profile()["latency_calls"] == 0
-    assert np.array_equal(out, tm.Sampler(A, b).sample(X0, 5, seed=1))
+    assert np.array_equal(out, tm.Sampler(A, b, latency=0).sample(X0, 5, seed=1))

@@ -67,7 +67,7 @@ def test_ozaki_within_stated_bound(slices, R, S, K):
 def test_ozaki_step_parity(name, k, kw, C):
     A, b, x0 = synth.make_instance(k, **kw)
     cfg = synth.CONFIGS[k]
-    s = tm.Sampler(A, b, projection=1)
+    s = tm.Sampler(A, b, latency=0, projection=1)
     X = np.tile(x0, (C, 1))
     r = oracle.run(A, b, X[: min(C, 16)], 30, seed=cfg.chain_seed + 1000)
     X[: r["X"].shape[0]] = r["X"]
@@ -86,7 +86,7 @@ def test_ozaki_step_parity(name, k, kw, C):
 def test_ozaki_production_loop_parity_and_sharding():
     A, b, x0 = synth.make_instance(3, m=400, d=120)
     C, T = 200, 70
-    s = tm.Sampler(A, b, projection=1)
+    s = tm.Sampler(A, b, latency=0, projection=1)
     chains = np.array([0, 1, 63, 64, 199])
     trace, out = s.test_trace(np.tile(x0, (C, 1)), T, seed=103, chains=chains)
     bad = 0
@@ -100,9 +100,9 @@ def test_ozaki_production_loop_parity_and_sharding():
     assert s.stats()["rejections"] == 0
     # sharding by chain_offset is bitwise invariant (per-element integer MMA, fixed Horner)
     X0 = np.tile(x0, (C, 1))
-    full = tm.Sampler(A, b, projection=1).sample(X0, 40, seed=9)
-    h1 = tm.Sampler(A, b, projection=1, chain_offset=0).sample(X0[:77], 40, seed=9)
-    h2 = tm.Sampler(A, b, projection=1, chain_offset=77).sample(X0[77:], 40, seed=9)
+    full = tm.Sampler(A, b, latency=0, projection=1).sample(X0, 40, seed=9)
+    h1 = tm.Sampler(A, b, latency=0, projection=1, chain_offset=0).sample(X0[:77], 40, seed=9)
+    h2 = tm.Sampler(A, b, latency=0, projection=1, chain_offset=77).sample(X0[77:], 40, seed=9)
     assert np.array_equal(np.concatenate([h1, h2]), full)
 
 
@@ -110,7 +110,7 @@ def test_ozaki_full_size_config3_sampled():
     """BASELINE config 3 at full size through the int8 projection (bench launch config)."""
     A, b, x0 = synth.make_instance(3)
     C = 4096
-    s = tm.Sampler(A, b, projection=1)
+    s = tm.Sampler(A, b, latency=0, projection=1)
     X = s.sample(np.tile(x0, (C, 1)), 20, seed=103)
     assert s.stats()["rejections"] == 0
     g = s.test_step(X, 103, 20, seg_cap=64)
@@ -123,6 +123,6 @@ def test_ozaki_full_size_config3_sampled():
 
 def test_ozaki_rejects_large_d():
     A = np.ones((2, 4097)) / 100.0
-    s = tm.Sampler(A, np.ones(2))
+    s = tm.Sampler(A, np.ones(2), latency=0)
     with pytest.raises(tm.TmvnError):
         s.set_options(projection=1)

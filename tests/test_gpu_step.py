@@ -101,7 +101,7 @@ def test_step_parity_from_start_and_along_oracle_path(name, projection):
     m, d = A.shape
     C = {1: 16, 2: 130, 3: 131, 4: 37, 5: 129}[k]
     cfg = synth.CONFIGS[k]
-    s = tm.Sampler(A, b, projection=projection)
+    s = tm.Sampler(A, b, latency=0, projection=projection)
     rng = np.random.default_rng(k)
     # interior points: x0, and points reached by oracle chains (stationary-ish)
     X = np.tile(x0, (C, 1))
@@ -123,7 +123,7 @@ def test_trace_production_loop_parity():
     m, d = A.shape
     C, T = 200, 70
     for K in (32, 1):
-        s = tm.Sampler(A, b, recompute_every=K, projection=2)
+        s = tm.Sampler(A, b, latency=0, recompute_every=K, projection=2)
         chains = np.array([0, 1, 57, 128, 199])
         trace, out = s.test_trace(np.tile(x0, (C, 1)), T, seed=103, chains=chains)
         assert np.array_equal(trace[-1], out[chains])
@@ -147,7 +147,7 @@ def test_full_size_config3_sampled():
     """BASELINE config 3 at full size (d=1000, m=2000, C=4096) in the bench launch config."""
     A, b, x0 = synth.make_instance(3)
     C = 4096
-    s = tm.Sampler(A, b, projection=2)
+    s = tm.Sampler(A, b, latency=0, projection=2)
     X = s.sample(np.tile(x0, (C, 1)), 20, seed=103)
     assert s.stats()["rejections"] == 0
     g = s.test_step(X, 103, 20, seg_cap=64)
@@ -163,7 +163,7 @@ def test_full_size_config4_sampled():
     A, b, x0 = synth.make_instance(4)
     C = 1024
     for projection in (2, 1):
-        s = tm.Sampler(A, b, projection=projection)
+        s = tm.Sampler(A, b, latency=0, projection=projection)
         X = s.sample(np.tile(x0, (C, 1)), 5, seed=104)
         g = s.test_step(X, 104, 5, seg_cap=64)
         log = []

@@ -241,94 +241,113 @@ def main():
     ms_iso = timed_pass(args.steps)
     prof = s.profile()
     s.set_options(streams=opts.streams, profile=0)
-    peaks = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")))
-    gemm_avg_ms = prof["gemm_ms"] / max(1, prof["gemm_launches"])
-    gemm_flops = prof["gemm_flops"] / max(1, prof["gemm_launches"])
-    achieved = gemm_flops / (gemm_avg_ms * 1e-3) / 1e12 if gemm_avg_ms > 0 else 0.0
-    peak = peaks["dmma_tflops_w8"]
-    ess_avg_ms = prof["ess_ms"] / max(1, prof["ess_launches"])
-    ess_gbs = prof["ess_bytes"] / max(1, prof["ess_launches"]) / (ess_avg_ms * 1e-3) / 1e9
-    try:
-        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-        hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
-    except Exception:
-        hbm, hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
-    traffic, traffic_src = None, None
-    try:  # dram__bytes_read + dram__bytes_write per launch from the committed ncu --set full capture
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_gemm_traffic.json")))
-        if args.config == 3 and world == 1:
-            traffic, traffic_src = tj["traffic_bytes"], "profiles/r01/ncu_gemm_traffic.json"
-    except Exception:
-        pass
-    roofline = {"bound": "tensor", "kernel": "gemm_tn_f64_kernel (Q = N A^T and P = X A^T, FP64 DMMA)",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_source": traffic_src,
-                "peak_source": "measured FP64 DMMA pipe peak on this pool's B200 (profiles/peaks_fp64_r01.json: "
-                               f"mma.sync f64 micro-benchmark; cuBLAS DGEMM measured {peaks['dgemm_tflops_burst']} TF/s)",
-                "algorithmic_flops_per_launch": gemm_flops, "avg_launch_ms": gemm_avg_ms,
-                "share_of_step": prof["gemm_ms"] / ms_iso,
-                "measured_in": "second timed pass of the same workload with options.streams=1 (no kernel "
-                               "overlap), CUDA events around every launch on the library stream; the main "
-                               f"pass overlaps GEMM and per-chain kernel on {opts.streams or 'auto'} streams "
-                               f"({ms_max / args.steps:.2f} ms/step vs {ms_iso / args.steps:.2f} ms/step here)",
-                "ess_kernel": {"bound": "hbm", "achieved": ess_gbs, "peak": hbm, "unit": "GB/s",
-                               "frac": ess_gbs / hbm, "peak_source": hbm_src, "avg_launch_ms": ess_avg_ms,
-                               "share_of_step": prof["ess_ms"] / ms_iso,
-                               "algorithmic_bytes_per_launch": prof["ess_bytes"] / max(1, prof["ess_launches"])}}
-    if oz:
-        # dominant kernel: the int8 tcgen05 projection; peak = measured dense bf16 x the
-        # nominal int8 / bf16 ratio (4.5 / 2.25 PFLOP/s), sustained figure (timed inside a long step)
-        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        tc_avg_ms = prof["tc_ms"] / max(1, prof["tc_launches"])
-        tc_ops = prof["tc_ops"] / max(1, prof["tc_launches"])
-        tc_achieved = tc_ops / (tc_avg_ms * 1e-3) / 1e12
-        tc_peak = 2.0 * mp["bf16_tflops"]
-        oz_traffic, oz_traffic_src = None, None
-        try:  # dram bytes read + written per launch, committed ncu --set full capture (config 3, N=1)
-            tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_oz_traffic.json")))
-            if args.config == 3 and (opts.ozaki_slices or 7) == 7:
-                oz_traffic, oz_traffic_src = tj["traffic_bytes"], "profiles/r01/ncu_oz_traffic.json"
-        except Exception:
-            pass
-        tc_peak_sus = 2.0 * mp["bf16_tflops_sustained"]
-        dmma = {"kernel": "oz_slice_kernel + ozaki_gemm_kernel (P = X A'^T refresh every recompute_every: "
-                          "X cut into digits with one exponent per chain, int8 tcgen05)",
-                "avg_launch_ms": roofline["avg_launch_ms"],
-                "fp64_equivalent_tflops": roofline["achieved"],
-                "share_of_step": roofline["share_of_step"]}
-        roofline = {"bound": "tensor",
-                    "kernel": "ozaki_gemm_kernel (Q = N A'^T, int8 tcgen05.mma, TMEM accumulators, "
-                              f"{opts.ozaki_slices or 7} digits: FP64-accurate)",
-                    "achieved": tc_achieved, "peak": tc_peak, "unit": "TOP/s (int8)",
-                    "frac": tc_achieved / tc_peak, "traffic": oz_traffic, "traffic_source": oz_traffic_src,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x 2 = nominal int8/bf16 dense "
-                                   "ratio 4.5/2.25 (B200_PROFILING.md); burst, not sustained, because the "
-                                   "clocks stay at sm_max during this step (see clocks)",
-                    "frac_vs_sustained_peak": tc_achieved / tc_peak_sus,
-                    "algorithmic_ops_per_launch": tc_ops,
-                    "fp64_equivalent_tflops": prof["tc_flops"] / max(1, prof["tc_launches"]) / (tc_avg_ms * 1e-3) / 1e12,
-                    "avg_launch_ms": tc_avg_ms, "share_of_step": prof["tc_ms"] / ms_iso,
-                    "measured_in": roofline["measured_in"],
-                    "refresh_gemm": dmma, "ess_kernel": roofline["ess_kernel"]}
-    # the contract's roofline is the DOMINANT kernel's: when the fused per-chain kernel
-    # takes the larger share of the step it moves to the top level (HBM roofline of its
-    # algorithmic bytes), the projection GEMM nested beside it
-    if roofline["ess_kernel"]["share_of_step"] > roofline["share_of_step"]:
-        ess = dict(roofline.pop("ess_kernel"))
-        ess["kernel"] = "ess_kernel (arcs, Alg. 3 intervals, theta, P', safeguard, x update, moments, next nu)"
-        ess["traffic"], ess["traffic_source"] = None, None
+    if prof["latency_calls"] > 0:
+        # latency mode (few chains: one thread-block cluster per chain, one launch per call):
+        # each cluster streams its chain's A . nu (m x d FP64) from L2 every iteration
         try:
-            sj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_full_int8_summary.json")))
-            e = sj["ess_kernel<8>"]
+            hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+            hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
+        except Exception:
+            hbm, hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+        launch_ms = ms_iso / args.steps
+        abytes = float(C) * ips * m * d * 8
+        roofline = {"bound": "hbm", "kernel": "latency_kernel (one cluster per chain: nu, A nu, arcs, "
+                                               "two-level Alg. 3 intervals, theta, P', safeguard, x update)",
+                    "achieved": abytes / (launch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": abytes / (launch_ms * 1e-3) / 1e9 / hbm, "traffic": None, "traffic_source": None,
+                    "peak_source": hbm_src + "; A (8 m d bytes per chain-iteration, the algorithmic bytes "
+                                   "counted here) is served from L2, so this is a bandwidth-equivalent figure",
+                    "algorithmic_bytes_per_launch": abytes, "avg_launch_ms": launch_ms, "share_of_step": 1.0,
+                    "latency_calls": prof["latency_calls"], "latency_fallbacks": prof["latency_fallbacks"]}
+    else:
+        peaks = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")))
+        gemm_avg_ms = prof["gemm_ms"] / max(1, prof["gemm_launches"])
+        gemm_flops = prof["gemm_flops"] / max(1, prof["gemm_launches"])
+        achieved = gemm_flops / (gemm_avg_ms * 1e-3) / 1e12 if gemm_avg_ms > 0 else 0.0
+        peak = peaks["dmma_tflops_w8"]
+        ess_avg_ms = prof["ess_ms"] / max(1, prof["ess_launches"])
+        ess_gbs = prof["ess_bytes"] / max(1, prof["ess_launches"]) / (ess_avg_ms * 1e-3) / 1e9
+        try:
+            hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+            hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
+        except Exception:
+            hbm, hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+        traffic, traffic_src = None, None
+        try:  # dram__bytes_read + dram__bytes_write per launch from the committed ncu --set full capture
+            tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_gemm_traffic.json")))
             if args.config == 3 and world == 1:
-                ess["traffic"] = (float(e["dram__bytes_read.sum"]["value"]) +
-                                  float(e["dram__bytes_write.sum"]["value"])) * 1e6
-                ess["traffic_source"] = "profiles/r01/ncu_full_int8_summary.json"
+                traffic, traffic_src = tj["traffic_bytes"], "profiles/r01/ncu_gemm_traffic.json"
         except Exception:
             pass
-        ess["measured_in"] = roofline["measured_in"]
-        ess["projection_gemm"] = roofline
-        roofline = ess
+        roofline = {"bound": "tensor", "kernel": "gemm_tn_f64_kernel (Q = N A^T and P = X A^T, FP64 DMMA)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": traffic, "traffic_source": traffic_src,
+                    "peak_source": "measured FP64 DMMA pipe peak on this pool's B200 (profiles/peaks_fp64_r01.json: "
+                                   f"mma.sync f64 micro-benchmark; cuBLAS DGEMM measured {peaks['dgemm_tflops_burst']} TF/s)",
+                    "algorithmic_flops_per_launch": gemm_flops, "avg_launch_ms": gemm_avg_ms,
+                    "share_of_step": prof["gemm_ms"] / ms_iso,
+                    "measured_in": "second timed pass of the same workload with options.streams=1 (no kernel "
+                                   "overlap), CUDA events around every launch on the library stream; the main "
+                                   f"pass overlaps GEMM and per-chain kernel on {opts.streams or 'auto'} streams "
+                                   f"({ms_max / args.steps:.2f} ms/step vs {ms_iso / args.steps:.2f} ms/step here)",
+                    "ess_kernel": {"bound": "hbm", "achieved": ess_gbs, "peak": hbm, "unit": "GB/s",
+                                   "frac": ess_gbs / hbm, "peak_source": hbm_src, "avg_launch_ms": ess_avg_ms,
+                                   "share_of_step": prof["ess_ms"] / ms_iso,
+                                   "algorithmic_bytes_per_launch": prof["ess_bytes"] / max(1, prof["ess_launches"])}}
+        if oz:
+            # dominant kernel: the int8 tcgen05 projection; peak = measured dense bf16 x the
+            # nominal int8 / bf16 ratio (4.5 / 2.25 PFLOP/s), sustained figure (timed inside a long step)
+            mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            tc_avg_ms = prof["tc_ms"] / max(1, prof["tc_launches"])
+            tc_ops = prof["tc_ops"] / max(1, prof["tc_launches"])
+            tc_achieved = tc_ops / (tc_avg_ms * 1e-3) / 1e12
+            tc_peak = 2.0 * mp["bf16_tflops"]
+            oz_traffic, oz_traffic_src = None, None
+            try:  # dram bytes read + written per launch, committed ncu --set full capture (config 3, N=1)
+                tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_oz_traffic.json")))
+                if args.config == 3 and (opts.ozaki_slices or 7) == 7:
+                    oz_traffic, oz_traffic_src = tj["traffic_bytes"], "profiles/r01/ncu_oz_traffic.json"
+            except Exception:
+                pass
+            tc_peak_sus = 2.0 * mp["bf16_tflops_sustained"]
+            dmma = {"kernel": "oz_slice_kernel + ozaki_gemm_kernel (P = X A'^T refresh every recompute_every: "
+                              "X cut into digits with one exponent per chain, int8 tcgen05)",
+                    "avg_launch_ms": roofline["avg_launch_ms"],
+                    "fp64_equivalent_tflops": roofline["achieved"],
+                    "share_of_step": roofline["share_of_step"]}
+            roofline = {"bound": "tensor",
+                        "kernel": "ozaki_gemm_kernel (Q = N A'^T, int8 tcgen05.mma, TMEM accumulators, "
+                                  f"{opts.ozaki_slices or 7} digits: FP64-accurate)",
+                        "achieved": tc_achieved, "peak": tc_peak, "unit": "TOP/s (int8)",
+                        "frac": tc_achieved / tc_peak, "traffic": oz_traffic, "traffic_source": oz_traffic_src,
+                        "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x 2 = nominal int8/bf16 dense "
+                                       "ratio 4.5/2.25 (B200_PROFILING.md); burst, not sustained, because the "
+                                       "clocks stay at sm_max during this step (see clocks)",
+                        "frac_vs_sustained_peak": tc_achieved / tc_peak_sus,
+                        "algorithmic_ops_per_launch": tc_ops,
+                        "fp64_equivalent_tflops": prof["tc_flops"] / max(1, prof["tc_launches"]) / (tc_avg_ms * 1e-3) / 1e12,
+                        "avg_launch_ms": tc_avg_ms, "share_of_step": prof["tc_ms"] / ms_iso,
+                        "measured_in": roofline["measured_in"],
+                        "refresh_gemm": dmma, "ess_kernel": roofline["ess_kernel"]}
+        # the contract's roofline is the DOMINANT kernel's: when the fused per-chain kernel
+        # takes the larger share of the step it moves to the top level (HBM roofline of its
+        # algorithmic bytes), the projection GEMM nested beside it
+        if roofline["ess_kernel"]["share_of_step"] > roofline["share_of_step"]:
+            ess = dict(roofline.pop("ess_kernel"))
+            ess["kernel"] = "ess_kernel (arcs, Alg. 3 intervals, theta, P', safeguard, x update, moments, next nu)"
+            ess["traffic"], ess["traffic_source"] = None, None
+            try:
+                sj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_full_int8_summary.json")))
+                e = sj["ess_kernel<8>"]
+                if args.config == 3 and world == 1:
+                    ess["traffic"] = (float(e["dram__bytes_read.sum"]["value"]) +
+                                      float(e["dram__bytes_write.sum"]["value"])) * 1e6
+                    ess["traffic_source"] = "profiles/r01/ncu_full_int8_summary.json"
+            except Exception:
+                pass
+            ess["measured_in"] = roofline["measured_in"]
+            ess["projection_gemm"] = roofline
+            roofline = ess
     gpu_launches = prof_main["launches"]
 
     # ---- end to end through the public API with host buffers (pinned), rank-local
@@ -354,7 +373,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+i8" if oz else "f64",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+i8" if oz and prof["latency_calls"] == 0 else "f64",
                 "data": "synthetic (seeded Gaussian polytope of BASELINE config; no dataset)",
                 "config": config_dict(cfg, args, world),
                 "chain_iters_per_s": total_iters / (ms_max * 1e-3),

@@ -152,8 +152,18 @@ typedef struct {
    * if some iteration has more, the call is rerun on the default path from the
    * same start (tmvn_profile.latency_fallbacks).  2 (default): auto -- latency
    * mode when the chains are at most half the SMs (clusters of two or more
-   * CTAs), else the default path.  0: off (always the default path). */
+   * CTAs) and a cost model fitted to B200 measurements expects it to be
+   * faster (it re-reads A from L2 for every chain), else the default path.  0: off (always the default path). */
   int32_t latency;
+  /* 1: FP32 arithmetic, the paper's precision (S3.3): A . nu,
+   * A . x, the arcs, P' and the safeguard, x in single precision; the interval
+   * comparisons and the inverse-CDF draw in FP64 on the (exactly widened) FP32
+   * endpoints.  Runs in the latency mode only (whatever options.latency says,
+   * as long as it fits: no affine change of variable; TMVN_E_ARG otherwise); a
+   * live-arc overflow reruns the call on the FP64 default path.  Use with
+   * trim_eps > 0 (S3.3 trimming); the safeguard rejects the rare infeasible
+   * proposal.  Parity with the FP64 oracle is statistical.  0 (default): FP64. */
+  int32_t precision;
 } tmvn_options;
 
 typedef struct {

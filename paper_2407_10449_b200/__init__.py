@@ -50,7 +50,7 @@ class options(ctypes.Structure):
                 ("graphs", ctypes.c_int32), ("projection", ctypes.c_int32),
                 ("ozaki_slices", ctypes.c_int32), ("rng_ahead", ctypes.c_int32),
                 ("schedule", ctypes.c_int32), ("pipeline", ctypes.c_int32),
-                ("latency", ctypes.c_int32)]
+                ("latency", ctypes.c_int32), ("precision", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):

@@ -242,6 +242,16 @@ __global__ void test_arcs_kernel(const double* __restrict__ p, const double* __r
 
 __global__ void set_u32_kernel(uint32_t* dst, uint32_t value) { *dst = value; }
 
+// FP32 copy of a row-major R x K matrix into rows of K_pad (zero padding): FP32 mode
+__global__ void to_f32_kernel(const double* __restrict__ src, int64_t R, int64_t K, int64_t ld,
+                              float* __restrict__ dst, int64_t K_pad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * K_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / K_pad, k = i - r * K_pad;
+    dst[i] = k < K ? (float)src[r * ld + k] : 0.0f;
+  }
+}
+
 inline int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 64) g = 148 * 64;
@@ -249,6 +259,13 @@ inline int grid_for(int64_t n, int threads = 256) {
 }
 
 }  // namespace
+
+cudaError_t launch_to_f32(const double* src, int64_t R, int64_t K, int64_t ld, float* dst, int64_t K_pad,
+                          cudaStream_t st) {
+  if (R * K_pad == 0) return cudaSuccess;
+  to_f32_kernel<<<grid_for(R * K_pad), 256, 0, st>>>(src, R, K, ld, dst, K_pad);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pack(const double* src, int64_t R, int64_t K, int64_t ld, double* dst,
                         int64_t K_pad, cudaStream_t st) {

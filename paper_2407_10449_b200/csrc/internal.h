@@ -52,6 +52,9 @@ struct LatParams {
   int64_t* rej;      // per chain
   int* err;          // set when a chain's live arcs overflow CTA 0's buffer
   int cap;           // live arcs CTA 0 holds per iteration (latency_cap)
+  int fp32;          // options.precision = 1: FP32 arithmetic (A32, b32), else FP64 (A, b)
+  const float* A32;  // m x d_pad, zero-padded rows
+  const float* b32;  // m
 };
 size_t latency_smem_bytes(int64_t d_pad, int m, int cs, int cap);
 int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max);
@@ -158,6 +161,8 @@ void oz_cycles(unsigned long long* out8, bool reset);
 
 // ---- auxiliary kernels (aux_kernels.cu) -------------------------------------
 // row-major [R x K] (leading dim ld) -> tiled [R_pad x K_pad]; padding is left untouched.
+cudaError_t launch_to_f32(const double* src, int64_t R, int64_t K, int64_t ld, float* dst, int64_t K_pad,
+                          cudaStream_t st);
 cudaError_t launch_pack(const double* src, int64_t R, int64_t K, int64_t ld, double* dst,
                         int64_t K_pad, cudaStream_t st);
 cudaError_t launch_unpack(const double* src, int64_t R, int64_t K, int64_t K_pad, double* dst,

@@ -121,59 +121,100 @@ __device__ __forceinline__ int lat_bucket(double a, double scale) {
   return k < kLNB - 1 ? k : kLNB - 1;
 }
 
+// 16-byte vectors of the arithmetic type: FP64 (default) or FP32 (options.precision = 1)
+template <typename T> struct LVec;
+template <> struct LVec<double> { using V = double2; static constexpr int N = 2; };
+template <> struct LVec<float> { using V = float4; static constexpr int N = 4; };
+__device__ __forceinline__ double vdot(const double2 a, const double2 w, double s) {
+  return fma(a.y, w.y, fma(a.x, w.x, s));
+}
+__device__ __forceinline__ float vdot(const float4 a, const float4 w, float s) {
+  return fmaf(a.w, w.w, fmaf(a.z, w.z, fmaf(a.y, w.y, fmaf(a.x, w.x, s))));
+}
+
 // dot products of up to four rows of A (row stride d_pad, zero-padded, 16-byte aligned)
 // with v (shared, d_pad), one warp, fixed order: 16-byte loads, four partial sums per
 // row, so that sixteen loads per lane are in flight (A is streamed from L2 every
 // iteration: memory-level parallelism bounds this step)
-__device__ __forceinline__ void lat_dot4(const double* __restrict__ A, int nrow, int64_t d_pad,
-                                         const double* v, int lane, double o[4]) {
-  const double2* __restrict__ R[4];
+template <typename T>
+__device__ __forceinline__ void lat_dot4(const T* __restrict__ A, int nrow, int64_t d_pad, const T* v, int lane,
+                                         T o[4]) {
+  using V = typename LVec<T>::V;
+  const V* __restrict__ R[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) R[q] = reinterpret_cast<const double2*>(A + (q < nrow ? q : 0) * d_pad);
-  const double2* V = reinterpret_cast<const double2*>(v);
-  const int np = (int)(d_pad / 2);
-  double s[4][4];
+  for (int q = 0; q < 4; ++q) R[q] = reinterpret_cast<const V*>(A + (q < nrow ? q : 0) * d_pad);
+  const V* Vv = reinterpret_cast<const V*>(v);
+  const int np = (int)(d_pad / LVec<T>::N);
+  T s[4][4];
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) s[q][u] = 0.0;
-  // blocks of 128 pairs; the last block's loads past the row are predicated off
+    for (int u = 0; u < 4; ++u) s[q][u] = T(0);
+  // blocks of 128 vectors; the last block's loads past the row are predicated off
   // (zero), so every block is one round trip with sixteen loads per lane in flight
   for (int j = lane; j < np; j += 128) {
-    double2 a[4][4];
+    V a[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        a[q][u] = j + 32 * u < np ? __ldg(R[q] + j + 32 * u) : make_double2(0.0, 0.0);
+      for (int u = 0; u < 4; ++u) a[q][u] = j + 32 * u < np ? __ldg(R[q] + j + 32 * u) : V{};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double2 w = j + 32 * u < np ? V[j + 32 * u] : make_double2(0.0, 0.0);
+      const V w = j + 32 * u < np ? Vv[j + 32 * u] : V{};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) s[q][u] = fma(a[q][u].y, w.y, fma(a[q][u].x, w.x, s[q][u]));
+      for (int q = 0; q < 4; ++q) s[q][u] = vdot(a[q][u], w, s[q][u]);
     }
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    double t = (s[q][0] + s[q][1]) + (s[q][2] + s[q][3]);
+    T t = (s[q][0] + s[q][1]) + (s[q][2] + s[q][3]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
     o[q] = t;
   }
 }
 // rows [0, nr) of this CTA's slice (global rows i0 + r) . v -> out[r]; warps take row quads
-__device__ __forceinline__ void lat_rows(const double* __restrict__ A, int i0, int nr, int64_t d_pad,
-                                         const double* v, double* out, int warp, int lane) {
+template <typename T>
+__device__ __forceinline__ void lat_rows(const T* __restrict__ A, int i0, int nr, int64_t d_pad, const T* v,
+                                         T* out, int warp, int lane) {
   for (int r = 4 * warp; r < nr; r += 4 * (kLT / 32)) {
     const int nrow = min(4, nr - r);
-    double o[4];
-    lat_dot4(A + (int64_t)(i0 + r) * d_pad, nrow, d_pad, v, lane, o);
+    T o[4];
+    lat_dot4<T>(A + (int64_t)(i0 + r) * d_pad, nrow, d_pad, v, lane, o);
     if (lane == 0) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (q < nrow) out[r + q] = o[q];
     }
   }
+}
+
+// the arc of one constraint in the arithmetic type, returned in FP64 (exact widening)
+// for the interval machinery; FP32: the same construction (eq:roots, C1-C5) with
+// single-precision atan2 / sqrt, 2 pi rounded to float, endpoints clamped to FP64 2 pi
+__device__ __forceinline__ bool lat_arc(double p, double q, double b, double& al, double& be) {
+  return arc_of(p, q, b, al, be);
+}
+__device__ __forceinline__ bool lat_arc(float p, float q, float b, double& al, double& be) {
+  const float s2 = fmaf(p, p, fmaf(q, q, -b * b));
+  if (!(b < 0.0f || s2 > 0.0f)) return false;
+  const float s = sqrtf(fmaxf(s2, 0.0f));
+  const float tau = atan2f(q, p), delta = atan2f(s, b);
+  constexpr float kTwoPiF = 6.28318530717958647692f;
+  float lo = tau - delta, hi = tau + delta;
+  if (hi <= 0.0f) {
+    lo += kTwoPiF;
+    hi += kTwoPiF;
+  } else if (lo >= 0.0f) {
+  } else if (-lo <= hi) {
+    lo = 0.0f;  // straddle (rounding only): snap the shorter side (C1)
+  } else {
+    lo += kTwoPiF;
+    hi = kTwoPiF;
+  }
+  al = fmin((double)lo, kTwoPi);
+  be = fmin((double)hi, kTwoPi);
+  return true;
 }
 
 // canonical segments (merge touching), trim (C7), L and theta = inverse CDF at u (C10);
@@ -246,6 +287,7 @@ __device__ unsigned long long g_lat_cycles[16];
   } while (0)
 #endif
 
+template <typename T>
 __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
@@ -267,19 +309,25 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   double* r_lval0 = cluster.map_shared_rank(S.lval, 0);
   double* r_dbl0 = cluster.map_shared_rank(S.dbl, 0);
   const double scale = __ddiv_rn((double)kLNB, kTwoPi);
+  // the arithmetic type's views (x, nu, P, Q live in FP64-sized slots either way)
+  const T* A = static_cast<const T*>(sizeof(T) == 8 ? (const void*)p.A : (const void*)p.A32);
+  const T* bv = static_cast<const T*>(sizeof(T) == 8 ? (const void*)p.b : (const void*)p.b32);
+  T* Sx = reinterpret_cast<T*>(S.x);
+  T* Snu = reinterpret_cast<T*>(S.nu);
+  T* SQ = reinterpret_cast<T*>(S.Q);
 
   // x_{t0} (all d) and P = A x for this CTA's rows
-  for (int j = tid; j < p.d_pad; j += kLT) S.x[j] = j < d ? p.X[tiled_offset(chain, j, p.d_pad)] : 0.0;
+  for (int j = tid; j < p.d_pad; j += kLT) Sx[j] = j < d ? (T)p.X[tiled_offset(chain, j, p.d_pad)] : T(0);
   if (tid < 8) S.ints[tid] = 0;
   for (int k = 0; k < nk; ++k) {
     S.M1[k * kLT + tid] = 0.0;
     S.M2[k * kLT + tid] = 0.0;
   }
   __syncthreads();
-  double* Pc = S.P0;  // P = A x for this CTA's rows
-  double* Pn = S.P1;  // the proposal P'
-  auto gemv = [&](const double* v, double* out) { lat_rows(p.A, i0, nr, p.d_pad, v, out, warp, lane); };
-  gemv(S.x, Pc);
+  T* Pc = reinterpret_cast<T*>(S.P0);  // P = A x for this CTA's rows
+  T* Pn = reinterpret_cast<T*>(S.P1);  // the proposal P'
+  auto gemv = [&](const T* v, T* out) { lat_rows<T>(A, i0, nr, p.d_pad, v, out, warp, lane); };
+  gemv(Sx, Pc);
   int64_t rej = 0;
   cluster.sync();
 #ifdef TMVN_PHASE_TIMING
@@ -292,8 +340,8 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     // (a) nu_t, u_t
     for (int pk = tid; pk < (int)(p.d_pad / 2); pk += kLT) {
       const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
-      S.nu[2 * pk] = v.x;
-      S.nu[2 * pk + 1] = v.y;
+      Snu[2 * pk] = (T)v.x;
+      Snu[2 * pk + 1] = (T)v.y;
     }
     if (rank == 0 && tid == 0) S.dbl[2] = theta_uniform(p.seed, t, gchain);
     for (int j = tid; j < kLNB; j += kLT) {
@@ -305,13 +353,13 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     __syncthreads();
     LPH(0);
     // (b) Q for this CTA's rows
-    gemv(S.nu, S.Q);
+    gemv(Snu, SQ);
     __syncthreads();
     LPH(1);
     // (c) arcs of the active rows + bucket statistics (high words, then low words)
     for (int r = tid; r < nr; r += kLT) {
       double al, be;
-      if (arc_of(Pc[r], S.Q[r], __ldg(p.b + i0 + r), al, be)) {
+      if (lat_arc(Pc[r], SQ[r], __ldg(bv + i0 + r), al, be)) {
         const int slot = atomicAdd(&S.ints[0], 1);
         S.st[slot] = make_double2(al, be);
         const int k = lat_bucket(al, scale);
@@ -548,14 +596,14 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     cluster.sync();  // #3: theta and L in CTA 0
     LPH(7);
     const double theta = r_dbl0[0], L = r_dbl0[1];
-    double sn = 0.0, cs = 1.0;
-    if (L > 0.0) sincos(theta, &sn, &cs);
+    T sn = T(0), cs = T(1);
+    if (L > 0.0) sincos((T)theta, &sn, &cs);
     int viol = 0;
     if (L > 0.0) {
       for (int r = tid; r < nr; r += kLT) {
-        const double pn = Pc[r] * cs + S.Q[r] * sn;
+        const T pn = Pc[r] * cs + SQ[r] * sn;
         Pn[r] = pn;
-        viol |= (pn - __ldg(p.b + i0 + r)) > 0.0 ? 1 : 0;
+        viol |= (pn - __ldg(bv + i0 + r)) > T(0) ? 1 : 0;
       }
     }
     viol = __syncthreads_or(viol);
@@ -566,10 +614,10 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     const int any = __syncthreads_or(tid < CS ? *cluster.map_shared_rank(S.ints + 2, tid) : 0);
     const bool accept = L > 0.0 && !any;
     if (accept) {
-      double* tmp = Pc;
+      T* tmp = Pc;
       Pc = Pn;
       Pn = tmp;
-      for (int j = tid; j < p.d_pad; j += kLT) S.x[j] = S.x[j] * cs + S.nu[j] * sn;
+      for (int j = tid; j < p.d_pad; j += kLT) Sx[j] = Sx[j] * cs + Snu[j] * sn;
     } else {
       ++rej;
     }
@@ -577,13 +625,13 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     const int64_t tt = (int64_t)t;
     if (p.record && tt >= p.burn_in && ((tt - p.burn_in) % (p.thin < 1 ? 1 : p.thin)) == 0) {
       for (int k = 0, j = rank * kLT + tid; j < d; ++k, j += CS * kLT) {  // this CTA's coordinates
-        const double xv = S.x[j];
+        const double xv = (double)Sx[j];
         S.M1[k * kLT + tid] += xv;
         S.M2[k * kLT + tid] += xv * xv;
       }
     }
     if ((int64_t)(t + 1) % p.K == 0) {  // refresh P = A x (C13)
-      gemv(S.x, Pc);
+      gemv(Sx, Pc);
     }
     __syncthreads();
     LPH(10);
@@ -600,7 +648,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     }
   }
   if (rank == 0) {
-    for (int j = tid; j < d; j += kLT) p.X[tiled_offset(chain, j, p.d_pad)] = S.x[j];
+    for (int j = tid; j < d; j += kLT) p.X[tiled_offset(chain, j, p.d_pad)] = (double)Sx[j];
     if (tid == 0) {
       p.rej[chain] += rej;
       if (S.ints[4]) atomicExch(p.err, 1);
@@ -647,12 +695,13 @@ int latency_cluster_size(int C, int sms) {
   return cs;
 }
 
-cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st) {
+template <typename T>
+cudaError_t launch_latency_t(const LatParams& p, int cs, cudaStream_t st) {
   const size_t smem = latency_smem_bytes(p.d_pad, p.m, cs, p.cap);
-  cudaError_t e = cudaFuncSetAttribute(latency_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (cs > 8) {
-    e = cudaFuncSetAttribute(latency_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -667,7 +716,11 @@ cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, latency_kernel, p);
+  return cudaLaunchKernelEx(&cfg, latency_kernel<T>, p);
+}
+
+cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st) {
+  return p.fp32 ? launch_latency_t<float>(p, cs, st) : launch_latency_t<double>(p, cs, st);
 }
 
 }  // namespace tmvn

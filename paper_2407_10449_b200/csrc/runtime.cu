@@ -35,6 +35,8 @@ struct tmvn_ctx {
   // constraints
   double* A_row = nullptr;  // m x d (original)
   double* A_pad = nullptr;  // m x d_pad, zero-padded rows (latency mode; made on first use)
+  float* A32 = nullptr;     // FP32 copies for options.precision = 1 (made on first use)
+  float* b32 = nullptr;
   double* b_orig = nullptr; // m
   double* A_tiled = nullptr;  // tiled m_pad x d_pad of the ORIGINAL A (for A L)
   double* At = nullptr;     // tiled m_pad x d_pad of A' (= A L if affine)
@@ -881,6 +883,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->schedule = 0;
   o->pipeline = 0;
   o->latency = 2;
+  o->precision = 0;
   return TMVN_OK;
 }
 
@@ -1002,6 +1005,8 @@ tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* o) {
       o->chain_warps != 8)
     return fail(h, TMVN_E_ARG, "chain_warps must be 0, 1, 2, 4 or 8");
   if (o->projection < 0 || o->projection > 2) return fail(h, TMVN_E_ARG, "projection must be 0, 1 or 2");
+  if (o->latency < 0 || o->latency > 2) return fail(h, TMVN_E_ARG, "latency must be 0, 1 or 2");
+  if (o->precision < 0 || o->precision > 1) return fail(h, TMVN_E_ARG, "precision must be 0 (FP64) or 1 (FP32)");
   if (o->ozaki_slices != 0 && (o->ozaki_slices < 6 || o->ozaki_slices > 8))
     return fail(h, TMVN_E_ARG, "ozaki_slices must be 0, 6, 7 or 8");
   if (o->projection == 1 && h->d > 4096)
@@ -1020,14 +1025,15 @@ tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
 // iteration in one launch (latency.cu).  Taken when the problem fits its limits (no
 // affine change of variable, shared memory), else the throughput loop runs.
 // options.latency = 2 (auto) takes it when there are at most SMs / 2 chains (clusters of
-// two or more CTAs).
+// two or more CTAs) and the cost model below expects it to be faster.
 bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
-  if (h->opt.latency == 0 || h->affine) return false;
+  const bool fp32 = h->opt.precision == 1;  // FP32 runs in this mode whenever it fits
+  if ((h->opt.latency == 0 && !fp32) || h->affine) return false;
   int dev = 0, sms = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (h->opt.latency == 2 && 2 * C > sms) return false;
+  if (h->opt.latency == 2 && !fp32 && 2 * C > sms) return false;
   int cs = latency_cluster_size((int)C, sms);
   int cap = latency_cap(h->d_pad, (int)h->m, cs, (size_t)smem_max);
   while (cs < 16 && cap == 0) {
@@ -1035,6 +1041,17 @@ bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
     cap = latency_cap(h->d_pad, (int)h->m, cs, (size_t)smem_max);
   }
   if (cap == 0) return false;
+  if (h->opt.latency == 2 && !fp32) {
+    // auto: a cost model fitted to B200 measurements (S12) -- the latency mode
+    // streams a CTA's rows of A (8 B per element) each iteration at ~120 GB/s per SM when
+    // A is L2-resident (~50 GB/s when it is not) plus ~12 us of per-iteration latency;
+    // the default path costs ~50 us + 7.8 ps per element of A at few chains
+    const double abytes = 8.0 * (double)h->m * (double)h->d_pad;
+    const double r_sm = abytes <= 80e6 ? 120e9 : 50e9;
+    const double t_lat = 12e-6 + (double)((h->m + cs - 1) / cs) * (double)h->d_pad * 8.0 / r_sm;
+    const double t_def = 50e-6 + 7.8e-12 * (double)h->m * (double)h->d;
+    if (t_lat >= t_def) return false;
+  }
   if (h->lat_cap_max > 0 && cap > h->lat_cap_max) cap = h->lat_cap_max;
   *cs_out = cs;
   *cap_out = cap;
@@ -1054,6 +1071,17 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
   }
   LatParams p;
   std::memset(&p, 0, sizeof(p));
+  if (h->opt.precision == 1) {
+    if (!h->A32) {
+      CK(h, dalloc(&h->A32, (size_t)(h->m * h->d_pad)));
+      KL(h, launch_to_f32(h->A_row, h->m, h->d, h->d, h->A32, h->d_pad, st));
+    }
+    if (!h->b32) CK(h, dalloc(&h->b32, (size_t)h->m));
+    KL(h, launch_to_f32(h->b_eff, 1, h->m, h->m, h->b32, h->m, st));  // b' may change (set_affine)
+    p.fp32 = 1;
+    p.A32 = h->A32;
+    p.b32 = h->b32;
+  }
   p.A = h->A_pad;
   p.b = h->b_eff;
   p.m = (int)h->m;
@@ -1103,7 +1131,12 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   int64_t nrec = 0;
   int lcs = 0, lcap = 0;
   bool done = false;
-  if (n_iter > 0 && latency_fits(h, C, &lcs, &lcap)) {
+  const bool lat = n_iter > 0 && latency_fits(h, C, &lcs, &lcap);
+  if (h->opt.precision == 1 && n_iter > 0 && !lat)
+    return fail(h, TMVN_E_ARG,
+                "options.precision = 1 (FP32) runs in the latency mode only, which does not fit here "
+                "(affine change of variable, or shared memory)");
+  if (lat) {
     // X is kept so that an overflowing call can rerun on the default path
     const size_t cd = (size_t)h->C_pad * h->d_pad;
     if (h->Xsnap_n < cd) {
@@ -1185,7 +1218,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->dyn);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
-  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->b_orig); dfree(h->b_eff);
+  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
   dfree(h->As); dfree(h->rowscale);

@@ -140,3 +140,90 @@ def test_latency_auto_selection():
     out = many.sample(X0, 5, seed=1)
     assert many.profile()["latency_calls"] == 0
     assert np.array_equal(out, tm.Sampler(A, b, latency=0).sample(X0, 5, seed=1))
+    # the cost model declines it when every chain would stream a large A from HBM
+    # (d = m = 4000, 32 chains: ~0.56 ms vs ~0.17 ms per iteration measured)
+    A4, b4, x4 = synth.paper_random(4000, seed=4000)
+    big = tm.Sampler(A4, b4)
+    big.sample(np.tile(x4, (32, 1)), 1, seed=1)
+    assert big.profile()["latency_calls"] == 0
+    one = tm.Sampler(A4, b4)
+    one.sample(np.tile(x4, (1, 1)), 1, seed=1)
+    assert one.profile()["latency_calls"] == 1
+
+
+# ---------------------------------------------------------------- FP32 (NEXT-2)
+# options.precision = 1: the paper's single precision with S3.3's trimming and
+# safeguard.  Parity with the FP64 oracle is statistical: the paper's own
+# S4.1 table and rejection rate, the orthant closed form, and the
+# first step against the oracle to FP32 accuracy.
+EPS32 = 1e-5
+
+
+def _trunc_normal_moments(lo, hi):
+    phi = lambda z: math.exp(-0.5 * z * z) / math.sqrt(2 * math.pi)
+    if lo > 0:
+        Z = 0.5 * (math.erfc(lo / math.sqrt(2)) - math.erfc(hi / math.sqrt(2)))
+    else:
+        Z = 0.5 * (math.erf(hi / math.sqrt(2)) - math.erf(lo / math.sqrt(2)))
+    mu = (phi(lo) - phi(hi)) / Z
+    return mu, 1.0 + (lo * phi(lo) - hi * phi(hi)) / Z - mu * mu
+
+
+def test_fp32_first_step_close_to_oracle():
+    A, b, x0 = synth.paper_random(300, seed=300)
+    C = 10
+    s = tm.Sampler(A, b, precision=1, trim_eps=EPS32, record=0)
+    X = np.tile(x0, (C, 1))
+    Xn = s.sample(X, 1, seed=42)
+    assert s.profile()["latency_calls"] == 1
+    for c in range(C):
+        xn, _ = oracle.step(A, b, X[c], 42, 0, c, eps=EPS32)
+        assert np.max(np.abs(Xn[c] - xn)) <= 1e-3 * max(1.0, np.max(np.abs(xn)))
+
+
+@pytest.mark.parametrize("interval,max_rej", [((-1.0, 3.0), 20), ((15.0, 16.0), 200)])
+def test_fp32_section_4_1_protocol(interval, max_rej):
+    """2000 chains, burn-in 500, thinning 10, 1e5 samples in FP32: moments
+    within 0.01 of the closed form; rejections at most 0.01 % of the 2e6 steps (the
+    paper saw 0 on [-1, 3] and 8 on [15, 16])."""
+    A, b, x0 = synth.one_dim(interval)
+    s = tm.Sampler(A, b, precision=1, trim_eps=EPS32, burn_in=500, thin=10)
+    out = s.sample(np.tile(x0, (2000, 1)), 1000, seed=2024)
+    sm, sq, n = s.moments()
+    assert n == 100000
+    mu, var = _trunc_normal_moments(*interval)
+    m1 = sm[0] / n
+    assert abs(m1 - mu) < 0.01 and abs(sq[0] / n - m1 * m1 - var) < 0.01
+    st = s.stats()
+    assert st["steps"] == 2_000_000 and st["rejections"] <= max_rej, st
+    assert np.all(out >= interval[0] - 1e-5) and np.all(out <= interval[1] + 1e-5)
+
+
+def test_fp32_orthant_moments():
+    A, b, x0 = synth.make_instance(2)
+    s = tm.Sampler(A, b, precision=1, trim_eps=EPS32, burn_in=15000)
+    s.sample(np.tile(x0, (256, 1)), 20000, seed=102)
+    sm, sq, n = s.moments()
+    mean, var = sm / n, sq / n - (sm / n) ** 2
+    assert abs(mean.mean() - math.sqrt(2 / math.pi)) < 0.01
+    assert abs(var.mean() - (1 - 2 / math.pi)) < 0.01
+
+
+@pytest.mark.parametrize("d,chains", [(1000, 10), (4000, 1)])
+def test_fp32_section_4_2_no_rejections(d, chains):
+    """S4.2 in FP32: the paper saw no safeguard rejection in high dimension."""
+    A, b, x0 = synth.paper_random(d, seed=d)
+    s = tm.Sampler(A, b, precision=1, trim_eps=EPS32)
+    out = s.sample(np.tile(x0, (chains, 1)), 200, seed=42)
+    assert s.stats()["rejections"] == 0
+    slack = out @ A.T - b
+    assert np.max(slack) <= 1e-4 * np.max(np.abs(A @ x0))  # feasible to FP32 rounding
+
+
+def test_fp32_needs_latency_mode():
+    A, b, x0 = synth.make_instance(3, m=40, d=6)
+    L, mu = synth.random_spd_factor(6, seed=1)
+    s = tm.Sampler(A, b, mu=np.zeros(6), L=L, precision=1)
+    with pytest.raises(tm.TmvnError) as ei:
+        s.sample(np.zeros((4, 6)), 2, seed=1)
+    assert ei.value.status == -1 and "FP32" in str(ei.value)

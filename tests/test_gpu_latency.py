@@ -227,3 +227,25 @@ def test_fp32_needs_latency_mode():
     with pytest.raises(tm.TmvnError) as ei:
         s.sample(np.zeros((4, 6)), 2, seed=1)
     assert ei.value.status == -1 and "FP32" in str(ei.value)
+
+
+def test_latency_shard_invariance_and_resume_bitwise():
+    """A row's dot product has a fixed order whichever CTA (and cluster size) holds it,
+    so the latency mode is bitwise invariant to the chain split (multi-GPU sharding:
+    chain_offset) and a call split at a multiple of recompute_every resumes bitwise."""
+    A, b, x0 = synth.paper_random(300, seed=301)
+    C, T = 10, 64
+    X0 = np.tile(x0, (C, 1))
+    full = tm.Sampler(A, b, latency=1).sample(X0, T, seed=5)
+    h1 = tm.Sampler(A, b, latency=1, chain_offset=0).sample(X0[:3], T, seed=5)
+    h2 = tm.Sampler(A, b, latency=1, chain_offset=3).sample(X0[3:], T, seed=5)
+    assert np.array_equal(np.concatenate([h1, h2]), full)
+    s = tm.Sampler(A, b, latency=1)
+    a = s.sample(X0, 32, seed=5)
+    a = s.sample(a, 32, seed=5)
+    assert np.array_equal(a, full)
+    # FP32 too
+    f = tm.Sampler(A, b, precision=1, trim_eps=1e-5).sample(X0, T, seed=5)
+    g1 = tm.Sampler(A, b, precision=1, trim_eps=1e-5, chain_offset=0).sample(X0[:4], T, seed=5)
+    g2 = tm.Sampler(A, b, precision=1, trim_eps=1e-5, chain_offset=4).sample(X0[4:], T, seed=5)
+    assert np.array_equal(np.concatenate([g1, g2]), f)

@@ -58,7 +58,7 @@ struct LatParams {
 };
 size_t latency_smem_bytes(int64_t d_pad, int m, int cs, int cap);
 int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max);
-int latency_cluster_size(int C, int sms);
+int latency_cluster_size(int C, int64_t m, int64_t d_pad, size_t smem_max, bool fp32, int* cap_out);
 cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st);
 
 // ---- fused per-chain ESS kernel (ess_chain.cu) -----------------------------

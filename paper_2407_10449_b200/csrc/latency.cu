@@ -40,6 +40,7 @@ constexpr int kLNB = 128;     // level-1 buckets over [0, 2 pi]
 // live arcs CTA 0 can hold per iteration: p.cap, sized on the host from the shared
 // memory left (up to m); more in some iteration -> the call reruns on the default path
 constexpr int kLNF = 1024;    // level-2 slots CTA 0 splits the live level-1 buckets into
+constexpr int kLSmall = 64;   // up to this many live arcs CTA 0 skips level 2
 
 __device__ __forceinline__ uint64_t lbits(double x) { return (uint64_t)__double_as_longlong(x); }
 __device__ __forceinline__ double lbitsd(uint64_t b) { return __longlong_as_double((long long)b); }
@@ -459,115 +460,139 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
         // start. Arcs of such slots get gamma from the slot's earlier arcs (alpha order,
         // equal alphas by index: the same gap either way); the gaps are ranked by alpha.
         // (S4.2's arcs all start just past theta = 0: one live level-1 bucket holds them.)
-        if (tid < kLNB) {
-          const int lv = S.live[tid] ? 1 : 0;
-          int ci = lv;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int n = __shfl_up_sync(0xffffffffu, ci, o);
-            if (lane >= o) ci += n;
-          }
-          if (lane == 31) S.scr[warp] = (uint64_t)ci;
-        }
-        for (int f = tid; f < kLNF; f += kLT) {
-          S.fb[f] = 0;
-          S.fa[f] = 0;
-          S.fc[f] = 0;
-        }
-        if (tid == 0) {
-          S.ints[3] = 0;
-          S.ints[5] = 0;
-        }
-        __syncthreads();
-        if (tid < kLNB) {
-          int rk = 0;
-          for (int w = 0; w < warp; ++w) rk += (int)S.scr[w];
-          const int lv = S.live[tid] ? 1 : 0;
-          int ci = lv;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int n = __shfl_up_sync(0xffffffffu, ci, o);
-            if (lane >= o) ci += n;
-          }
-          rk += ci - lv;
-          S.lrk[tid] = rk;
-          if (lv) S.lb[rk] = tid;
-        }
-        int nlb = 0;
-        for (int w = 0; w < kLNB / 32; ++w) nlb += (int)S.scr[w];
-        const int SUB = kLNF / (nlb > 0 ? nlb : 1);
-        __syncthreads();
-        LPH(12);
-        for (int e = tid; e < total; e += kLT) {
-          const uint64_t key = S.lkey[e];
-          const double u = __dmul_rn(lbitsd(key), scale);
-          const int k = lat_bucket(lbitsd(key), scale);
-          const int sub = min(SUB - 1, (int)__dmul_rn(__dsub_rn(u, (double)k), (double)SUB));
-          const int f = S.lrk[k] * SUB + sub;
-          S.fid[e] = f;
-          atomicMax(reinterpret_cast<unsigned long long*>(&S.fb[f]), (unsigned long long)lbits(S.lval[e]));
-          atomicMax(reinterpret_cast<unsigned long long*>(&S.fa[f]), (unsigned long long)key);
-          atomicAdd(&S.fc[f], 1);
-        }
-        __syncthreads();
-        LPH(13);
-        {  // exclusive prefix max of the slots' max beta (four slots per thread)
-          constexpr int FP = kLNF / kLT;
-          uint64_t mb[FP];
-          uint64_t run = 0;
-#pragma unroll
-          for (int q = 0; q < FP; ++q) {
-            mb[q] = S.fb[tid * FP + q];
-            run = run > mb[q] ? run : mb[q];
-          }
-          uint64_t inc = run;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t n = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc = inc > n ? inc : n;
-          }
-          if (lane == 31) S.scr[8 + warp] = inc;
+        if (total <= kLSmall) {
+          // few live arcs (small m, or the usual case far from the boundary): gamma before
+          // each from the arcs of its own level-1 bucket directly, no level 2
+          if (tid == 0) S.ints[3] = 0;
           __syncthreads();
-          uint64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-          if (lane == 0) ex = 0;
-          for (int w = 0; w < warp; ++w) ex = ex > S.scr[8 + w] ? ex : S.scr[8 + w];
-#pragma unroll
-          for (int q = 0; q < FP; ++q) {
-            const int f = tid * FP + q;
-            const int rk = f / SUB;
-            if (rk < nlb) {
-              const uint64_t gk = S.gin[S.lb[rk]];
-              const uint64_t g = ex > gk ? ex : gk;
-              const bool live = S.fc[f] > 0 && S.fa[f] > g;
-              S.fb[f] = g;
-              S.fc[f] = live ? 1 : 0;
+          for (int e = tid; e < total; e += kLT) {
+            const uint64_t key = S.lkey[e];
+            const int k = lat_bucket(lbitsd(key), scale);
+            uint64_t gm = S.gin[k];
+            for (int f = 0; f < total; ++f) {
+              const uint64_t kf = S.lkey[f];
+              if ((kf < key || (kf == key && f < e)) && lat_bucket(lbitsd(kf), scale) == k) {
+                const uint64_t vf = lbits(S.lval[f]);
+                gm = gm > vf ? gm : vf;
+              }
             }
-            ex = ex > mb[q] ? ex : mb[q];
-          }
-        }
-        __syncthreads();
-        LPH(15);
-        for (int e = tid; e < total; e += kLT)
-          if (S.fc[S.fid[e]]) S.cl[atomicAdd(&S.ints[5], 1)] = e;
-        __syncthreads();
-        const int nl2 = S.ints[5];
-        for (int c = tid; c < nl2; c += kLT) {
-          const int e = S.cl[c], f = S.fid[e];
-          const uint64_t key = S.lkey[e];
-          uint64_t gm = S.fb[f];
-          for (int c2 = 0; c2 < nl2; ++c2) {
-            const int e2 = S.cl[c2];
-            if (S.fid[e2] != f) continue;
-            const uint64_t k2 = S.lkey[e2];
-            if (k2 < key || (k2 == key && e2 < e)) {
-              const uint64_t v2 = lbits(S.lval[e2]);
-              gm = gm > v2 ? gm : v2;
+            if (key > gm) {
+              const int c3 = atomicAdd(&S.ints[3], 1);
+              S.cand[2 * c3] = key;
+              S.cand[2 * c3 + 1] = gm;
             }
           }
-          if (key > gm) {
-            const int c3 = atomicAdd(&S.ints[3], 1);
-            S.cand[2 * c3] = key;
-            S.cand[2 * c3 + 1] = gm;
+        } else {
+          if (tid < kLNB) {
+            const int lv = S.live[tid] ? 1 : 0;
+            int ci = lv;
+  #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int n = __shfl_up_sync(0xffffffffu, ci, o);
+              if (lane >= o) ci += n;
+            }
+            if (lane == 31) S.scr[warp] = (uint64_t)ci;
+          }
+          for (int f = tid; f < kLNF; f += kLT) {
+            S.fb[f] = 0;
+            S.fa[f] = 0;
+            S.fc[f] = 0;
+          }
+          if (tid == 0) {
+            S.ints[3] = 0;
+            S.ints[5] = 0;
+          }
+          __syncthreads();
+          if (tid < kLNB) {
+            int rk = 0;
+            for (int w = 0; w < warp; ++w) rk += (int)S.scr[w];
+            const int lv = S.live[tid] ? 1 : 0;
+            int ci = lv;
+  #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int n = __shfl_up_sync(0xffffffffu, ci, o);
+              if (lane >= o) ci += n;
+            }
+            rk += ci - lv;
+            S.lrk[tid] = rk;
+            if (lv) S.lb[rk] = tid;
+          }
+          int nlb = 0;
+          for (int w = 0; w < kLNB / 32; ++w) nlb += (int)S.scr[w];
+          const int SUB = kLNF / (nlb > 0 ? nlb : 1);
+          __syncthreads();
+          LPH(12);
+          for (int e = tid; e < total; e += kLT) {
+            const uint64_t key = S.lkey[e];
+            const double u = __dmul_rn(lbitsd(key), scale);
+            const int k = lat_bucket(lbitsd(key), scale);
+            const int sub = min(SUB - 1, (int)__dmul_rn(__dsub_rn(u, (double)k), (double)SUB));
+            const int f = S.lrk[k] * SUB + sub;
+            S.fid[e] = f;
+            atomicMax(reinterpret_cast<unsigned long long*>(&S.fb[f]), (unsigned long long)lbits(S.lval[e]));
+            atomicMax(reinterpret_cast<unsigned long long*>(&S.fa[f]), (unsigned long long)key);
+            atomicAdd(&S.fc[f], 1);
+          }
+          __syncthreads();
+          LPH(13);
+          {  // exclusive prefix max of the slots' max beta (four slots per thread)
+            constexpr int FP = kLNF / kLT;
+            uint64_t mb[FP];
+            uint64_t run = 0;
+  #pragma unroll
+            for (int q = 0; q < FP; ++q) {
+              mb[q] = S.fb[tid * FP + q];
+              run = run > mb[q] ? run : mb[q];
+            }
+            uint64_t inc = run;
+  #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint64_t n = __shfl_up_sync(0xffffffffu, inc, o);
+              if (lane >= o) inc = inc > n ? inc : n;
+            }
+            if (lane == 31) S.scr[8 + warp] = inc;
+            __syncthreads();
+            uint64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+            if (lane == 0) ex = 0;
+            for (int w = 0; w < warp; ++w) ex = ex > S.scr[8 + w] ? ex : S.scr[8 + w];
+  #pragma unroll
+            for (int q = 0; q < FP; ++q) {
+              const int f = tid * FP + q;
+              const int rk = f / SUB;
+              if (rk < nlb) {
+                const uint64_t gk = S.gin[S.lb[rk]];
+                const uint64_t g = ex > gk ? ex : gk;
+                const bool live = S.fc[f] > 0 && S.fa[f] > g;
+                S.fb[f] = g;
+                S.fc[f] = live ? 1 : 0;
+              }
+              ex = ex > mb[q] ? ex : mb[q];
+            }
+          }
+          __syncthreads();
+          LPH(15);
+          for (int e = tid; e < total; e += kLT)
+            if (S.fc[S.fid[e]]) S.cl[atomicAdd(&S.ints[5], 1)] = e;
+          __syncthreads();
+          const int nl2 = S.ints[5];
+          for (int c = tid; c < nl2; c += kLT) {
+            const int e = S.cl[c], f = S.fid[e];
+            const uint64_t key = S.lkey[e];
+            uint64_t gm = S.fb[f];
+            for (int c2 = 0; c2 < nl2; ++c2) {
+              const int e2 = S.cl[c2];
+              if (S.fid[e2] != f) continue;
+              const uint64_t k2 = S.lkey[e2];
+              if (k2 < key || (k2 == key && e2 < e)) {
+                const uint64_t v2 = lbits(S.lval[e2]);
+                gm = gm > v2 ? gm : v2;
+              }
+            }
+            if (key > gm) {
+              const int c3 = atomicAdd(&S.ints[3], 1);
+              S.cand[2 * c3] = key;
+              S.cand[2 * c3 + 1] = gm;
+            }
           }
         }
         __syncthreads();
@@ -688,11 +713,58 @@ int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max) {
   return lo;
 }
 
-// cluster size: the largest power of two <= 16 with C clusters fitting the SMs (>= 1)
-int latency_cluster_size(int C, int sms) {
-  int cs = 16;
-  while (cs > 1 && (int64_t)C * cs > sms) cs >>= 1;
-  return cs;
+// clusters of cs CTAs (smem bytes each) that can be resident at once
+template <typename T>
+int latency_max_clusters_t(int cs, size_t smem) {
+  if (cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 0;
+  if (cs > 8 && cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cs);
+  cfg.blockDim = dim3(kLT);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, latency_kernel<T>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// cluster size and live-arc capacity: the largest power of two cs <= 16 such that the
+// shared memory fits, all C clusters are resident at once (clusters live inside one
+// GPC: 16 chains x 8 CTAs do not all fit on 148 SMs), and each CTA keeps at least
+// 32 K elements of A (smaller slices only add barrier and merge latency); if no cs
+// keeps every cluster resident, the largest that fits (the clusters run in waves)
+int latency_cluster_size(int C, int64_t m, int64_t d_pad, size_t smem_max, bool fp32, int* cap_out) {
+  int cs_work = 1;
+  while (cs_work < 16 && (int64_t)(2 * cs_work) * 32768 <= m * d_pad) cs_work <<= 1;
+  int fallback = 0, fallback_cap = 0;
+  for (int cs = 16; cs >= 1; cs >>= 1) {
+    const int cap = latency_cap(d_pad, (int)m, cs, smem_max);
+    if (cap == 0) continue;
+    if (!fallback) {
+      fallback = cs;
+      fallback_cap = cap;
+    }
+    if (cs > cs_work) continue;
+    const size_t smem = latency_smem_bytes(d_pad, (int)m, cs, cap);
+    const int n = fp32 ? latency_max_clusters_t<float>(cs, smem) : latency_max_clusters_t<double>(cs, smem);
+    if (n >= C) {
+      *cap_out = cap;
+      return cs;
+    }
+  }
+  *cap_out = fallback_cap;
+  return fallback;  // 0: does not fit
 }
 
 template <typename T>

@@ -1034,13 +1034,9 @@ bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (h->opt.latency == 2 && !fp32 && 2 * C > sms) return false;
-  int cs = latency_cluster_size((int)C, sms);
-  int cap = latency_cap(h->d_pad, (int)h->m, cs, (size_t)smem_max);
-  while (cs < 16 && cap == 0) {
-    cs <<= 1;
-    cap = latency_cap(h->d_pad, (int)h->m, cs, (size_t)smem_max);
-  }
-  if (cap == 0) return false;
+  int cap = 0;
+  const int cs = latency_cluster_size((int)C, h->m, h->d_pad, (size_t)smem_max, fp32, &cap);
+  if (cs == 0 || cap == 0) return false;
   if (h->opt.latency == 2 && !fp32) {
     // auto: a cost model fitted to B200 measurements (S12) -- the latency mode
     // streams a CTA's rows of A (8 B per element) each iteration at ~120 GB/s per SM when

@@ -51,6 +51,7 @@ struct LatParams {
   double* S2;
   int64_t* rej;      // per chain
   int* err;          // set when a chain's live arcs overflow CTA 0's buffer
+  unsigned long long* startflag;  // non-null: check the start; lowest chain * m + i violating
   int cap;           // live arcs CTA 0 holds per iteration (latency_cap)
   int fp32;          // options.precision = 1: FP32 arithmetic (A32, b32), else FP64 (A, b)
   const float* A32;  // m x d_pad, zero-padded rows

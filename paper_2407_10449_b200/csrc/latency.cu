@@ -329,14 +329,31 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   T* Pn = reinterpret_cast<T*>(S.P1);  // the proposal P'
   auto gemv = [&](const T* v, T* out) { lat_rows<T>(A, i0, nr, p.d_pad, v, out, warp, lane); };
   gemv(Sx, Pc);
+  __syncthreads();
+  // strict start a_i . x0 < b_i (C18), checked here on the first P (FP64 mode; the
+  // host checks FP32 starts in FP64 itself): lowest (chain, constraint) to the host,
+  // and the cluster runs no iteration
+  if (p.startflag) {
+    int bad = 0;
+    for (int r = tid; r < nr; r += kLT) {
+      if (!((double)Pc[r] - (double)bv[i0 + r] < 0.0)) {  // NaN also fails
+        atomicMin(p.startflag, (unsigned long long)chain * (unsigned long long)m + (unsigned long long)(i0 + r));
+        bad = 1;
+      }
+    }
+    bad = __syncthreads_or(bad);
+    if (tid == 0) S.ints[6] = bad;
+  }
   int64_t rej = 0;
   cluster.sync();
+  const int n_iter = (p.startflag && __syncthreads_or(tid < CS ? *cluster.map_shared_rank(S.ints + 6, tid) : 0))
+                         ? 0 : p.n_iter;
 #ifdef TMVN_PHASE_TIMING
   long long lph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long lt_prev = clock64();
 #endif
 
-  for (int it = 0; it < p.n_iter; ++it) {
+  for (int it = 0; it < n_iter; ++it) {
     const uint32_t t = p.t0 + (uint32_t)it;
     // (a) nu_t, u_t
     for (int pk = tid; pk < (int)(p.d_pad / 2); pk += kLT) {

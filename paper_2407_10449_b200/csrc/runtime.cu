@@ -72,8 +72,13 @@ struct tmvn_ctx {
   double* Xsnap = nullptr;  // X before a latency-mode call (its overflow fallback)
   size_t Xsnap_n = 0;
   int lat_cap_max = 0;  // test hook: latency-mode live-arc capacity cap (0 = automatic)
+  int64_t lat_memo_C = -1;  // latency_cluster_size's answer for this C (m, d fixed per handle)
+  int lat_memo_fp32 = -1, lat_memo_cs = 0, lat_memo_cap = 0;
   int64_t* dsum = nullptr;
-  double* msum = nullptr;  // d (device) moment reduction target
+  double* msum = nullptr;  // 2 d (device) moment reduction targets (sum, sum of squares)
+  // pinned host landing area for the small per-call reads (flags, counters, the two
+  // moment vectors): async copies to pageable memory would stage through the driver
+  double* pin = nullptr;    // 8 + 2 d doubles
   unsigned long long* dflag = nullptr;
   double2 *gstash = nullptr, *ggaps = nullptr;
   int64_t scratch_groups = 0;  // chain groups the scratch is sized for
@@ -403,9 +408,10 @@ tmvn_status start_check(tmvn_ctx* h, int64_t C, double* P) {
   KL(h, launch_refresh(h, 0, C, P, st));
   CK(h, cudaMemsetAsync(h->dflag, 0xff, sizeof(unsigned long long), st));
   KL(h, launch_start_check(P, h->m_pad, h->b_eff, (int)C, (int)h->m, h->dflag, st));
-  unsigned long long flag = 0;
-  CK(h, cudaMemcpyAsync(&flag, h->dflag, sizeof(flag), cudaMemcpyDeviceToHost, st));
+  unsigned long long* fp = reinterpret_cast<unsigned long long*>(h->pin);
+  CK(h, cudaMemcpyAsync(fp, h->dflag, sizeof(*fp), cudaMemcpyDeviceToHost, st));
   CK(h, cudaStreamSynchronize(st));
+  const unsigned long long flag = *fp;
   if (flag != ~0ull) {
     char buf[256];
     snprintf(buf, sizeof(buf),
@@ -781,36 +787,37 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
 tmvn_status finish_stats(tmvn_ctx* h, int64_t C, int64_t n_iter, int64_t nrec) {
   cudaStream_t st = stream_of(h);
   const int64_t d = h->d;
-  int64_t rej = 0;
+  int64_t* rp = reinterpret_cast<int64_t*>(h->pin);
+  double* s = h->pin + 8;
+  double* q = s + d;
   KL(h, launch_sum_i64(h->rej, (int)C, h->dsum, st));
-  CK(h, cudaMemcpyAsync(&rej, h->dsum, sizeof(rej), cudaMemcpyDeviceToHost, st));
-  std::vector<double> s(d, 0.0), q(d, 0.0);
+  CK(h, cudaMemcpyAsync(rp, h->dsum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   if (nrec > 0) {
+    // the two sums land in separate halves of msum: one host sync for both
+    double* m2 = h->msum + d;
     if (h->affine) {
       // row-major C x d accumulators: reuse the tiled reducer through a pack
       KL(h, launch_pack(h->S1x, C, d, d, h->stage2, h->d_pad, st));
       KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
       h->prof.launches += 1;  // two kernels
-      CK(h, cudaMemcpyAsync(s.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(h, cudaStreamSynchronize(st));
       KL(h, launch_pack(h->S2x, C, d, d, h->stage2, h->d_pad, st));
-      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
+      KL(h, launch_chain_sum(h->stage2, (int)C, (int)d, h->d_pad, m2, h->stage, st));
       h->prof.launches += 1;  // two kernels
-      CK(h, cudaMemcpyAsync(q.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
     } else {
       KL(h, launch_chain_sum(h->S1, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
       h->prof.launches += 1;  // two kernels
-      CK(h, cudaMemcpyAsync(s.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(h, cudaStreamSynchronize(st));
-      KL(h, launch_chain_sum(h->S2, (int)C, (int)d, h->d_pad, h->msum, h->stage, st));
+      KL(h, launch_chain_sum(h->S2, (int)C, (int)d, h->d_pad, m2, h->stage, st));
       h->prof.launches += 1;  // two kernels
-      CK(h, cudaMemcpyAsync(q.data(), h->msum, d * sizeof(double), cudaMemcpyDeviceToHost, st));
     }
+    CK(h, cudaMemcpyAsync(s, h->msum, 2 * d * sizeof(double), cudaMemcpyDeviceToHost, st));
   }
   CK(h, cudaStreamSynchronize(st));
-  for (int64_t j = 0; j < d; ++j) {
-    h->mom_sum[j] += s[j];
-    h->mom_sq[j] += q[j];
+  const int64_t rej = *rp;
+  if (nrec > 0) {
+    for (int64_t j = 0; j < d; ++j) {
+      h->mom_sum[j] += s[j];
+      h->mom_sq[j] += q[j];
+    }
   }
   h->stats.steps += C * n_iter;
   h->stats.rejections += rej;
@@ -931,7 +938,11 @@ tmvn_status tmvn_create(const double* A, const double* b, int64_t m, int64_t d, 
   h->At = h->A_tiled;
   if ((e = dalloc(&h->dflag, 1)) != cudaSuccess) return bad(e, "alloc flag");
   if ((e = dalloc(&h->dsum, 1)) != cudaSuccess) return bad(e, "alloc sum");
-  if ((e = dalloc(&h->msum, (size_t)d)) != cudaSuccess) return bad(e, "alloc msum");
+  if ((e = dalloc(&h->msum, (size_t)2 * d)) != cudaSuccess) return bad(e, "alloc msum");
+  if ((e = cudaMallocHost(&h->pin, (size_t)(8 + 2 * d) * sizeof(double))) != cudaSuccess) {
+    h->pin = nullptr;
+    return bad(e, "alloc pinned scratch");
+  }
   cudaMemcpy(h->A_row, hA.data(), hA.size() * sizeof(double), cudaMemcpyHostToDevice);
   // b padded to m_pad with +inf: padded constraints (zero rows of A) are never active
   std::vector<double> hb_pad(hb);
@@ -1026,7 +1037,7 @@ tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
 // affine change of variable, shared memory), else the throughput loop runs.
 // options.latency = 2 (auto) takes it when there are at most SMs / 2 chains (clusters of
 // two or more CTAs) and the cost model below expects it to be faster.
-bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
+bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
   const bool fp32 = h->opt.precision == 1;  // FP32 runs in this mode whenever it fits
   if ((h->opt.latency == 0 && !fp32) || h->affine) return false;
   int dev = 0, sms = 0, smem_max = 0;
@@ -1034,8 +1045,17 @@ bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (h->opt.latency == 2 && !fp32 && 2 * C > sms) return false;
-  int cap = 0;
-  const int cs = latency_cluster_size((int)C, h->m, h->d_pad, (size_t)smem_max, fp32, &cap);
+  int cap = 0, cs = 0;
+  if (h->lat_memo_C == C && h->lat_memo_fp32 == (int)fp32) {  // occupancy queries cost ~10 us each
+    cs = h->lat_memo_cs;
+    cap = h->lat_memo_cap;
+  } else {
+    cs = latency_cluster_size((int)C, h->m, h->d_pad, (size_t)smem_max, fp32, &cap);
+    h->lat_memo_C = C;
+    h->lat_memo_fp32 = (int)fp32;
+    h->lat_memo_cs = cs;
+    h->lat_memo_cap = cap;
+  }
   if (cs == 0 || cap == 0) return false;
   if (h->opt.latency == 2 && !fp32) {
     // auto: a cost model fitted to B200 measurements (S12) -- the latency mode
@@ -1057,7 +1077,7 @@ bool latency_fits(const tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
 // returns TMVN_OK with *overflow = true (nothing usable written) when some iteration had
 // more live arcs than the capacity: the caller restores X and runs the default path
 tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int cs, int cap,
-                        int64_t* n_recorded, bool* overflow) {
+                        bool check_start, int64_t* n_recorded, bool* overflow) {
   cudaStream_t st = stream_of(h);
   if (!h->A_pad) {
     CK(h, dalloc(&h->A_pad, (size_t)(h->m * h->d_pad)));
@@ -1101,10 +1121,27 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   p.err = h->dyn + 64 * 16 - 1;
   CK(h, cudaMemsetAsync(p.err, 0, sizeof(int), st));
+  if (check_start) {
+    p.startflag = h->dflag;
+    CK(h, cudaMemsetAsync(h->dflag, 0xff, sizeof(unsigned long long), st));
+  }
   KL(h, launch_latency(p, cs, st));
-  int err = 0;
-  CK(h, cudaMemcpyAsync(&err, p.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int* ep = reinterpret_cast<int*>(h->pin);
+  unsigned long long* fp = reinterpret_cast<unsigned long long*>(h->pin + 1);
+  *fp = ~0ull;
+  CK(h, cudaMemcpyAsync(ep, p.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (check_start) CK(h, cudaMemcpyAsync(fp, h->dflag, sizeof(*fp), cudaMemcpyDeviceToHost, st));
   CK(h, cudaStreamSynchronize(st));
+  const int err = *ep;
+  const unsigned long long flag = *fp;
+  if (flag != ~0ull) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "infeasible start: chain %lld violates constraint %lld (a_i . x0 >= b_i; the start "
+             "must be strictly interior)",
+             (long long)(flag / h->m), (long long)(flag % h->m));
+    return fail(h, TMVN_E_INFEASIBLE_START, buf);
+  }
   *overflow = err != 0;
   if (err) return TMVN_OK;
   int64_t nrec = 0;
@@ -1122,16 +1159,18 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = plan_ess(h, C)) != TMVN_OK) return s;
   if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
-  if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;
-  if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
-  int64_t nrec = 0;
   int lcs = 0, lcap = 0;
-  bool done = false;
   const bool lat = n_iter > 0 && latency_fits(h, C, &lcs, &lcap);
   if (h->opt.precision == 1 && n_iter > 0 && !lat)
     return fail(h, TMVN_E_ARG,
                 "options.precision = 1 (FP32) runs in the latency mode only, which does not fit here "
                 "(affine change of variable, or shared memory)");
+  // the FP64 latency kernel checks the start on its own first P = A x0 (no GEMM here)
+  const bool kernel_checks = lat && h->opt.precision == 0;
+  if (!kernel_checks && (s = start_check(h, C, h->P0)) != TMVN_OK) return s;
+  if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
+  int64_t nrec = 0;
+  bool done = false;
   if (lat) {
     // X is kept so that an overflowing call can rerun on the default path
     const size_t cd = (size_t)h->C_pad * h->d_pad;
@@ -1145,12 +1184,13 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
     cudaStream_t st = stream_of(h);
     CK(h, cudaMemcpyAsync(h->Xsnap, h->X, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
     bool overflow = false;
-    if ((s = run_latency(h, C, n_iter, seed, lcs, lcap, &nrec, &overflow)) != TMVN_OK) return s;
+    if ((s = run_latency(h, C, n_iter, seed, lcs, lcap, kernel_checks, &nrec, &overflow)) != TMVN_OK) return s;
     done = !overflow;
     h->prof.latency_calls += 1;
     h->prof.latency_fallbacks += overflow ? 1 : 0;
     if (overflow) {
       CK(h, cudaMemcpyAsync(h->X, h->Xsnap, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if (kernel_checks && (s = start_check(h, C, h->P0)) != TMVN_OK) return s;  // P0 for run_loop
       if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
     }
   }
@@ -1217,6 +1257,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
+  if (h->pin) cudaFreeHost(h->pin);
   dfree(h->As); dfree(h->rowscale);
   delete h;
 }

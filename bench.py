@@ -31,6 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "constraint-evals/sec (chain-iterations/sec x m), FP64, whole job"
+METRIC32 = "constraint-evals/sec (chain-iterations/sec x m), FP32-class (--precision 1), whole job"
 UNIT = "constraint-evals/s"
 
 
@@ -48,6 +49,9 @@ def parse():
     ap.add_argument("--projection", type=int, default=0,
                     help="options.projection: 0 auto (int8 when d <= 4096), 1 int8 Ozaki split on "
                          "tcgen05 (FP64-accurate), 2 FP64 DMMA")
+    ap.add_argument("--precision", type=int, default=0,
+                    help="options.precision: 0 FP64 (the BASELINE metric), 1 the paper's FP32-class "
+                         "mode (int8 projection at 4 digits / FP32 latency kernel; trim_eps 1e-5)")
     return ap.parse_args()
 
 
@@ -197,6 +201,8 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     s = tm.Sampler(torch.tensor(A, device=dev), torch.tensor(b, device=dev), chain_offset=offset)
     s.set_options(stream=stream, projection=args.projection)
+    if args.precision:
+        s.set_options(precision=1, trim_eps=1e-5)
     oz = args.projection == 1 or (args.projection == 0 and d <= 4096)
     X = torch.tensor(np.tile(x0, (C, 1)), device=dev)
 
@@ -305,7 +311,7 @@ def main():
             oz_traffic, oz_traffic_src = None, None
             try:  # dram bytes read + written per launch, committed ncu --set full capture (config 3, N=1)
                 tj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_oz_traffic.json")))
-                if args.config == 3 and (opts.ozaki_slices or 7) == 7:
+                if args.config == 3 and (opts.ozaki_slices or 7) == 7 and not args.precision:
                     oz_traffic, oz_traffic_src = tj["traffic_bytes"], "profiles/r01/ncu_oz_traffic.json"
             except Exception:
                 pass
@@ -317,7 +323,8 @@ def main():
                     "share_of_step": roofline["share_of_step"]}
             roofline = {"bound": "tensor",
                         "kernel": "ozaki_gemm_kernel (Q = N A'^T, int8 tcgen05.mma, TMEM accumulators, "
-                                  f"{opts.ozaki_slices or 7} digits: FP64-accurate)",
+                                  + ("4 digits: FP32-class, options.precision = 1)" if args.precision
+                                 else f"{opts.ozaki_slices or 7} digits: FP64-accurate)"),
                         "achieved": tc_achieved, "peak": tc_peak, "unit": "TOP/s (int8)",
                         "frac": tc_achieved / tc_peak, "traffic": oz_traffic, "traffic_source": oz_traffic_src,
                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x 2 = nominal int8/bf16 dense "
@@ -339,7 +346,7 @@ def main():
             try:
                 sj = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_full_int8_summary.json")))
                 e = sj["ess_kernel<8>"]
-                if args.config == 3 and world == 1:
+                if args.config == 3 and world == 1 and not args.precision:
                     ess["traffic"] = (float(e["dram__bytes_read.sum"]["value"]) +
                                       float(e["dram__bytes_write.sum"]["value"])) * 1e6
                     ess["traffic_source"] = "profiles/r01/ncu_full_int8_summary.json"
@@ -371,9 +378,10 @@ def main():
         cpu = oracle_rate(A, b, x0, seed, args.cpu_seconds, C)
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        line = {"metric": METRIC32 if args.precision else METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+i8" if oz and prof["latency_calls"] == 0 else "f64",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": ("f32-class (int8 x4 projection, f64 elsewhere)" if prof["latency_calls"] == 0 else "f32")
+                if args.precision else ("f64+i8" if oz and prof["latency_calls"] == 0 else "f64"),
                 "data": "synthetic (seeded Gaussian polytope of BASELINE config; no dataset)",
                 "config": config_dict(cfg, args, world),
                 "chain_iters_per_s": total_iters / (ms_max * 1e-3),

@@ -155,14 +155,17 @@ typedef struct {
    * CTAs) and a cost model fitted to B200 measurements expects it to be
    * faster (it re-reads A from L2 for every chain), else the default path.  0: off (always the default path). */
   int32_t latency;
-  /* 1: FP32 arithmetic, the paper's precision (S3.3): A . nu,
-   * A . x, the arcs, P' and the safeguard, x in single precision; the interval
-   * comparisons and the inverse-CDF draw in FP64 on the (exactly widened) FP32
-   * endpoints.  Runs in the latency mode only (whatever options.latency says,
-   * as long as it fits: no affine change of variable; TMVN_E_ARG otherwise); a
-   * live-arc overflow reruns the call on the FP64 default path.  Use with
-   * trim_eps > 0 (S3.3 trimming); the safeguard rejects the rare infeasible
-   * proposal.  Parity with the FP64 oracle is statistical.  0 (default): FP64. */
+  /* 1: FP32-class arithmetic, the paper's precision (S3.3).
+   * In the latency mode (options.latency, auto as in FP64): A . nu, A . x, the arcs, P' and the safeguard, x in single
+   * precision; the interval comparisons and the inverse-CDF draw in FP64 on the
+   * (exactly widened) FP32 endpoints; a live-arc overflow reruns the call on
+   * the throughput path.  Otherwise (many chains, affine change of variable)
+   * the throughput path with the int8 projection at 4 digits per operand
+   * (bound below with S = 4: ~2^-26 relative, FP32-class) for Q, the refresh
+   * and the start check; the rest stays FP64.  Use with trim_eps > 0 (S3.3
+   * trimming); the safeguard rejects the rare infeasible proposal; iterates
+   * are feasible to FP32 rounding.  Parity with the FP64 oracle is
+   * statistical.  0 (default): FP64. */
   int32_t precision;
 } tmvn_options;
 
@@ -272,7 +275,7 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
                                 int64_t seg_cap, int64_t* nseg, double* L, double* theta);
 /* The production int8 tcgen05 projection: out[R x S] = X[R x K] . W[S x K]^T with
  * W's rows scaled per row, X by the power of two above max |X|, `slices` digits
- * (6, 7, 8); K <= 4096. */
+ * (4: the FP32-class projection of options.precision = 1; 6, 7, 8); K <= 4096. */
 tmvn_status tmvn_test_ozaki_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
                                  int32_t slices, double* out);
 /* Latency mode's live-arc capacity per chain and iteration: cap > 0 lowers it

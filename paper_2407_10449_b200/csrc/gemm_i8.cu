@@ -492,6 +492,7 @@ cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns,
                     : launch_oz_t<SS, ST, false>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st);
   if (compact) {
     switch (S) {
+      TMVN_OZ_CASE(4, 3)
       TMVN_OZ_CASE(6, 3)
       TMVN_OZ_CASE(7, 3)
       TMVN_OZ_CASE(8, 3)
@@ -499,6 +500,7 @@ cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns,
     }
   }
   switch (S) {
+    TMVN_OZ_CASE(4, 0)
     TMVN_OZ_CASE(6, 0)
     TMVN_OZ_CASE(7, 0)
     TMVN_OZ_CASE(8, 0)

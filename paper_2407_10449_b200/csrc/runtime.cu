@@ -244,7 +244,12 @@ tmvn_status ensure_affine_moments(tmvn_ctx* h) {
 bool use_oz(const tmvn_ctx* h) {
   return h->opt.projection == 1 || (h->opt.projection == 0 && h->d <= 4096);
 }
-int oz_slices(const tmvn_ctx* h) { return h->opt.ozaki_slices ? h->opt.ozaki_slices : 7; }
+// digits per operand: 7 (FP64-class, default), 6 or 8 by option; options.precision = 1
+// (FP32) takes 4 (31 fraction bits: FP32-class, 10 digit-pair MMAs instead of 28)
+int oz_slices(const tmvn_ctx* h) {
+  if (h->opt.precision == 1) return 4;
+  return h->opt.ozaki_slices ? h->opt.ozaki_slices : 7;
+}
 
 // Digits of A' (once per A' and digit count) and the nu digit buffer (per C_pad).
 tmvn_status ensure_ozaki(tmvn_ctx* h) {
@@ -1038,13 +1043,13 @@ tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
 // options.latency = 2 (auto) takes it when there are at most SMs / 2 chains (clusters of
 // two or more CTAs) and the cost model below expects it to be faster.
 bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
-  const bool fp32 = h->opt.precision == 1;  // FP32 runs in this mode whenever it fits
-  if ((h->opt.latency == 0 && !fp32) || h->affine) return false;
+  const bool fp32 = h->opt.precision == 1;
+  if (h->opt.latency == 0 || h->affine) return false;
   int dev = 0, sms = 0, smem_max = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (h->opt.latency == 2 && !fp32 && 2 * C > sms) return false;
+  if (h->opt.latency == 2 && 2 * C > sms) return false;
   int cap = 0, cs = 0;
   if (h->lat_memo_C == C && h->lat_memo_fp32 == (int)fp32) {  // occupancy queries cost ~10 us each
     cs = h->lat_memo_cs;
@@ -1057,14 +1062,15 @@ bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
     h->lat_memo_cap = cap;
   }
   if (cs == 0 || cap == 0) return false;
-  if (h->opt.latency == 2 && !fp32) {
+  if (h->opt.latency == 2) {
     // auto: a cost model fitted to B200 measurements (S12) -- the latency mode
     // streams a CTA's rows of A (8 B per element) each iteration at ~120 GB/s per SM when
     // A is L2-resident (~50 GB/s when it is not) plus ~12 us of per-iteration latency;
     // the default path costs ~50 us + 7.8 ps per element of A at few chains
-    const double abytes = 8.0 * (double)h->m * (double)h->d_pad;
+    const double eb = fp32 ? 4.0 : 8.0;  // bytes per element of A
+    const double abytes = eb * (double)h->m * (double)h->d_pad;
     const double r_sm = abytes <= 80e6 ? 120e9 : 50e9;
-    const double t_lat = 12e-6 + (double)((h->m + cs - 1) / cs) * (double)h->d_pad * 8.0 / r_sm;
+    const double t_lat = 12e-6 + (double)((h->m + cs - 1) / cs) * (double)h->d_pad * eb / r_sm;
     const double t_def = 50e-6 + 7.8e-12 * (double)h->m * (double)h->d;
     if (t_lat >= t_def) return false;
   }
@@ -1161,10 +1167,6 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
   int lcs = 0, lcap = 0;
   const bool lat = n_iter > 0 && latency_fits(h, C, &lcs, &lcap);
-  if (h->opt.precision == 1 && n_iter > 0 && !lat)
-    return fail(h, TMVN_E_ARG,
-                "options.precision = 1 (FP32) runs in the latency mode only, which does not fit here "
-                "(affine change of variable, or shared memory)");
   // the FP64 latency kernel checks the start on its own first P = A x0 (no GEMM here)
   const bool kernel_checks = lat && h->opt.precision == 0;
   if (!kernel_checks && (s = start_check(h, C, h->P0)) != TMVN_OK) return s;
@@ -1404,7 +1406,7 @@ tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t 
 
 tmvn_status tmvn_test_ozaki_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
                                  int32_t slices, double* out) {
-  if (!X || !W || !out || R < 1 || S < 1 || K < 1 || K > 4096 || slices < 6 || slices > 8)
+  if (!X || !W || !out || R < 1 || S < 1 || K < 1 || K > 4096 || !(slices == 4 || (slices >= 6 && slices <= 8)))
     return fail(nullptr, TMVN_E_ARG, "bad args");
   const int64_t Rp = round_up(R, kTileR), Sp = round_up(S, kTileR), Kp = round_up(K, kTileK);
   const int64_t KB = (K + kOzStepK - 1) / kOzStepK;

@@ -220,13 +220,49 @@ def test_fp32_section_4_2_no_rejections(d, chains):
     assert np.max(slack) <= 1e-4 * np.max(np.abs(A @ x0))  # feasible to FP32 rounding
 
 
-def test_fp32_needs_latency_mode():
-    A, b, x0 = synth.make_instance(3, m=40, d=6)
-    L, mu = synth.random_spd_factor(6, seed=1)
-    s = tm.Sampler(A, b, mu=np.zeros(6), L=L, precision=1)
-    with pytest.raises(tm.TmvnError) as ei:
-        s.sample(np.zeros((4, 6)), 2, seed=1)
-    assert ei.value.status == -1 and "FP32" in str(ei.value)
+def test_fp32_throughput_path_section_4_1():
+    """precision = 1 on the throughput path (latency = 0: 2000 chains, int8 projection at
+    4 digits, FP32-class): the paper's S4.1 protocol and table."""
+    for interval, max_rej in (((-1.0, 3.0), 20), ((15.0, 16.0), 200)):
+        A, b, x0 = synth.one_dim(interval)
+        s = tm.Sampler(A, b, precision=1, latency=0, trim_eps=EPS32, burn_in=500, thin=10)
+        s.sample(np.tile(x0, (2000, 1)), 1000, seed=2024)
+        assert s.profile()["latency_calls"] == 0
+        sm, sq, n = s.moments()
+        mu, var = _trunc_normal_moments(*interval)
+        m1 = sm[0] / n
+        assert abs(m1 - mu) < 0.01 and abs(sq[0] / n - m1 * m1 - var) < 0.01
+        assert s.stats()["rejections"] <= max_rej, s.stats()
+
+
+def test_fp32_throughput_path_steps_close_to_oracle():
+    """Every traced step of the FP32-class throughput path against the FP64 oracle
+    step from the same state (same nu, u, trim): the 4-digit projection's ~1e-8
+    relative error moves the arc endpoints and the iterate by far less than 1e-5."""
+    A, b, x0 = synth.make_instance(3, m=300, d=70)
+    C, T = 150, 6
+    s = tm.Sampler(A, b, precision=1, latency=0, trim_eps=EPS32)
+    chains = np.array([0, 77, 149])
+    trace, out = s.test_trace(np.tile(x0, (C, 1)), T, seed=103, chains=chains)
+    for it in range(T):
+        for k, c in enumerate(chains):
+            xn, _ = oracle.step(A, b, trace[it, k], 103, it, int(c), eps=EPS32)
+            assert np.max(np.abs(trace[it + 1, k] - xn)) <= 1e-5 * max(1.0, np.max(np.abs(xn)))
+    assert np.max(out @ A.T - b) <= 1e-6
+
+
+def test_fp32_affine_on_throughput_path():
+    """App. A with precision = 1 runs on the throughput path: x ~ N(2, 4) on [1, 5]."""
+    s = tm.Sampler(np.array([[1.0], [-1.0]]), np.array([5.0, -1.0]), mu=np.array([2.0]),
+                   L=np.array([[2.0]]), burn_in=100, precision=1, trim_eps=EPS32)
+    out = s.sample(np.full((2000, 1), 3.0), 600, seed=77)
+    sm, sq, n = s.moments()
+    mu_u, var_u = _trunc_normal_moments(-0.5, 1.5)
+    m1 = sm[0] / n
+    assert abs(m1 - (2 + 2 * mu_u)) < 0.01
+    assert abs(sq[0] / n - m1 * m1 - 4 * var_u) < 0.03
+    assert np.all(out >= 1.0 - 1e-6) and np.all(out <= 5.0 + 1e-6)
+
 
 
 def test_latency_shard_invariance_and_resume_bitwise():

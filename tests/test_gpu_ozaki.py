@@ -21,7 +21,7 @@ from test_gpu_step import REL, compare_step, ozaki_qbound
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("slices", [6, 7, 8])
+@pytest.mark.parametrize("slices", [4, 6, 7, 8])
 @pytest.mark.parametrize("R,S,K", [(1, 1, 1), (130, 200, 100), (64, 128, 32), (257, 129, 1000)])
 def test_ozaki_exact_on_dyadic_inputs(slices, R, S, K):
     rng = np.random.default_rng(R * 7 + S + K)
@@ -37,7 +37,7 @@ def test_ozaki_exact_on_dyadic_inputs(slices, R, S, K):
     assert np.array_equal(out, ref)
 
 
-@pytest.mark.parametrize("slices", [6, 7, 8])
+@pytest.mark.parametrize("slices", [4, 6, 7, 8])
 @pytest.mark.parametrize("R,S,K", [(200, 300, 1000), (65, 131, 4096), (128, 256, 37)])
 def test_ozaki_within_stated_bound(slices, R, S, K):
     rng = np.random.default_rng(R + S + K + slices)

@@ -285,3 +285,27 @@ def test_latency_shard_invariance_and_resume_bitwise():
     g1 = tm.Sampler(A, b, precision=1, trim_eps=1e-5, chain_offset=0).sample(X0[:4], T, seed=5)
     g2 = tm.Sampler(A, b, precision=1, trim_eps=1e-5, chain_offset=4).sample(X0[4:], T, seed=5)
     assert np.array_equal(np.concatenate([g1, g2]), f)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_latency_random_shapes_vs_oracle(case):
+    """Ragged shapes through the latency mode (forced): d, m, C drawn per case, unit
+    and unnormalised rows, one iteration per call against the oracle step."""
+    rng = np.random.default_rng(1000 + case)
+    d = int(rng.integers(1, 90))
+    m = int(rng.integers(1, 400))
+    C = int(rng.integers(1, 40))
+    A = rng.standard_normal((m, d))
+    if case % 2:
+        A /= np.linalg.norm(A, axis=1, keepdims=True)
+    b = rng.uniform(0.05, 2.0, m)
+    x0 = np.zeros(d)
+    s = tm.Sampler(A, b, latency=1, record=0)
+    X = np.tile(x0, (C, 1))
+    for t in range(4):
+        Xn = s.sample(X, 1, seed=case)
+        assert s.profile()["latency_calls"] == t + 1
+        for c in range(C):
+            xn, _ = oracle.step(A, b, X[c], case, t, c)
+            assert np.max(np.abs(Xn[c] - xn)) <= REL * max(1.0, np.max(np.abs(xn))), (d, m, C, t, c)
+        X = Xn

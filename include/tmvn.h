@@ -242,6 +242,38 @@ tmvn_status tmvn_reset_stats(tmvn_handle h);  /* also resets the profile */
 /* Kernel timings collected while options.profile != 0 (launch counts always). */
 tmvn_status tmvn_get_profile(tmvn_handle h, tmvn_profile* prof);
 
+/* ------------------------------------------------------------------------ */
+/* Constraint-parallel iterations (Prop. 1): for an A
+ * too large for one GPU, rank r creates its handle with its own rows A_r, b_r
+ * (tmvn_create) and every rank holds all C chains.  One iteration t is
+ *   tmvn_cp_stats -> all-reduce (gx: max, ma: max, cnt: sum)
+ *   tmvn_cp_live  -> all-gather (live, nlive) in rank order
+ *   tmvn_cp_theta -> all-reduce (flags: max)
+ *   tmvn_cp_commit
+ * with the collectives run by the caller (torch.distributed / NCCL; the
+ * Python class paper_2407_10449_b200.ConstraintParallel does it).  Every rank
+ * draws the same nu and u (Philox counters), the merged bucket tables and the
+ * gathered live arcs give every rank the same I_act and theta, and the
+ * projection rows are computed per element in a fixed order, so the chains
+ * are bitwise those of one GPU holding all rows.  All exchange buffers are
+ * caller-owned device memory on the handle's stream:
+ *   gx, ma: uint64 C x 128 (bucket max beta bits exact, max alpha high word),
+ *   cnt: int32 C x 128, live: double C x cap x 2 (alpha, beta), nlive: int32 C
+ *   (may exceed cap: the caller must then stop -- arcs were dropped),
+ *   all_live: world x C x cap x 2, all_n: world x C, flags: int32 C.
+ * FP64 only, no affine change of variable; stats / moments as for tmvn_sample
+ * after tmvn_cp_end (per rank: identical on every rank).  Errors: TMVN_E_ARG,
+ * TMVN_E_STATE (no tmvn_cp_begin), TMVN_E_INFEASIBLE_START (this rank's rows). */
+tmvn_status tmvn_cp_begin(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed);
+tmvn_status tmvn_cp_stats(tmvn_handle h, int64_t t, uint64_t* gx, uint64_t* ma, int32_t* cnt);
+tmvn_status tmvn_cp_live(tmvn_handle h, const uint64_t* gx, const uint64_t* ma, const int32_t* cnt, int32_t cap,
+                         double* live, int32_t* nlive);
+tmvn_status tmvn_cp_theta(tmvn_handle h, int64_t t, const uint64_t* gx, const uint64_t* ma, const int32_t* cnt,
+                          const double* all_live, const int32_t* all_n, int32_t world, int32_t cap,
+                          int32_t* flags);
+tmvn_status tmvn_cp_commit(tmvn_handle h, int64_t t, const int32_t* flags);
+tmvn_status tmvn_cp_end(tmvn_handle h, int64_t n_iter, double* out);
+
 /* Last error message of this handle (or of the calling thread's last failed
  * tmvn_create when h is NULL).  Valid until the next call on the handle. */
 const char* tmvn_last_error(tmvn_handle h);

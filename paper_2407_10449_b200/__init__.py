@@ -31,7 +31,8 @@ EXPORTS = ["tmvn_default_options", "tmvn_create", "tmvn_set_affine", "tmvn_set_o
            "tmvn_reset_stats", "tmvn_get_profile", "tmvn_last_error", "tmvn_version",
            "tmvn_destroy", "tmvn_test_philox", "tmvn_test_curand_philox", "tmvn_test_normals", "tmvn_test_arcs",
            "tmvn_test_intervals", "tmvn_test_gemm", "tmvn_test_ozaki_gemm", "tmvn_test_step",
-           "tmvn_test_trace", "tmvn_test_latency_cap"]
+           "tmvn_test_trace", "tmvn_test_latency_cap", "tmvn_cp_begin", "tmvn_cp_stats", "tmvn_cp_live",
+           "tmvn_cp_theta", "tmvn_cp_commit", "tmvn_cp_end"]
 
 
 class TmvnError(RuntimeError):
@@ -112,6 +113,12 @@ def lib():
             "tmvn_test_step": [H, P, i64, u64, i64, P],
             "tmvn_test_trace": [H, P, i64, i64, u64, P, i64, P, P],
             "tmvn_test_latency_cap": [H, ctypes.c_int32],
+            "tmvn_cp_begin": [H, P, i64, i64, u64],
+            "tmvn_cp_stats": [H, i64, P, P, P],
+            "tmvn_cp_live": [H, P, P, P, ctypes.c_int32, P, P],
+            "tmvn_cp_theta": [H, i64, P, P, P, P, P, ctypes.c_int32, ctypes.c_int32, P],
+            "tmvn_cp_commit": [H, i64, P],
+            "tmvn_cp_end": [H, i64, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -378,3 +385,6 @@ def test_ozaki_gemm(X, W, slices=7):
     out = np.zeros((R, S))
     _check(lib().tmvn_test_ozaki_gemm(_ptr(X), R, _ptr(W), S, K, slices, _ptr(out)))
     return out
+
+
+from .cp import ConstraintParallel  # noqa: E402  (constraint-parallel driver)

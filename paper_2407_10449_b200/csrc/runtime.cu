@@ -72,6 +72,11 @@ struct tmvn_ctx {
   double* Xsnap = nullptr;  // X before a latency-mode call (its overflow fallback)
   size_t Xsnap_n = 0;
   int lat_cap_max = 0;  // test hook: latency-mode live-arc capacity cap (0 = automatic)
+  // constraint-parallel iterations (tmvn_cp_*): chains, seed, first iteration, scratch
+  int64_t cp_C = 0, cp_t0 = 0;
+  uint64_t cp_seed = 0;
+  int64_t cp_nrec = 0;
+  double* cp_tl = nullptr;  // 2 C_pad: theta, L per chain
   int64_t lat_memo_C = -1;  // latency_cluster_size's answer for this C (m, d fixed per handle)
   int lat_memo_fp32 = -1, lat_memo_cs = 0, lat_memo_cap = 0;
   int64_t* dsum = nullptr;
@@ -1256,7 +1261,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->dyn);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
-  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
+  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->cp_tl); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
   if (h->pin) cudaFreeHost(h->pin);
@@ -1547,6 +1552,79 @@ tmvn_status tmvn_test_trace(tmvn_handle h, const double* X0, int64_t C, int64_t 
   if ((s = finish_stats(h, C, n_iter, nrec)) != TMVN_OK) return s;
   CK(h, tmp_out(trace, tr, (size_t)(n_iter + 1) * n_trace * h->d));
   if (h->opt.auto_advance) h->opt.iter_offset += n_iter;
+  return TMVN_OK;
+}
+
+// ---- constraint-parallel iterations (cp.cu) ---------------------------
+tmvn_status tmvn_cp_begin(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed) {
+  tmvn_status s = check_sample_args(h, X0, C, n_iter, X0);
+  if (s != TMVN_OK) return s;
+  if (h->affine) return fail(h, TMVN_E_ARG, "constraint-parallel iterations: no affine change of variable");
+  if ((s = set_device(h)) != TMVN_OK) return s;
+  if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
+  if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
+  if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
+  if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;  // this rank's rows
+  if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
+  dfree(h->cp_tl);
+  h->cp_tl = nullptr;
+  CK(h, dalloc(&h->cp_tl, (size_t)2 * h->C_pad));
+  h->cp_C = C;
+  h->cp_seed = seed;
+  h->cp_t0 = h->opt.iter_offset;
+  h->cp_nrec = 0;
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_cp_stats(tmvn_handle h, int64_t t, uint64_t* gx, uint64_t* ma, int32_t* cnt) {
+  if (!h || !h->cp_C || !gx || !ma || !cnt) return fail(h, TMVN_E_STATE, "tmvn_cp_stats: call tmvn_cp_begin first");
+  cudaStream_t st = stream_of(h);
+  const int64_t C = h->cp_C;
+  KL(h, launch_first_nu(h, C, h->cp_seed, (uint32_t)t, st));  // nu_t (+ digits), every rank alike
+  KL(h, launch_projection(h, 0, round_up(C, kTileR), st));    // Q_r = nu A_r^T
+  KL(h, launch_cp_stats(h->P0, h->Q, h->m_pad, h->b_eff, (int)h->m, (int)C, gx, ma, cnt, st));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_cp_live(tmvn_handle h, const uint64_t* gx, const uint64_t* ma, const int32_t* cnt, int32_t cap,
+                         double* live, int32_t* nlive) {
+  if (!h || !h->cp_C || !live || !nlive || cap < 1) return fail(h, TMVN_E_ARG, "tmvn_cp_live: bad arguments");
+  KL(h, launch_cp_live(h->P0, h->Q, h->m_pad, h->b_eff, (int)h->m, (int)h->cp_C, gx, ma, cnt, cap,
+                       reinterpret_cast<double2*>(live), nlive, stream_of(h)));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_cp_theta(tmvn_handle h, int64_t t, const uint64_t* gx, const uint64_t* ma, const int32_t* cnt,
+                          const double* all_live, const int32_t* all_n, int32_t world, int32_t cap, int32_t* flags) {
+  if (!h || !h->cp_C || !all_live || !all_n || !flags || world < 1 || cap < 1)
+    return fail(h, TMVN_E_ARG, "tmvn_cp_theta: bad arguments");
+  KL(h, launch_cp_theta(gx, ma, cnt, reinterpret_cast<const double2*>(all_live), all_n, world, cap, h->cp_seed,
+                        (uint32_t)t, (uint32_t)h->opt.chain_offset, h->opt.trim_eps, h->P0, h->Q, h->m_pad,
+                        h->b_eff, (int)h->m, (int)h->cp_C, h->P1, flags, h->cp_tl, h->cp_tl + h->C_pad,
+                        stream_of(h)));
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_cp_commit(tmvn_handle h, int64_t t, const int32_t* flags) {
+  if (!h || !h->cp_C || !flags) return fail(h, TMVN_E_ARG, "tmvn_cp_commit: bad arguments");
+  cudaStream_t st = stream_of(h);
+  const bool rec = recorded_iter(h->opt, t);
+  h->cp_nrec += rec ? 1 : 0;
+  KL(h, launch_cp_commit(flags, h->cp_tl, h->cp_tl + h->C_pad, h->X, h->N, h->d_pad, (int)h->d, h->P0, h->P1,
+                         h->m_pad, (int)h->m, (int)h->cp_C, rec ? 1 : 0, h->S1, h->S2, h->rej, st));
+  const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
+  if ((t + 1) % K == 0) KL(h, launch_refresh(h, 0, h->cp_C, h->P0, st));  // C13
+  return TMVN_OK;
+}
+
+tmvn_status tmvn_cp_end(tmvn_handle h, int64_t n_iter, double* out) {
+  if (!h || !h->cp_C || !out) return fail(h, TMVN_E_ARG, "tmvn_cp_end: bad arguments");
+  tmvn_status s;
+  const int64_t C = h->cp_C;
+  if ((s = store_X(h, C, out)) != TMVN_OK) return s;
+  if ((s = finish_stats(h, C, n_iter, h->cp_nrec)) != TMVN_OK) return s;
+  if (h->opt.auto_advance) h->opt.iter_offset = h->cp_t0 + n_iter;
+  h->cp_C = 0;
   return TMVN_OK;
 }
 

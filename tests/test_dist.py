@@ -71,3 +71,61 @@ def test_two_rank_gloo_matches_single_process():
     assert np.allclose(red[d:2 * d], ref["sumsq"], rtol=1e-13, atol=1e-13)
     assert int(red[2 * d]) == ref["n_rec"] and int(red[2 * d + 1]) == ref["rejections"]
     assert red[2 * d + 2] == 2.0  # MAX over ranks
+
+
+def test_row_shard():
+    from paper_2407_10449_b200.cp import row_shard
+    for m in (1, 5, 2000, 16384):
+        for world in (1, 2, 3, 8):
+            parts = [row_shard(m, world, r) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == m
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            sizes = [h - l for l, h in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _cp_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+    import oracle
+    from paper_2407_10449_b200 import synth
+    from paper_2407_10449_b200.cp import _Coll, row_shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    coll = _Coll(None)
+    assert coll.world == world and coll.rank == rank
+    # the collectives the constraint-parallel loop runs, on CPU tensors
+    g = torch.tensor([[rank * 10 + 1, 5 - rank]], dtype=torch.int64)
+    coll.all_reduce(g, "max")
+    c = torch.tensor([rank + 1], dtype=torch.int32)
+    coll.all_reduce(c, "sum")
+    parts = torch.zeros((world, 3), dtype=torch.float64)
+    coll.all_gather(parts, torch.full((3,), float(rank), dtype=torch.float64))
+    # Prop. 1 on the oracle: the rows split over the ranks, each rank's
+    # infeasible arcs gathered, I_act of the union equals I_act over all rows
+    A, b, x0 = synth.make_instance(3, m=90, d=10)
+    lo, hi = row_shard(A.shape[0], world, rank)
+    nu = oracle.normals(7, 0, 0, A.shape[1])
+    al, be, act = oracle.arcs(A[lo:hi] @ x0, A[lo:hi] @ nu, b[lo:hi])
+    mine = torch.zeros((A.shape[0], 2), dtype=torch.float64)
+    mine[lo:hi, 0] = torch.tensor(np.where(act, al, 0.0))
+    mine[lo:hi, 1] = torch.tensor(np.where(act, be, 0.0))
+    coll.all_reduce(mine, "sum")  # disjoint rows: the sum is the concatenation
+    if rank == 0:
+        segs = oracle.intervals(mine[:, 0].numpy(), mine[:, 1].numpy())
+        al0, be0, act0 = oracle.arcs(A @ x0, A @ nu, b)
+        ref = oracle.intervals(np.where(act0, al0, 0.0), np.where(act0, be0, 0.0))
+        np.save(os.path.join(outdir, "cp.npy"), np.array([
+            g.tolist() == [[(world - 1) * 10 + 1, 5]], int(c[0]) == world * (world + 1) // 2,
+            parts.tolist() == [[float(r)] * 3 for r in range(world)],
+            len(segs) == len(ref) and all(np.allclose(a, b_, rtol=0, atol=0) for a, b_ in zip(segs, ref))]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_constraint_parallel_collectives_gloo():
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_cp_worker, args=(2, _free_port(), td), nprocs=2, join=True)
+        ok = np.load(os.path.join(td, "cp.npy"))
+    assert ok.all(), ok

@@ -35,7 +35,10 @@ namespace cg = cooperative_groups;
 namespace tmvn {
 namespace {
 
-constexpr int kLT = 256;      // threads per CTA
+#ifndef TMVN_LAT_THREADS
+#define TMVN_LAT_THREADS 256
+#endif
+constexpr int kLT = TMVN_LAT_THREADS;  // threads per CTA
 constexpr int kLNB = 128;     // level-1 buckets over [0, 2 pi]
 // live arcs CTA 0 can hold per iteration: p.cap, sized on the host from the shared
 // memory left (up to m); more in some iteration -> the call reruns on the default path
@@ -67,7 +70,7 @@ struct LatShared {
   int* cl;         // cap: live arcs in live level-2 slots
   int* lrk;        // kLNB: rank of a live level-1 bucket among the live ones
   int* lb;         // kLNB: live level-1 bucket of each rank
-  uint64_t* scr;   // 16 words of scan scratch
+  uint64_t* scr;   // 8 + kLT / 32 words of scan scratch
   uint64_t* cand;  // 2 cap
   double* M1;      // nk x kLT: this CTA's moment sums over the call (flushed at the end)
   double* M2;
@@ -100,7 +103,7 @@ __host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, 
   S.live = reinterpret_cast<int*>(take(kLNB * 4));
   S.lrk = reinterpret_cast<int*>(take(kLNB * 4));
   S.lb = reinterpret_cast<int*>(take(kLNB * 4));
-  S.scr = reinterpret_cast<uint64_t*>(take(16 * 8));
+  S.scr = reinterpret_cast<uint64_t*>(take((8 + kLT / 32) * 8));
   S.M1 = reinterpret_cast<double*>(take((size_t)nk * kLT * 8));
   S.M2 = reinterpret_cast<double*>(take((size_t)nk * kLT * 8));
   S.ints = reinterpret_cast<int*>(take(8 * 4));

@@ -102,25 +102,31 @@ class ConstraintParallel:
         all_live = torch.zeros((W, C, self.cap, 2), dtype=torch.float64, device=dev)
         all_n = torch.zeros((W, C), dtype=torch.int32, device=dev)
         flags = torch.zeros(C, dtype=torch.int32, device=dev)
+        maxn = torch.zeros((), dtype=torch.int32, device=dev)
+        # the library launches on torch's current stream: the NCCL collectives are ordered
+        # on it (no host synchronisation per iteration); gloo's host copies synchronise
+        self.s.set_options(stream=torch.cuda.current_stream())
         for it in range(n_iter):
             t = t0 + it
             _check(L.tmvn_cp_stats(h, t, _ptr(gx), _ptr(ma), _ptr(cnt)), h)
-            torch.cuda.synchronize()
             self.coll.all_reduce(gx, "max")
             self.coll.all_reduce(ma, "max")
             self.coll.all_reduce(cnt, "sum")
             _check(L.tmvn_cp_live(h, _ptr(gx), _ptr(ma), _ptr(cnt), self.cap, _ptr(live), _ptr(nlive)), h)
-            torch.cuda.synchronize()
-            self.coll.all_gather(all_live, live)
-            self.coll.all_gather(all_n, nlive)
-            if int(all_n.max()) > self.cap:
-                raise RuntimeError(f"constraint-parallel: more than cap={self.cap} live arcs of one chain on one "
-                                   "rank in an iteration; raise cap")
-            _check(L.tmvn_cp_theta(h, t, _ptr(gx), _ptr(ma), _ptr(cnt), _ptr(all_live), _ptr(all_n), W, self.cap,
-                                   _ptr(flags)), h)
-            torch.cuda.synchronize()
+            if W == 1:
+                all_n_it, all_live_it = nlive, live  # no copies on one rank
+            else:
+                self.coll.all_gather(all_live, live)
+                self.coll.all_gather(all_n, nlive)
+                all_n_it, all_live_it = all_n, all_live
+            maxn = torch.maximum(maxn, all_n_it.max())  # checked once, at the end
+            _check(L.tmvn_cp_theta(h, t, _ptr(gx), _ptr(ma), _ptr(cnt), _ptr(all_live_it), _ptr(all_n_it), W,
+                                   self.cap, _ptr(flags)), h)
             self.coll.all_reduce(flags, "max")
             _check(L.tmvn_cp_commit(h, t, _ptr(flags)), h)
+        if int(maxn) > self.cap:
+            raise RuntimeError(f"constraint-parallel: more than cap={self.cap} live arcs of one chain on one rank "
+                               "in some iteration (arcs were dropped); raise cap")
         out = torch.empty((C, d), dtype=torch.float64, device=dev)
         _check(L.tmvn_cp_end(h, n_iter, _ptr(out)), h)
         torch.cuda.synchronize()

@@ -67,3 +67,24 @@ def test_cp_two_ranks_bitwise_equal_one_rank():
     assert np.array_equal(out1, out2)
     sm, sq, n = cp.moments()
     assert np.array_equal(np.concatenate([sm, sq, [n, cp.stats()["rejections"]]]), mom2)
+
+
+def test_cp_resume_and_trim():
+    """A call split at a multiple of recompute_every resumes bitwise (iter_offset
+    auto-advances); the trim epsilon (C7) follows the oracle step."""
+    A, b, x0 = synth.make_instance(3, m=200, d=40)
+    X0 = np.tile(x0, (7, 1))
+    full = tm.ConstraintParallel(A, b).sample(X0, 64, seed=9).cpu().numpy()
+    cp = tm.ConstraintParallel(A, b)
+    a = cp.sample(X0, 32, seed=9)
+    a = cp.sample(a, 32, seed=9).cpu().numpy()
+    assert np.array_equal(a, full)
+    eps = 1e-3
+    ct = tm.ConstraintParallel(A, b, trim_eps=eps, record=0)
+    X = X0.copy()
+    for t in range(4):
+        Xn = ct.sample(X, 1, seed=9).cpu().numpy()
+        for c in range(7):
+            xn, _ = oracle.step(A, b, X[c], 9, t, c, eps=eps)
+            assert np.max(np.abs(Xn[c] - xn)) <= 1e-10 * max(1.0, np.max(np.abs(xn)))
+        X = Xn

@@ -14,7 +14,7 @@
 //              (C7), theta by the inverse CDF (C10); P' = P cos + Q sin for the rank's
 //              rows and the safeguard (C8)   -> all-reduce (max)
 //   cp_commit  accept iff no rank saw a violation: x <- x cos + nu sin (every rank, the
-//              same), P_r <- P'_r, moments; else stay (C8)
+//              same), P_r <- P'_r (a per-chain buffer flip, no copy), moments; else stay (C8)
 //
 // The union of the infeasible arcs is associative (Prop. 1), so the merged tables and
 // the gathered live arcs give every rank the same I_act as one GPU holding all m rows;
@@ -38,10 +38,12 @@ __device__ __forceinline__ int cbucket(double a, double scale) {
   return k < kCNB - 1 ? k : kCNB - 1;
 }
 
-__global__ void __launch_bounds__(kCT) cp_stats_kernel(const double* __restrict__ P, const double* __restrict__ Q,
-                                                       int64_t ldp, const double* __restrict__ b, int m,
+__global__ void __launch_bounds__(kCT) cp_stats_kernel(const double* __restrict__ P0, const double* __restrict__ P1,
+                                                       const unsigned char* __restrict__ cur,
+                                                       const double* __restrict__ Q, int64_t ldp,
+                                                       const double* __restrict__ b, int m,
                                                        uint64_t* __restrict__ gx, uint64_t* __restrict__ ma,
-                                                       int* __restrict__ cnt) {
+                                                       int* __restrict__ cnt, double2* __restrict__ arcs) {
   __shared__ uint64_t sG[kCNB], sA[kCNB];
   __shared__ int sC[kCNB];
   const int c = blockIdx.x, tid = threadIdx.x;
@@ -52,8 +54,10 @@ __global__ void __launch_bounds__(kCT) cp_stats_kernel(const double* __restrict_
     sC[k] = 0;
   }
   __syncthreads();
-  const double* Pc = P + (int64_t)c * ldp;
+  const double* Pc = (cur[c] ? P1 : P0) + (int64_t)c * ldp;  // this chain's current P buffer
   const double* Qc = Q + (int64_t)c * ldp;
+  double2* Ac = arcs + (int64_t)c * ldp;  // the row's arc, (-1, -1) when inactive: read by
+                                          // the low-word pass and by cp_live (no recompute)
   for (int i = tid; i < m; i += kCT) {
     double al, be;
     if (arc_of(Pc[i], Qc[i], __ldg(b + i), al, be)) {
@@ -61,15 +65,18 @@ __global__ void __launch_bounds__(kCT) cp_stats_kernel(const double* __restrict_
       atomicMax(reinterpret_cast<uint32_t*>(&sG[k]) + 1, (uint32_t)(cbits(be) >> 32));
       atomicMax(reinterpret_cast<uint32_t*>(&sA[k]) + 1, (uint32_t)(cbits(al) >> 32));
       atomicAdd(&sC[k], 1);
+      Ac[i] = make_double2(al, be);
+    } else {
+      Ac[i] = make_double2(-1.0, -1.0);
     }
   }
   __syncthreads();
-  for (int i = tid; i < m; i += kCT) {  // exact max beta: the low words (same arcs, recomputed)
-    double al, be;
-    if (arc_of(Pc[i], Qc[i], __ldg(b + i), al, be)) {
-      const int k = cbucket(al, scale);
-      if ((uint32_t)(cbits(be) >> 32) == (uint32_t)(sG[k] >> 32))
-        atomicMax(reinterpret_cast<uint32_t*>(&sG[k]), (uint32_t)cbits(be));
+  for (int i = tid; i < m; i += kCT) {  // exact max beta: the low words
+    const double2 ab = Ac[i];
+    if (ab.x >= 0.0) {
+      const int k = cbucket(ab.x, scale);
+      if ((uint32_t)(cbits(ab.y) >> 32) == (uint32_t)(sG[k] >> 32))
+        atomicMax(reinterpret_cast<uint32_t*>(&sG[k]), (uint32_t)cbits(ab.y));
     }
   }
   __syncthreads();
@@ -108,8 +115,7 @@ __device__ void cp_gamma(const uint64_t* gx, const uint64_t* ma, const int* cnt,
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kCT) cp_live_kernel(const double* __restrict__ P, const double* __restrict__ Q,
-                                                      int64_t ldp, const double* __restrict__ b, int m,
+__global__ void __launch_bounds__(kCT) cp_live_kernel(const double2* __restrict__ arcs, int64_t ldp, int m,
                                                       const uint64_t* __restrict__ gx, const uint64_t* __restrict__ ma,
                                                       const int* __restrict__ cnt, int cap,
                                                       double2* __restrict__ live_out, int* __restrict__ nlive) {
@@ -119,11 +125,11 @@ __global__ void __launch_bounds__(kCT) cp_live_kernel(const double* __restrict__
   const double scale = __ddiv_rn((double)kCNB, kTwoPi);
   if (tid == 0) count = 0;
   cp_gamma(gx + (int64_t)c * kCNB, ma + (int64_t)c * kCNB, cnt + (int64_t)c * kCNB, gin, live, &gtot, wscr);
-  const double* Pc = P + (int64_t)c * ldp;
-  const double* Qc = Q + (int64_t)c * ldp;
+  const double2* Ac = arcs + (int64_t)c * ldp;
   for (int i = tid; i < m; i += kCT) {
-    double al, be;
-    if (arc_of(Pc[i], Qc[i], __ldg(b + i), al, be)) {
+    const double2 ab = Ac[i];
+    const double al = ab.x, be = ab.y;
+    if (al >= 0.0) {
       const int k = cbucket(al, scale);
       // beta <= gamma in: inside the earlier arc that set gamma in (it starts before the
       // bucket): changes neither the union nor any later gamma
@@ -193,9 +199,9 @@ __device__ void cp_sample(double2* gaps, int ngap, double u, double eps, double*
 __global__ void __launch_bounds__(kCT) cp_theta_kernel(
     const uint64_t* __restrict__ gx, const uint64_t* __restrict__ ma, const int* __restrict__ cnt,
     const double2* __restrict__ all_live, const int* __restrict__ all_n, int world, int cap, uint64_t seed,
-    uint32_t t, uint32_t chain_offset, double eps, const double* __restrict__ P, const double* __restrict__ Q,
-    int64_t ldp, const double* __restrict__ b, int m, double* __restrict__ Pn, int* __restrict__ flags,
-    double* __restrict__ theta_out, double* __restrict__ L_out) {
+    uint32_t t, uint32_t chain_offset, double eps, double* __restrict__ P0, double* __restrict__ P1,
+    const unsigned char* __restrict__ cur, const double* __restrict__ Q, int64_t ldp, const double* __restrict__ b,
+    int m, int* __restrict__ flags, double* __restrict__ theta_out, double* __restrict__ L_out) {
   extern __shared__ __align__(16) unsigned char csm[];
   __shared__ uint64_t gin[kCNB], wscr[8], gtot;
   __shared__ int live[kCNB], ncand, total_s, viol_s;
@@ -273,9 +279,9 @@ __global__ void __launch_bounds__(kCT) cp_theta_kernel(
   double sn = 0.0, cs = 1.0;
   if (L > 0.0) sincos(th_s, &sn, &cs);
   int viol = 0;
-  const double* Pc = P + (int64_t)c * ldp;
+  const double* Pc = (cur[c] ? P1 : P0) + (int64_t)c * ldp;  // this chain's P, and P' in the other
   const double* Qc = Q + (int64_t)c * ldp;
-  double* Pnc = Pn + (int64_t)c * ldp;
+  double* Pnc = (cur[c] ? P0 : P1) + (int64_t)c * ldp;
   if (L > 0.0) {
     for (int i = tid; i < m; i += kCT) {
       const double pn = Pc[i] * cs + Qc[i] * sn;
@@ -290,9 +296,9 @@ __global__ void __launch_bounds__(kCT) cp_theta_kernel(
 __global__ void __launch_bounds__(kCT) cp_commit_kernel(const int* __restrict__ flags, const double* __restrict__ theta,
                                                         const double* __restrict__ Lv, double* __restrict__ X,
                                                         const double* __restrict__ N, int64_t d_pad, int d,
-                                                        double* __restrict__ P, const double* __restrict__ Pn,
-                                                        int64_t ldp, int m, int record, double* __restrict__ S1,
-                                                        double* __restrict__ S2, int64_t* __restrict__ rej) {
+                                                        unsigned char* __restrict__ cur, int record,
+                                                        double* __restrict__ S1, double* __restrict__ S2,
+                                                        int64_t* __restrict__ rej) {
   const int c = blockIdx.x, tid = threadIdx.x;
   const double L = Lv[c];
   const bool accept = L > 0.0 && flags[c] == 0;
@@ -310,24 +316,23 @@ __global__ void __launch_bounds__(kCT) cp_commit_kernel(const int* __restrict__ 
       S2[o] += xv * xv;
     }
   }
-  if (accept) {
-    for (int i = tid; i < m; i += kCT) P[(int64_t)c * ldp + i] = Pn[(int64_t)c * ldp + i];
-  } else if (tid == 0) {
-    rej[c] += 1;
+  if (tid == 0) {
+    if (accept) cur[c] ^= 1;  // P' becomes P: no copy
+    else rej[c] += 1;
   }
 }
 
 }  // namespace
 
-cudaError_t launch_cp_stats(const double* P, const double* Q, int64_t ldp, const double* b, int m, int C,
-                            uint64_t* gx, uint64_t* ma, int* cnt, cudaStream_t st) {
-  cp_stats_kernel<<<C, kCT, 0, st>>>(P, Q, ldp, b, m, gx, ma, cnt);
+cudaError_t launch_cp_stats(const double* P0, const double* P1, const unsigned char* cur, const double* Q, int64_t ldp,
+                            const double* b, int m, int C, uint64_t* gx, uint64_t* ma, int* cnt, double2* arcs,
+                            cudaStream_t st) {
+  cp_stats_kernel<<<C, kCT, 0, st>>>(P0, P1, cur, Q, ldp, b, m, gx, ma, cnt, arcs);
   return cudaGetLastError();
 }
-cudaError_t launch_cp_live(const double* P, const double* Q, int64_t ldp, const double* b, int m, int C,
-                           const uint64_t* gx, const uint64_t* ma, const int* cnt, int cap, double2* live,
-                           int* nlive, cudaStream_t st) {
-  cp_live_kernel<<<C, kCT, 0, st>>>(P, Q, ldp, b, m, gx, ma, cnt, cap, live, nlive);
+cudaError_t launch_cp_live(const double2* arcs, int64_t ldp, int m, int C, const uint64_t* gx, const uint64_t* ma,
+                           const int* cnt, int cap, double2* live, int* nlive, cudaStream_t st) {
+  cp_live_kernel<<<C, kCT, 0, st>>>(arcs, ldp, m, gx, ma, cnt, cap, live, nlive);
   return cudaGetLastError();
 }
 size_t cp_theta_smem(int world, int cap) {
@@ -336,19 +341,20 @@ size_t cp_theta_smem(int world, int cap) {
 }
 cudaError_t launch_cp_theta(const uint64_t* gx, const uint64_t* ma, const int* cnt, const double2* all_live,
                             const int* all_n, int world, int cap, uint64_t seed, uint32_t t, uint32_t chain_offset,
-                            double eps, const double* P, const double* Q, int64_t ldp, const double* b, int m,
-                            int C, double* Pn, int* flags, double* theta, double* L, cudaStream_t st) {
+                            double eps, double* P0, double* P1, const unsigned char* cur, const double* Q,
+                            int64_t ldp, const double* b, int m, int C, int* flags, double* theta, double* L,
+                            cudaStream_t st) {
   const size_t smem = cp_theta_smem(world, cap);
   cudaError_t e = cudaFuncSetAttribute(cp_theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  cp_theta_kernel<<<C, kCT, smem, st>>>(gx, ma, cnt, all_live, all_n, world, cap, seed, t, chain_offset, eps, P, Q,
-                                        ldp, b, m, Pn, flags, theta, L);
+  cp_theta_kernel<<<C, kCT, smem, st>>>(gx, ma, cnt, all_live, all_n, world, cap, seed, t, chain_offset, eps, P0, P1,
+                                        cur, Q, ldp, b, m, flags, theta, L);
   return cudaGetLastError();
 }
 cudaError_t launch_cp_commit(const int* flags, const double* theta, const double* L, double* X, const double* N,
-                             int64_t d_pad, int d, double* P, const double* Pn, int64_t ldp, int m, int C,
-                             int record, double* S1, double* S2, int64_t* rej, cudaStream_t st) {
-  cp_commit_kernel<<<C, kCT, 0, st>>>(flags, theta, L, X, N, d_pad, d, P, Pn, ldp, m, record, S1, S2, rej);
+                             int64_t d_pad, int d, unsigned char* cur, int C, int record, double* S1, double* S2,
+                             int64_t* rej, cudaStream_t st) {
+  cp_commit_kernel<<<C, kCT, 0, st>>>(flags, theta, L, X, N, d_pad, d, cur, record, S1, S2, rej);
   return cudaGetLastError();
 }
 

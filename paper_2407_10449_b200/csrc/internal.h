@@ -59,18 +59,19 @@ struct LatParams {
 };
 // constraint-parallel iterations (cp.cu)
 constexpr int kCpBuckets = 128;
-cudaError_t launch_cp_stats(const double* P, const double* Q, int64_t ldp, const double* b, int m, int C,
-                            uint64_t* gx, uint64_t* ma, int* cnt, cudaStream_t st);
-cudaError_t launch_cp_live(const double* P, const double* Q, int64_t ldp, const double* b, int m, int C,
-                           const uint64_t* gx, const uint64_t* ma, const int* cnt, int cap, double2* live,
-                           int* nlive, cudaStream_t st);
+cudaError_t launch_cp_stats(const double* P0, const double* P1, const unsigned char* cur, const double* Q, int64_t ldp,
+                            const double* b, int m, int C, uint64_t* gx, uint64_t* ma, int* cnt, double2* arcs,
+                            cudaStream_t st);
+cudaError_t launch_cp_live(const double2* arcs, int64_t ldp, int m, int C, const uint64_t* gx, const uint64_t* ma,
+                           const int* cnt, int cap, double2* live, int* nlive, cudaStream_t st);
 cudaError_t launch_cp_theta(const uint64_t* gx, const uint64_t* ma, const int* cnt, const double2* all_live,
                             const int* all_n, int world, int cap, uint64_t seed, uint32_t t, uint32_t chain_offset,
-                            double eps, const double* P, const double* Q, int64_t ldp, const double* b, int m,
-                            int C, double* Pn, int* flags, double* theta, double* L, cudaStream_t st);
+                            double eps, double* P0, double* P1, const unsigned char* cur, const double* Q,
+                            int64_t ldp, const double* b, int m, int C, int* flags, double* theta, double* L,
+                            cudaStream_t st);
 cudaError_t launch_cp_commit(const int* flags, const double* theta, const double* L, double* X, const double* N,
-                             int64_t d_pad, int d, double* P, const double* Pn, int64_t ldp, int m, int C,
-                             int record, double* S1, double* S2, int64_t* rej, cudaStream_t st);
+                             int64_t d_pad, int d, unsigned char* cur, int C, int record, double* S1, double* S2,
+                             int64_t* rej, cudaStream_t st);
 size_t latency_smem_bytes(int64_t d_pad, int m, int cs, int cap);
 int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max);
 int latency_cluster_size(int C, int64_t m, int64_t d_pad, size_t smem_max, bool fp32, int* cap_out);

@@ -77,6 +77,9 @@ struct tmvn_ctx {
   uint64_t cp_seed = 0;
   int64_t cp_nrec = 0;
   double* cp_tl = nullptr;  // 2 C_pad: theta, L per chain
+  double2* cp_arcs = nullptr;  // C_pad x m_pad: this iteration's arcs ((-1, -1): inactive)
+  unsigned char* cp_cur = nullptr;  // C_pad: which of P0 / P1 holds each chain's P
+  int64_t cp_rows = 0;              // chains the scratch above is sized for
   int64_t lat_memo_C = -1;  // latency_cluster_size's answer for this C (m, d fixed per handle)
   int lat_memo_fp32 = -1, lat_memo_cs = 0, lat_memo_cap = 0;
   int64_t* dsum = nullptr;
@@ -1261,7 +1264,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->dyn);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
-  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->cp_tl); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
+  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->cp_tl); dfree(h->cp_arcs); dfree(h->cp_cur); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
   if (h->pin) cudaFreeHost(h->pin);
@@ -1566,9 +1569,20 @@ tmvn_status tmvn_cp_begin(tmvn_handle h, const double* X0, int64_t C, int64_t n_
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
   if ((s = start_check(h, C, h->P0)) != TMVN_OK) return s;  // this rank's rows
   if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
-  dfree(h->cp_tl);
-  h->cp_tl = nullptr;
-  CK(h, dalloc(&h->cp_tl, (size_t)2 * h->C_pad));
+  if (h->cp_rows < h->C_pad) {  // scratch kept across calls (re-allocated only to grow)
+    dfree(h->cp_tl);
+    dfree(h->cp_arcs);
+    dfree(h->cp_cur);
+    h->cp_tl = nullptr;
+    h->cp_arcs = nullptr;
+    h->cp_cur = nullptr;
+    h->cp_rows = 0;
+    CK(h, dalloc(&h->cp_tl, (size_t)2 * h->C_pad));
+    CK(h, dalloc(&h->cp_arcs, (size_t)h->C_pad * h->m_pad));
+    CK(h, dalloc(&h->cp_cur, (size_t)h->C_pad));
+    h->cp_rows = h->C_pad;
+  }
+  CK(h, cudaMemsetAsync(h->cp_cur, 0, (size_t)h->C_pad, stream_of(h)));  // P in P0 (start check)
   h->cp_C = C;
   h->cp_seed = seed;
   h->cp_t0 = h->opt.iter_offset;
@@ -1582,14 +1596,15 @@ tmvn_status tmvn_cp_stats(tmvn_handle h, int64_t t, uint64_t* gx, uint64_t* ma, 
   const int64_t C = h->cp_C;
   KL(h, launch_first_nu(h, C, h->cp_seed, (uint32_t)t, st));  // nu_t (+ digits), every rank alike
   KL(h, launch_projection(h, 0, round_up(C, kTileR), st));    // Q_r = nu A_r^T
-  KL(h, launch_cp_stats(h->P0, h->Q, h->m_pad, h->b_eff, (int)h->m, (int)C, gx, ma, cnt, st));
+  KL(h, launch_cp_stats(h->P0, h->P1, h->cp_cur, h->Q, h->m_pad, h->b_eff, (int)h->m, (int)C, gx, ma, cnt,
+                        h->cp_arcs, st));
   return TMVN_OK;
 }
 
 tmvn_status tmvn_cp_live(tmvn_handle h, const uint64_t* gx, const uint64_t* ma, const int32_t* cnt, int32_t cap,
                          double* live, int32_t* nlive) {
   if (!h || !h->cp_C || !live || !nlive || cap < 1) return fail(h, TMVN_E_ARG, "tmvn_cp_live: bad arguments");
-  KL(h, launch_cp_live(h->P0, h->Q, h->m_pad, h->b_eff, (int)h->m, (int)h->cp_C, gx, ma, cnt, cap,
+  KL(h, launch_cp_live(h->cp_arcs, h->m_pad, (int)h->m, (int)h->cp_C, gx, ma, cnt, cap,
                        reinterpret_cast<double2*>(live), nlive, stream_of(h)));
   return TMVN_OK;
 }
@@ -1599,8 +1614,8 @@ tmvn_status tmvn_cp_theta(tmvn_handle h, int64_t t, const uint64_t* gx, const ui
   if (!h || !h->cp_C || !all_live || !all_n || !flags || world < 1 || cap < 1)
     return fail(h, TMVN_E_ARG, "tmvn_cp_theta: bad arguments");
   KL(h, launch_cp_theta(gx, ma, cnt, reinterpret_cast<const double2*>(all_live), all_n, world, cap, h->cp_seed,
-                        (uint32_t)t, (uint32_t)h->opt.chain_offset, h->opt.trim_eps, h->P0, h->Q, h->m_pad,
-                        h->b_eff, (int)h->m, (int)h->cp_C, h->P1, flags, h->cp_tl, h->cp_tl + h->C_pad,
+                        (uint32_t)t, (uint32_t)h->opt.chain_offset, h->opt.trim_eps, h->P0, h->P1, h->cp_cur,
+                        h->Q, h->m_pad, h->b_eff, (int)h->m, (int)h->cp_C, flags, h->cp_tl, h->cp_tl + h->C_pad,
                         stream_of(h)));
   return TMVN_OK;
 }
@@ -1610,10 +1625,13 @@ tmvn_status tmvn_cp_commit(tmvn_handle h, int64_t t, const int32_t* flags) {
   cudaStream_t st = stream_of(h);
   const bool rec = recorded_iter(h->opt, t);
   h->cp_nrec += rec ? 1 : 0;
-  KL(h, launch_cp_commit(flags, h->cp_tl, h->cp_tl + h->C_pad, h->X, h->N, h->d_pad, (int)h->d, h->P0, h->P1,
-                         h->m_pad, (int)h->m, (int)h->cp_C, rec ? 1 : 0, h->S1, h->S2, h->rej, st));
+  KL(h, launch_cp_commit(flags, h->cp_tl, h->cp_tl + h->C_pad, h->X, h->N, h->d_pad, (int)h->d, h->cp_cur,
+                         (int)h->cp_C, rec ? 1 : 0, h->S1, h->S2, h->rej, st));
   const int64_t K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
-  if ((t + 1) % K == 0) KL(h, launch_refresh(h, 0, h->cp_C, h->P0, st));  // C13
+  if ((t + 1) % K == 0) {  // C13: fresh P = X A_r^T into P0 for every chain
+    KL(h, launch_refresh(h, 0, h->cp_C, h->P0, st));
+    CK(h, cudaMemsetAsync(h->cp_cur, 0, (size_t)h->C_pad, st));
+  }
   return TMVN_OK;
 }
 

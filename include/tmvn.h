@@ -313,6 +313,9 @@ tmvn_status tmvn_test_ozaki_gemm(const double* X, int64_t R, const double* W, in
 /* Latency mode's live-arc capacity per chain and iteration: cap > 0 lowers it
  * (to exercise the overflow fallback), 0 restores the automatic choice. */
 tmvn_status tmvn_test_latency_cap(tmvn_handle h, int32_t cap);
+/* Latency mode's grid variant (a cooperative grid of SMs / C CTAs per chain instead
+ * of a cluster): mode 1 forces it whenever it fits, -1 never, 0 automatic. */
+tmvn_status tmvn_test_latency_grid(tmvn_handle h, int32_t mode);
 /* The production FP64 GEMM: out[R x S] = X[R x K] . W[S x K]^T (all row-major). */
 tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
                            double* out);

@@ -31,7 +31,7 @@ EXPORTS = ["tmvn_default_options", "tmvn_create", "tmvn_set_affine", "tmvn_set_o
            "tmvn_reset_stats", "tmvn_get_profile", "tmvn_last_error", "tmvn_version",
            "tmvn_destroy", "tmvn_test_philox", "tmvn_test_curand_philox", "tmvn_test_normals", "tmvn_test_arcs",
            "tmvn_test_intervals", "tmvn_test_gemm", "tmvn_test_ozaki_gemm", "tmvn_test_step",
-           "tmvn_test_trace", "tmvn_test_latency_cap", "tmvn_cp_begin", "tmvn_cp_stats", "tmvn_cp_live",
+           "tmvn_test_trace", "tmvn_test_latency_cap", "tmvn_test_latency_grid", "tmvn_cp_begin", "tmvn_cp_stats", "tmvn_cp_live",
            "tmvn_cp_theta", "tmvn_cp_commit", "tmvn_cp_end"]
 
 
@@ -113,6 +113,7 @@ def lib():
             "tmvn_test_step": [H, P, i64, u64, i64, P],
             "tmvn_test_trace": [H, P, i64, i64, u64, P, i64, P, P],
             "tmvn_test_latency_cap": [H, ctypes.c_int32],
+            "tmvn_test_latency_grid": [H, ctypes.c_int32],
             "tmvn_cp_begin": [H, P, i64, i64, u64],
             "tmvn_cp_stats": [H, i64, P, P, P],
             "tmvn_cp_live": [H, P, P, P, ctypes.c_int32, P, P],
@@ -287,6 +288,10 @@ class Sampler:
     def test_latency_cap(self, cap):
         """Test hook: cap latency mode's live-arc capacity (0 = automatic)."""
         _check(lib().tmvn_test_latency_cap(self.h, int(cap)), self.h)
+
+    def test_latency_grid(self, mode):
+        """Test hook: latency mode's cooperative-grid variant (1 force, -1 never, 0 auto)."""
+        _check(lib().tmvn_test_latency_grid(self.h, int(mode)), self.h)
 
     def close(self):
         if getattr(self, "h", None):

@@ -56,6 +56,18 @@ struct LatParams {
   int fp32;          // options.precision = 1: FP32 arithmetic (A32, b32), else FP64 (A, b)
   const float* A32;  // m x d_pad, zero-padded rows
   const float* b32;  // m
+  // grid mode (gsz > 0: gsz CTAs of a cooperative grid per chain, no clusters): global
+  // exchange scratch, zeroed by the host before the launch where noted
+  int gsz;
+  uint64_t *gtab_g, *gtab_a;  // C x gsz x 128 bucket tables
+  int* gtab_c;
+  uint64_t *gmrg_g, *gmrg_a;  // C x 128 merged tables
+  int* gmrg_c;
+  double2* glive;             // C x cap live arcs
+  int* gcount;                // C x 2 (iteration parity; zeroed)
+  double* gth;                // C x 2: theta, L
+  int* gviol;                 // C x 2 (parity; zeroed)
+  int* gstart;                // C (zeroed)
 };
 // constraint-parallel iterations (cp.cu)
 constexpr int kCpBuckets = 128;

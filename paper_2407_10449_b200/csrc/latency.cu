@@ -291,11 +291,20 @@ __device__ unsigned long long g_lat_cycles[16];
   } while (0)
 #endif
 
-template <typename T>
+// kGrid: the chain's CTAs are p.gsz CTAs of a cooperative grid instead of a thread-block
+// cluster (more SMs per chain than a cluster's 16 when there are few chains and a large
+// A): the exchanges go through global scratch instead of distributed shared memory and
+// the barriers are grid barriers (one more, to merge the bucket tables bucket-parallel)
+template <typename T, bool kGrid>
 __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   cg::cluster_group cluster = cg::this_cluster();
-  const int CS = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
+  cg::grid_group grid = cg::this_grid();
+  const int CS = kGrid ? p.gsz : (int)cluster.num_blocks();
+  const int rank = kGrid ? (int)(blockIdx.x % p.gsz) : (int)cluster.block_rank();
+  auto csync = [&]() {
+    if constexpr (kGrid) grid.sync();
+    else cluster.sync();
+  };
   const int chain = (int)(blockIdx.x / CS);
   if (chain >= p.C) return;  // whole clusters only: uniform across the cluster
   const uint32_t gchain = p.chain_offset + (uint32_t)chain;
@@ -307,11 +316,11 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   LatShared S;
   const int nk = lat_nk(p.d_pad, CS);
   lat_carve(lsm, p.d_pad, mr, nk, p.cap, S);
-  // CTA 0's buffers and flags, seen from every CTA of the cluster
-  int* r_ints0 = cluster.map_shared_rank(S.ints, 0);
-  uint64_t* r_lkey0 = cluster.map_shared_rank(S.lkey, 0);
-  double* r_lval0 = cluster.map_shared_rank(S.lval, 0);
-  double* r_dbl0 = cluster.map_shared_rank(S.dbl, 0);
+  // CTA 0's buffers and flags, seen from every CTA of the cluster (grid: global scratch)
+  int* r_ints0 = kGrid ? nullptr : cluster.map_shared_rank(S.ints, 0);
+  uint64_t* r_lkey0 = kGrid ? nullptr : cluster.map_shared_rank(S.lkey, 0);
+  double* r_lval0 = kGrid ? nullptr : cluster.map_shared_rank(S.lval, 0);
+  double* r_dbl0 = kGrid ? p.gth + 2 * chain : cluster.map_shared_rank(S.dbl, 0);
   const double scale = __ddiv_rn((double)kLNB, kTwoPi);
   // the arithmetic type's views (x, nu, P, Q live in FP64-sized slots either way)
   const T* A = static_cast<const T*>(sizeof(T) == 8 ? (const void*)p.A : (const void*)p.A32);
@@ -346,11 +355,16 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     }
     bad = __syncthreads_or(bad);
     if (tid == 0) S.ints[6] = bad;
+    if (kGrid && tid == 0 && bad) atomicOr(p.gstart + chain, 1);
   }
   int64_t rej = 0;
-  cluster.sync();
-  const int n_iter = (p.startflag && __syncthreads_or(tid < CS ? *cluster.map_shared_rank(S.ints + 6, tid) : 0))
-                         ? 0 : p.n_iter;
+  csync();
+  int start_bad = 0;
+  if (p.startflag) {
+    if constexpr (kGrid) start_bad = *(volatile int*)(p.gstart + chain);
+    else start_bad = __syncthreads_or(tid < CS ? *cluster.map_shared_rank(S.ints + 6, tid) : 0);
+  }
+  const int n_iter = start_bad ? 0 : p.n_iter;
 #ifdef TMVN_PHASE_TIMING
   long long lph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long lt_prev = clock64();
@@ -398,7 +412,61 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
         atomicMax(reinterpret_cast<uint32_t*>(&S.Gx[k]), (uint32_t)lbits(ab.y));
     }
     LPH(2);
-    cluster.sync();  // #1: every CTA's bucket table is complete
+    const int par = it & 1;
+    if constexpr (kGrid) {  // this CTA's table to global scratch (after the low-word pass)
+      __syncthreads();
+      for (int k = tid; k < kLNB; k += kLT) {
+        const int64_t o = ((int64_t)chain * CS + rank) * kLNB + k;
+        p.gtab_g[o] = S.Gx[k];
+        p.gtab_a[o] = S.mA[k];
+        p.gtab_c[o] = S.cnt[k];
+      }
+    }
+    csync();  // #1: every CTA's bucket table is complete
+    if constexpr (kGrid) {
+      // bucket-parallel merge: CTA r reduces buckets r, r + CS, ... over the CS tables
+      uint64_t* red = reinterpret_cast<uint64_t*>(S.cand);  // scratch (16 words per warp)
+      for (int k = rank; k < kLNB; k += CS) {
+        uint64_t g = 0, a = 0;
+        int c = 0;
+        for (int r = tid; r < CS; r += kLT) {
+          const int64_t o = ((int64_t)chain * CS + r) * kLNB + k;
+          const uint64_t gv = __ldcg(p.gtab_g + o), av = __ldcg(p.gtab_a + o);  // other SMs' writes: L2
+          g = g > gv ? g : gv;
+          a = a > av ? a : av;
+          c += __ldcg(p.gtab_c + o);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t g2 = __shfl_xor_sync(0xffffffffu, g, o), a2 = __shfl_xor_sync(0xffffffffu, a, o);
+          g = g > g2 ? g : g2;
+          a = a > a2 ? a : a2;
+          c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0) {
+          red[3 * warp] = g;
+          red[3 * warp + 1] = a;
+          red[3 * warp + 2] = (uint64_t)c;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          for (int w = 1; w < kLT / 32; ++w) {
+            g = g > red[3 * w] ? g : red[3 * w];
+            a = a > red[3 * w + 1] ? a : red[3 * w + 1];
+            c += (int)red[3 * w + 2];
+          }
+          p.gmrg_g[(int64_t)chain * kLNB + k] = g;
+          p.gmrg_a[(int64_t)chain * kLNB + k] = a;
+          p.gmrg_c[(int64_t)chain * kLNB + k] = c;
+        }
+        __syncthreads();
+      }
+      if (rank == 0 && tid == 0) {  // the slots of iteration it + 1 (last read in it - 1)
+        p.gcount[2 * chain + (par ^ 1)] = 0;
+        p.gviol[2 * chain + (par ^ 1)] = 0;
+      }
+      csync();  // #1b: the merged table is complete
+    }
     LPH(3);
     // merge the CS tables (every CTA, redundantly): thread j < kLNB owns bucket j and
     // reads it from every CTA (independent DSMEM loads, in flight together); gamma
@@ -407,14 +475,20 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
       uint64_t g = 0, a = 0;
       int c = 0;
       if (tid < kLNB) {
+        if constexpr (kGrid) {
+          g = __ldcg(p.gmrg_g + (int64_t)chain * kLNB + tid);
+          a = __ldcg(p.gmrg_a + (int64_t)chain * kLNB + tid);
+          c = __ldcg(p.gmrg_c + (int64_t)chain * kLNB + tid);
+        } else {
 #pragma unroll 4
-        for (int r = 0; r < CS; ++r) {
-          const uint64_t gv = cluster.map_shared_rank(S.Gx, r)[tid];
-          const uint64_t av = cluster.map_shared_rank(S.mA, r)[tid];
-          const int cv = cluster.map_shared_rank(S.cnt, r)[tid];
-          g = g > gv ? g : gv;
-          a = a > av ? a : av;
-          c += cv;
+          for (int r = 0; r < CS; ++r) {
+            const uint64_t gv = cluster.map_shared_rank(S.Gx, r)[tid];
+            const uint64_t av = cluster.map_shared_rank(S.mA, r)[tid];
+            const int cv = cluster.map_shared_rank(S.cnt, r)[tid];
+            g = g > gv ? g : gv;
+            a = a > av ? a : av;
+            c += cv;
+          }
         }
       }
       uint64_t inc = g;
@@ -450,15 +524,32 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
       const double2 ab = S.st[s];
       const int k = lat_bucket(ab.x, scale);
       if (S.live[k] && lbits(ab.y) > S.gin[k]) {
-        const int pos = atomicAdd(r_ints0 + 1, 1);
-        if (pos < p.cap) {
-          r_lkey0[pos] = lbits(ab.x);
-          r_lval0[pos] = ab.y;
+        if constexpr (kGrid) {
+          const int pos = atomicAdd(p.gcount + 2 * chain + par, 1);
+          if (pos < p.cap) p.glive[(int64_t)chain * p.cap + pos] = ab;
+        } else {
+          const int pos = atomicAdd(r_ints0 + 1, 1);
+          if (pos < p.cap) {
+            r_lkey0[pos] = lbits(ab.x);
+            r_lval0[pos] = ab.y;
+          }
         }
       }
     }
     LPH(4);
-    cluster.sync();  // #2: the live arcs are in CTA 0
+    csync();  // #2: the live arcs are in CTA 0 (grid: in global scratch)
+    if constexpr (kGrid) {
+      if (rank == 0) {
+        const int total = *(volatile int*)(p.gcount + 2 * chain + par);
+        if (tid == 0) S.ints[1] = total;
+        for (int e = tid; e < total && e < p.cap; e += kLT) {
+          const double2 ab = __ldcg(p.glive + (int64_t)chain * p.cap + e);
+          S.lkey[e] = lbits(ab.x);
+          S.lval[e] = ab.y;
+        }
+        __syncthreads();
+      }
+    }
     LPH(5);
 #ifdef TMVN_PHASE_TIMING
     if (blockIdx.x == 0 && tid == 0) lph[11] += S.ints[1];
@@ -636,11 +727,16 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
         }
       }
       if (tid == 0) S.ints[1] = 0;  // the live buffer is free for the next iteration
+      if (kGrid && tid == 0) {
+        p.gth[2 * chain] = S.dbl[0];
+        p.gth[2 * chain + 1] = S.dbl[1];
+      }
     }
     LPH(6);
-    cluster.sync();  // #3: theta and L in CTA 0
+    csync();  // #3: theta and L in CTA 0
     LPH(7);
-    const double theta = r_dbl0[0], L = r_dbl0[1];
+    const double theta = kGrid ? *(volatile double*)(r_dbl0) : r_dbl0[0];
+    const double L = kGrid ? *(volatile double*)(r_dbl0 + 1) : r_dbl0[1];
     T sn = T(0), cs = T(1);
     if (L > 0.0) sincos((T)theta, &sn, &cs);
     int viol = 0;
@@ -653,10 +749,13 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     }
     viol = __syncthreads_or(viol);
     if (tid == 0) S.ints[2] = viol;
+    if (kGrid && tid == 0 && viol) atomicOr(p.gviol + 2 * chain + par, 1);
     LPH(8);
-    cluster.sync();  // #4: every CTA's safeguard verdict
+    csync();  // #4: every CTA's safeguard verdict
     LPH(9);
-    const int any = __syncthreads_or(tid < CS ? *cluster.map_shared_rank(S.ints + 2, tid) : 0);
+    int any;
+    if constexpr (kGrid) any = *(volatile int*)(p.gviol + 2 * chain + par);
+    else any = __syncthreads_or(tid < CS ? *cluster.map_shared_rank(S.ints + 2, tid) : 0);
     const bool accept = L > 0.0 && !any;
     if (accept) {
       T* tmp = Pc;
@@ -699,7 +798,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
       if (S.ints[4]) atomicExch(p.err, 1);
     }
   }
-  cluster.sync();  // no CTA leaves while another may still read its shared memory
+  if constexpr (!kGrid) cluster.sync();  // no CTA leaves while another may still read its shared memory
 }
 
 }  // namespace
@@ -736,9 +835,11 @@ int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max) {
 // clusters of cs CTAs (smem bytes each) that can be resident at once
 template <typename T>
 int latency_max_clusters_t(int cs, size_t smem) {
-  if (cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (cudaFuncSetAttribute(latency_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
     return 0;
-  if (cs > 8 && cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+  if (cs > 8 &&
+      cudaFuncSetAttribute(latency_kernel<T, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
     return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cs);
@@ -752,7 +853,7 @@ int latency_max_clusters_t(int cs, size_t smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, latency_kernel<T>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, latency_kernel<T, false>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -790,25 +891,33 @@ int latency_cluster_size(int C, int64_t m, int64_t d_pad, size_t smem_max, bool 
 template <typename T>
 cudaError_t launch_latency_t(const LatParams& p, int cs, cudaStream_t st) {
   const size_t smem = latency_smem_bytes(p.d_pad, p.m, cs, p.cap);
-  cudaError_t e = cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  if (cs > 8) {
-    e = cudaFuncSetAttribute(latency_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.C * cs));
   cfg.blockDim = dim3(kLT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (p.gsz > 0) {  // cooperative grid of C x gsz CTAs (all resident: one per SM)
+    cudaError_t e =
+        cudaFuncSetAttribute(latency_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    return cudaLaunchKernelEx(&cfg, latency_kernel<T, true>, p);
+  }
+  cudaError_t e = cudaFuncSetAttribute(latency_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8) {
+    e = cudaFuncSetAttribute(latency_kernel<T, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, latency_kernel<T>, p);
+  return cudaLaunchKernelEx(&cfg, latency_kernel<T, false>, p);
 }
 
 cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st) {

@@ -72,6 +72,9 @@ struct tmvn_ctx {
   double* Xsnap = nullptr;  // X before a latency-mode call (its overflow fallback)
   size_t Xsnap_n = 0;
   int lat_cap_max = 0;  // test hook: latency-mode live-arc capacity cap (0 = automatic)
+  int lat_grid_mode = 0;  // test hook: 0 automatic, 1 grid mode whenever it fits, -1 never
+  unsigned char* lat_gscratch = nullptr;  // grid-mode exchange scratch
+  size_t lat_gscratch_n = 0;
   // constraint-parallel iterations (tmvn_cp_*): chains, seed, first iteration, scratch
   int64_t cp_C = 0, cp_t0 = 0;
   uint64_t cp_seed = 0;
@@ -1050,7 +1053,7 @@ tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
 // affine change of variable, shared memory), else the throughput loop runs.
 // options.latency = 2 (auto) takes it when there are at most SMs / 2 chains (clusters of
 // two or more CTAs) and the cost model below expects it to be faster.
-bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
+bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_out) {
   const bool fp32 = h->opt.precision == 1;
   if (h->opt.latency == 0 || h->affine) return false;
   int dev = 0, sms = 0, smem_max = 0;
@@ -1070,27 +1073,46 @@ bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out) {
     h->lat_memo_cap = cap;
   }
   if (cs == 0 || cap == 0) return false;
+  // Cost model (S12, fitted to B200 measurements, tools/grid_probe.py): a CTA
+  // streams its rows of A (eb bytes per element) each iteration at ~100 GB/s when A is
+  // L2-resident, ~57 GB/s when it is not; besides, a cluster iteration costs ~12.8 us,
+  // a cooperative-grid one (SMs / C CTAs per chain, six grid barriers) ~20 + 0.9 C us;
+  // the default path ~50 us + 7.8 ps per element of A at few chains.
+  const double eb = fp32 ? 4.0 : 8.0;
+  const double abytes = eb * (double)h->m * (double)h->d_pad;
+  const double r_sm = abytes <= 80e6 ? 100e9 : 57e9;
+  auto q_time = [&](int n) { return (double)((h->m + n - 1) / n) * (double)h->d_pad * eb / r_sm; };
+  double t_lat = 12.8e-6 + q_time(cs);
+  int gsz = 0;
+  {
+    const int G = sms / (int)C;
+    const double t_grid = (20.0 + 0.9 * (double)C) * 1e-6 + q_time(G > 0 ? G : 1);
+    const bool better = t_grid < 0.9 * t_lat;
+    const bool want = h->lat_grid_mode == 1 || (h->lat_grid_mode == 0 && better);
+    if (want && G > cs && G >= 2) {
+      const int capg = latency_cap(h->d_pad, (int)h->m, G, (size_t)smem_max);
+      if (capg > 0) {
+        gsz = G;
+        cs = G;
+        cap = capg;
+        t_lat = t_grid;
+      }
+    }
+  }
   if (h->opt.latency == 2) {
-    // auto: a cost model fitted to B200 measurements (S12) -- the latency mode
-    // streams a CTA's rows of A (8 B per element) each iteration at ~120 GB/s per SM when
-    // A is L2-resident (~50 GB/s when it is not) plus ~12 us of per-iteration latency;
-    // the default path costs ~50 us + 7.8 ps per element of A at few chains
-    const double eb = fp32 ? 4.0 : 8.0;  // bytes per element of A
-    const double abytes = eb * (double)h->m * (double)h->d_pad;
-    const double r_sm = abytes <= 80e6 ? 120e9 : 50e9;
-    const double t_lat = 12e-6 + (double)((h->m + cs - 1) / cs) * (double)h->d_pad * eb / r_sm;
     const double t_def = 50e-6 + 7.8e-12 * (double)h->m * (double)h->d;
     if (t_lat >= t_def) return false;
   }
   if (h->lat_cap_max > 0 && cap > h->lat_cap_max) cap = h->lat_cap_max;
   *cs_out = cs;
   *cap_out = cap;
+  *gsz_out = gsz;
   return true;
 }
 
 // returns TMVN_OK with *overflow = true (nothing usable written) when some iteration had
 // more live arcs than the capacity: the caller restores X and runs the default path
-tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int cs, int cap,
+tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int cs, int cap, int gsz,
                         bool check_start, int64_t* n_recorded, bool* overflow) {
   cudaStream_t st = stream_of(h);
   if (!h->A_pad) {
@@ -1132,6 +1154,35 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
   p.S2 = h->S2;
   p.rej = h->rej;
   p.cap = cap;
+  p.gsz = gsz;
+  if (gsz > 0) {  // grid-mode exchange scratch (zeroed: counters, flags)
+    auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+    const size_t n_tab = (size_t)C * gsz * 128, n_mrg = (size_t)C * 128;
+    const size_t b_tg = al(n_tab * 8), b_tc = al(n_tab * 4), b_mg = al(n_mrg * 8), b_mc = al(n_mrg * 4);
+    const size_t b_live = al((size_t)C * cap * 16), b_small = al((size_t)C * 2 * 8);
+    const size_t total = 2 * b_tg + b_tc + 2 * b_mg + b_mc + b_live + 4 * b_small;
+    if (h->lat_gscratch_n < total) {
+      dfree(h->lat_gscratch);
+      h->lat_gscratch = nullptr;
+      h->lat_gscratch_n = 0;
+      CK(h, dalloc(&h->lat_gscratch, total));
+      h->lat_gscratch_n = total;
+    }
+    unsigned char* q = h->lat_gscratch;
+    p.gtab_g = reinterpret_cast<uint64_t*>(q); q += b_tg;
+    p.gtab_a = reinterpret_cast<uint64_t*>(q); q += b_tg;
+    p.gtab_c = reinterpret_cast<int*>(q); q += b_tc;
+    p.gmrg_g = reinterpret_cast<uint64_t*>(q); q += b_mg;
+    p.gmrg_a = reinterpret_cast<uint64_t*>(q); q += b_mg;
+    p.gmrg_c = reinterpret_cast<int*>(q); q += b_mc;
+    p.glive = reinterpret_cast<double2*>(q); q += b_live;
+    unsigned char* zero0 = q;
+    p.gcount = reinterpret_cast<int*>(q); q += b_small;
+    p.gviol = reinterpret_cast<int*>(q); q += b_small;
+    p.gstart = reinterpret_cast<int*>(q); q += b_small;
+    CK(h, cudaMemsetAsync(zero0, 0, (size_t)(q - zero0), stream_of(h)));
+    p.gth = reinterpret_cast<double*>(q); q += b_small;
+  }
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   p.err = h->dyn + 64 * 16 - 1;
   CK(h, cudaMemsetAsync(p.err, 0, sizeof(int), st));
@@ -1174,7 +1225,8 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
   int lcs = 0, lcap = 0;
-  const bool lat = n_iter > 0 && latency_fits(h, C, &lcs, &lcap);
+  int lgsz = 0;
+  const bool lat = n_iter > 0 && latency_fits(h, C, &lcs, &lcap, &lgsz);
   // the FP64 latency kernel checks the start on its own first P = A x0 (no GEMM here)
   const bool kernel_checks = lat && h->opt.precision == 0;
   if (!kernel_checks && (s = start_check(h, C, h->P0)) != TMVN_OK) return s;
@@ -1194,7 +1246,8 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
     cudaStream_t st = stream_of(h);
     CK(h, cudaMemcpyAsync(h->Xsnap, h->X, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
     bool overflow = false;
-    if ((s = run_latency(h, C, n_iter, seed, lcs, lcap, kernel_checks, &nrec, &overflow)) != TMVN_OK) return s;
+    if ((s = run_latency(h, C, n_iter, seed, lcs, lcap, lgsz, kernel_checks, &nrec, &overflow)) != TMVN_OK)
+      return s;
     done = !overflow;
     h->prof.latency_calls += 1;
     h->prof.latency_fallbacks += overflow ? 1 : 0;
@@ -1264,7 +1317,7 @@ void tmvn_destroy(tmvn_handle h) {
   dfree(h->dyn);
   free_chain_buffers(h);
   if (h->At != h->A_tiled) dfree(h->At);
-  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->cp_tl); dfree(h->cp_arcs); dfree(h->cp_cur); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
+  dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->lat_gscratch); dfree(h->cp_tl); dfree(h->cp_arcs); dfree(h->cp_cur); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
   dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
   if (h->pin) cudaFreeHost(h->pin);
@@ -1646,6 +1699,12 @@ tmvn_status tmvn_cp_end(tmvn_handle h, int64_t n_iter, double* out) {
   return TMVN_OK;
 }
 
+tmvn_status tmvn_test_latency_grid(tmvn_handle h, int32_t mode) {
+  if (!h || mode < -1 || mode > 1) return fail(h, TMVN_E_ARG, "latency grid mode must be -1, 0 or 1");
+  h->lat_grid_mode = mode;
+  h->lat_memo_C = -1;
+  return TMVN_OK;
+}
 tmvn_status tmvn_test_latency_cap(tmvn_handle h, int32_t cap) {
   if (!h || cap < 0) return fail(h, TMVN_E_ARG, "latency cap must be >= 0");
   h->lat_cap_max = cap;

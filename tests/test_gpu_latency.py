@@ -309,3 +309,30 @@ def test_latency_random_shapes_vs_oracle(case):
             xn, _ = oracle.step(A, b, X[c], case, t, c)
             assert np.max(np.abs(Xn[c] - xn)) <= REL * max(1.0, np.max(np.abs(xn))), (d, m, C, t, c)
         X = Xn
+
+
+@pytest.mark.parametrize("d,m,C,prec", [(60, 200, 1, 0), (150, 700, 3, 0), (1000, 1000, 1, 0), (300, 300, 2, 1)])
+def test_latency_grid_variant(d, m, C, prec):
+    """The cooperative-grid variant (SMs / C CTAs per chain, exchanges through global
+    scratch and grid barriers): oracle steps (FP64) and bitwise equality with the
+    cluster variant (each row's dot product has one fixed order in both)."""
+    A, b, x0 = synth.paper_random(d, seed=d + m) if d == m else synth.make_instance(3, m=m, d=d)
+    kw = dict(latency=1, record=0, precision=prec, trim_eps=1e-5 if prec else 0.0)
+    g = tm.Sampler(A, b, **kw)
+    g.test_latency_grid(1)
+    c = tm.Sampler(A, b, **kw)
+    c.test_latency_grid(-1)
+    X = np.tile(x0, (C, 1))
+    for t in range(5):
+        Xg = g.sample(X, 1, seed=17)
+        Xc = c.sample(X, 1, seed=17)
+        assert np.array_equal(Xg, Xc), t
+        if prec == 0:
+            for k in range(C):
+                xn, _ = oracle.step(A, b, X[k], 17, t, k)
+                assert np.max(np.abs(Xg[k] - xn)) <= REL * max(1.0, np.max(np.abs(xn)))
+        X = Xg
+    long_g = g.sample(X, 40, seed=17)
+    long_c = c.sample(X, 40, seed=17)
+    assert np.array_equal(long_g, long_c)
+    assert g.profile()["latency_calls"] == 6

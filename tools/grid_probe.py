@@ -11,8 +11,8 @@ for d in (1000, 2000, 4000):
     for C in (1, 2, 4, 10):
         for prec in (0, 1):
             res = []
-            for mode in (-1, 1):
-                s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"), latency=1,
+            for mode in (-1, 1, 0):
+                s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"), latency=1 if mode else 2,
                                precision=prec, trim_eps=1e-5 if prec else 0.0)
                 s.test_latency_grid(mode)
                 X = torch.tensor(np.tile(x0, (C, 1)), device="cuda")
@@ -21,4 +21,5 @@ for d in (1000, 2000, 4000):
                 s.sample(X, 200, 42, out=X)
                 torch.cuda.synchronize(); res.append((time.perf_counter() - t0) / 200 * 1e6)
                 s.close()
-            print(f"d=m={d} C={C} precision={prec}: cluster {res[0]:.1f} us/iter, grid {res[1]:.1f} us/iter", flush=True)
+            print(f"d=m={d} C={C} precision={prec}: cluster {res[0]:.1f} us/iter, grid {res[1]:.1f} us/iter, "
+                  f"auto {res[2]:.1f} us/iter", flush=True)

@@ -301,6 +301,8 @@ def test_latency_random_shapes_vs_oracle(case):
     b = rng.uniform(0.05, 2.0, m)
     x0 = np.zeros(d)
     s = tm.Sampler(A, b, latency=1, record=0)
+    if case % 3 == 0:
+        s.test_latency_grid(1)  # the cooperative-grid variant
     X = np.tile(x0, (C, 1))
     for t in range(4):
         Xn = s.sample(X, 1, seed=case)

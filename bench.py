@@ -257,14 +257,17 @@ def main():
             hbm, hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
         launch_ms = ms_iso / args.steps
         abytes = float(C) * ips * m * d * 8
-        roofline = {"bound": "hbm", "kernel": "latency_kernel (one cluster per chain: nu, A nu, arcs, "
+        variant = ("a cooperative grid of SMs / C CTAs per chain" if prof.get("latency_grid_calls", 0)
+                   else "one thread-block cluster per chain")
+        roofline = {"bound": "hbm", "kernel": f"latency_kernel ({variant}: nu, A nu, arcs, "
                                                "two-level Alg. 3 intervals, theta, P', safeguard, x update)",
                     "achieved": abytes / (launch_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                     "frac": abytes / (launch_ms * 1e-3) / 1e9 / hbm, "traffic": None, "traffic_source": None,
                     "peak_source": hbm_src + "; A (8 m d bytes per chain-iteration, the algorithmic bytes "
                                    "counted here) is served from L2, so this is a bandwidth-equivalent figure",
                     "algorithmic_bytes_per_launch": abytes, "avg_launch_ms": launch_ms, "share_of_step": 1.0,
-                    "latency_calls": prof["latency_calls"], "latency_fallbacks": prof["latency_fallbacks"]}
+                    "latency_calls": prof["latency_calls"], "latency_fallbacks": prof["latency_fallbacks"],
+                    "latency_grid_calls": prof.get("latency_grid_calls", 0)}
     else:
         peaks = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")))
         gemm_avg_ms = prof["gemm_ms"] / max(1, prof["gemm_launches"])

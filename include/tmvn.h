@@ -191,6 +191,7 @@ typedef struct {
   double tc_flops;       /* FP64-equivalent algorithmic flops of those launches: 2 C m d     */
   int64_t latency_calls;      /* tmvn_sample calls run in latency mode (options.latency)      */
   int64_t latency_fallbacks;  /* of those, calls rerun on the default path (live-arc overflow) */
+  int64_t latency_grid_calls; /* of those, calls run by the cooperative-grid variant          */
 } tmvn_profile;
 
 /* Fills *opt with the defaults listed above. */

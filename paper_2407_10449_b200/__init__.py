@@ -61,7 +61,7 @@ class profile(ctypes.Structure):
                 ("ess_bytes", ctypes.c_double), ("tc_launches", ctypes.c_int64),
                 ("tc_ms", ctypes.c_double), ("tc_ops", ctypes.c_double),
                 ("tc_flops", ctypes.c_double), ("latency_calls", ctypes.c_int64),
-                ("latency_fallbacks", ctypes.c_int64)]
+                ("latency_fallbacks", ctypes.c_int64), ("latency_grid_calls", ctypes.c_int64)]
 
 
 class stats(ctypes.Structure):

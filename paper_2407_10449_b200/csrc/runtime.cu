@@ -1250,6 +1250,7 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
       return s;
     done = !overflow;
     h->prof.latency_calls += 1;
+    h->prof.latency_grid_calls += lgsz > 0 ? 1 : 0;
     h->prof.latency_fallbacks += overflow ? 1 : 0;
     if (overflow) {
       CK(h, cudaMemcpyAsync(h->X, h->Xsnap, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));

@@ -43,6 +43,8 @@ CONFIGS = {
     # b = A x0 + U[0,1]^d, 10 chains
     6: Config("paper_s42", 1000, 1000, 10, 1000, 42, 106,
               "paper S4.2: d=m=1000, A iid N(0,1), x0 ~ N(0,I), b = A x0 + U[0,1]^d, 10 chains"),
+    7: Config("paper_s42_single", 4000, 4000, 1, 1000, 4000, 107,
+              "paper S4.2 single chain at the high end of Fig. 4 (P:839-842): d=m=4000, 1 chain"),
 }
 
 _B_RANGE = {1: (0.5, 1.5), 3: (0.1, 1.0), 4: (0.5, 2.0), 5: (0.2, 1.0)}
@@ -58,7 +60,7 @@ def make_instance(k: int, m: int | None = None, d: int | None = None):
     m = cfg.m if m is None else m
     d = cfg.d if d is None else d
     rng = np.random.default_rng(cfg.inst_seed)
-    if k == 6:
+    if k in (6, 7):
         return paper_random(d, seed=cfg.inst_seed)
     if k == 2:
         A = -np.eye(d, dtype=np.float64)[:m]

@@ -68,6 +68,7 @@ struct LatParams {
   double* gth;                // C x 2: theta, L
   int* gviol;                 // C x 2 (parity; zeroed)
   int* gstart;                // C (zeroed)
+  double* gnu;                // C x d_pad: nu_{t+1} drawn by CTA 1 for CTA 0 (T-typed)
 };
 // constraint-parallel iterations (cp.cu)
 constexpr int kCpBuckets = 128;

@@ -51,6 +51,7 @@ __device__ __forceinline__ double lbitsd(uint64_t b) { return __longlong_as_doub
 struct LatShared {
   double* x;       // d_pad
   double* nu;      // d_pad
+  double* nu2;     // d_pad: nu of the next iteration, drawn by CTAs 1.. while CTA 0 samples theta
   double* P0;      // mr each: current / proposal, swapped on accept
   double* P1;
   double* Q;       // mr
@@ -92,6 +93,7 @@ __host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, 
   };
   S.x = reinterpret_cast<double*>(take(d_pad * 8));
   S.nu = reinterpret_cast<double*>(take(d_pad * 8));
+  S.nu2 = reinterpret_cast<double*>(take(d_pad * 8));
   S.P0 = reinterpret_cast<double*>(take((size_t)mr * 8));
   S.P1 = reinterpret_cast<double*>(take((size_t)mr * 8));
   S.Q = reinterpret_cast<double*>(take((size_t)mr * 8));
@@ -326,7 +328,9 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   const T* A = static_cast<const T*>(sizeof(T) == 8 ? (const void*)p.A : (const void*)p.A32);
   const T* bv = static_cast<const T*>(sizeof(T) == 8 ? (const void*)p.b : (const void*)p.b32);
   T* Sx = reinterpret_cast<T*>(S.x);
-  T* Snu = reinterpret_cast<T*>(S.nu);
+  T* Snu = reinterpret_cast<T*>(S.nu);    // nu_t
+  T* SnuN = reinterpret_cast<T*>(S.nu2);  // nu_{t+1} (CTAs 1..CS-1 draw it during CTA 0's theta)
+  bool have_nu = false;                   // nu_t already drawn (by this CTA, or by CTA 1 for CTA 0)
   T* SQ = reinterpret_cast<T*>(S.Q);
 
   // x_{t0} (all d) and P = A x for this CTA's rows
@@ -372,11 +376,23 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
 
   for (int it = 0; it < n_iter; ++it) {
     const uint32_t t = p.t0 + (uint32_t)it;
-    // (a) nu_t, u_t
-    for (int pk = tid; pk < (int)(p.d_pad / 2); pk += kLT) {
-      const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
-      Snu[2 * pk] = (T)v.x;
-      Snu[2 * pk + 1] = (T)v.y;
+    // (a) nu_t, u_t: drawn here on the first iteration (and with one CTA per chain); else
+    // the CTAs 1.. drew it during the previous iteration's theta phase and CTA 0 copies
+    // CTA 1's (distributed shared memory, or global scratch in the grid variant)
+    if (!have_nu) {
+      for (int pk = tid; pk < (int)(p.d_pad / 2); pk += kLT) {
+        const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
+        Snu[2 * pk] = (T)v.x;
+        Snu[2 * pk + 1] = (T)v.y;
+      }
+    } else if (rank == 0) {
+      if constexpr (kGrid) {
+        const T* src = reinterpret_cast<const T*>(p.gnu) + (int64_t)chain * p.d_pad;
+        for (int j = tid; j < p.d_pad; j += kLT) Snu[j] = __ldcg(src + j);
+      } else {
+        const T* src = cluster.map_shared_rank(Snu, 1);
+        for (int j = tid; j < p.d_pad; j += kLT) Snu[j] = src[j];
+      }
     }
     if (rank == 0 && tid == 0) S.dbl[2] = theta_uniform(p.seed, t, gchain);
     for (int j = tid; j < kLNB; j += kLT) {
@@ -551,6 +567,18 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
       }
     }
     LPH(5);
+    if (rank != 0 && it + 1 < n_iter) {  // nu_{t+1} while CTA 0 builds I_act and theta
+      for (int pk = tid; pk < (int)(p.d_pad / 2); pk += kLT) {
+        const double2 v = normal_pair_at(p.seed, t + 1, gchain, 2 * pk, d);
+        SnuN[2 * pk] = (T)v.x;
+        SnuN[2 * pk + 1] = (T)v.y;
+        if (kGrid && rank == 1) {
+          T* dst = reinterpret_cast<T*>(p.gnu) + (int64_t)chain * p.d_pad;
+          dst[2 * pk] = (T)v.x;
+          dst[2 * pk + 1] = (T)v.y;
+        }
+      }
+    }
 #ifdef TMVN_PHASE_TIMING
     if (blockIdx.x == 0 && tid == 0) lph[11] += S.ints[1];
 #endif
@@ -776,6 +804,12 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     }
     if ((int64_t)(t + 1) % p.K == 0) {  // refresh P = A x (C13)
       gemv(Sx, Pc);
+    }
+    if (CS > 1) {  // nu_{t+1} is in SnuN (CTAs 1..) or arrives from CTA 1 (CTA 0)
+      T* tmp = Snu;
+      Snu = SnuN;
+      SnuN = tmp;
+      have_nu = true;
     }
     __syncthreads();
     LPH(10);

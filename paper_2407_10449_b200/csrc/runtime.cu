@@ -1160,7 +1160,8 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
     const size_t n_tab = (size_t)C * gsz * 128, n_mrg = (size_t)C * 128;
     const size_t b_tg = al(n_tab * 8), b_tc = al(n_tab * 4), b_mg = al(n_mrg * 8), b_mc = al(n_mrg * 4);
     const size_t b_live = al((size_t)C * cap * 16), b_small = al((size_t)C * 2 * 8);
-    const size_t total = 2 * b_tg + b_tc + 2 * b_mg + b_mc + b_live + 4 * b_small;
+    const size_t b_nu = al((size_t)C * h->d_pad * 8);
+    const size_t total = 2 * b_tg + b_tc + 2 * b_mg + b_mc + b_live + 4 * b_small + b_nu;
     if (h->lat_gscratch_n < total) {
       dfree(h->lat_gscratch);
       h->lat_gscratch = nullptr;
@@ -1182,6 +1183,7 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
     p.gstart = reinterpret_cast<int*>(q); q += b_small;
     CK(h, cudaMemsetAsync(zero0, 0, (size_t)(q - zero0), stream_of(h)));
     p.gth = reinterpret_cast<double*>(q); q += b_small;
+    p.gnu = reinterpret_cast<double*>(q); q += b_nu;
   }
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   p.err = h->dyn + 64 * 16 - 1;

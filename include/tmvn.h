@@ -144,7 +144,9 @@ typedef struct {
   int32_t pipeline;
   /* 1: latency mode -- one thread-block cluster (1-16 CTAs, distributed shared
    * memory) per chain runs all n_iter iterations in a single launch (the
-   * regime of few chains, e.g. the paper's 1 or 10).  Same RNG
+   * regime of few chains, e.g. the paper's 1 or 10); with very
+   * few chains and a large A, a cooperative grid of SMs / C CTAs per chain
+   * instead (same results bitwise; chosen by the cost model).  Same RNG
    * counters and readings; the dot products sum in another order, so results
    * agree with the default path to rounding, not bitwise.  Not with the affine
    * change of variable (the default path runs then).  CTA 0 of a cluster holds
@@ -153,7 +155,8 @@ typedef struct {
    * same start (tmvn_profile.latency_fallbacks).  2 (default): auto -- latency
    * mode when the chains are at most half the SMs (clusters of two or more
    * CTAs) and a cost model fitted to B200 measurements expects it to be
-   * faster (it re-reads A from L2 for every chain), else the default path.  0: off (always the default path). */
+   * faster (it re-reads A from L2 for every chain), else the default path.
+   * 0: off (always the default path). */
   int32_t latency;
   /* 1: FP32-class arithmetic, the paper's precision (S3.3).
    * In the latency mode (options.latency, auto as in FP64): A . nu, A . x, the arcs, P' and the safeguard, x in single

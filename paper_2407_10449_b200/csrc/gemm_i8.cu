@@ -54,7 +54,10 @@ constexpr int kASlice = kOzBM * kOzBK;  // 4096 bytes
 constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
 // 4 epilogue warps (one per TMEM lane quadrant): 320 threads x 128 registers leave
 // room on the SM for the RNG kernel that draws the next nu beside the GEMM
-constexpr int kOzEpiWarps = 4;
+#ifndef TMVN_OZ_EPI
+#define TMVN_OZ_EPI 4
+#endif
+constexpr int kOzEpiWarps = TMVN_OZ_EPI;
 constexpr int kOzThreads = 32 * (6 + kOzEpiWarps);  // producer, MMA, 4 A loaders, epilogue
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
 int g_oz_launch_seq = 0;  // host-side launch counter (timeline builds label launches with it)

@@ -179,11 +179,16 @@ __device__ __forceinline__ void lat_dot4(const T* __restrict__ A, int nrow, int6
     o[q] = t;
   }
 }
-// rows [0, nr) of this CTA's slice (global rows i0 + r) . v -> out[r]; warps take row quads
+// rows [0, nr) of this CTA's slice (global rows i0 + r) . v -> out[r]; warps take row
+// quads, in reverse order on alternate calls: when A exceeds L2, the rows streamed last
+// (still in L2) are read first, instead of LRU evicting each just before its reuse.
+// A row's sum has the same order either way.
 template <typename T>
 __device__ __forceinline__ void lat_rows(const T* __restrict__ A, int i0, int nr, int64_t d_pad, const T* v,
-                                         T* out, int warp, int lane) {
-  for (int r = 4 * warp; r < nr; r += 4 * (kLT / 32)) {
+                                         T* out, int warp, int lane, bool reverse = false) {
+  const int nq = (nr + 3) / 4;
+  for (int k = warp; k < nq; k += kLT / 32) {
+    const int r = 4 * (reverse ? nq - 1 - k : k);
     const int nrow = min(4, nr - r);
     T o[4];
     lat_dot4<T>(A + (int64_t)(i0 + r) * d_pad, nrow, d_pad, v, lane, o);
@@ -343,7 +348,11 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   __syncthreads();
   T* Pc = reinterpret_cast<T*>(S.P0);  // P = A x for this CTA's rows
   T* Pn = reinterpret_cast<T*>(S.P1);  // the proposal P'
-  auto gemv = [&](const T* v, T* out) { lat_rows<T>(A, i0, nr, p.d_pad, v, out, warp, lane); };
+  bool rev = false;  // alternate the row order of successive products (L2 reuse)
+  auto gemv = [&](const T* v, T* out) {
+    lat_rows<T>(A, i0, nr, p.d_pad, v, out, warp, lane, rev);
+    rev = !rev;
+  };
   gemv(Sx, Pc);
   __syncthreads();
   // strict start a_i . x0 < b_i (C18), checked here on the first P (FP64 mode; the

@@ -169,3 +169,18 @@ def test_full_size_config4_sampled():
         log = []
         assert compare_step(A, b, X, g, 104, 5, [0, 511, 1023], log=log, projection=projection) <= 1, log
         s.close()
+
+
+def test_full_size_config5_sampled():
+    """BASELINE config 5 at full single-GPU size (d=4096, m=16384, C=65536; ~25 GB of
+    device state) through the production loop: sampled chains against the oracle run
+    from the same start (global chain index in the RNG counters)."""
+    A, b, x0 = synth.make_instance(5)
+    C, T, seed = 65536, 3, 105
+    s = tm.Sampler(A, b, latency=0)
+    X = s.sample(np.tile(x0, (C, 1)), T, seed=seed)
+    assert s.stats()["rejections"] == 0
+    for c in (0, 40000, C - 1):
+        ref = oracle.run(A, b, x0[None, :], T, seed=seed, chain_offset=c)["X"][0]
+        assert np.max(np.abs(X[c] - ref)) <= 1e-9 * max(1.0, np.max(np.abs(ref))), c
+    s.close()

@@ -80,8 +80,9 @@ typedef struct {
    * CUDA events on `stream` and accumulate their durations (tmvn_get_profile).
    * Default 0. */
   int32_t profile;
-  /* Warps of the fused per-chain kernel that own one chain: 1, 2, 4 or 8;
-   * 0 (default) = chosen from C and m. */
+  /* Warps of the fused per-chain kernel that own one chain: 1, 2, 4, 8 or 16
+   * (16: one 512-thread CTA per chain); 0 (default) = chosen from C and m.
+   * Results do not depend on it. */
   int32_t chain_warps;
   /* Chain shards run as independent GEMM -> ESS sequences on concurrent streams
    * (forked from / joined to `stream`), so the FP64 tensor GEMM of one shard

@@ -671,15 +671,19 @@ __device__ __forceinline__ void stash_arc(const Smem& S, Ctl& ctl, double2* stas
 #ifndef TMVN_ESS_MIN_BLOCKS
 #define TMVN_ESS_MIN_BLOCKS 3
 #endif
+// threads per CTA: 256 (8 / W chain groups), or one 32 W-thread group when W = 16
+__host__ __device__ constexpr int ess_threads(int W) { return W > 8 ? 32 * W : kEssThreads; }
+__host__ __device__ constexpr int ess_groups(int W) { return W >= 8 ? 1 : 8 / W; }
 template <int W, bool kRing, bool kSmemStash>
 constexpr int ess_min_blocks() {
-  return (W == 8 && kSmemStash && !kRing) ? (TMVN_ESS_MIN_BLOCKS > 4 ? TMVN_ESS_MIN_BLOCKS : 4)
-                                          : TMVN_ESS_MIN_BLOCKS;
+  return W > 8 ? 2
+               : (W == 8 && kSmemStash && !kRing) ? (TMVN_ESS_MIN_BLOCKS > 4 ? TMVN_ESS_MIN_BLOCKS : 4)
+                                                  : TMVN_ESS_MIN_BLOCKS;
 }
 template <int W, bool kGiven, bool kRing, bool kSmemStash>
-__global__ void __launch_bounds__(kEssThreads, (ess_min_blocks<W, kRing, kSmemStash>())) ess_kernel(
+__global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSmemStash>())) ess_kernel(
     const EssParams p) {
-  constexpr int kGroups = 8 / W;
+  constexpr int kGroups = ess_groups(W);
   constexpr int T = Grp<W>::kThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Ctl ctl_all[kGroups];
@@ -1132,7 +1136,7 @@ cudaError_t launch_k(const EssParams& p, int grid, size_t smem, cudaStream_t st)
   cudaError_t e = cudaFuncSetAttribute(ess_kernel<W, kGiven, kRing, kSmemStash>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  ess_kernel<W, kGiven, kRing, kSmemStash><<<grid, kEssThreads, smem, st>>>(p);
+  ess_kernel<W, kGiven, kRing, kSmemStash><<<grid, ess_threads(W), smem, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -1150,12 +1154,13 @@ cudaError_t launch_w(const EssParams& p, int grid, size_t smem, cudaStream_t st)
 template <bool kGiven>
 cudaError_t launch_any(const EssParams& p, int grid, cudaStream_t st) {
   if (grid < 1) return cudaSuccess;
-  const size_t smem = (size_t)(8 / p.W) * ess_group_smem_bytes(p.m, p.NB, p.stash_smem, p.CH);
+  const size_t smem = (size_t)ess_groups(p.W) * ess_group_smem_bytes(p.m, p.NB, p.stash_smem, p.CH);
   switch (p.W) {
     case 1: return launch_w<1, kGiven>(p, grid, smem, st);
     case 2: return launch_w<2, kGiven>(p, grid, smem, st);
     case 4: return launch_w<4, kGiven>(p, grid, smem, st);
     case 8: return launch_w<8, kGiven>(p, grid, smem, st);
+    case 16: return launch_w<16, kGiven>(p, grid, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1166,7 +1171,7 @@ int occupancy_k(size_t smem) {
   cudaFuncSetAttribute(ess_kernel<W, false, kRing, kSmemStash>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ess_kernel<W, false, kRing, kSmemStash>,
-                                                kEssThreads, smem);
+                                                ess_threads(W), smem);
   return per_sm;
 }
 
@@ -1200,18 +1205,21 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
   // warps per chain: as few as still give every SM several chains in flight;
   // more warps per chain when chains are few or constraints many
   int W = W_req;
-  if (W != 1 && W != 2 && W != 4 && W != 8) {
+  if (W != 1 && W != 2 && W != 4 && W != 8 && W != 16) {
     // measured on B200 (tools/ab_time.py): a full CTA per chain once rows are long;
     // fewer warps per chain (more chains in flight) for short rows
     W = m >= 1024 ? 8 : m >= 256 ? 4 : m >= 48 ? 2 : 1;
     // fewer chains than SMs: a whole CTA per chain (latency-bound regime; the paper's
     // S4.2 workload, 10 chains at d = m = 1000: 47 -> 34 us per launch)
     if (C <= g_sms && m >= 48) W = 8;
+    // up to two chains per SM with long rows: a 512-thread CTA per chain (C = 80..256,
+    // d = m = 1000: 5-9 % per iteration; beyond 2 x SMs chains, 16 warps lose)
+    if (C <= 2 * g_sms && m >= 512) W = 16;
   }
   // buckets: about 16 constraints (~8 arcs) per level-1 bucket, 64 .. 1024
   int NB = 64;
   while (NB < m / 16 && NB < 1024) NB <<= 1;
-  const int groups = 8 / W;
+  const int groups = ess_groups(W);
   // P/Q chunk: 256 W constraints (64 KB ring for a full CTA), never beyond the row;
   // CH = 0: no ring, P and Q are read from global memory
   const int mm = (m + 1) & ~1;
@@ -1227,6 +1235,7 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
     case 1: per_sm = occupancy_w<1>(smem, CH > 0, stash_smem); break;
     case 2: per_sm = occupancy_w<2>(smem, CH > 0, stash_smem); break;
     case 4: per_sm = occupancy_w<4>(smem, CH > 0, stash_smem); break;
+    case 16: per_sm = occupancy_w<16>(smem, CH > 0, stash_smem); break;
     default: per_sm = occupancy_w<8>(smem, CH > 0, stash_smem); break;
   }
   if (per_sm < 1) per_sm = 1;

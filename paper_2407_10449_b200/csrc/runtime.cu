@@ -1029,8 +1029,8 @@ tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* o) {
   if (o->recompute_every < 1 || o->thin < 1 || o->burn_in < 0) return fail(h, TMVN_E_ARG, "bad recompute_every / thin / burn_in");
   if (o->chain_offset < 0 || o->iter_offset < 0) return fail(h, TMVN_E_ARG, "offsets must be >= 0");
   if (o->chain_warps != 0 && o->chain_warps != 1 && o->chain_warps != 2 && o->chain_warps != 4 &&
-      o->chain_warps != 8)
-    return fail(h, TMVN_E_ARG, "chain_warps must be 0, 1, 2, 4 or 8");
+      o->chain_warps != 8 && o->chain_warps != 16)
+    return fail(h, TMVN_E_ARG, "chain_warps must be 0, 1, 2, 4, 8 or 16");
   if (o->projection < 0 || o->projection > 2) return fail(h, TMVN_E_ARG, "projection must be 0, 1 or 2");
   if (o->latency < 0 || o->latency > 2) return fail(h, TMVN_E_ARG, "latency must be 0, 1 or 2");
   if (o->precision < 0 || o->precision > 1) return fail(h, TMVN_E_ARG, "precision must be 0 (FP64) or 1 (FP32)");

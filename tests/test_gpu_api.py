@@ -200,6 +200,9 @@ def test_rng_ahead_and_projection_options_bitwise():
                            (0, 0, 2, 0), (0, 1, 2, 0), (0, 0, 0, 1), (0, 1, 0, 1)):
         out = tm.Sampler(A, b, rng_ahead=ra, graphs=gr, schedule=sc, pipeline=pi).sample(X0, 70, seed=11)
         assert np.array_equal(out, ref), (ra, gr, sc, pi)
+    for W in (1, 2, 4, 8, 16):  # warps per chain (16: one 512-thread CTA per chain)
+        out = tm.Sampler(A, b, chain_warps=W).sample(X0, 70, seed=11)
+        assert np.array_equal(out, ref), W
     for n in (1, 2, 3):  # short calls through the pipelined prologue
         o1 = tm.Sampler(A, b, pipeline=1).sample(X0, n, seed=11)
         o0 = tm.Sampler(A, b).sample(X0, n, seed=11)

@@ -44,6 +44,7 @@ constexpr int kLNB = 128;     // level-1 buckets over [0, 2 pi]
 // memory left (up to m); more in some iteration -> the call reruns on the default path
 constexpr int kLNF = 1024;    // level-2 slots CTA 0 splits the live level-1 buckets into
 constexpr int kLSmall = 64;   // up to this many live arcs CTA 0 skips level 2
+constexpr int kLMinCap = 64;  // live-arc buffers hold at least this many (p.cap may be lower: test hook)
 
 __device__ __forceinline__ uint64_t lbits(double x) { return (uint64_t)__double_as_longlong(x); }
 __device__ __forceinline__ double lbitsd(uint64_t b) { return __longlong_as_double((long long)b); }
@@ -122,9 +123,27 @@ __host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, 
   return o;
 }
 
-__device__ __forceinline__ int lat_bucket(double a, double scale) {
-  const int k = (int)__dmul_rn(a, scale);
+// Level-1 bucket of an angle in [0, 2 pi] from its FP64 bit pattern (monotone in the
+// angle, which is all Alg. 3's bucketing needs): 8 buckets per octave over
+// [2^-12, 8) -- buckets 1 .. 120 -- and everything below 2^-12 in bucket 0.  At
+// S4.2 states the arcs start just past theta = 0 (alpha ~ slack / |q|), where a
+// linear grid put every one of them into its first bucket; octaves spread them,
+// and the buckets after the first arcs' ends are dead (max alpha <= gamma in).
+constexpr int kLExpLo = 1023 - 12;
+__device__ __forceinline__ int lat_bucket(double a, double /*unused*/) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(a);
+  const int e = (int)(bits >> 52);  // a >= 0
+  if (e < kLExpLo) return 0;
+  const int k = 1 + ((e - kLExpLo) << 3) + (int)((bits >> 49) & 7);
   return k < kLNB - 1 ? k : kLNB - 1;
+}
+// position in [0, SUB) of an angle inside its level-1 bucket (level 2): the next 32
+// mantissa bits, monotone within a bucket of one octave slice; bucket 0 spans many
+// octaves and is one slot
+__device__ __forceinline__ int lat_sub(double a, int k, int SUB) {
+  if (k == 0) return 0;
+  const uint64_t bits = (uint64_t)__double_as_longlong(a);
+  return (int)((((bits >> 17) & 0xFFFFFFFFull) * (uint64_t)SUB) >> 32);
 }
 
 // 16-byte vectors of the arithmetic type: FP64 (default) or FP32 (options.precision = 1)
@@ -322,7 +341,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   extern __shared__ __align__(16) unsigned char lsm[];
   LatShared S;
   const int nk = lat_nk(p.d_pad, CS);
-  lat_carve(lsm, p.d_pad, mr, nk, p.cap, S);
+  lat_carve(lsm, p.d_pad, mr, nk, p.cap > kLMinCap ? p.cap : kLMinCap, S);  // buffers >= kLMinCap
   // CTA 0's buffers and flags, seen from every CTA of the cluster (grid: global scratch)
   int* r_ints0 = kGrid ? nullptr : cluster.map_shared_rank(S.ints, 0);
   uint64_t* r_lkey0 = kGrid ? nullptr : cluster.map_shared_rank(S.lkey, 0);
@@ -672,9 +691,8 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
           LPH(12);
           for (int e = tid; e < total; e += kLT) {
             const uint64_t key = S.lkey[e];
-            const double u = __dmul_rn(lbitsd(key), scale);
             const int k = lat_bucket(lbitsd(key), scale);
-            const int sub = min(SUB - 1, (int)__dmul_rn(__dsub_rn(u, (double)k), (double)SUB));
+            const int sub = lat_sub(lbitsd(key), k, SUB);
             const int f = S.lrk[k] * SUB + sub;
             S.fid[e] = f;
             atomicMax(reinterpret_cast<unsigned long long*>(&S.fb[f]), (unsigned long long)lbits(S.lval[e]));
@@ -859,12 +877,12 @@ void lat_cycles(unsigned long long* out, bool reset) {
 
 size_t latency_smem_bytes(int64_t d_pad, int m, int cs, int cap) {
   LatShared S;
-  return lat_carve(nullptr, d_pad, (m + cs - 1) / cs, lat_nk(d_pad, cs), cap, S);
+  return lat_carve(nullptr, d_pad, (m + cs - 1) / cs, lat_nk(d_pad, cs), cap > kLMinCap ? cap : kLMinCap, S);
 }
 
 // live-arc capacity: m if it fits, else as many as fit (0: the mode does not fit)
 int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max) {
-  constexpr int kMinCap = 64;
+  constexpr int kMinCap = kLMinCap;
   if (latency_smem_bytes(d_pad, m, cs, kMinCap) > smem_max) return 0;
   int lo = kMinCap, hi = m > kMinCap ? m : kMinCap;
   while (lo < hi) {

@@ -110,7 +110,7 @@ def test_latency_overflow_falls_back_to_default_path():
     ref_s = tm.Sampler(A, b, latency=0, burn_in=5)
     ref = ref_s.sample(X0, T, seed=42)
     s = tm.Sampler(A, b, latency=1, burn_in=5)
-    s.test_latency_cap(64)  # S4.2 at d = 300 has ~100 live arcs per iteration
+    s.test_latency_cap(1)  # some iteration of S4.2 at d = 300 has more than one live arc
     out = s.sample(X0, T, seed=42)
     pr = s.profile()
     assert pr["latency_calls"] == 1 and pr["latency_fallbacks"] == 1

@@ -213,3 +213,33 @@ def test_rng_ahead_and_projection_options_bitwise():
         a = s.sample(X0, 32, seed=11)
         a = s.sample(a, 38, seed=11)
         assert np.array_equal(a, ref), kw
+
+
+@pytest.mark.parametrize("latency", [0, 1])
+def test_degenerate_inputs(latency):
+    """n_iter = 0, one chain, one dimension, no active constraint (every arc inactive:
+    the whole ellipse, L = 2 pi), and a polytope whose every constraint is active at
+    every step (orthant) -- on both execution paths."""
+    A, b, x0 = synth.make_instance(3, m=40, d=7)
+    s = tm.Sampler(A, b, latency=latency)
+    X0 = np.tile(x0, (3, 1))
+    out = s.sample(X0, 0, seed=1)
+    assert np.array_equal(out, X0) and s.stats()["steps"] == 0
+    # one chain, one dimension: N(0,1) on [-1, 3]
+    A1, b1, x1 = synth.one_dim((-1.0, 3.0))
+    s1 = tm.Sampler(A1, b1, latency=latency)
+    o1 = s1.sample(x1[None, :], 5, seed=2)
+    for t in range(5):
+        xn, _ = oracle.step(A1, b1, x1, 2, t, 0)
+        x1 = xn
+    assert np.allclose(o1[0], x1, rtol=1e-12, atol=1e-12)
+    # no active constraint: b far outside the reachable ellipse
+    Ab = A.copy()
+    bb = np.full(40, 1e6)
+    s2 = tm.Sampler(Ab, bb, latency=latency, record=0)
+    X = np.tile(x0, (4, 1))
+    Xn = s2.sample(X, 1, seed=3)
+    for c in range(4):
+        xn, _ = oracle.step(Ab, bb, X[c], 3, 0, c)
+        assert np.allclose(Xn[c], xn, rtol=1e-12, atol=1e-12)
+    assert s2.stats()["rejections"] == 0

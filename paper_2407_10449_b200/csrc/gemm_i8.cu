@@ -170,6 +170,25 @@ __device__ __forceinline__ void issue_stage(uint64_t da, uint64_t dn, uint32_t a
   PairMma<0, 0, S, FIRST>::run(da, dn, abuf);
 }
 
+// Tile order: bands of kOzBand chain blocks; inside a band the chain block varies
+// fastest, so each A' digit block is read once per band (from L2 for the band's
+// other chain blocks) and the band's nu blocks stay in L2 across the constraint
+// blocks.  With A' digits larger than L2 (config 5: 470 MB) the plain
+// constraint-fastest order streamed them once per chain block.  Results do not
+// depend on the order (every tile sums its whole K range).
+#ifndef TMVN_OZ_BAND
+#define TMVN_OZ_BAND 8
+#endif
+__device__ __forceinline__ void oz_tile(int tile, int MB, int NBt, int& mb, int& nb) {
+  constexpr int GN = TMVN_OZ_BAND;
+  const int band = tile / (MB * GN);
+  const int nb0 = band * GN;
+  const int gn = NBt - nb0 < GN ? NBt - nb0 : GN;
+  const int r = tile - band * MB * GN;
+  mb = r / gn;
+  nb = nb0 + r % gn;
+}
+
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint4& a, const uint4& b) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
@@ -250,7 +269,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (lane == 0) {  // ---- producer
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int mb = tile % MB, nb = tile / MB;
+        int mb, nb;
+        oz_tile(tile, MB, NBt, mb, nb);
         const int8_t* ga = As + (size_t)mb * KB * S * kASlice;
         const int8_t* gn = Ns + (size_t)nb * KB * S * kNSlice;
         for (int kb = 0; kb < KB; ++kb, ++it) {
@@ -347,7 +367,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     const int row_in_tile = quad * 32 + lane;
     uint32_t tcount = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
-      const int mb = tile % MB, nb = tile / MB;
+      int mb, nb;
+      oz_tile(tile, MB, NBt, mb, nb);
       const int64_t row = (int64_t)mb * kOzBM + row_in_tile;
       const double scale = __ldg(rowscale + row);
       OZT(g0);

@@ -82,3 +82,18 @@ def test_arg_errors_without_gpu_are_loud():
     with pytest.raises(tm.TmvnError) as ei:
         tm.tmvn_create(None, None, 0, 0)
     assert ei.value.status == -1
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/tmvn.h is a C ABI: it compiles as C99 with warnings as errors."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "h.c"
+    src.write_text('#include "tmvn.h"\nint main(void) { tmvn_options o; tmvn_profile p; (void)o; (void)p; return 0; }\n')
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
+                        "-c", str(src), "-o", str(tmp_path / "h.o")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

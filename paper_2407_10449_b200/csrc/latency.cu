@@ -40,6 +40,9 @@ namespace {
 #endif
 constexpr int kLT = TMVN_LAT_THREADS;  // threads per CTA
 constexpr int kLNB = 128;     // level-1 buckets over [0, 2 pi]
+#ifndef TMVN_LAT_PIPE
+#define TMVN_LAT_PIPE 1
+#endif
 // live arcs CTA 0 can hold per iteration: p.cap, sized on the host from the shared
 // memory left (up to m); more in some iteration -> the call reruns on the default path
 constexpr int kLNF = 1024;    // level-2 slots CTA 0 splits the live level-1 buckets into
@@ -175,6 +178,33 @@ __device__ __forceinline__ void lat_dot4(const T* __restrict__ A, int nrow, int6
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int u = 0; u < 4; ++u) s[q][u] = T(0);
+#if TMVN_LAT_PIPE
+  // blocks of 128 vectors in two halves, software-pipelined: the loads of the next
+  // half are in flight while the current half is multiplied (same accumulation order
+  // as the plain loop below); loads past the row are predicated off (zero)
+  V a[4][2], bq[4][2];
+  auto ld = [&](V (&dst)[4][2], int j0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) dst[q][u] = j0 + 32 * u < np ? __ldg(R[q] + j0 + 32 * u) : V{};
+  };
+  auto mul = [&](const V (&src)[4][2], int j0, int u0) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const V w = j0 + 32 * u < np ? Vv[j0 + 32 * u] : V{};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[q][u0 + u] = vdot(src[q][u], w, s[q][u0 + u]);
+    }
+  };
+  ld(a, lane);
+  for (int j = lane; j < np; j += 128) {
+    ld(bq, j + 64);
+    mul(a, j, 0);
+    if (j + 128 < np) ld(a, j + 128);
+    mul(bq, j + 64, 2);
+  }
+#else
   // blocks of 128 vectors; the last block's loads past the row are predicated off
   // (zero), so every block is one round trip with sixteen loads per lane in flight
   for (int j = lane; j < np; j += 128) {
@@ -190,6 +220,7 @@ __device__ __forceinline__ void lat_dot4(const T* __restrict__ A, int nrow, int6
       for (int q = 0; q < 4; ++q) s[q][u] = vdot(a[q][u], w, s[q][u]);
     }
   }
+#endif
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     T t = (s[q][0] + s[q][1]) + (s[q][2] + s[q][3]);

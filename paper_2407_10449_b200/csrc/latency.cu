@@ -133,7 +133,14 @@ __host__ __device__ inline size_t lat_carve(unsigned char* base, int64_t d_pad, 
 // linear grid put every one of them into its first bucket; octaves spread them,
 // and the buckets after the first arcs' ends are dead (max alpha <= gamma in).
 constexpr int kLExpLo = 1023 - 12;
-__device__ __forceinline__ int lat_bucket(double a, double /*unused*/) {
+#ifndef TMVN_LAT_OCTAVE
+#define TMVN_LAT_OCTAVE 1
+#endif
+__device__ __forceinline__ int lat_bucket(double a, double scale) {
+#if !TMVN_LAT_OCTAVE
+  const int kl = (int)__dmul_rn(a, scale);
+  return kl < kLNB - 1 ? kl : kLNB - 1;
+#endif
   const uint64_t bits = (uint64_t)__double_as_longlong(a);
   const int e = (int)(bits >> 52);  // a >= 0
   if (e < kLExpLo) return 0;
@@ -143,7 +150,11 @@ __device__ __forceinline__ int lat_bucket(double a, double /*unused*/) {
 // position in [0, SUB) of an angle inside its level-1 bucket (level 2): the next 32
 // mantissa bits, monotone within a bucket of one octave slice; bucket 0 spans many
 // octaves and is one slot
-__device__ __forceinline__ int lat_sub(double a, int k, int SUB) {
+__device__ __forceinline__ int lat_sub(double a, int k, int SUB, double scale) {
+#if !TMVN_LAT_OCTAVE
+  const double u = __dmul_rn(a, scale);
+  return min(SUB - 1, (int)__dmul_rn(__dsub_rn(u, (double)k), (double)SUB));
+#endif
   if (k == 0) return 0;
   const uint64_t bits = (uint64_t)__double_as_longlong(a);
   return (int)((((bits >> 17) & 0xFFFFFFFFull) * (uint64_t)SUB) >> 32);
@@ -723,7 +734,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
           for (int e = tid; e < total; e += kLT) {
             const uint64_t key = S.lkey[e];
             const int k = lat_bucket(lbitsd(key), scale);
-            const int sub = lat_sub(lbitsd(key), k, SUB);
+            const int sub = lat_sub(lbitsd(key), k, SUB, scale);
             const int f = S.lrk[k] * SUB + sub;
             S.fid[e] = f;
             atomicMax(reinterpret_cast<unsigned long long*>(&S.fb[f]), (unsigned long long)lbits(S.lval[e]));

@@ -9,3 +9,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --clock-control none --import-source on -k regex:ozaki_gemm -s 4 -c 1 -o gpurun_out/prof_oz $CMD > gpurun_out/ncu_oz.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:ess_kernel -s 4 -c 1 -o gpurun_out/prof_ess $CMD > gpurun_out/ncu_ess.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/rc.txt
+# the other workloads (latency mode, FP32-class, configs 4/5)
+timeout 600 python bench.py --config 6 --steps 5 --warmup 3 > gpurun_out/bench_c6.log 2>&1; echo "c6 rc=$?" >> gpurun_out/rc.txt
+timeout 600 python bench.py --config 7 --steps 3 --warmup 3 > gpurun_out/bench_c7.log 2>&1; echo "c7 rc=$?" >> gpurun_out/rc.txt
+timeout 600 python bench.py --precision 1 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_fp32.log 2>&1; echo "fp32 rc=$?" >> gpurun_out/rc.txt
+timeout 900 python bench.py --config 5 --steps 3 --warmup 3 --iters-per-step 20 > gpurun_out/bench_c5.log 2>&1; echo "c5 rc=$?" >> gpurun_out/rc.txt

@@ -208,7 +208,7 @@ __device__ unsigned long long g_oz_cycles[8];
 #define OZADD(i, v)
 #endif
 
-// warps: 0 producer, 1 MMA issuer, 2-5 A loaders, 6-9 epilogue (warp w may access
+// warps: 0 producer, 1 MMA issuer, 2-5 A loaders, 6.. epilogue (warp w may access
 // TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31 only: each role covers the 4 quadrants)
 // STAGES: ring depth (0 = as many as fit; 3 = the compact variant that leaves room
 // on the SM for a CTA of the per-chain kernel when the two run concurrently)

@@ -59,7 +59,11 @@ constexpr int kNSlice = kOzBN * kOzBK;  // 2048 bytes
 #define TMVN_OZ_EPI 8
 #endif
 constexpr int kOzEpiWarps = TMVN_OZ_EPI;
-constexpr int kOzThreads = 32 * (6 + kOzEpiWarps);  // producer, MMA, 4 A loaders, epilogue warps
+#ifndef TMVN_OZ_LOADERS
+#define TMVN_OZ_LOADERS 4
+#endif
+constexpr int kOzLoadWarps = TMVN_OZ_LOADERS;  // 4, or 8 (a second set after the epilogue warps)
+constexpr int kOzThreads = 32 * (2 + kOzLoadWarps + kOzEpiWarps);  // producer, MMA, loaders, epilogue
 __host__ __device__ constexpr int oz_stage_bytes(int S) { return S * (kASlice + kNSlice); }
 int g_oz_launch_seq = 0;  // host-side launch counter (timeline builds label launches with it)
 // ring depth: as many stages as fit in 226 KB of shared memory (S = 6: 6, 7: 5, 8: 4)
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     mbar_init(tfull, 1);
     mbar_init(tempty, kOzEpiWarps);  // one arrive per epilogue warp
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&afull[b], 4);
+      mbar_init(&afull[b], kOzLoadWarps);
       mbar_init(&aempty[b], 1);
     }
     mbar_fence_init();
@@ -334,9 +338,11 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         __syncwarp();
       }
     }
-  } else if (warp < 6) {  // ---- A loaders: row 32 (warp % 4) + lane of each TS slice into TMEM
-    if (NTS > 0) {
+  } else if (warp < 6 || warp >= 6 + kOzEpiWarps) {  // ---- A loaders: row 32 (warp % 4) + lane
+    if (NTS > 0) {                                    // of each TS slice into TMEM
       const int quad = warp & 3;
+      const int li = warp < 6 ? warp - 2 : 4 + warp - (6 + kOzEpiWarps);
+      const int i0 = kOzLoadWarps == 8 ? (li >> 2) : 0, istep = kOzLoadWarps == 8 ? 2 : 1;
       const int row = quad * 32 + lane;
       const uint32_t roff = (uint32_t)((row / 8) * 128 + (row % 8) * 16);
       const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           tc_fence_after();
           const unsigned char* st = ring + s * kStage + roff;
 #pragma unroll
-          for (int i = 0; i < NTS; ++i) {
+          for (int i = i0; i < NTS; i += istep) {
             const uint4 lo = *reinterpret_cast<const uint4*>(st + i * kASlice);
             const uint4 hi = *reinterpret_cast<const uint4*>(st + i * kASlice + (kOzBM / 8) * 128);
             tmem_st8(tmem + lanebase + (b ? oz_acol<S>(1, i) : oz_acol<S>(0, i)), lo, hi);

@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   T* Sx = reinterpret_cast<T*>(S.x);
   T* Snu = reinterpret_cast<T*>(S.nu);    // nu_t
   T* SnuN = reinterpret_cast<T*>(S.nu2);  // nu_{t+1} (CTAs 1..CS-1 draw it during CTA 0's theta)
-  bool have_nu = false;                   // nu_t already drawn (by this CTA, or by CTA 1 for CTA 0)
+
   T* SQ = reinterpret_cast<T*>(S.Q);
 
   // x_{t0} (all d) and P = A x for this CTA's rows
@@ -444,27 +444,29 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
   long long lt_prev = clock64();
 #endif
 
-  for (int it = 0; it < n_iter; ++it) {
-    const uint32_t t = p.t0 + (uint32_t)it;
-    // (a) nu_t, u_t: drawn here on the first iteration (and with one CTA per chain); else
-    // the CTAs 1.. drew it during the previous iteration's theta phase and CTA 0 copies
-    // CTA 1's (distributed shared memory, or global scratch in the grid variant)
-    if (!have_nu) {
+  // (a) nu, u and cleared bucket tables for iteration tt, (b) Q = A nu for this CTA's
+  // rows.  nu is drawn here, unless the CTAs 1.. drew it during the previous
+  // iteration's theta phase, in which case CTA 0 copies CTA 1's (distributed shared
+  // memory, or global scratch in the grid variant).  From the second iteration on this
+  // runs between the two halves of the safeguard barrier: it does not depend on the
+  // verdict, only x, P and the arcs do.
+  auto prep = [&](uint32_t tt, T* nu_dst, bool drawn) {
+    if (!drawn) {
       for (int pk = tid; pk < (int)(p.d_pad / 2); pk += kLT) {
-        const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
-        Snu[2 * pk] = (T)v.x;
-        Snu[2 * pk + 1] = (T)v.y;
+        const double2 v = normal_pair_at(p.seed, tt, gchain, 2 * pk, d);
+        nu_dst[2 * pk] = (T)v.x;
+        nu_dst[2 * pk + 1] = (T)v.y;
       }
     } else if (rank == 0) {
       if constexpr (kGrid) {
         const T* src = reinterpret_cast<const T*>(p.gnu) + (int64_t)chain * p.d_pad;
-        for (int j = tid; j < p.d_pad; j += kLT) Snu[j] = __ldcg(src + j);
+        for (int j = tid; j < p.d_pad; j += kLT) nu_dst[j] = __ldcg(src + j);
       } else {
-        const T* src = cluster.map_shared_rank(Snu, 1);
-        for (int j = tid; j < p.d_pad; j += kLT) Snu[j] = src[j];
+        const T* src = cluster.map_shared_rank(nu_dst, 1);
+        for (int j = tid; j < p.d_pad; j += kLT) nu_dst[j] = src[j];
       }
     }
-    if (rank == 0 && tid == 0) S.dbl[2] = theta_uniform(p.seed, t, gchain);
+    if (rank == 0 && tid == 0) S.dbl[2] = theta_uniform(p.seed, tt, gchain);
     for (int j = tid; j < kLNB; j += kLT) {
       S.Gx[j] = 0;
       S.mA[j] = 0;
@@ -472,10 +474,14 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     }
     if (tid == 0) S.ints[0] = 0;
     __syncthreads();
-    LPH(0);
-    // (b) Q for this CTA's rows
-    gemv(Snu, SQ);
+    gemv(nu_dst, SQ);
     __syncthreads();
+  };
+  if (n_iter > 0) prep(p.t0, Snu, false);
+
+  for (int it = 0; it < n_iter; ++it) {
+    const uint32_t t = p.t0 + (uint32_t)it;
+    LPH(0);
     LPH(1);
     // (c) arcs of the active rows + bucket statistics (high words, then low words)
     for (int r = tid; r < nr; r += kLT) {
@@ -848,7 +854,11 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     if (tid == 0) S.ints[2] = viol;
     if (kGrid && tid == 0 && viol) atomicOr(p.gviol + 2 * chain + par, 1);
     LPH(8);
-    csync();  // #4: every CTA's safeguard verdict
+    // #4: every CTA's safeguard verdict -- split: the next iteration's nu and Q in between
+    if constexpr (kGrid) grid.sync();
+    else asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if (it + 1 < n_iter) prep(t + 1, SnuN, CS > 1);
+    if constexpr (!kGrid) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     LPH(9);
     int any;
     if constexpr (kGrid) any = *(volatile int*)(p.gviol + 2 * chain + par);
@@ -874,11 +884,10 @@ __global__ void __launch_bounds__(kLT, 1) latency_kernel(const LatParams p) {
     if ((int64_t)(t + 1) % p.K == 0) {  // refresh P = A x (C13)
       gemv(Sx, Pc);
     }
-    if (CS > 1) {  // nu_{t+1} is in SnuN (CTAs 1..) or arrives from CTA 1 (CTA 0)
+    {  // nu_{t+1} is in SnuN
       T* tmp = Snu;
       Snu = SnuN;
       SnuN = tmp;
-      have_nu = true;
     }
     __syncthreads();
     LPH(10);

@@ -27,7 +27,11 @@
  *  - Determinism: the output is a pure function of (A, b, mu, L, X0, seed,
  *    chain_offset, iter_offset, n_iter, options); it does not depend on how the
  *    chains are split across calls or GPUs (global chain index in the RNG
- *    counter, no split-K in the projection GEMM).
+ *    counter, no split-K in the projection GEMM) provided every shard takes the
+ *    same execution path: options.latency 0 or 1, or the automatic choice with
+ *    options.total_chains set to the job's chain count (the latency mode sums
+ *    its dot products in another order than the throughput path).  Moment sums
+ *    agree across splits to rounding (different summation order), not bitwise.
  */
 #ifndef TMVN_H_
 #define TMVN_H_
@@ -154,10 +158,10 @@ typedef struct {
    * every live arc of an iteration (up to m, or what its shared memory allows);
    * if some iteration has more, the call is rerun on the default path from the
    * same start (tmvn_profile.latency_fallbacks).  2 (default): auto -- latency
-   * mode when the chains are at most half the SMs (clusters of two or more
-   * CTAs) and a cost model fitted to B200 measurements expects it to be
-   * faster (it re-reads A from L2 for every chain), else the default path.
-   * 0: off (always the default path). */
+   * mode when the job's chains (total_chains below) are at most half the SMs
+   * (clusters of two or more CTAs) and a cost model fitted to B200 measurements
+   * expects it to be faster (it re-reads A from L2 for every chain), else the
+   * default path.  0: off (always the default path). */
   int32_t latency;
   /* 1: FP32-class arithmetic, the paper's precision (S3.3).
    * In the latency mode (options.latency, auto as in FP64): A . nu, A . x, the arcs, P' and the safeguard, x in single
@@ -169,8 +173,18 @@ typedef struct {
    * and the start check; the rest stays FP64.  Use with trim_eps > 0 (S3.3
    * trimming); the safeguard rejects the rare infeasible proposal; iterates
    * are feasible to FP32 rounding.  Parity with the FP64 oracle is
-   * statistical.  0 (default): FP64. */
+   * statistical.  On the throughput path this is an "FP32-class projection,
+   * FP64 elsewhere" mode: only Q, the refresh and the products feeding them are
+   * FP32-class; arcs, I_act, theta, P' and x stay FP64.  The strict start check
+   * (C18) always runs on an FP64-class product (FP64 DMMA) whatever this
+   * setting.  0 (default): FP64. */
   int32_t precision;
+  /* Chains of the whole job across every shard / rank (0 = this call's C).  The
+   * automatic execution-path choice (latency = 2) is made from it, so that the
+   * shards of one job (chain_offset) all take the same path and their chains
+   * equal those of an unsharded run bitwise.  Set it whenever a job is split
+   * (paper_2407_10449_b200.dist.shard does).  Default 0. */
+  int64_t total_chains;
 } tmvn_options;
 
 typedef struct {
@@ -264,9 +278,14 @@ tmvn_status tmvn_get_profile(tmvn_handle h, tmvn_profile* prof);
  * caller-owned device memory on the handle's stream:
  *   gx, ma: uint64 C x 128 (bucket max beta bits exact, max alpha high word),
  *   cnt: int32 C x 128, live: double C x cap x 2 (alpha, beta), nlive: int32 C
- *   (may exceed cap: the caller must then stop -- arcs were dropped),
- *   all_live: world x C x cap x 2, all_n: world x C, flags: int32 C.
- * FP64 only, no affine change of variable; stats / moments as for tmvn_sample
+ *   (may exceed cap: arcs were dropped -- tmvn_cp_theta then sets that
+ *   chain's flag to 2 and tmvn_cp_commit holds the chain; the caller must stop),
+ *   all_live: world x C x cap x 2, all_n: world x C, flags: int32 C
+ *   (0 accept, 1 safeguard violation, 2 live-arc overflow; all-reduced MAX).
+ *   tmvn_cp_theta keeps world * cap arcs per chain in shared memory (48 B each):
+ *   TMVN_E_ARG when that exceeds the device's opt-in limit (B200: world * cap
+ *   <= 4842).
+ * FP64 only (precision != 0: TMVN_E_ARG), no affine change of variable; stats / moments as for tmvn_sample
  * after tmvn_cp_end (per rank: identical on every rank).  Errors: TMVN_E_ARG,
  * TMVN_E_STATE (no tmvn_cp_begin), TMVN_E_INFEASIBLE_START (this rank's rows). */
 tmvn_status tmvn_cp_begin(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed);
@@ -345,7 +364,9 @@ typedef struct {
 } tmvn_step_dump;
 
 /* One iteration t of the production kernels from the given X_t (C x d, in the
- * handle's u-space; P recomputed from X_t), with every intermediate dumped. */
+ * handle's u-space; P recomputed from X_t by the production refresh product --
+ * the int8 projection's digits of X when it is active, else FP64 DMMA), with every
+ * intermediate dumped. */
 tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t seed, int64_t t,
                            tmvn_step_dump* dump);
 /* tmvn_sample (production loop: incremental P, periodic refresh, fused RNG)

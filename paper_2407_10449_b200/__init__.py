@@ -51,7 +51,8 @@ class options(ctypes.Structure):
                 ("graphs", ctypes.c_int32), ("projection", ctypes.c_int32),
                 ("ozaki_slices", ctypes.c_int32), ("rng_ahead", ctypes.c_int32),
                 ("schedule", ctypes.c_int32), ("pipeline", ctypes.c_int32),
-                ("latency", ctypes.c_int32), ("precision", ctypes.c_int32)]
+                ("latency", ctypes.c_int32), ("precision", ctypes.c_int32),
+                ("total_chains", ctypes.c_int64)]
 
 
 class profile(ctypes.Structure):
@@ -164,6 +165,27 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+def _expect(a, shape, name, writable=False):
+    """Shape / dtype / layout check before a pointer crosses the ABI (the library copies
+    prod(shape) doubles with cudaMemcpyDefault: a narrower or float32 buffer would be an
+    out-of-bounds read or write, not an error)."""
+    if hasattr(a, "data_ptr"):
+        import torch
+        if a.dtype != torch.float64:
+            raise TypeError(f"{name} must be float64, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    else:
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64:
+            raise TypeError(f"{name} must be a float64 array")
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name} must be C-contiguous")
+        if writable and not a.flags["WRITEABLE"]:
+            raise ValueError(f"{name} must be writable")
+    if tuple(int(x) for x in a.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(a.shape)}")
+
+
 # ---------------------------------------------------------------- C-ABI mirrors
 def default_options():
     o = options()
@@ -240,7 +262,10 @@ class Sampler:
 
     def __init__(self, A, b, mu=None, L=None, **opts):
         A, b = _f64(A), _f64(b)
+        if len(A.shape) != 2:
+            raise ValueError(f"A must be m x d, got shape {tuple(A.shape)}")
         self.m, self.d = int(A.shape[0]), int(A.shape[1])
+        _expect(b, (self.m,), "b")
         self.h = tmvn_create(A, b, self.m, self.d)
         if mu is not None or L is not None:
             self.set_affine(mu, L)
@@ -248,7 +273,12 @@ class Sampler:
             self.set_options(**opts)
 
     def set_affine(self, mu=None, L=None):
-        tmvn_set_affine(self.h, _f64(mu), _f64(L))
+        mu, L = _f64(mu), _f64(L)
+        if mu is not None:
+            _expect(mu, (self.d,), "mu")
+        if L is not None:
+            _expect(L, (self.d, self.d), "L")
+        tmvn_set_affine(self.h, mu, L)
 
     def set_options(self, **kw):
         o = tmvn_get_options(self.h)
@@ -263,9 +293,13 @@ class Sampler:
 
     def sample(self, X0, n_iter, seed, out=None):
         X0 = _f64(X0)
+        if len(X0.shape) != 2 or int(X0.shape[1]) != self.d:
+            raise ValueError(f"X0 must be C x {self.d}, got shape {tuple(X0.shape)}")
         C = int(X0.shape[0])
         if out is None:
             out = X0.new_empty(X0.shape) if hasattr(X0, "new_empty") else np.empty_like(X0)
+        else:
+            _expect(out, (C, self.d), "out", writable=True)
         tmvn_sample(self.h, X0, C, n_iter, seed, out)
         return out
 

@@ -64,13 +64,26 @@ class ConstraintParallel:
     >>> out = cp.sample(X0, n_iter, seed)      # identical on every rank
     """
 
-    def __init__(self, A_rows, b_rows, group=None, cap=1024, **opts):
+    # cp_theta keeps world * cap gathered arcs of a chain in shared memory (48 B each):
+    # at most (227 KB - 32) / 48 per chain on B200
+    SMEM_ARCS = (227 * 1024 - 32) // 48
+
+    def __init__(self, A_rows, b_rows, group=None, cap=None, check_every=None, **opts):
         import torch
         from . import Sampler
         self.torch = torch
+        if opts.get("precision", 0) != 0:
+            raise ValueError("constraint-parallel iterations are FP64 only (precision 0)")
         self.s = Sampler(A_rows, b_rows, latency=0, **opts)
         self.coll = _Coll(group)
-        self.cap = int(cap)
+        limit = self.SMEM_ARCS // self.coll.world
+        self.cap = min(1024, limit) if cap is None else int(cap)
+        if self.cap > limit:
+            raise ValueError(f"cap={self.cap} x world={self.coll.world} live arcs per chain exceed the "
+                             f"shared memory of cp_theta (cap <= {limit})")
+        # live-arc overflow is flagged on the device in the iteration it happens (the chain
+        # stays); the host reads the flag every check_every iterations (default: K)
+        self.check_every = int(check_every or self.s.options().recompute_every or 32)
 
     def sample(self, X0, n_iter, seed):
         torch = self.torch
@@ -85,6 +98,10 @@ class ConstraintParallel:
         dev = X0.device
         t0 = int(self.s.options().iter_offset)
         err = torch.zeros(1, dtype=torch.int64, device=dev)
+        # the library launches on torch's current stream (set BEFORE tmvn_cp_begin, whose
+        # load of X0 must follow the copy above): the NCCL collectives are ordered on it
+        # (no host synchronisation per iteration); gloo's host copies synchronise
+        self.s.set_options(stream=torch.cuda.current_stream())
         st = L.tmvn_cp_begin(h, _ptr(X0), C, n_iter, seed)
         err[0] = 1 if st != 0 else 0
         self.coll.all_reduce(err, "max")
@@ -102,10 +119,7 @@ class ConstraintParallel:
         all_live = torch.zeros((W, C, self.cap, 2), dtype=torch.float64, device=dev)
         all_n = torch.zeros((W, C), dtype=torch.int32, device=dev)
         flags = torch.zeros(C, dtype=torch.int32, device=dev)
-        maxn = torch.zeros((), dtype=torch.int32, device=dev)
-        # the library launches on torch's current stream: the NCCL collectives are ordered
-        # on it (no host synchronisation per iteration); gloo's host copies synchronise
-        self.s.set_options(stream=torch.cuda.current_stream())
+        ovf = torch.zeros((), dtype=torch.int32, device=dev)
         for it in range(n_iter):
             t = t0 + it
             _check(L.tmvn_cp_stats(h, t, _ptr(gx), _ptr(ma), _ptr(cnt)), h)
@@ -119,14 +133,17 @@ class ConstraintParallel:
                 self.coll.all_gather(all_live, live)
                 self.coll.all_gather(all_n, nlive)
                 all_n_it, all_live_it = all_n, all_live
-            maxn = torch.maximum(maxn, all_n_it.max())  # checked once, at the end
             _check(L.tmvn_cp_theta(h, t, _ptr(gx), _ptr(ma), _ptr(cnt), _ptr(all_live_it), _ptr(all_n_it), W,
                                    self.cap, _ptr(flags)), h)
             self.coll.all_reduce(flags, "max")
-            _check(L.tmvn_cp_commit(h, t, _ptr(flags)), h)
-        if int(maxn) > self.cap:
-            raise RuntimeError(f"constraint-parallel: more than cap={self.cap} live arcs of one chain on one rank "
-                               "in some iteration (arcs were dropped); raise cap")
+            _check(L.tmvn_cp_commit(h, t, _ptr(flags)), h)  # flag 2 (overflow): the chain stays
+            ovf = torch.maximum(ovf, flags.max())
+            if (it + 1) % self.check_every == 0 or it + 1 == n_iter:
+                if int(ovf) >= 2:
+                    raise RuntimeError(
+                        f"constraint-parallel: more than cap={self.cap} live arcs of one chain on one rank "
+                        f"in iterations {t0 + it + 1 - ((it % self.check_every) + 1)}..{t0 + it} (flagged chains "
+                        "were held, not advanced, from the overflowing iteration on); raise cap")
         out = torch.empty((C, d), dtype=torch.float64, device=dev)
         _check(L.tmvn_cp_end(h, n_iter, _ptr(out)), h)
         torch.cuda.synchronize()

@@ -209,8 +209,12 @@ __global__ void __launch_bounds__(kCT) cp_theta_kernel(
   const int c = blockIdx.x, tid = threadIdx.x;
   const double scale = __ddiv_rn((double)kCNB, kTwoPi);
   // the gathered arcs of every rank, then the gap candidates (key, gamma) after them
-  int total = 0;
-  for (int r = 0; r < world; ++r) total += min(all_n[(int64_t)r * gridDim.x + c], cap);
+  int total = 0, overflow = 0;
+  for (int r = 0; r < world; ++r) {
+    const int n = all_n[(int64_t)r * gridDim.x + c];
+    total += min(n, cap);
+    overflow |= n > cap;  // some rank dropped live arcs of this chain: I_act would be wrong
+  }
   uint64_t* key = reinterpret_cast<uint64_t*>(csm);
   double* val = reinterpret_cast<double*>(key + total);
   uint64_t* cand = reinterpret_cast<uint64_t*>(val + total);
@@ -290,7 +294,9 @@ __global__ void __launch_bounds__(kCT) cp_theta_kernel(
     }
   }
   viol = __syncthreads_or(viol);
-  if (tid == 0) flags[c] = viol;
+  // 2: live-arc overflow -- the chain stays (no commit of a wrong I_act) and the caller
+  // aborts at the next check (ConstraintParallel: every recompute_every iterations)
+  if (tid == 0) flags[c] = overflow ? 2 : viol;
 }
 
 __global__ void __launch_bounds__(kCT) cp_commit_kernel(const int* __restrict__ flags, const double* __restrict__ theta,

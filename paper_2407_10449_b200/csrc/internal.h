@@ -77,6 +77,8 @@ cudaError_t launch_cp_stats(const double* P0, const double* P1, const unsigned c
                             cudaStream_t st);
 cudaError_t launch_cp_live(const double2* arcs, int64_t ldp, int m, int C, const uint64_t* gx, const uint64_t* ma,
                            const int* cnt, int cap, double2* live, int* nlive, cudaStream_t st);
+// dynamic shared memory of cp_theta for world * cap gathered arcs: 48 B per arc + 32
+size_t cp_theta_smem(int world, int cap);
 cudaError_t launch_cp_theta(const uint64_t* gx, const uint64_t* ma, const int* cnt, const double2* all_live,
                             const int* all_n, int world, int cap, uint64_t seed, uint32_t t, uint32_t chain_offset,
                             double eps, double* P0, double* P1, const unsigned char* cur, const double* Q,

@@ -422,8 +422,17 @@ tmvn_status start_check(tmvn_ctx* h, int64_t C, double* P) {
   // the same product as the periodic refresh, so that a call resumed at a multiple of
   // recompute_every continues bitwise like an uninterrupted one
   KL(h, launch_refresh(h, 0, C, P, st));
+  // the strict check itself always on an FP64-class product: with the FP32-class
+  // projection (precision = 1, 4 digits) a start within ~1e-6 relative of a face could be
+  // misjudged, so there it is checked on an FP64 DMMA product in the other P buffer
+  const double* Pchk = P;
+  if (use_oz(h) && oz_slices(h) < 7) {
+    double* Po = (P == h->P0) ? h->P1 : h->P0;
+    KL(h, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, Po, h->m_pad, st));
+    Pchk = Po;
+  }
   CK(h, cudaMemsetAsync(h->dflag, 0xff, sizeof(unsigned long long), st));
-  KL(h, launch_start_check(P, h->m_pad, h->b_eff, (int)C, (int)h->m, h->dflag, st));
+  KL(h, launch_start_check(Pchk, h->m_pad, h->b_eff, (int)C, (int)h->m, h->dflag, st));
   unsigned long long* fp = reinterpret_cast<unsigned long long*>(h->pin);
   CK(h, cudaMemcpyAsync(fp, h->dflag, sizeof(*fp), cudaMemcpyDeviceToHost, st));
   CK(h, cudaStreamSynchronize(st));
@@ -1053,14 +1062,12 @@ tmvn_status tmvn_get_options(tmvn_handle h, tmvn_options* o) {
 // affine change of variable, shared memory), else the throughput loop runs.
 // options.latency = 2 (auto) takes it when there are at most SMs / 2 chains (clusters of
 // two or more CTAs) and the cost model below expects it to be faster.
-bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_out) {
+// Latency-mode configuration for C chains: cluster size (or cooperative-grid CTAs per
+// chain), live-arc capacity and the cost model's time per iteration.  False when the
+// mode cannot run.
+bool latency_config(tmvn_ctx* h, int64_t C, int sms, int smem_max, int* cs_out, int* cap_out,
+                    int* gsz_out, double* t_out) {
   const bool fp32 = h->opt.precision == 1;
-  if (h->opt.latency == 0 || h->affine) return false;
-  int dev = 0, sms = 0, smem_max = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (h->opt.latency == 2 && 2 * C > sms) return false;
   int cap = 0, cs = 0;
   if (h->lat_memo_C == C && h->lat_memo_fp32 == (int)fp32) {  // occupancy queries cost ~10 us each
     cs = h->lat_memo_cs;
@@ -1076,8 +1083,7 @@ bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_ou
   // Cost model (S12, fitted to B200 measurements, tools/grid_probe.py): a CTA
   // streams its rows of A (eb bytes per element) each iteration at ~100 GB/s when A is
   // L2-resident, ~57 GB/s when it is not; besides, a cluster iteration costs ~12.8 us,
-  // a cooperative-grid one (SMs / C CTAs per chain, six grid barriers) ~20 + 0.9 C us;
-  // the default path ~50 us + 7.8 ps per element of A at few chains.
+  // a cooperative-grid one (SMs / C CTAs per chain, six grid barriers) ~20 + 0.9 C us.
   const double eb = fp32 ? 4.0 : 8.0;
   const double abytes = eb * (double)h->m * (double)h->d_pad;
   const double r_sm = abytes <= 80e6 ? 100e9 : 57e9;
@@ -1099,10 +1105,33 @@ bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_ou
       }
     }
   }
+  *cs_out = cs;
+  *cap_out = cap;
+  *gsz_out = gsz;
+  *t_out = t_lat;
+  return true;
+}
+
+bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_out) {
+  if (h->opt.latency == 0 || h->affine) return false;
+  int dev = 0, sms = 0, smem_max = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int cs = 0, cap = 0, gsz = 0;
+  double t_lat = 0.0;
   if (h->opt.latency == 2) {
+    // auto: decided from the JOB's chain count (options.total_chains; 0 = this call's C),
+    // so that every shard of a job takes the same path (the two paths sum in different
+    // orders: results agree to rounding, not bitwise)
+    const int64_t Cj = h->opt.total_chains > 0 ? h->opt.total_chains : C;
+    if (2 * Cj > sms) return false;
+    if (!latency_config(h, Cj, sms, smem_max, &cs, &cap, &gsz, &t_lat)) return false;
+    // the default path: ~50 us + 7.8 ps per element of A at few chains
     const double t_def = 50e-6 + 7.8e-12 * (double)h->m * (double)h->d;
     if (t_lat >= t_def) return false;
   }
+  if (!latency_config(h, C, sms, smem_max, &cs, &cap, &gsz, &t_lat)) return false;
   if (h->lat_cap_max > 0 && cap > h->lat_cap_max) cap = h->lat_cap_max;
   *cs_out = cs;
   *cap_out = cap;
@@ -1510,7 +1539,9 @@ tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t 
   // X_t is given in u-space
   CK(h, cudaMemcpyAsync(h->stage, Xt, (size_t)C * d * sizeof(double), cudaMemcpyDefault, st));
   CK(h, launch_pack(h->stage, C, d, d, h->X, h->d_pad, st));
-  CK(h, launch_gemm_tn(h->X, h->C_pad, h->At, h->m_pad, h->d_pad, h->P0, h->m_pad, st));
+  // P = X_t A'^T by the production refresh product (int8 digits of X per chain with the
+  // int8 projection, FP64 DMMA otherwise), as at the start check and every K iterations
+  CK(h, launch_refresh(h, 0, C, h->P0, st));
   CK(h, launch_first_nu(h, C, seed, (uint32_t)t, st));
   CK(h, launch_projection(h, 0, h->C_pad, st));
   CK(h, cudaMemsetAsync(h->rej, 0, (size_t)h->C_pad * sizeof(int64_t), st));
@@ -1619,6 +1650,7 @@ tmvn_status tmvn_cp_begin(tmvn_handle h, const double* X0, int64_t C, int64_t n_
   tmvn_status s = check_sample_args(h, X0, C, n_iter, X0);
   if (s != TMVN_OK) return s;
   if (h->affine) return fail(h, TMVN_E_ARG, "constraint-parallel iterations: no affine change of variable");
+  if (h->opt.precision != 0) return fail(h, TMVN_E_ARG, "constraint-parallel iterations are FP64 only (precision 0)");
   if ((s = set_device(h)) != TMVN_OK) return s;
   if ((s = ensure_chains(h, C)) != TMVN_OK) return s;
   if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
@@ -1669,6 +1701,17 @@ tmvn_status tmvn_cp_theta(tmvn_handle h, int64_t t, const uint64_t* gx, const ui
                           const double* all_live, const int32_t* all_n, int32_t world, int32_t cap, int32_t* flags) {
   if (!h || !h->cp_C || !all_live || !all_n || !flags || world < 1 || cap < 1)
     return fail(h, TMVN_E_ARG, "tmvn_cp_theta: bad arguments");
+  {
+    int smem_max = 0;
+    CK(h, cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    if (cp_theta_smem(world, cap) > (size_t)smem_max) {
+      char buf[200];
+      snprintf(buf, sizeof(buf), "tmvn_cp_theta: world * cap = %lld live arcs per chain need %zu B of shared "
+               "memory (> %d): lower cap to at most %lld", (long long)world * cap, cp_theta_smem(world, cap),
+               smem_max, (long long)(((size_t)smem_max - 32) / 48 / (size_t)world));
+      return fail(h, TMVN_E_ARG, buf);
+    }
+  }
   KL(h, launch_cp_theta(gx, ma, cnt, reinterpret_cast<const double2*>(all_live), all_n, world, cap, h->cp_seed,
                         (uint32_t)t, (uint32_t)h->opt.chain_offset, h->opt.trim_eps, h->P0, h->P1, h->cp_cur,
                         h->Q, h->m_pad, h->b_eff, (int)h->m, (int)h->cp_C, flags, h->cp_tl, h->cp_tl + h->C_pad,

@@ -21,6 +21,14 @@ def shard(total: int, rank: int, world: int):
     return offset, count
 
 
+def shard_options(total: int, rank: int, world: int):
+    """Sampler options of rank's shard: its global chain offset and the job's chain count
+    (options.total_chains: the automatic execution-path choice is then the same on every
+    rank, so the shards' chains equal an unsharded run's bitwise)."""
+    offset, count = shard(total, rank, world)
+    return dict(chain_offset=offset, total_chains=total), count
+
+
 def weak_shard(per_rank: int, rank: int):
     """(offset, count) when every rank runs `per_rank` chains (weak scaling)."""
     return rank * per_rank, per_rank
@@ -44,4 +52,11 @@ def max_over_ranks(x: float, device) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=device)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, device) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())

@@ -129,3 +129,43 @@ def test_constraint_parallel_collectives_gloo():
         mp.spawn(_cp_worker, args=(2, _free_port(), td), nprocs=2, join=True)
         ok = np.load(os.path.join(td, "cp.npy"))
     assert ok.all(), ok
+
+
+def _bench_worker(rank, world, port, outdir):
+    """bench.py's rank plumbing under gloo: strong-scaling shard plan (global chain
+    blocks + options.total_chains), whole-job units = SUM over ranks, device time = MAX
+    over ranks, and the moment / counter reduction."""
+    import torch.distributed as dist
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = []
+    for C_cfg in (4096, 65536, 16, 7):
+        opts, cnt = bench.plan_shard(C_cfg, rank, world, "strong")
+        wopts, wcnt = bench.plan_shard(C_cfg, rank, world, "weak")
+        # rank r "ran" cnt chains x 100 iterations in (10 + r) ms
+        units, ms_max, rate = bench.job_rate(float(cnt * 100), 10.0 + rank, "cpu")
+        res.append([opts["chain_offset"], cnt, opts["total_chains"], wopts["chain_offset"], wcnt,
+                    wopts["total_chains"], units, ms_max, rate])
+    np.save(os.path.join(outdir, f"b{rank}.npy"), np.array(res, dtype=np.float64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_rank_plumbing_gloo():
+    world = 2
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_bench_worker, args=(world, _free_port(), td), nprocs=world, join=True)
+        R = [np.load(os.path.join(td, f"b{r}.npy")) for r in range(world)]
+    for i, C_cfg in enumerate((4096, 65536, 16, 7)):
+        offs = [int(R[r][i, 0]) for r in range(world)]
+        cnts = [int(R[r][i, 1]) for r in range(world)]
+        assert offs[0] == 0 and offs[1] == cnts[0] and sum(cnts) == C_cfg  # strong: the config's C split
+        assert all(int(R[r][i, 2]) == C_cfg for r in range(world))        # every rank: the job's total
+        assert [int(R[r][i, 3]) for r in range(world)] == [0, C_cfg]         # weak: C per rank
+        assert all(int(R[r][i, 4]) == C_cfg and int(R[r][i, 5]) == world * C_cfg for r in range(world))
+        for r in range(world):
+            units, ms_max, rate = R[r][i, 6:9]
+            assert units == C_cfg * 100 and ms_max == 10.0 + world - 1
+            assert abs(rate - C_cfg * 100 / (ms_max * 1e-3)) <= 1e-9 * rate

@@ -103,20 +103,36 @@ def trunc_normal_moments(lo, hi):
 
 @pytest.mark.parametrize("interval", [(-1.0, 3.0), (15.0, 16.0)])
 def test_section_4_1_protocol(interval):
-    """2000 chains, burn-in 500, thinning 10, 1e5 samples."""
+    """2000 chains, burn-in 500, thinning 10, 1e5 samples.  The chains run as
+    20 shards of 100 (chain_offset: bitwise the same chains as one call, global RNG
+    counters), so each shard's moments are an independent estimate: the pooled mean and
+    variance must lie within 4 standard errors of the closed form (SURVEY 8(c)
+    statistical recipe; on [15, 16] sigma^2 = 0.0043, so the paper's 0.01 alone would be
+    vacuous) and within the paper's 0.01."""
     A, b, x0 = synth.one_dim(interval)
-    s = tm.Sampler(A, b, burn_in=500, thin=10)
-    out = s.sample(np.tile(x0, (2000, 1)), 1000, seed=2024)
-    sm, sq, n = s.moments()
-    assert n == 100000
+    G, Cg = 20, 100
     mu, var = trunc_normal_moments(*interval)
-    m1 = sm[0] / n
-    v1 = sq[0] / n - m1 * m1
+    means, vars_, ntot, steps, rej = [], [], 0, 0, 0
+    for g in range(G):
+        s = tm.Sampler(A, b, burn_in=500, thin=10, chain_offset=g * Cg)
+        out = s.sample(np.tile(x0, (Cg, 1)), 1000, seed=2024)
+        sm, sq, n = s.moments()
+        assert n == Cg * 50
+        means.append(sm[0] / n)
+        vars_.append(sq[0] / n - (sm[0] / n) ** 2)
+        ntot += n
+        st = s.stats()
+        steps += st["steps"]
+        rej += st["rejections"]
+        assert np.all(out >= interval[0]) and np.all(out <= interval[1])
+    assert ntot == 100000 and steps == 2_000_000
+    means, vars_ = np.array(means), np.array(vars_)
+    m1, v1 = means.mean(), vars_.mean()
+    se_m, se_v = means.std(ddof=1) / np.sqrt(G), vars_.std(ddof=1) / np.sqrt(G)
+    assert abs(m1 - mu) <= 4 * se_m, (m1, mu, se_m)
+    assert abs(v1 - var) <= 4 * se_v, (v1, var, se_v)
     assert abs(m1 - mu) < 0.01 and abs(v1 - var) < 0.01
-    st = s.stats()
-    assert st["steps"] == 2_000_000
-    assert st["rejections"] <= 200  # FP64: the paper saw 8 in FP32 on [15, 16]
-    assert np.all(out >= interval[0]) and np.all(out <= interval[1])
+    assert rej <= 200  # FP64: the paper saw 8 in FP32 on [15, 16]
 
 
 def test_orthant_config2_moments():
@@ -161,7 +177,18 @@ def test_affine_change_of_variable():
     u0 = oracle.whiten_point(x_start, mu, L)
     r = oracle.run(Aw, bw, np.tile(u0, (C, 1)), 5, seed=11)
     xo = np.array([oracle.unwhiten_point(u, mu, L) for u in r["X"]])
-    assert np.allclose(out, xo, rtol=1e-9, atol=1e-9)
+    assert np.max(np.abs(out - xo)) <= 1e-10 * max(1.0, np.max(np.abs(xo)))  # north_star bar
+    # per step in x-space, each from the GPU's own x_t (x -> u by the library's trsv, the
+    # oracle's own forward substitution on its side): x_{t+1} within 1e-10
+    s2 = tm.Sampler(A, b, mu=mu, L=L, record=0)
+    X = X0.copy()
+    for t in range(6):
+        Xn = s2.sample(X, 1, seed=11)
+        for c in range(0, C, 9):
+            un, _ = oracle.step(Aw, bw, oracle.whiten_point(X[c], mu, L), 11, t, c)
+            xn = oracle.unwhiten_point(un, mu, L)
+            assert np.max(np.abs(Xn[c] - xn)) <= 1e-10 * max(1.0, np.max(np.abs(xn))), (t, c)
+        X = Xn
     # 1-D closed form: x ~ N(2, 4) truncated to [1, 5]
     s1 = tm.Sampler(np.array([[1.0], [-1.0]]), np.array([5.0, -1.0]), mu=np.array([2.0]),
                     L=np.array([[2.0]]), burn_in=100)

@@ -16,7 +16,7 @@ import pytest
 import oracle
 import paper_2407_10449_b200 as tm
 from paper_2407_10449_b200 import synth
-from test_gpu_step import REL, compare_step, ozaki_qbound
+from test_gpu_step import REL, check_trace, compare_step, ozaki_qbound
 
 pytestmark = pytest.mark.gpu
 
@@ -89,14 +89,9 @@ def test_ozaki_production_loop_parity_and_sharding():
     s = tm.Sampler(A, b, latency=0, projection=1)
     chains = np.array([0, 1, 63, 64, 199])
     trace, out = s.test_trace(np.tile(x0, (C, 1)), T, seed=103, chains=chains)
-    bad = 0
-    for it in range(T):
-        for kk, c in enumerate(chains):
-            xn, _ = oracle.step(A, b, trace[it, kk], 103, it, c)
-            if np.max(np.abs(trace[it + 1, kk] - xn)) > REL * max(1.0, np.max(np.abs(xn))):
-                bad += 1
-            assert np.max(A @ trace[it + 1, kk] - b) <= 1e-12
-    assert bad <= 1, bad
+    log = []
+    check_trace(A, b, trace, 103, chains, projection=1, log=log)
+    print("exempt steps", log)
     assert s.stats()["rejections"] == 0
     # sharding by chain_offset is bitwise invariant (per-element integer MMA, fixed Horner)
     X0 = np.tile(x0, (C, 1))

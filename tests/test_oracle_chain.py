@@ -46,20 +46,30 @@ def _per_chain_stat(res_sum, n_per_chain):
 
 @pytest.mark.parametrize("interval", [(-1.0, 3.0), (15.0, 16.0)])
 def test_one_dim_section_4_1(interval):
-    """S4.1 protocol: 2000 chains, burn-in 500, thinning 10, 1e5 samples."""
+    """S4.1 protocol: 2000 chains, burn-in 500, thinning 10, 1e5 samples, run
+    as 20 independent groups of 100 chains (chain_offset): pooled mean and variance
+    within 4 standard errors of the closed form (on [15, 16] sigma^2 = 0.0043, so the
+    paper's 0.01 alone would say nothing) and within the paper's 0.01."""
     A, b, x0 = synth.one_dim(interval)
-    C, burn, thin, n_iter = 2000, 500, 10, 1000
-    X0 = np.tile(x0, (C, 1))
-    # run chains one by one to get per-chain statistics (oracle.run reduces over chains)
+    G, Cg, burn, thin, n_iter = 20, 100, 500, 10, 1000
     mu, var = trunc_normal_moments(*interval)
-    res = oracle.run(A, b, X0, n_iter, seed=2024, burn_in=burn, thin=thin)
-    n = res["n_rec"]
-    assert n == C * (n_iter - burn) // thin
-    m1 = res["sum"][0] / n
-    m2 = res["sumsq"][0] / n - m1 * m1
+    means, vars_, rej, n = [], [], 0, 0
+    for g in range(G):
+        res = oracle.run(A, b, np.tile(x0, (Cg, 1)), n_iter, seed=2024, chain_offset=g * Cg,
+                         burn_in=burn, thin=thin)
+        ng = res["n_rec"]
+        assert ng == Cg * (n_iter - burn) // thin
+        means.append(res["sum"][0] / ng)
+        vars_.append(res["sumsq"][0] / ng - means[-1] ** 2)
+        rej += res["rejections"]
+        n += ng
+        assert np.all(res["X"] >= interval[0]) and np.all(res["X"] <= interval[1])
+    means, vars_ = np.array(means), np.array(vars_)
+    m1, m2 = means.mean(), vars_.mean()
+    assert abs(m1 - mu) <= 4 * means.std(ddof=1) / np.sqrt(G), (m1, mu)
+    assert abs(m2 - var) <= 4 * vars_.std(ddof=1) / np.sqrt(G), (m2, var)
     assert abs(m1 - mu) < 0.01 and abs(m2 - var) < 0.01  # "accurate to the 2nd digit" (P:782)
-    assert np.all(res["X"] >= interval[0]) and np.all(res["X"] <= interval[1])
-    assert res["rejections"] <= 1e-4 * C * n_iter  # FP64: practically zero (P:763-764)
+    assert rej <= 1e-4 * G * Cg * n_iter  # FP64: practically zero (P:763-764)
 
 
 def _chains_in_batches(A, b, x0, C, T, seed, batch):

@@ -104,7 +104,9 @@ typedef struct {
    * no x-space moment recording); 0: one launch per kernel. */
   int32_t graphs;
   /* Projection GEMM Q = N A'^T (Alg. 1's A nu):
-   *   0 (default): automatic = 1 when d <= 4096, else 2;
+   *   0 (default): automatic = 1 when d <= 4096 and every row passes the dynamic-
+   *      range guard (tmvn_profile.oz_guard_ratio <= 16: the int8 bound below is at
+   *      most 16x the DMMA bound evaluated at the expected |nu|), else 2;
    *   1: int8 Ozaki split on the tcgen05 tensor cores (TMEM accumulators): A'
    *      row i scaled by 2^e_i > max_j |a_ij|, nu by 2^4 (Box-Muller |nu| < 8.58),
    *      both truncated to fixed point with 8S - 1 fraction bits and cut into S
@@ -185,6 +187,18 @@ typedef struct {
    * equal those of an unsharded run bitwise.  Set it whenever a job is split
    * (paper_2407_10449_b200.dist.shard does).  Default 0. */
   int64_t total_chains;
+  /* 1: with the int8 projection (projection 0/1), the arcs of eq:roots
+   * (readings C1-C5) are computed in the projection GEMM's epilogue
+   * while the tensor cores run the next tile: each (chain, constraint) pair is
+   * tested there against P = A x_t, and the active ones are appended to per-chain
+   * arc lists, which the fused per-chain kernel reads instead of the P and Q rows
+   * (same arc function, bit-identical arcs; list order is irrelevant to Alg. 3).
+   * Not with options.pipeline (the projection of t + 1 would read P while the
+   * per-chain kernel of t writes it).  0 (default): the per-chain kernel computes
+   * them (measured faster on B200 at config 3: the epilogue's arc work, latency-
+   * bound on 8 warps, doubles the projection's time, 0.177 -> 0.321 ms, while the
+   * per-chain kernel gains 0.017-0.040 ms).  Results do not depend on it. */
+  int32_t fuse_arcs;
 } tmvn_options;
 
 typedef struct {
@@ -210,6 +224,13 @@ typedef struct {
   int64_t latency_calls;      /* tmvn_sample calls run in latency mode (options.latency)      */
   int64_t latency_fallbacks;  /* of those, calls rerun on the default path (live-arc overflow) */
   int64_t latency_grid_calls; /* of those, calls run by the cooperative-grid variant          */
+  /* dynamic-range guard of the automatic projection (options.projection = 0): max over
+   * rows of A' of the int8 projection's stated bound at S = 7 over the FP64 DMMA bound
+   * at the expected |nu|, 2^(e_i+4) d 8 2^-54 / (2 d 2^-53 sqrt(2/pi) ||a_i||_1); the
+   * int8 projection is used only when it is <= 16 (else FP64 DMMA).  Set by
+   * tmvn_create / tmvn_set_affine (kept by tmvn_reset_stats). */
+  double oz_guard_ratio;
+  int32_t projection_used;    /* projection of the last throughput-path call: 1 int8, 2 DMMA */
 } tmvn_profile;
 
 /* Fills *opt with the defaults listed above. */

@@ -52,7 +52,7 @@ class options(ctypes.Structure):
                 ("ozaki_slices", ctypes.c_int32), ("rng_ahead", ctypes.c_int32),
                 ("schedule", ctypes.c_int32), ("pipeline", ctypes.c_int32),
                 ("latency", ctypes.c_int32), ("precision", ctypes.c_int32),
-                ("total_chains", ctypes.c_int64)]
+                ("total_chains", ctypes.c_int64), ("fuse_arcs", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):
@@ -62,7 +62,8 @@ class profile(ctypes.Structure):
                 ("ess_bytes", ctypes.c_double), ("tc_launches", ctypes.c_int64),
                 ("tc_ms", ctypes.c_double), ("tc_ops", ctypes.c_double),
                 ("tc_flops", ctypes.c_double), ("latency_calls", ctypes.c_int64),
-                ("latency_fallbacks", ctypes.c_int64), ("latency_grid_calls", ctypes.c_int64)]
+                ("latency_fallbacks", ctypes.c_int64), ("latency_grid_calls", ctypes.c_int64),
+                ("oz_guard_ratio", ctypes.c_double), ("projection_used", ctypes.c_int32)]
 
 
 class stats(ctypes.Structure):

@@ -304,6 +304,41 @@ cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, in
   start_check_kernel<<<grid_for((int64_t)C * m), 256, 0, st>>>(P, ldp, b, C, m, flag);
   return cudaGetLastError();
 }
+// Dynamic-range guard of the int8 projection (options.projection = 0): per row of A',
+// ratio_i = (stated int8 bound at S = 7) / (FP64 DMMA bound at the expected |nu|)
+//         = 2^(e_i + 4) d 8 2^-54 / (2 d 2^-53 sqrt(2 / pi) ||a_i||_1),
+// max_j |a_ij| < 2^e_i; the maximum over rows lands in *out (as ordered bits).
+__global__ void oz_guard_kernel(const double* __restrict__ At, int m, int d, int64_t d_pad,
+                                unsigned long long* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  double mx = 0.0, l1 = 0.0;
+  for (int k = lane; k < d; k += 32) {
+    const double v = fabs(At[tiled_offset(warp, k, d_pad)]);
+    mx = fmax(mx, v);
+    l1 += v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  }
+  if (lane == 0 && mx > 0.0) {
+    int e = 0;
+    frexp(mx, &e);
+    const double ratio = scalbn(1.0, e + 4) * 8.0 * 0.5 / (0.7978845608028654 * l1);  // 2^-54 / 2^-53 = 1/2
+    atomicMax(out, (unsigned long long)__double_as_longlong(ratio));
+  }
+}
+
+cudaError_t launch_oz_guard(const double* At, int m, int d, int64_t d_pad, unsigned long long* out,
+                            cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  oz_guard_kernel<<<(unsigned)(((int64_t)m * 32 + 255) / 256), 256, 0, st>>>(At, m, d, d_pad, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_chain_sum(const double* S, int C, int d, int64_t d_pad, double* out,
                              double* part, cudaStream_t st) {
   int nparts = (C + kSumChunk - 1) / kSumChunk;

@@ -40,6 +40,13 @@ __host__ __device__ inline int64_t tiled_offset(int64_t r, int64_t k, int64_t K_
   return run_offset(r, k / 8, K_pad) + (k % 8);
 }
 
+// The tiled offset separates into a row part and a column part:
+// tiled_offset(r, k) = tiled_row(r) + tiled_col(k) (hot loops step k with 32-bit adds).
+__host__ __device__ inline int64_t tiled_row(int64_t r, int64_t K_pad) {
+  return (r / kTileR) * (K_pad / kTileK) * kChunk + ((r % kTileR) / 8) * 128 + (r % 8) * 8;
+}
+__host__ __device__ inline int tiled_col(int k) { return (k >> 4) * kChunk + ((k >> 3) & 1) * 64 + (k & 7); }
+
 // ----------------------------------------------------------------------------
 // mbarrier + cp.async.bulk (TMA bulk engine, SASS UBLKCP) helpers.
 // ----------------------------------------------------------------------------
@@ -171,6 +178,14 @@ __host__ __device__ inline int64_t oz_offset(int64_t r, int64_t k, int s, int S,
          ((r % BR) / 8) * 128 + (r % 8) * 16 + (k % 16);
 }
 
+// oz_offset(r, k, s, S, KB, BR) = oz_row(r) + oz_col(k) + s BR 32 (row / column parts)
+__host__ __device__ inline int64_t oz_row(int64_t r, int S, int64_t KB, int BR) {
+  return (r / BR) * KB * S * (int64_t)(BR * kOzStepK) + ((r % BR) / 8) * 128 + (r % 8) * 16;
+}
+__host__ __device__ inline int oz_col(int k, int S, int BR) {
+  return (k / kOzStepK) * S * (BR * kOzStepK) + ((k % kOzStepK) / 16) * (BR / 8) * 128 + (k % 16);
+}
+
 __device__ __forceinline__ int64_t oz_fixed(double v, int S, int e) {
   return __double2ll_rz(scalbn(v, 8 * S - 1 - e));  // any e (A' rows may be tiny)
 }
@@ -202,6 +217,30 @@ __device__ __forceinline__ void oz_store_nu_pair(int8_t* Ns, int64_t r, int k, d
                                : __byte_perm(hi0, hi1, (uint32_t)((b - 4) | (b << 4)));
       *reinterpret_cast<uint16_t*>(base + s * (kOzNuRows * kOzStepK)) = (uint16_t)w;
     }
+  }
+}
+
+// The same S digits at a precomputed address (digit 0 of the pair); S a compile-time
+// constant: the byte selectors fold into the permutes.
+template <int S>
+__device__ __forceinline__ void oz_put_nu_pair(int8_t* base, double v0, double v1) {
+  const int64_t X0 = oz_fixed_nu(v0, S), X1 = oz_fixed_nu(v1, S);
+  const uint32_t lo0 = (uint32_t)X0, hi0 = (uint32_t)((uint64_t)X0 >> 32);
+  const uint32_t lo1 = (uint32_t)X1, hi1 = (uint32_t)((uint64_t)X1 >> 32);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int b = S - 1 - s;
+    const uint32_t w = b < 4 ? __byte_perm(lo0, lo1, (uint32_t)(b | ((b + 4) << 4)))
+                             : __byte_perm(hi0, hi1, (uint32_t)((b - 4) | (b << 4)));
+    *reinterpret_cast<uint16_t*>(base + s * (kOzNuRows * kOzStepK)) = (uint16_t)w;
+  }
+}
+__device__ __forceinline__ void oz_put_nu_pair_s(int8_t* base, double v0, double v1, int S) {
+  switch (S) {  // uniform
+    case 4: oz_put_nu_pair<4>(base, v0, v1); break;
+    case 6: oz_put_nu_pair<6>(base, v0, v1); break;
+    case 8: oz_put_nu_pair<8>(base, v0, v1); break;
+    default: oz_put_nu_pair<7>(base, v0, v1); break;
   }
 }
 

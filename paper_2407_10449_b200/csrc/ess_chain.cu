@@ -21,8 +21,9 @@
 //                accept iff max_i (P'_i - b_i) <= 0 (C8),
 //                x <- x cos(theta) + nu sin(theta), moments, then nu for t+1.
 //
-// A chain is owned by a group of W warps (W in {1, 2, 4, 8}); the 8 warps of a
-// CTA form 8/W independent groups that synchronise only among themselves
+// A chain is owned by a group of W warps (W in {1, 2, 4, 8, 16}); the 8 warps of a
+// CTA (W <= 8; W = 16: one 512-thread CTA per chain) form 8/W independent groups
+// that synchronise only among themselves
 // (named barriers `bar.sync id, 32 W`, or __syncwarp for W = 1), each looping
 // over chains (persistent grid).  Small W keeps many chains in flight per SM and
 // turns most synchronisation into warp-level shuffles; large W suits few
@@ -680,9 +681,14 @@ constexpr int ess_min_blocks() {
                : (W == 8 && kSmemStash && !kRing) ? (TMVN_ESS_MIN_BLOCKS > 4 ? TMVN_ESS_MIN_BLOCKS : 4)
                                                   : TMVN_ESS_MIN_BLOCKS;
 }
-template <int W, bool kGiven, bool kRing, bool kSmemStash>
-__global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSmemStash>())) ess_kernel(
+// kSrc: where phase A's arcs come from -- 0: P and Q rows read from global memory (the
+// active test and eq:roots here), 1: the same through a shared-memory bulk-copy ring,
+// 2: the projection GEMM's epilogue (options.fuse_arcs: compacted arc lists per chain)
+template <int W, bool kGiven, int kSrc, bool kSmemStash>
+__global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, kSmemStash>())) ess_kernel(
     const EssParams p) {
+  constexpr bool kRing = kSrc == 1;
+  constexpr bool kArcsIn = kSrc == 2;
   constexpr int kGroups = ess_groups(W);
   constexpr int T = Grp<W>::kThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -771,10 +777,13 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
 
   // dynamic scheduling: a group grabs its next chain one round ahead (so its rows can
   // be prefetched); groups that finish early take more chains
-  const bool dyn = !kGiven && !kRing && p.dyn_ctr != nullptr;
+  // Recorded iterations run round-robin (the host clears dyn_use; group g owns chains g,
+  // g + G, ...): each group adds its chains' iterates into its own moment row (row g of
+  // S1 / S2) in chain order, so the sums are deterministic without per-chain accumulators
+  const bool dyn = !kGiven && !kRing && p.dyn_ctr != nullptr && p.dyn_use;
   int* ctr = dyn ? p.dyn_ctr + (t_it & 63) : nullptr;
+  if (!kGiven && p.dyn_ctr != nullptr && blockIdx.x == 0 && threadIdx.x == 0) p.dyn_ctr[(t_it + 32) & 63] = 0;
   if (dyn) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.dyn_ctr[(t_it + 32) & 63] = 0;
     if (g.tid == T - 1) ctl.next = atomicAdd(ctr, 1);
     g.sync();
   }
@@ -799,7 +808,13 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
       ctl.u = theta_uniform(p.seed, t_it, gchain);
       if (dyn) ctl.next = atomicAdd(ctr, 1);
       const int64_t cn = dyn ? (int64_t)ctl.next : cc + ngroups;
-      if (!kRing && cn < p.C) {
+      if (kArcsIn && cn < p.C) {  // the next chain's activity masks and arcs into L2
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.amask + cn * p.mw),
+                     "r"((uint32_t)((p.mw * 4 + 15) & ~15)) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.arcs + cn * p.ald),
+                     "r"((uint32_t)m * 16u) : "memory");
+      }
+      if (!kRing && !kArcsIn && cn < p.C) {
         const uint32_t bytes = (uint32_t)(((int64_t)m * 8 + 15) & ~15ll);
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.P_cur + cn * p.ldp), "r"(bytes)
                      : "memory");
@@ -807,18 +822,13 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
                      : "memory");
       }
     }
-    if (!kGiven) {  // phase D's x, nu (and moment) rows of this chain into L2 early
-      const int kp = (int)(p.d_pad / 2);
-      for (int pk = g.tid; pk < kp; pk += T) {
-        const int64_t o = tiled_offset(c, 2 * pk, p.d_pad);
-        if ((pk & 3) == 0) {  // one 64-byte run = 4 pairs
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.X + o));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p.N + o));
-          if (record) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.S1 + o));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.S2 + o));
-          }
-        }
+    if (!kGiven) {  // phase D's x and nu rows of this chain into L2 early (64-byte runs)
+      const int nruns = (int)(p.d_pad / 8);
+      const int64_t xrow = tiled_row(c, p.d_pad);
+      for (int ru = g.tid; ru < nruns; ru += T) {
+        const int64_t o = xrow + tiled_col(8 * ru);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.X + o));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p.N + o));
       }
     }
     clear_buckets(g, S, NB);
@@ -828,7 +838,54 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
     // ---------------- A: arcs -> stash + level-1 bucket statistics ----------------
     const double* Prow = p.P_cur + (int64_t)c * p.ldp;
     const double* Qrow = p.Q + (int64_t)c * p.ldp;
-    if (kGiven) {
+    if (kArcsIn) {
+      // this chain's P and Q rows (read by phase D) into L2 while the arcs are processed
+      if (g.tid == T - 1) {
+        const uint32_t bytes = (uint32_t)(((int64_t)m * 8 + 15) & ~15ll);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Prow), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Qrow), "r"(bytes) : "memory");
+      }
+      // the arcs of the active constraints from the projection's epilogue (eq:roots with
+      // C1-C5 by the same arc_of): warp w takes the 32-constraint blocks w, w + W, ..., its
+      // lanes load the activity masks, then four blocks' arcs at a time are in flight;
+      // stash (compacted) + level-1 bucket statistics
+      const uint32_t* am = p.amask + (int64_t)c * p.mw;
+      const double2* arow = p.arcs + (int64_t)c * p.ald;
+      const int nbw = (p.mw - g.warp + W - 1) / W;
+      for (int k0 = 0; k0 < nbw; k0 += 32) {
+        const uint32_t mine = k0 + g.lane < nbw ? am[g.warp + W * (k0 + g.lane)] : 0u;
+        const int kn = min(32, nbw - k0);
+        for (int k = 0; k < kn; k += 4) {
+          uint32_t mk[4];
+          double2 ab[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            mk[u] = __shfl_sync(0xffffffffu, mine, (k + u) & 31);
+            if (k + u >= kn) mk[u] = 0u;
+            ab[u] = make_double2(0.0, 0.0);
+            if ((mk[u] >> g.lane) & 1u) ab[u] = arow[32 * (g.warp + W * (k0 + k + u)) + g.lane];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (mk[u] == 0u) continue;  // warp-uniform
+            const bool act = (mk[u] >> g.lane) & 1u;
+            int sb = 0;
+            if (g.lane == 0) sb = atomicAdd(&ctl.n_act, __popc(mk[u]));
+            sb = __shfl_sync(0xffffffffu, sb, 0);
+            if (act) {
+              stash[sb + __popc(mk[u] & ((1u << g.lane) - 1u))] = ab[u];
+              bucket_add<false>(S, bucket_key(ab[u].x, ctl, NB, scale), ab[u].x, ab[u].y);
+              if (p.d_alpha) {
+                const int i = 32 * (g.warp + W * (k0 + k + u)) + g.lane;
+                p.d_alpha[(int64_t)c * m + i] = ab[u].x;
+                p.d_beta[(int64_t)c * m + i] = ab[u].y;
+                p.d_active[(int64_t)c * m + i] = 1;
+              }
+            }
+          }
+        }
+      }
+    } else if (kGiven) {
       for (int i0 = 0; i0 < m; i0 += T) {
         const int i = i0 + g.tid;
         double al = 0.0, be = 0.0;
@@ -1018,6 +1075,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
 
     // ---------------- D: safeguard, P', x update, moments, next nu ----------------
     const double L = ctl.L;
+    // sin / cos by every thread: on the critical path in parallel, not behind a barrier
     double st = 0.0, ct = 1.0;
     if (L > 0.0) sincos(ctl.theta, &st, &ct);
     const int npairs = (m + 1) / 2;
@@ -1085,10 +1143,15 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
     if (!accept) {
       for (int pi = g.tid; pi < npairs; pi += T) Pn2[pi] = P2[pi];  // stay at x_t
     }
-    // x (and moments, next nu) by coordinate pairs: one double2 of the tiled X / N each
+    // x (and moments, next nu) by coordinate pairs: one double2 of the tiled X / N each;
+    // offsets = row part (per chain) + column part (stepped by 32-bit adds)
     const int kpairs = (int)(p.d_pad / 2);
+    const int64_t xrow = tiled_row(c, p.d_pad);
+    const int64_t mrow = tiled_row(gglobal + p.group_base, p.d_pad) - xrow;  // this group's moment row
+    const int64_t zrow = p.Ns ? oz_row(c, p.ozS, p.ozKB, kOzNuRows) : 0;
     for (int pk = g.tid; pk < kpairs; pk += T) {
-      const int64_t o = tiled_offset(c, 2 * pk, p.d_pad);
+      const int k = 2 * pk;
+      const int64_t o = xrow + tiled_col(k);
       double2* xr = reinterpret_cast<double2*>(p.X + o);
       double2* nr = reinterpret_cast<double2*>(p.N + o);
       double2 xv = *xr;
@@ -1098,9 +1161,9 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
         xv.y = xv.y * ct + nv.y * st;
         *xr = xv;
       }
-      if (record) {
-        double2* s1 = reinterpret_cast<double2*>(p.S1 + o);
-        double2* s2 = reinterpret_cast<double2*>(p.S2 + o);
+      if (record) {  // the group's moment row (L2-resident): deterministic chain order
+        double2* s1 = reinterpret_cast<double2*>(p.S1 + (o + mrow));
+        double2* s2 = reinterpret_cast<double2*>(p.S2 + (o + mrow));
         double2 a1 = *s1, a2 = *s2;
         a1.x += xv.x;
         a1.y += xv.y;
@@ -1110,9 +1173,9 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
         *s2 = a2;
       }
       if (p.gen_next) {
-        const double2 nv = normal_pair_at(p.seed, t_it + 1, gchain, 2 * pk, p.d);
+        const double2 nv = normal_pair_at(p.seed, t_it + 1, gchain, k, p.d);
         *nr = nv;
-        if (p.Ns) oz_store_nu_pair(p.Ns, c, 2 * pk, nv.x, nv.y, p.ozS, p.ozKB);
+        if (p.Ns) oz_put_nu_pair_s(p.Ns + (zrow + oz_col(k, p.ozS, kOzNuRows)), nv.x, nv.y, p.ozS);
       }
     }
     if (g.tid == 0) {
@@ -1131,24 +1194,28 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kRing, kSme
 #endif
 }
 
-template <int W, bool kGiven, bool kRing, bool kSmemStash>
+template <int W, bool kGiven, int kSrc, bool kSmemStash>
 cudaError_t launch_k(const EssParams& p, int grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(ess_kernel<W, kGiven, kRing, kSmemStash>,
+  cudaError_t e = cudaFuncSetAttribute(ess_kernel<W, kGiven, kSrc, kSmemStash>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  ess_kernel<W, kGiven, kRing, kSmemStash><<<grid, ess_threads(W), smem, st>>>(p);
+  ess_kernel<W, kGiven, kSrc, kSmemStash><<<grid, ess_threads(W), smem, st>>>(p);
   return cudaGetLastError();
 }
 
 template <int W, bool kGiven>
 cudaError_t launch_w(const EssParams& p, int grid, size_t smem, cudaStream_t st) {
+  if (!kGiven && p.arcs) {
+    return p.stash_smem ? launch_k<W, kGiven, 2, true>(p, grid, smem, st)
+                        : launch_k<W, kGiven, 2, false>(p, grid, smem, st);
+  }
   const bool ring = !kGiven && p.CH > 0;
   if (ring) {
-    return p.stash_smem ? launch_k<W, kGiven, true, true>(p, grid, smem, st)
-                        : launch_k<W, kGiven, true, false>(p, grid, smem, st);
+    return p.stash_smem ? launch_k<W, kGiven, 1, true>(p, grid, smem, st)
+                        : launch_k<W, kGiven, 1, false>(p, grid, smem, st);
   }
-  return p.stash_smem ? launch_k<W, kGiven, false, true>(p, grid, smem, st)
-                      : launch_k<W, kGiven, false, false>(p, grid, smem, st);
+  return p.stash_smem ? launch_k<W, kGiven, 0, true>(p, grid, smem, st)
+                      : launch_k<W, kGiven, 0, false>(p, grid, smem, st);
 }
 
 template <bool kGiven>
@@ -1165,20 +1232,20 @@ cudaError_t launch_any(const EssParams& p, int grid, cudaStream_t st) {
   }
 }
 
-template <int W, bool kRing, bool kSmemStash>
+template <int W, int kSrc, bool kSmemStash>
 int occupancy_k(size_t smem) {
   int per_sm = 0;
-  cudaFuncSetAttribute(ess_kernel<W, false, kRing, kSmemStash>,
+  cudaFuncSetAttribute(ess_kernel<W, false, kSrc, kSmemStash>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ess_kernel<W, false, kRing, kSmemStash>,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ess_kernel<W, false, kSrc, kSmemStash>,
                                                 ess_threads(W), smem);
   return per_sm;
 }
 
 template <int W>
 int occupancy_w(size_t smem, bool ring, bool smem_stash) {
-  if (ring) return smem_stash ? occupancy_k<W, true, true>(smem) : occupancy_k<W, true, false>(smem);
-  return smem_stash ? occupancy_k<W, false, true>(smem) : occupancy_k<W, false, false>(smem);
+  if (ring) return smem_stash ? occupancy_k<W, 1, true>(smem) : occupancy_k<W, 1, false>(smem);
+  return smem_stash ? occupancy_k<W, 0, true>(smem) : occupancy_k<W, 0, false>(smem);
 }
 
 }  // namespace

@@ -25,7 +25,7 @@
 // of C; the result is a deterministic function of (A', nu) (no split-K, fixed
 // reconstruction order), so chains are bitwise independent of the sharding.
 //
-// Kernel.  Persistent, one 192-thread CTA per SM (TMEM: all 512 columns).
+// Kernel.  Persistent, one 448-thread CTA per SM (TMEM: all 512 columns).
 // Output tile: 128 constraints (MMA M, TMEM lanes) x 64 chains (MMA N); the
 // S accumulators take S x 64 TMEM columns.  K steps of 32 bytes: one stage =
 // S A' digit slices (S x 4 KB) + S nu digit slices (S x 2 KB), each a single
@@ -33,10 +33,14 @@
 // canonical K-major SWIZZLE_NONE layout by the slicing kernels below and by the
 // fused per-chain kernel, which writes nu's digits as it draws nu).
 //   warp 0 lane 0: producer (bulk copies into a kStages ring, mbarrier tx)
-//   warp 1 lane 0: MMA issuer (S(S+1)/2 tcgen05.mma per stage, tcgen05.commit
-//                  frees the ring slot; after the tile, commits to tmem_full)
-//   warps 2-5:     epilogue (tcgen05.ld 32x32b, FP64 Horner, coalesced stores
-//                  of Q[chain][constraint]), then arrive on tmem_empty.
+//   warp 1:        MMA issuer (elect.sync; S(S+1)/2 tcgen05.mma per stage,
+//                  tcgen05.commit frees the ring slot; after the tile, commits
+//                  to tmem_full)
+//   warps 2-5:     A loaders (digit slices 0-3 of each stage into TMEM,
+//                  tcgen05.st, double-buffered)
+//   warps 6-13:    epilogue (tcgen05.ld 32x32b, FP64 Horner, coalesced stores
+//                  of Q[chain][constraint]), then arrive on tmem_empty;
+//                  with options.fuse_arcs also the arcs of eq:roots.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -216,11 +220,12 @@ __device__ unsigned long long g_oz_cycles[8];
 // TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31 only: each role covers the 4 quadrants)
 // STAGES: ring depth (0 = as many as fit; 3 = the compact variant that leaves room
 // on the SM for a CTA of the per-chain kernel when the two run concurrently)
-template <int S, int STAGES, bool CS>
+template <int S, int STAGES, bool CS, bool ARCS>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
                       const double* __restrict__ rowscale, const double* __restrict__ colscale,
-                      double* __restrict__ Q, int64_t ldq, int MB, int NBt, int KB, int dbg_seq) {
+                      double* __restrict__ Q, int64_t ldq, int MB, int NBt, int KB, int dbg_seq,
+                      const OzArcs arc) {
   constexpr int kStage = oz_stage_bytes(S);
   constexpr int kOzStages = STAGES ? STAGES : oz_stages(S);
   constexpr int NTS = oz_nts<S>();
@@ -406,6 +411,39 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty);
+      // Fused arc construction (options.fuse_arcs; eq:roots P:922-934 with C1-C5): with the
+      // accumulators released, while the MMAs of the next tile run, this thread's
+      // constraint `row` is tested against each of its chains -- p from P = A x_t, q the
+      // value just stored (re-read from L2, program order) -- and an active constraint's
+      // arc is stored at its own index in the chain's row of `arcs`, the warp's ballot as
+      // the activity mask of the 32 constraints (no atomics, no ordering: fire-and-forget)
+      if (ARCS) {
+        const bool rv = row < arc.m;
+        const double bi = rv ? __ldg(arc.b + row) : 0.0;
+#pragma unroll 1
+        for (int cc = c0; cc < c0 + kOzBN * 4 / kOzEpiWarps; cc += 8) {
+          double pv[8], qv[8];
+          const int64_t ch0 = (int64_t)nb * kOzBN + cc;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            pv[j] = 0.0;
+            qv[j] = 0.0;
+            if (rv && ch0 + j < arc.C) {
+              pv[j] = arc.P[(ch0 + j) * arc.ldp + row];
+              qv[j] = qcol[(int64_t)(cc + j) * ldq];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (ch0 + j >= arc.C) break;  // uniform: padded chains
+            double al = 0.0, be = 0.0;
+            const bool act = rv && arc_of(pv[j], qv[j], bi, al, be);
+            const unsigned mask = __ballot_sync(0xffffffffu, act);
+            if (act) arc.arcs[(ch0 + j) * arc.ald + row] = make_double2(al, be);
+            if (lane == 0 && (row >> 5) < arc.mw) arc.amask[(ch0 + j) * arc.mw + (row >> 5)] = mask;
+          }
+        }
+      }
 #ifdef TMVN_PHASE_TIMING
       acc1 += clock64() - g1;
 #endif
@@ -491,10 +529,10 @@ cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64
   return cudaGetLastError();
 }
 
-template <int S, int STAGES, bool CS>
+template <int S, int STAGES, bool CS, bool ARCS>
 static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                                int64_t KB, const double* rowscale, const double* colscale, double* Q,
-                               int64_t ldq, cudaStream_t st) {
+                               int64_t ldq, cudaStream_t st, const OzArcs& arc) {
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -502,25 +540,36 @@ static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t smem = ozaki_smem_bytes(S, STAGES);
-  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, STAGES, CS>,
+  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, STAGES, CS, ARCS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int MB = (int)(M_pad / kOzBM), NBt = (int)(N_pad / kOzBN);
   const int tiles = MB * NBt;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  ozaki_gemm_kernel<S, STAGES, CS><<<grid, kOzThreads, smem, st>>>(As, Ns, rowscale, colscale, Q, ldq, MB, NBt,
-                                                                (int)KB, g_oz_launch_seq++);
+  ozaki_gemm_kernel<S, STAGES, CS, ARCS><<<grid, kOzThreads, smem, st>>>(
+      As, Ns, rowscale, colscale, Q, ldq, MB, NBt, (int)KB, g_oz_launch_seq++, arc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
-                              cudaStream_t st, bool compact, const double* colscale) {
+                              cudaStream_t st, bool compact, const double* colscale, const OzArcs* arcs) {
   if (M_pad % kOzBM || N_pad % kOzBN || KB < 1) return cudaErrorInvalidValue;
+  if (arcs && (colscale || compact)) return cudaErrorInvalidValue;
+  const OzArcs none{};
+  if (arcs) {
+    switch (S) {
+      case 4: return launch_oz_t<4, 0, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, *arcs);
+      case 6: return launch_oz_t<6, 0, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, *arcs);
+      case 7: return launch_oz_t<7, 0, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, *arcs);
+      case 8: return launch_oz_t<8, 0, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, *arcs);
+      default: return cudaErrorInvalidValue;
+    }
+  }
 #define TMVN_OZ_CASE(SS, ST)                                                                  \
   case SS:                                                                                    \
-    return colscale ? launch_oz_t<SS, ST, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st) \
-                    : launch_oz_t<SS, ST, false>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st);
+    return colscale ? launch_oz_t<SS, ST, true, false>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, none) \
+                    : launch_oz_t<SS, ST, false, false>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, none);
   if (compact) {
     switch (S) {
       TMVN_OZ_CASE(4, 3)

@@ -17,13 +17,25 @@ cudaError_t launch_gemm_tn(const double* Xt, int64_t R_pad, const double* Wt, in
 // rows, blocks of 64), KB steps of 32 along d, S digits (6, 7 or 8);
 // rowscale[i] = 2^(e_i + e_nu - 14).
 size_t ozaki_smem_bytes(int S, int stages = 0);
-// compact: the 3-stage ring (126 KB at S = 7), which leaves room on the SM for one
-// CTA of the per-chain kernel (pipelined schedule, options.pipeline)
-// colscale (nullable, N_pad): an extra power of two per output column (row of Ns):
-// the refresh P = X A'^T slices X with one exponent per chain.
+// Fused arc construction in the projection's epilogue (options.fuse_arcs): for every
+// chain c < C and constraint i < m, bit i % 32 of amask[c][i / 32] says whether
+// hypot(P[c][i], Q[c][i]) > b[i] (C3), and then arcs[c][i] holds its arc (alpha, beta)
+// of eq:roots (other entries are stale).  P: C_pad x ldp (= A x_t); arcs: C_pad x ald;
+// amask: C_pad x mw (mw = ceil(m / 32)).
+struct OzArcs {
+  const double* P;
+  int64_t ldp;
+  const double* b;
+  int m, C;
+  double2* arcs;
+  int64_t ald;
+  uint32_t* amask;
+  int mw;
+};
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
-                              cudaStream_t st, bool compact = false, const double* colscale = nullptr);
+                              cudaStream_t st, bool compact = false, const double* colscale = nullptr,
+                              const OzArcs* arcs = nullptr);
 // digits of the R rows of a fragment-tiled FP64 matrix into the oz layout with BR
 // rows per block; per_row: exponent from each row's max |v| (rowscale[r] =
 // 2^(e_r + e_other - 14)), else the fixed exponent e_fixed (|v| < 2^e_fixed).
@@ -117,6 +129,15 @@ struct EssParams {
   int64_t group_base;  // scratch index of this launch's first group (split launches)
   int* dyn_ctr;     // non-null: chains handed out dynamically by atomicAdd on dyn_ctr[t & 63]
                     // (the launch for t zeroes the slot of t + 32); null: round-robin
+  int dyn_use;      // 0: round-robin even with dyn_ctr set (recorded iterations: the moment
+                    // rows are per group, so the chain -> group map must be fixed)
+  // fused arcs (options.fuse_arcs): per chain, the activity bitmask of the constraints
+  // (amask, C_pad x mw words) and the arcs at their constraint index (arcs, C_pad x ald)
+  // from the projection's epilogue; null: phase A computes the arcs from P and Q
+  const double2* arcs;
+  int64_t ald;
+  const uint32_t* amask;
+  int mw;
   int8_t* Ns;       // non-null: also write nu_{t+1}'s S digits (int8 projection, gemm_i8.cu)
   int ozS;
   int64_t ozKB;
@@ -207,6 +228,10 @@ cudaError_t launch_normals(double* N, int C, int d, int64_t d_pad, uint64_t seed
 cudaError_t launch_nu(double* N, int8_t* Ns, int S, int64_t KB, int C, int d, int64_t d_pad,
                       uint64_t seed, uint32_t t, const uint32_t* t_dev, uint32_t chain_offset,
                       cudaStream_t st, int ctas_per_sm);
+// max over rows of A' (tiled) of the int8 projection's stated bound over the FP64 DMMA
+// bound at the expected |nu| (positive double bits in *out; 0 for an all-zero A').
+cudaError_t launch_oz_guard(const double* At, int m, int d, int64_t d_pad, unsigned long long* out,
+                            cudaStream_t st);
 // first (c, i) with P[c, i] - b[i] >= 0 (strict start, C18); *flag = c * m + i or -1.
 cudaError_t launch_start_check(const double* P, int64_t ldp, const double* b, int C, int m,
                                unsigned long long* flag, cudaStream_t st);

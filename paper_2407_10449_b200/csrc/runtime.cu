@@ -12,6 +12,8 @@
 #include <vector>
 #include <algorithm>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/tmvn.h"
 #include "common.cuh"
 #include "internal.h"
@@ -21,6 +23,15 @@ using namespace tmvn;
 namespace {
 
 thread_local std::string g_create_error;
+
+// NVTX range (header-only NVTX v3: a no-op unless a tool such as nsys / ncu is attached)
+// around each host-side stage of the call and each hot-loop launch, named by SURVEY 8(a) row
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 struct DevBuf {
   void* p = nullptr;
@@ -57,6 +68,10 @@ struct tmvn_ctx {
   // int8 refresh of P = X A'^T: digits of X (C_pad rows) and 2^(e_c - 4) per chain
   int8_t* Xs = nullptr;
   double* xscale = nullptr;
+  // fused arcs (options.fuse_arcs): per-chain arc lists written by the projection's epilogue
+  double2* arcs = nullptr;  // C_pad x m_pad
+  uint32_t* amask = nullptr;  // C_pad x mw activity bits
+  int64_t arcs_rows = 0;
   cudaStream_t gemm_stream = nullptr;
   cudaEvent_t ev_q[2] = {nullptr, nullptr}, ev_nu[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_ess = nullptr, ev_join[2] = {nullptr, nullptr}, ev_essb = nullptr;
@@ -98,6 +113,7 @@ struct tmvn_ctx {
   int8_t* As = nullptr;       // digits of A' (m_pad rows), valid for ozS_A digits (0 = stale)
   double* rowscale = nullptr; // m_pad
   int ozS_A = 0;
+  double oz_ratio = 0.0;  // dynamic-range guard: max_i int8 bound / FP64 bound (use_oz)
   int8_t* Ns = nullptr;       // digits of nu (C_pad rows)
   int8_t* Ns2 = nullptr;      // second buffer (nu of odd iterations when the RNG runs ahead)
   int ozS_N = 0;
@@ -176,7 +192,13 @@ std::vector<double> to_host(const double* p, size_t n) {
 
 cudaStream_t stream_of(const tmvn_ctx* h) { return (cudaStream_t)h->opt.stream; }
 
+void free_arcs(tmvn_ctx* h) {
+  dfree(h->arcs); dfree(h->amask);
+  h->arcs_rows = 0;
+}
+
 void free_chain_buffers(tmvn_ctx* h) {
+  free_arcs(h);
   dfree(h->X); dfree(h->N); dfree(h->N2); dfree(h->N3); dfree(h->P0); dfree(h->P1); dfree(h->Q);
   dfree(h->Q2); dfree(h->Ns3); dfree(h->Xs); dfree(h->xscale);
   dfree(h->S1); dfree(h->S2); dfree(h->S1x); dfree(h->S2x);
@@ -252,14 +274,58 @@ tmvn_status ensure_affine_moments(tmvn_ctx* h) {
   return TMVN_OK;
 }
 
+// Automatic projection (options.projection = 0): the int8 Ozaki split when d <= 4096 and
+// its stated bound is within kOzGuard times the FP64 DMMA bound (at the expected |nu|) on
+// every row of A' (rows with a wide dynamic range, where a row's
+// max |a_ij| sets the int8 grid but its L1 norm sets the DMMA bound, take DMMA).
+constexpr double kOzGuard = 16.0;
 bool use_oz(const tmvn_ctx* h) {
-  return h->opt.projection == 1 || (h->opt.projection == 0 && h->d <= 4096);
+  return h->opt.projection == 1 || (h->opt.projection == 0 && h->d <= 4096 && h->oz_ratio <= kOzGuard);
 }
 // digits per operand: 7 (FP64-class, default), 6 or 8 by option; options.precision = 1
 // (FP32) takes 4 (31 fraction bits: FP32-class, 10 digit-pair MMAs instead of 28)
 int oz_slices(const tmvn_ctx* h) {
   if (h->opt.precision == 1) return 4;
   return h->opt.ozaki_slices ? h->opt.ozaki_slices : 7;
+}
+
+tmvn_status update_oz_guard(tmvn_ctx* h, cudaStream_t st) {
+  CK(h, launch_oz_guard(h->At, (int)h->m, (int)h->d, h->d_pad, h->dflag, st));
+  unsigned long long bits = 0;
+  CK(h, cudaMemcpyAsync(&bits, h->dflag, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  std::memcpy(&h->oz_ratio, &bits, sizeof(double));
+  h->prof.oz_guard_ratio = h->oz_ratio;
+  return TMVN_OK;
+}
+
+// Arc construction fused into the int8 projection's epilogue (options.fuse_arcs): the
+// per-chain kernel then starts from compacted arc lists instead of the P and Q rows.
+bool fuse_arcs(const tmvn_ctx* h) { return use_oz(h) && h->opt.fuse_arcs != 0; }
+// activity-mask words per chain: ceil(m / 32), padded to 16 bytes (bulk-prefetched rows)
+int amask_words(const tmvn_ctx* h) { return (int)round_up((h->m + 31) / 32, 4); }
+
+tmvn_status ensure_arcs(tmvn_ctx* h) {
+  if (!fuse_arcs(h) || h->arcs_rows >= h->C_pad) return TMVN_OK;
+  free_arcs(h);
+  CK(h, dalloc(&h->arcs, (size_t)h->C_pad * h->m_pad));
+  CK(h, dalloc(&h->amask, (size_t)h->C_pad * amask_words(h)));
+  h->arcs_rows = h->C_pad;
+  return TMVN_OK;
+}
+
+OzArcs arcs_for(const tmvn_ctx* h, int64_t c0, int64_t C, const double* Pb) {
+  OzArcs a;
+  a.P = Pb;
+  a.ldp = h->m_pad;
+  a.b = h->b_eff;
+  a.m = (int)h->m;
+  a.C = (int)C;
+  a.arcs = h->arcs + c0 * h->m_pad;
+  a.ald = h->m_pad;
+  a.mw = amask_words(h);
+  a.amask = h->amask + c0 * a.mw;
+  return a;
 }
 
 // Digits of A' (once per A' and digit count) and the nu digit buffer (per C_pad).
@@ -276,6 +342,10 @@ tmvn_status ensure_ozaki(tmvn_ctx* h) {
                           h->rowscale, st));
     h->ozS_A = S;
     h->ozKB = KB;
+  }
+  if (fuse_arcs(h)) {
+    tmvn_status as = ensure_arcs(h);
+    if (as != TMVN_OK) return as;
   }
   if (h->ozS_N != S || h->Ns_rows < h->C_pad || !h->Xs) {
     dfree(h->Ns); dfree(h->Ns2); dfree(h->Ns3); dfree(h->Xs); dfree(h->xscale);
@@ -299,12 +369,13 @@ int8_t* oz_rows(const tmvn_ctx* h, int64_t c0, int b = 0) {
 }
 
 // Q rows [c0, c0 + Rp) = nu A'^T by the configured projection (nu from buffer b).
+// arcs (nullable, int8 projection only): fuse the arc construction into its epilogue
 cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStream_t st, int b = 0,
-                              double* Qout = nullptr, bool compact = false) {
+                              double* Qout = nullptr, bool compact = false, const OzArcs* arcs = nullptr) {
   double* Qb = (Qout ? Qout : h->Q) + c0 * h->m_pad;
   if (use_oz(h))
     return launch_ozaki_gemm(h->As, h->m_pad, oz_rows(h, c0, b), Rp, h->ozKB, oz_slices(h), h->rowscale,
-                             Qb, h->m_pad, st, compact);
+                             Qb, h->m_pad, st, compact, nullptr, arcs);
   return launch_gemm_tn(nu_f64(h, b) + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad, Qb, h->m_pad, st);
 }
 
@@ -383,6 +454,12 @@ EssParams base_params(tmvn_ctx* h, int C) {
   p.Ns = use_oz(h) ? h->Ns : nullptr;
   p.ozS = oz_slices(h);
   p.ozKB = h->ozKB;
+  if (fuse_arcs(h) && h->arcs) {
+    p.arcs = h->arcs;
+    p.ald = h->m_pad;
+    p.amask = h->amask;
+    p.mw = amask_words(h);
+  }
   return p;
 }
 
@@ -418,6 +495,7 @@ tmvn_status store_X(tmvn_ctx* h, int64_t C, double* out) {
 
 // P = X A'^T, then the strict start check (C18).
 tmvn_status start_check(tmvn_ctx* h, int64_t C, double* P) {
+  Nvtx nv("a0 start check (P = X A'^T, strict a_i.x0 < b_i)");
   cudaStream_t st = stream_of(h);
   // the same product as the periodic refresh, so that a call resumed at a multiple of
   // recompute_every continues bitwise like an uninterrupted one
@@ -464,6 +542,9 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
   EssParams p = base;
   p.t_dev = h->d_tbase;
   p.rec_dev = 1;
+  // one graph serves blocks with and without recorded iterations: round-robin chains
+  // whenever recording is on (the per-group moment rows need a fixed chain -> group map)
+  p.dyn_use = h->opt.record ? 0 : 1;
   p.gen_next = ahead ? 0 : 1;
   if (ahead) p.Ns = nullptr;
   p.t = 0;
@@ -502,7 +583,8 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
         break;
       if ((err = cudaEventRecord(h->ev_rng, h->rng_stream)) != cudaSuccess) break;
     }
-    err = launch_projection(h, 0, Rp, cs, ahead ? (int)(i & 1) : 0);
+    const OzArcs ga = arcs_for(h, 0, C, pc);
+    err = launch_projection(h, 0, Rp, cs, ahead ? (int)(i & 1) : 0, nullptr, false, p.arcs ? &ga : nullptr);
     if (err != cudaSuccess) break;
     p.t = (uint32_t)i;
     p.P_cur = pc;
@@ -569,6 +651,8 @@ tmvn_status run_loop_pipe(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed,
   p.seed = seed;
   p.gen_next = 0;
   p.Ns = nullptr;
+  p.arcs = nullptr;  // GEMM(t + 1) runs beside ESS(t), which is still writing P: no fused arcs
+  p.amask = nullptr;
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   CK(h, cudaMemsetAsync(h->dyn, 0, sizeof(int) * 64 * 16, A));
   p.dyn_ctr = h->dyn;
@@ -609,6 +693,7 @@ tmvn_status run_loop_pipe(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed,
     p.N = nu_f64(h, (int)(t % 3));
     p.t = (uint32_t)t;
     p.record = (rec && !h->affine) ? 1 : 0;
+    p.dyn_use = p.record ? 0 : 1;
     KL(h, launch_ess_step(p, h->plan.grid, A));
     std::swap(P_cur, P_next);
     if (rec && h->affine) {
@@ -636,6 +721,7 @@ tmvn_status run_loop_pipe(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed,
 // depend on the split (no split-K; global chain index in the RNG counters).
 tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, double* P_cur,
                      int64_t* n_recorded) {
+  h->prof.projection_used = use_oz(h) ? 1 : 2;
   if (h->opt.pipeline == 1 && h->nshards == 1 && !h->trace_dev && h->opt.profile == 0 && n_iter > 0)
     return run_loop_pipe(h, C, n_iter, seed, P_cur, n_recorded);
   cudaStream_t st = stream_of(h);
@@ -683,6 +769,10 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * ess_gstash_stride(h->m) : nullptr;
     x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
     x.p.Q = h->Q + x.c0 * h->m_pad;
+    if (x.p.arcs) {
+      x.p.arcs = h->arcs + x.c0 * h->m_pad;
+      x.p.amask = h->amask + x.c0 * x.p.mw;
+    }
     x.p.seed = seed;
     x.Pc = P_cur + x.c0 * h->m_pad;
     x.Pn = P_next + x.c0 * h->m_pad;
@@ -725,6 +815,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
       cudaGraphExec_t ge;
       tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, ahead, seed, &ge);
       if (gs != TMVN_OK) return gs;
+      Nvtx nv("graph block: (a2 projection, ess_kernel) x K, a3 refresh");
       KL(h, launch_set_u32(h->d_tbase, (uint32_t)t, st));
       CK(h, cudaGraphLaunch(ge, st));
       h->prof.launches += (ahead ? 3 : 2) * K + 1;
@@ -743,7 +834,12 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
         KL(h, launch_nu_ahead(h, C, seed, (uint32_t)(t + 1), nullptr, b ^ 1, h->rng_stream));
         CK(h, cudaEventRecord(h->ev_rng, h->rng_stream));
       }
-      TIMED(use_oz(h) ? 2 : 0, x.C, x.st, launch_projection(h, x.c0, Rp, x.st, b));
+      const OzArcs xa = arcs_for(h, x.c0, x.C, x.Pc);
+      {
+        Nvtx nv("a2 projection Q = N A'^T");
+        TIMED(use_oz(h) ? 2 : 0, x.C, x.st,
+              launch_projection(h, x.c0, Rp, x.st, b, nullptr, false, x.p.arcs ? &xa : nullptr));
+      }
       x.p.P_cur = x.Pc;
       x.p.P_next = x.Pn;
       x.p.t = (uint32_t)t;
@@ -753,7 +849,11 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
         x.p.Ns = nullptr;
       }
       x.p.record = (rec && !h->affine) ? 1 : 0;
-      TIMED(x.p.record ? 3 : 1, x.C, x.st, launch_ess_step(x.p, h->plan.grid, x.st));
+      x.p.dyn_use = x.p.record ? 0 : 1;  // recorded: round-robin (per-group moment rows)
+      {
+        Nvtx nv("a1,a3-a9 ess_kernel (arcs, Alg. 3, theta, P', safeguard, x, moments, nu_{t+1})");
+        TIMED(x.p.record ? 3 : 1, x.C, x.st, launch_ess_step(x.p, h->plan.grid, x.st));
+      }
       if (ahead && it + 1 < n_iter) CK(h, cudaStreamWaitEvent(x.st, h->ev_rng, 0));  // nu_{t+1} ready
       std::swap(x.Pc, x.Pn);
       if (rec && h->affine) {
@@ -762,8 +862,10 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
         KL(h, launch_accum_affine(stg, h->d_r128, h->mu, (int)x.C, (int)h->d, h->S1x + x.c0 * h->d,
                                   h->S2x + x.c0 * h->d, x.st));
       }
-      if ((t + 1) % K == 0 && it + 1 < n_iter)
+      if ((t + 1) % K == 0 && it + 1 < n_iter) {
+        Nvtx nv("a3 refresh P = X A'^T");
         TIMED(0, x.C, x.st, launch_refresh(h, x.c0, x.C, x.Pc, x.st));
+      }
     }
     if (rec) ++nrec;
     if (h->trace_dev) {  // S == 1 when tracing
@@ -797,11 +899,13 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
         h->prof.gemm_flops += 2.0 * nC * (double)h->m * (double)h->d;
       } else {
         // P, Q read + P' write (24 B per constraint-eval); X r/w, nu read + next nu write
-        // (32 B per chain-coordinate); moments S1, S2 r/w when recorded (32 B per
-        // chain-coordinate, kind 3)
+        // and its int8 digits (32 + S B per chain-coordinate); when recorded, the moment
+        // rows of the groups (S1, S2 r/w, 32 B per group-coordinate, L2-resident)
+        const double S = use_oz(h) ? (double)oz_slices(h) : 0.0;
         h->prof.ess_launches += 1;
         h->prof.ess_ms += ms;
-        h->prof.ess_bytes += 24.0 * nC * (double)h->m + (kinds[k] == 3 ? 64.0 : 32.0) * nC * (double)h->d;
+        h->prof.ess_bytes += 24.0 * nC * (double)h->m + (32.0 + S) * nC * (double)h->d +
+                             (kinds[k] == 3 ? 32.0 * (double)h->plan.groups * (double)h->d : 0.0);
       }
     }
   }
@@ -810,6 +914,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
 
 // Reduce per-chain moments / rejections into the handle's counters.
 tmvn_status finish_stats(tmvn_ctx* h, int64_t C, int64_t n_iter, int64_t nrec) {
+  Nvtx nv("a9 moment / counter reduction");
   cudaStream_t st = stream_of(h);
   const int64_t d = h->d;
   int64_t* rp = reinterpret_cast<int64_t*>(h->pin);
@@ -916,6 +1021,8 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->pipeline = 0;
   o->latency = 2;
   o->precision = 0;
+  o->total_chains = 0;
+  o->fuse_arcs = 0;  // measured slower on B200 (the epilogue outgrows the MMAs)
   return TMVN_OK;
 }
 
@@ -928,6 +1035,7 @@ tmvn_status tmvn_create(const double* A, const double* b, int64_t m, int64_t d, 
   *out = nullptr;
   if (!A || !b) return fail(nullptr, TMVN_E_ARG, "A and b must be non-null");
   if (m < 1 || d < 1) return fail(nullptr, TMVN_E_ARG, "need m >= 1 and d >= 1");
+  if (d > (1 << 24) || m > (1 << 30)) return fail(nullptr, TMVN_E_ARG, "need d <= 2^24 and m <= 2^30");
   if (m > (1 << 30) || d > (1 << 24)) return fail(nullptr, TMVN_E_ARG, "m or d too large");
   std::vector<double> hA = to_host(A, (size_t)m * d), hb = to_host(b, (size_t)m);
   if (!finite_all(hA) || !finite_all(hb)) return fail(nullptr, TMVN_E_ARG, "A and b must be finite");
@@ -976,6 +1084,11 @@ tmvn_status tmvn_create(const double* A, const double* b, int64_t m, int64_t d, 
   cudaMemcpy(h->b_eff, hb_pad.data(), hb_pad.size() * sizeof(double), cudaMemcpyHostToDevice);
   if ((e = launch_pack(h->A_row, m, d, d, h->A_tiled, h->d_pad, 0)) != cudaSuccess) return bad(e, "pack A");
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bad(e, "create");
+  if (update_oz_guard(h, 0) != TMVN_OK) {
+    std::string msg = h->err;
+    tmvn_destroy(h);
+    return fail(nullptr, TMVN_E_CUDA, msg);
+  }
   *out = h;
   return TMVN_OK;
 }
@@ -992,7 +1105,7 @@ tmvn_status tmvn_set_affine(tmvn_handle h, const double* mu, const double* L) {
     dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
     h->affine = false;
     h->ozS_A = 0;
-    return TMVN_OK;
+    return update_oz_guard(h, st);
   }
   std::vector<double> hmu = mu ? to_host(mu, d) : std::vector<double>(d, 0.0);
   std::vector<double> hL(d * d, 0.0);
@@ -1028,6 +1141,10 @@ tmvn_status tmvn_set_affine(tmvn_handle h, const double* mu, const double* L) {
   dfree(LT); dfree(LTt); dfree(Aprime);
   h->affine = true;
   h->ozS_A = 0;  // A' changed: digits stale
+  {
+    tmvn_status gs = update_oz_guard(h, st);
+    if (gs != TMVN_OK) return gs;
+  }
   dfree(h->S1x); dfree(h->S2x);
   return TMVN_OK;
 }
@@ -1248,6 +1365,7 @@ tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, i
 
 tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_iter, uint64_t seed,
                         double* out) {
+  Nvtx nv("tmvn_sample");
   tmvn_status s = check_sample_args(h, X0, C, n_iter, out);
   if (s != TMVN_OK) return s;
   if ((s = set_device(h)) != TMVN_OK) return s;
@@ -1277,6 +1395,7 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
     cudaStream_t st = stream_of(h);
     CK(h, cudaMemcpyAsync(h->Xsnap, h->X, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
     bool overflow = false;
+    Nvtx nl("latency mode (all iterations, one launch)");
     if ((s = run_latency(h, C, n_iter, seed, lcs, lcap, lgsz, kernel_checks, &nrec, &overflow)) != TMVN_OK)
       return s;
     done = !overflow;
@@ -1321,6 +1440,7 @@ tmvn_status tmvn_reset_stats(tmvn_handle h) {
   if (!h) return fail(nullptr, TMVN_E_ARG, "null handle");
   h->stats = tmvn_stats{};
   h->prof = tmvn_profile{};
+  h->prof.oz_guard_ratio = h->oz_ratio;
   std::fill(h->mom_sum.begin(), h->mom_sum.end(), 0.0);
   std::fill(h->mom_sq.begin(), h->mom_sq.end(), 0.0);
   return TMVN_OK;
@@ -1543,7 +1663,11 @@ tmvn_status tmvn_test_step(tmvn_handle h, const double* Xt, int64_t C, uint64_t 
   // int8 projection, FP64 DMMA otherwise), as at the start check and every K iterations
   CK(h, launch_refresh(h, 0, C, h->P0, st));
   CK(h, launch_first_nu(h, C, seed, (uint32_t)t, st));
-  CK(h, launch_projection(h, 0, h->C_pad, st));
+  {
+    const OzArcs ta = arcs_for(h, 0, C, h->P0);
+    const bool fa = fuse_arcs(h) && h->arcs;
+    CK(h, launch_projection(h, 0, h->C_pad, st, 0, nullptr, false, fa ? &ta : nullptr));
+  }
   CK(h, cudaMemsetAsync(h->rej, 0, (size_t)h->C_pad * sizeof(int64_t), st));
   const size_t cm = (size_t)C * m;
   const int64_t cap = dump->seg_cap > 0 ? dump->seg_cap : 0;

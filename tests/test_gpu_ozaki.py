@@ -121,3 +121,55 @@ def test_ozaki_rejects_large_d():
     s = tm.Sampler(A, np.ones(2), latency=0)
     with pytest.raises(tm.TmvnError):
         s.set_options(projection=1)
+
+
+def test_dynamic_range_guard_under_default_options():
+    """VERDICT r1 item 6 / App. A.  The automatic projection takes the int8
+    split only when its stated bound is within 16x the FP64 DMMA bound on every row
+    (tmvn_profile.oz_guard_ratio): rows whose entries span 1e-8..1, and A' = A L for an
+    ill-conditioned L, fall back to DMMA; unit Gaussian rows keep int8.  Either way the
+    step matches the oracle at the north_star bar (1e-10) under default options."""
+    rng = np.random.default_rng(11)
+    m, d, C, seed = 90, 60, 130, 21
+    A = rng.standard_normal((m, d)) * 10.0 ** rng.uniform(-8, 0, size=(m, d))
+    b = rng.uniform(0.3, 1.0, m)
+    x0 = np.zeros(d)
+    s = tm.Sampler(A, b)
+    pr = s.profile()
+    assert pr["oz_guard_ratio"] > 16
+    X = np.tile(x0, (C, 1))
+    r = oracle.run(A, b, X[:16], 20, seed=seed + 1000)
+    X[:16] = r["X"]
+    log = []
+    for t in (0, 7):
+        g = s.test_step(X, seed, t, seg_cap=64)
+        assert compare_step(A, b, X, g, seed, t, range(0, C, 5), log=log, projection=2) <= 2, log
+        X = np.where(g["accept"][:, None], g["x_next"], X)
+    s.sample(np.tile(x0, (C, 1)), 3, seed=seed)
+    assert s.profile()["projection_used"] == 2
+    # unit Gaussian rows: int8
+    Ag, bg, xg = synth.make_instance(3, m=90, d=60)
+    sg = tm.Sampler(Ag, bg)
+    assert sg.profile()["oz_guard_ratio"] <= 16
+    sg.sample(np.tile(xg, (C, 1)), 3, seed=seed)
+    assert sg.profile()["projection_used"] == 1
+    # App. A with an ill-conditioned L = D (I + N) (cond ~ 1e4: D spans four decades, N
+    # strictly lower with small entries): A' = A L spans four decades per row
+    D = np.diag(10.0 ** np.linspace(-4, 0, d))
+    L = D @ (np.eye(d) + np.tril(rng.standard_normal((d, d)) * 0.02, -1))
+    assert np.linalg.cond(L) > 1e3
+    mu = 0.1 * rng.standard_normal(d)
+    x_start = mu.copy()
+    bL = Ag @ x_start + rng.uniform(0.3, 1.0, m)
+    sa = tm.Sampler(Ag, bL, mu=mu, L=L, record=0)
+    assert sa.profile()["oz_guard_ratio"] > 16
+    Aw, bw = oracle.whiten(Ag, bL, mu, L)
+    X = np.tile(x_start, (C, 1))
+    for t in range(5):
+        Xn = sa.sample(X, 1, seed=seed)
+        for c in range(0, C, 13):
+            un, o = oracle.step(Aw, bw, oracle.whiten_point(X[c], mu, L), seed, t, c)
+            xn = oracle.unwhiten_point(un, mu, L)
+            assert np.max(np.abs(Xn[c] - xn)) <= 1e-10 * max(1.0, np.max(np.abs(xn))), (t, c)
+        X = Xn
+    assert sa.profile()["projection_used"] == 2

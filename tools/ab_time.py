@@ -22,7 +22,10 @@ for path in sys.argv[5:] * reps:
         s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
         s.set_options(profile=int(os.environ.get("PROFILE", "1")), chain_warps=W, streams=S, ring=R,
                       rng_ahead=int(os.environ.get("RNG_AHEAD", "0")), schedule=int(os.environ.get("SCHED", "0")),
-                      pipeline=int(os.environ.get("PIPE", "0")), latency=int(os.environ.get("LATENCY", "0")))
+                      pipeline=int(os.environ.get("PIPE", "0")), latency=int(os.environ.get("LATENCY", "0")),
+                      record=int(os.environ.get("RECORD", "1")))
+        if "FUSE" in os.environ:
+            s.set_options(fuse_arcs=int(os.environ["FUSE"]))
         X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
         s.sample(X, int(os.environ.get("WARM", "200" if k in (2, 3) else "10")), cfg.chain_seed, out=X)
         s.reset_stats()
@@ -30,7 +33,7 @@ for path in sys.argv[5:] * reps:
         s.sample(X, iters, cfg.chain_seed, out=X)
         torch.cuda.synchronize(); dt = time.perf_counter() - t0
         pr = s.profile()
-        print(f"{os.path.basename(path)} rng_ahead={os.environ.get('RNG_AHEAD', '0')} sched={os.environ.get('SCHED', '0')} pipe={os.environ.get('PIPE', '0')} lat={os.environ.get('LATENCY', '0')} W={W} S={S} R={R} cfg{k}: {dt/iters*1e3:.3f} ms/iter  gemm "
+        print(f"{os.path.basename(path)} fuse={os.environ.get('FUSE', '-')} rec={os.environ.get('RECORD', '1')} rng_ahead={os.environ.get('RNG_AHEAD', '0')} sched={os.environ.get('SCHED', '0')} pipe={os.environ.get('PIPE', '0')} lat={os.environ.get('LATENCY', '0')} W={W} S={S} R={R} cfg{k}: {dt/iters*1e3:.3f} ms/iter  gemm "
               f"{pr['gemm_ms']/max(1,pr['gemm_launches']):.3f} ms  tc {pr['tc_ms']/max(1,pr['tc_launches']):.3f} ms"
               f"  ess {pr['ess_ms']/max(1,pr['ess_launches']):.3f} ms"
               f"  evals/s {cfg.C*cfg.m*iters/dt:.3e}", flush=True)

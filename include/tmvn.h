@@ -199,6 +199,15 @@ typedef struct {
    * bound on 8 warps, doubles the projection's time, 0.177 -> 0.321 ms, while the
    * per-chain kernel gains 0.017-0.040 ms).  Results do not depend on it. */
   int32_t fuse_arcs;
+  /* 1: with the int8 projection, nu for iteration t + 1 (Philox4x32-10 +
+   * Box-Muller, C12, and its int8 digits) is drawn by the projection GEMM of
+   * iteration t in its epilogue warps between tiles -- while the tensor cores run
+   * -- instead of by the per-chain kernel after its update (nu double-buffered).
+   * Same device function and counters: bitwise the same chains.  Ignored with
+   * rng_ahead or pipeline.  0 (default): the per-chain kernel draws it (B200:
+   * the per-chain kernel gains ~26 us at config 3, the projection loses ~21 us --
+   * 0.384 vs 0.383 ms per iteration -- and config 5 loses 3 %). */
+  int32_t rng_gemm;
 } tmvn_options;
 
 typedef struct {

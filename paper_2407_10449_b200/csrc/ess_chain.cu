@@ -50,6 +50,7 @@ __device__ __forceinline__ double bitsd(uint64_t b) { return __longlong_as_doubl
 
 struct Ctl {
   uint64_t rlo, rhi, klo;
+  uint64_t pqbar;       // mbarrier: the chain's P and Q rows bulk-copied into shared memory
   int shift, mode;      // key: mode 0 linear on [0, 2 pi]; mode 1 (bits - klo) >> shift
   double G;             // running gamma: max beta over every arc already passed
   int n_act;
@@ -295,13 +296,33 @@ __device__ void grp_sort(const Grp<W>& g, const Smem& S, int n) {
   }
 }
 
+// Where the arcs of the active constraints live, by slot (compaction order):
+//   kRows = false: stash[slot] = (alpha, beta) (shared or global memory);
+//   kRows = true:  the chain's P and Q rows in shared memory (bulk-copied ahead of the
+//                  chain), the arc of constraint i written over (Ps[i], Qs[i]), and
+//                  idx[slot] = i.
+template <bool kRows>
+struct ArcStore {
+  double2* st;
+  double* Ps;
+  double* Qs;
+  int* idx;
+  __device__ __forceinline__ double2 get(int slot) const {
+    if (kRows) {
+      const int i = idx[slot];
+      return make_double2(Ps[i], Qs[i]);
+    }
+    return st[slot];
+  }
+};
+
 // Gather the arcs of live buckets with key < jo into keys/vals, sort, emit gaps.
-template <int W>
-__device__ void process_batch(const Grp<W>& g, const Smem& S, Ctl& ctl, const double2* stash,
+template <int W, bool kRows>
+__device__ void process_batch(const Grp<W>& g, const Smem& S, Ctl& ctl, const ArcStore<kRows>& stash,
                               int n_act, int jo, int n_live, int NB, double scale, double2* gg,
                               uint64_t* s_w64, int* s_w32) {
   for (int idx = g.tid; idx < n_act; idx += Grp<W>::kThreads) {
-    double2 ab = stash[idx];
+    double2 ab = stash.get(idx);
     uint64_t bits = dbits(ab.x);
     if (bits < ctl.rlo || bits > ctl.rhi) continue;
     int k = bucket_key(ab.x, ctl, NB, scale);
@@ -353,8 +374,8 @@ __device__ void process_batch(const Grp<W>& g, const Smem& S, Ctl& ctl, const do
 // used when more than 32 arcs are live.  On entry the level-1 bucket statistics
 // (linear keys on [0, 2 pi]; count, max beta exact, max alpha high word) are
 // filled and untouched.
-template <int W>
-__device__ void build_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const double2* stash,
+template <int W, bool kRows>
+__device__ void build_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const ArcStore<kRows>& stash,
                                 int NB, int log2NB, double scale, double2* gg, uint64_t* s_w64,
                                 int* s_w32) {
   constexpr int T = Grp<W>::kThreads;
@@ -365,14 +386,14 @@ __device__ void build_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const 
       clear_buckets(g, S, NB);
       g.sync();
       for (int idx = g.tid; idx < n_act; idx += T) {
-        double2 ab = stash[idx];
+        double2 ab = stash.get(idx);
         uint64_t bits = dbits(ab.x);
         if (bits < ctl.rlo || bits > ctl.rhi) continue;
         bucket_add<true>(S, bucket_key(ab.x, ctl, NB, scale), ab.x, ab.y);
       }
       g.sync();
       for (int idx = g.tid; idx < n_act; idx += T) {
-        double2 ab = stash[idx];
+        double2 ab = stash.get(idx);
         uint64_t bits = dbits(ab.x);
         if (bits < ctl.rlo || bits > ctl.rhi) continue;
         bucket_add_lo<true>(S, bucket_key(ab.x, ctl, NB, scale), ab.x, ab.y);
@@ -486,8 +507,8 @@ __device__ void build_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const 
 // false, touching only gin / cand / fill, when more than kLiveCap arcs are live:
 // the general path (build_intervals) then runs on the untouched statistics.
 // ---------------------------------------------------------------------------
-template <int W>
-__device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const double2* stash,
+template <int W, bool kRows>
+__device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const ArcStore<kRows>& stash,
                               int NB, double scale, double2* gg, uint64_t* s_w64, int* s_w32) {
   constexpr int T = Grp<W>::kThreads;
   const int per = (NB + T - 1) / T;
@@ -519,7 +540,7 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const do
   // B2: gather the live buckets' arcs, grouped by bucket
   const int n_act = ctl.n_act;
   for (int idx = g.tid; idx < n_act; idx += T) {
-    const double2 ab = stash[idx];
+    const double2 ab = stash.get(idx);
     const int k = bucket_key(ab.x, ctl, NB, scale);
     const int ok = S.off[k];
     if (ok >= 0) {
@@ -631,17 +652,19 @@ __device__ void theta_from_gaps(const Smem& S, Ctl& ctl, double2* gg, double u, 
 }
 
 // Per-group shared memory: bucket arrays, live buffer, gaps (stash after them).
+// The fixed-size arrays first (constant offsets from the group's base, folded into the
+// shared-memory instructions), then the NB-sized ones.
 __device__ __forceinline__ Smem carve(unsigned char* base, int NB) {
   Smem S;
-  S.maxA = reinterpret_cast<uint64_t*>(base);
-  S.Gx = S.maxA + NB;
-  S.minA = S.Gx + NB;
-  S.keys = S.minA + NB;
+  S.keys = reinterpret_cast<uint64_t*>(base);
   S.vals = reinterpret_cast<double*>(S.keys + kLiveCap);
   S.gaps = reinterpret_cast<double2*>(S.vals + kLiveCap);
-  S.gin = reinterpret_cast<uint64_t*>(S.gaps + kGapSmem);
-  S.cand = S.gin + NB;
-  S.cnt = reinterpret_cast<int*>(S.cand + 2 * kLiveCap);
+  S.cand = reinterpret_cast<uint64_t*>(S.gaps + kGapSmem);
+  S.maxA = S.cand + 2 * kLiveCap;
+  S.Gx = S.maxA + NB;
+  S.minA = S.Gx + NB;
+  S.gin = S.minA + NB;
+  S.cnt = reinterpret_cast<int*>(S.gin + NB);
   S.off = S.cnt + NB;
   S.fill = S.off + NB;
   return S;
@@ -672,13 +695,16 @@ __device__ __forceinline__ void stash_arc(const Smem& S, Ctl& ctl, double2* stas
 #ifndef TMVN_ESS_MIN_BLOCKS
 #define TMVN_ESS_MIN_BLOCKS 3
 #endif
+#ifndef TMVN_ESS_W8_BLOCKS
+#define TMVN_ESS_W8_BLOCKS 4
+#endif
 // threads per CTA: 256 (8 / W chain groups), or one 32 W-thread group when W = 16
 __host__ __device__ constexpr int ess_threads(int W) { return W > 8 ? 32 * W : kEssThreads; }
 __host__ __device__ constexpr int ess_groups(int W) { return W >= 8 ? 1 : 8 / W; }
 template <int W, bool kRing, bool kSmemStash>
 constexpr int ess_min_blocks() {
   return W > 8 ? 2
-               : (W == 8 && kSmemStash && !kRing) ? (TMVN_ESS_MIN_BLOCKS > 4 ? TMVN_ESS_MIN_BLOCKS : 4)
+               : (W == 8 && kSmemStash && !kRing) ? TMVN_ESS_W8_BLOCKS
                                                   : TMVN_ESS_MIN_BLOCKS;
 }
 // kSrc: where phase A's arcs come from -- 0: P and Q rows read from global memory (the
@@ -707,21 +733,39 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
   const int log2NB = 31 - __clz(NB);
   const int m = p.m;
   const int CH = p.CH;
-  const size_t gbytes = ess_group_smem_bytes(m, NB, p.stash_smem, CH);
-  unsigned char* gbase = smem_raw + (size_t)g.gid * gbytes;
+  // per-group layout offsets precomputed on the host (EssParams): no size arithmetic here
+  unsigned char* gbase = smem_raw + g.gid * p.grp_bytes;
   double* ring = reinterpret_cast<double*>(gbase);  // slot s: P at ring + 2 s CH, Q after it
   uint64_t* rbar = reinterpret_cast<uint64_t*>(gbase + (size_t)CH * 32);
-  Smem S = carve(gbase + ess_ring_bytes(CH), NB);
+  Smem S = carve(gbase + p.base_off, NB);
   const int64_t gglobal = (int64_t)blockIdx.x * kGroups + g.gid;  // group id in the grid
   // the stash's address space is a template parameter, so that every access
   // compiles to LDS/STS (shared) or LDG/STG (global) -- a run-time choice would
   // make them generic loads, ~2K cycles per dependent list hop
   double2* stash;   // arcs in production order
   if (kSmemStash) {
-    stash = reinterpret_cast<double2*>(gbase + ess_ring_bytes(CH) + ess_group_base_bytes(NB));
+    stash = reinterpret_cast<double2*>(gbase + p.stash_off);
   } else {
     stash = p.gstash + (gglobal + p.group_base) * ess_gstash_stride(m);
   }
+  // production path with the arcs in shared memory: the chain's P and Q rows are
+  // bulk-copied (cp.async.bulk, TMA engine: no registers, no load latency exposed)
+  // into the stash region while the previous chain runs phases D; phase A tests and
+  // computes the arcs from there
+  constexpr bool kRows = !kGiven && kSrc == 0 && kSmemStash;
+  const int mm = (m + 1) & ~1;
+  ArcStore<kRows> AS;
+  AS.st = stash;
+  AS.Ps = reinterpret_cast<double*>(stash);
+  AS.Qs = AS.Ps + mm;
+  AS.idx = reinterpret_cast<int*>(AS.Qs + mm);
+  uint32_t pqphase = 0;
+  auto pq_issue = [&](int64_t cn) {  // one thread
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&ctl.pqbar, (uint32_t)mm * 16u);
+    bulk_g2s(AS.Ps, p.P_cur + cn * p.ldp, (uint32_t)mm * 8u, &ctl.pqbar);
+    bulk_g2s(AS.Qs, p.Q + cn * p.ldp, (uint32_t)mm * 8u, &ctl.pqbar);
+  };
   double2* gg = p.ggaps + (gglobal + p.group_base) * (m + 2);
   const double scale = __ddiv_rn((double)NB, kTwoPi);
   const int64_t ngroups = (int64_t)gridDim.x * kGroups;
@@ -730,12 +774,11 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
   long long t_prev = clock64();
 #endif
 
-  // P/Q chunk stream (production path): the group's chains are gglobal + k ngroups;
+  // P/Q chunk stream (options.ring): the group's chains are gglobal + k ngroups;
   // chain k uses chunk sequence numbers k spc .. k spc + spc - 1 (A pass, then a D1
   // pass when the row spans several chunks); sequence q lives in ring slot q & 1.
   // Consuming q issues q + 1, so the next chunk -- the next chain's rows at the end
   // of a chain -- is in flight while this one is processed.
-  const int mm = (m + 1) & ~1;
   const int nch = (mm + CH - 1) / CH;
   const int spc = nch == 1 ? 1 : 2 * nch;
   const int64_t nmy = gglobal < p.C ? (p.C - gglobal + ngroups - 1) / ngroups : 0;
@@ -787,6 +830,15 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     if (g.tid == T - 1) ctl.next = atomicAdd(ctr, 1);
     g.sync();
   }
+  if (kRows) {  // the first chain's rows
+    if (g.tid == T - 1) {
+      mbar_init(&ctl.pqbar, 1);
+      mbar_fence_init();
+      const int64_t c0 = dyn ? (int64_t)ctl.next : gglobal;
+      if (c0 < p.C) pq_issue(c0);
+    }
+    g.sync();
+  }
   for (int64_t cc = dyn ? (int64_t)ctl.next : gglobal; cc < p.C;
        cc = dyn ? (int64_t)ctl.next : cc + ngroups) {
     const int c = (int)cc;
@@ -814,7 +866,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.arcs + cn * p.ald),
                      "r"((uint32_t)m * 16u) : "memory");
       }
-      if (!kRing && !kArcsIn && cn < p.C) {
+      if (!kRing && !kArcsIn && !kRows && cn < p.C) {
         const uint32_t bytes = (uint32_t)(((int64_t)m * 8 + 15) & ~15ll);
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.P_cur + cn * p.ldp), "r"(bytes)
                      : "memory");
@@ -954,6 +1006,66 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         ++qseq;
         g.sync();  // the slot may be refilled from now on
       }
+          } else if (kRows) {
+      // (1) the active test (C3/C25) on every constraint pair from the rows in shared
+      // memory, the active indices compacted; (2) the arcs of the active constraints,
+      // every lane busy, each written over its own (P, Q) entry
+      mbar_wait(&ctl.pqbar, pqphase);
+      pqphase ^= 1u;
+      const double2* P2 = reinterpret_cast<const double2*>(AS.Ps);
+      const double2* Q2 = reinterpret_cast<const double2*>(AS.Qs);
+      const double2* B2 = reinterpret_cast<const double2*>(p.b);
+      int* sidx = AS.idx;
+      const int npairs = (m + 1) / 2;
+      const int npr = (npairs + T - 1) / T * T;  // whole warps stay in the loop (ballots)
+      for (int pi = g.tid; pi < npr; pi += T) {
+        const bool in = pi < npairs;
+        double2 pp = make_double2(0.0, 0.0), qq = pp, bb = pp;
+        if (in) {
+          pp = P2[pi];
+          qq = Q2[pi];
+          bb = __ldg(B2 + pi);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = 2 * pi + h;
+          const bool act = in && i < m && arc_active(h ? pp.y : pp.x, h ? qq.y : qq.x, h ? bb.y : bb.x);
+          if (p.d_alpha && in && i < m && !act) {
+            p.d_alpha[(int64_t)c * m + i] = 0.0;
+            p.d_beta[(int64_t)c * m + i] = 0.0;
+            p.d_active[(int64_t)c * m + i] = 0;
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, act);
+          if (mask) {
+            const int leader = __ffs(mask) - 1;
+            int sb = 0;
+            if (g.lane == leader) sb = atomicAdd(&ctl.n_act, __popc(mask));
+            sb = __shfl_sync(0xffffffffu, sb, leader);
+            if (act) sidx[sb + __popc(mask & ((1u << g.lane) - 1u))] = i;
+          }
+        }
+      }
+      g.sync();
+      PHASE(10);  // A1: active test + compaction (the rest of phase A goes to slot 1)
+      if (g.tid == T - 1) {  // phase D's P and Q rows (global) back into L2 before it reads them
+        const uint32_t bytes = (uint32_t)mm * 8u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Prow), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Qrow), "r"(bytes) : "memory");
+      }
+      const int n_act = ctl.n_act;
+      for (int slot = g.tid; slot < n_act; slot += T) {
+        const int i = sidx[slot];
+        double al, be;
+        arc_of(AS.Ps[i], AS.Qs[i], __ldg(p.b + i), al, be);  // active by pass 1: same predicate
+        AS.Ps[i] = al;
+        AS.Qs[i] = be;
+        bucket_add<false>(S, bucket_key(al, ctl, NB, scale), al, be);
+        if (p.d_alpha) {
+          p.d_alpha[(int64_t)c * m + i] = al;
+          p.d_beta[(int64_t)c * m + i] = be;
+          p.d_active[(int64_t)c * m + i] = 1;
+        }
+      }
           } else {
       // two passes: (1) the active test (C3/C25) on every constraint pair, active
       // (p, q) and the index compacted into the stash; (2) the arcs of the active
@@ -1032,7 +1144,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     {
       const int n_act = ctl.n_act;
       for (int idx = g.tid; idx < n_act; idx += T) {
-        const double2 ab = stash[idx];
+        const double2 ab = AS.get(idx);
         bucket_add_lo<false>(S, bucket_key(ab.x, ctl, NB, scale), ab.x, ab.y);
       }
       g.sync();
@@ -1040,7 +1152,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     PHASE(2);  // low-word pass
 
     // ---------------- B + C: I_act by Alg. 3, then theta ----------------
-    const bool fast = par_intervals(g, S, ctl, stash, NB, scale, gg, s_w64, s_w32);
+    const bool fast = par_intervals(g, S, ctl, AS, NB, scale, gg, s_w64, s_w32);
     if (fast && g.tid == T - 1) {  // theta on the highest warp (arbiter: highest warp id first)
       const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : ctl.u;
       theta_from_gaps(S, ctl, gg, u, p.eps);
@@ -1049,7 +1161,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     PHASE(3);  // B (+C) on the parallel path
     PHASE_ADD(7, fast ? 0 : 1);
     if (!fast) {
-      build_intervals(g, S, ctl, stash, NB, log2NB, scale, gg, s_w64, s_w32);
+      build_intervals(g, S, ctl, AS, NB, log2NB, scale, gg, s_w64, s_w32);
       if (g.tid == 0) {
         const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : ctl.u;
         theta_from_gaps(S, ctl, gg, u, p.eps);
@@ -1058,6 +1170,10 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     }
     PHASE(4);  // B + C on the general path (rare)
     PHASE_ADD(9, ctl.ngap);
+    if (kRows && g.tid == T - 1) {  // stash free: the next chain's P and Q rows, beside phase D
+      const int64_t cn = dyn ? (int64_t)ctl.next : cc + ngroups;
+      if (cn < p.C) pq_issue(cn);
+    }
     if (g.tid == 0) {
       if (p.d_nseg) p.d_nseg[c] = ctl.nseg;
       if (p.d_L) p.d_L[c] = ctl.L;
@@ -1173,7 +1289,11 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         *s2 = a2;
       }
       if (p.gen_next) {
+#ifdef TMVN_EXP_NO_RNG  // timing experiment only (wrong results): the kernel without drawing nu
+        const double2 nv = make_double2(xv.y * 1e-3, xv.x * 1e-3);
+#else
         const double2 nv = normal_pair_at(p.seed, t_it + 1, gchain, k, p.d);
+#endif
         *nr = nv;
         if (p.Ns) oz_put_nu_pair_s(p.Ns + (zrow + oz_col(k, p.ozS, kOzNuRows)), nv.x, nv.y, p.ozS);
       }
@@ -1219,9 +1339,13 @@ cudaError_t launch_w(const EssParams& p, int grid, size_t smem, cudaStream_t st)
 }
 
 template <bool kGiven>
-cudaError_t launch_any(const EssParams& p, int grid, cudaStream_t st) {
+cudaError_t launch_any(const EssParams& p0, int grid, cudaStream_t st) {
   if (grid < 1) return cudaSuccess;
-  const size_t smem = (size_t)ess_groups(p.W) * ess_group_smem_bytes(p.m, p.NB, p.stash_smem, p.CH);
+  EssParams p = p0;
+  p.grp_bytes = (int)ess_group_smem_bytes(p.m, p.NB, p.stash_smem, p.CH);
+  p.base_off = (int)ess_ring_bytes(p.CH);
+  p.stash_off = p.base_off + (int)ess_group_base_bytes(p.NB);
+  const size_t smem = (size_t)ess_groups(p.W) * (size_t)p.grp_bytes;
   switch (p.W) {
     case 1: return launch_w<1, kGiven>(p, grid, smem, st);
     case 2: return launch_w<2, kGiven>(p, grid, smem, st);

@@ -220,12 +220,35 @@ __device__ unsigned long long g_oz_cycles[8];
 // TMEM lanes 32 (w % 4) .. 32 (w % 4) + 31 only: each role covers the 4 quadrants)
 // STAGES: ring depth (0 = as many as fit; 3 = the compact variant that leaves room
 // on the SM for a CTA of the per-chain kernel when the two run concurrently)
-template <int S, int STAGES, bool CS, bool ARCS>
+// nu_{t+1} drawn by the epilogue warps between tiles (options.rng_gemm): blocks of 256
+// coordinate pairs of the chains b, b + grid, ... of this CTA, a share after each tile
+// (the warps are otherwise waiting for the next tile's accumulators) and the rest at
+// the end.  Same device function and counters as everywhere (C12): bitwise the same nu.
+__device__ __forceinline__ void oz_rng_blocks(const OzRng& r, uint32_t t_gen, int et, int64_t& chain, int& pk0,
+                                              int nblk) {
+  const int kpairs = (int)(r.d_pad / 2);
+  for (int i = 0; i < nblk && chain < r.C; ++i) {
+    const int pk = pk0 + et;
+    if (pk < kpairs) {
+      const int k = 2 * pk;
+      const double2 nv = normal_pair_at(r.seed, t_gen, r.chain_offset + (uint32_t)chain, k, r.d);
+      *reinterpret_cast<double2*>(r.N + tiled_row(chain, r.d_pad) + tiled_col(k)) = nv;
+      oz_put_nu_pair_s(r.Ns + oz_row(chain, r.S, r.KB, kOzNuRows) + oz_col(k, r.S, kOzNuRows), nv.x, nv.y, r.S);
+    }
+    pk0 += 32 * kOzEpiWarps;
+    if (pk0 >= kpairs) {
+      pk0 = 0;
+      chain += gridDim.x;
+    }
+  }
+}
+
+template <int S, int STAGES, bool CS, bool ARCS, bool RNG>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ozaki_gemm_kernel(const int8_t* __restrict__ As, const int8_t* __restrict__ Ns,
                       const double* __restrict__ rowscale, const double* __restrict__ colscale,
                       double* __restrict__ Q, int64_t ldq, int MB, int NBt, int KB, int dbg_seq,
-                      const OzArcs arc) {
+                      const OzArcs arc, const OzRng rng) {
   constexpr int kStage = oz_stage_bytes(S);
   constexpr int kOzStages = STAGES ? STAGES : oz_stages(S);
   constexpr int NTS = oz_nts<S>();
@@ -378,6 +401,19 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     const int c0 = ((warp - 6) / 4) * (kOzBN * 4 / kOzEpiWarps);
     const int row_in_tile = quad * 32 + lane;
     uint32_t tcount = 0;
+    // RNG share per tile: this CTA's blocks of pairs spread over its tiles
+    const int et = threadIdx.x - 32 * 6;
+    int64_t rchain = blockIdx.x;
+    int rpk0 = 0;
+    int rshare = 0;
+    uint32_t t_gen = 0;
+    if (RNG) {
+      t_gen = (rng.t_dev ? *rng.t_dev : 0u) + rng.t + 1u;
+      const int nblk_chain = (int)((rng.d_pad / 2 + 32 * kOzEpiWarps - 1) / (32 * kOzEpiWarps));
+      const int64_t nch = blockIdx.x < rng.C ? (rng.C - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+      const int ntiles = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+      rshare = (int)((nch * nblk_chain + ntiles - 1) / (ntiles > 0 ? ntiles : 1));
+    }
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
       int mb, nb;
       oz_tile(tile, MB, NBt, mb, nb);
@@ -444,10 +480,12 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           }
         }
       }
+      if (RNG) oz_rng_blocks(rng, t_gen, et, rchain, rpk0, rshare);
 #ifdef TMVN_PHASE_TIMING
       acc1 += clock64() - g1;
 #endif
     }
+    if (RNG) oz_rng_blocks(rng, t_gen, et, rchain, rpk0, 1 << 30);  // the rest
   }
 #ifdef TMVN_PHASE_TIMING
   if (lane == 0) {
@@ -529,10 +567,10 @@ cudaError_t launch_oz_slice(const double* src_tiled, int64_t R, int64_t d, int64
   return cudaGetLastError();
 }
 
-template <int S, int STAGES, bool CS, bool ARCS>
+template <int S, int STAGES, bool CS, bool ARCS, bool RNG = false>
 static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                                int64_t KB, const double* rowscale, const double* colscale, double* Q,
-                               int64_t ldq, cudaStream_t st, const OzArcs& arc) {
+                               int64_t ldq, cudaStream_t st, const OzArcs& arc, const OzRng& rng = OzRng{}) {
   static int num_sms = 0;
   if (!num_sms) {
     int dev = 0;
@@ -540,23 +578,34 @@ static cudaError_t launch_oz_t(const int8_t* As, int64_t M_pad, const int8_t* Ns
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t smem = ozaki_smem_bytes(S, STAGES);
-  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, STAGES, CS, ARCS>,
+  cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, STAGES, CS, ARCS, RNG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int MB = (int)(M_pad / kOzBM), NBt = (int)(N_pad / kOzBN);
   const int tiles = MB * NBt;
   const int grid = tiles < num_sms ? tiles : num_sms;
-  ozaki_gemm_kernel<S, STAGES, CS, ARCS><<<grid, kOzThreads, smem, st>>>(
-      As, Ns, rowscale, colscale, Q, ldq, MB, NBt, (int)KB, g_oz_launch_seq++, arc);
+  ozaki_gemm_kernel<S, STAGES, CS, ARCS, RNG><<<grid, kOzThreads, smem, st>>>(
+      As, Ns, rowscale, colscale, Q, ldq, MB, NBt, (int)KB, g_oz_launch_seq++, arc, rng);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
-                              cudaStream_t st, bool compact, const double* colscale, const OzArcs* arcs) {
+                              cudaStream_t st, bool compact, const double* colscale, const OzArcs* arcs,
+                              const OzRng* rng) {
   if (M_pad % kOzBM || N_pad % kOzBN || KB < 1) return cudaErrorInvalidValue;
-  if (arcs && (colscale || compact)) return cudaErrorInvalidValue;
+  if ((arcs || rng) && (colscale || compact)) return cudaErrorInvalidValue;
+  if (arcs && rng) return cudaErrorInvalidValue;
   const OzArcs none{};
+  if (rng) {
+    switch (S) {
+      case 4: return launch_oz_t<4, 0, false, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, none, *rng);
+      case 6: return launch_oz_t<6, 0, false, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, none, *rng);
+      case 7: return launch_oz_t<7, 0, false, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, none, *rng);
+      case 8: return launch_oz_t<8, 0, false, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, none, *rng);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (arcs) {
     switch (S) {
       case 4: return launch_oz_t<4, 0, false, true>(As, M_pad, Ns, N_pad, KB, rowscale, colscale, Q, ldq, st, *arcs);

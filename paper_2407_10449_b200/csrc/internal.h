@@ -32,10 +32,25 @@ struct OzArcs {
   uint32_t* amask;
   int mw;
 };
+// nu_{t_gen} for chains [0, C) (global index chain_offset + c), t_gen = (*t_dev or 0) +
+// t + 1, drawn by the projection's epilogue warps between tiles into N (tiled C_pad x
+// d_pad FP64) and its S int8 digits into Ns (options.rng_gemm).
+struct OzRng {
+  uint64_t seed;
+  uint32_t t;
+  const uint32_t* t_dev;
+  uint32_t chain_offset;
+  int C, d;
+  int64_t d_pad;
+  double* N;
+  int8_t* Ns;
+  int S;
+  int64_t KB;
+};
 cudaError_t launch_ozaki_gemm(const int8_t* As, int64_t M_pad, const int8_t* Ns, int64_t N_pad,
                               int64_t KB, int S, const double* rowscale, double* Q, int64_t ldq,
                               cudaStream_t st, bool compact = false, const double* colscale = nullptr,
-                              const OzArcs* arcs = nullptr);
+                              const OzArcs* arcs = nullptr, const OzRng* rng = nullptr);
 // digits of the R rows of a fragment-tiled FP64 matrix into the oz layout with BR
 // rows per block; per_row: exponent from each row's max |v| (rowscale[r] =
 // 2^(e_r + e_other - 14)), else the fixed exponent e_fixed (|v| < 2^e_fixed).
@@ -157,6 +172,7 @@ struct EssParams {
   int W;            // warps per chain (1, 2, 4, 8)
   int stash_smem;   // 1: arcs stashed in shared memory
   int CH;           // constraints per P/Q chunk streamed into shared memory (even)
+  int grp_bytes, base_off, stash_off;  // per-group shared-memory layout (set by the launcher)
   // dumps (nullable)
   double* d_alpha;
   double* d_beta;
@@ -185,7 +201,9 @@ __host__ __device__ inline size_t ess_group_base_bytes(int NB) {
 }
 __host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_smem, int CH) {
   size_t s = ess_ring_bytes(CH) + ess_group_base_bytes(NB);
-  if (stash_smem) s += (size_t)m * 20;  // stash of the arcs + constraint index (phase A compaction)
+  // stash: the arcs + constraint index (phase A compaction), or the chain's P and Q rows
+  // (even length) + the compacted active indices
+  if (stash_smem) s += (size_t)((m + 1) & ~1) * 16 + (size_t)m * 4;
   return (s + 15) / 16 * 16;
 }
 

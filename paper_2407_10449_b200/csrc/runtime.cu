@@ -368,14 +368,38 @@ int8_t* oz_rows(const tmvn_ctx* h, int64_t c0, int b = 0) {
   return nu_dig(h, b) + (c0 / kOzNuRows) * h->ozKB * kOzStepK * oz_slices(h) * kOzNuRows;
 }
 
+// nu_{t+1} drawn by the int8 projection of iteration t in its epilogue warps (between
+// tiles, while the tensor cores run) instead of by the per-chain kernel after its update
+// (options.rng_gemm): nu_t then lives in buffer t & 1.  Not with rng_ahead / pipeline.
+bool rng_in_gemm(const tmvn_ctx* h) { return use_oz(h) && h->opt.rng_gemm != 0 && h->opt.rng_ahead == 0; }
+
+OzRng rng_for(const tmvn_ctx* h, int64_t c0, int64_t C, uint64_t seed, uint32_t t, const uint32_t* t_dev,
+              int b_out) {
+  OzRng r;
+  r.seed = seed;
+  r.t = t;
+  r.t_dev = t_dev;
+  r.chain_offset = (uint32_t)(h->opt.chain_offset + c0);
+  r.C = (int)C;
+  r.d = (int)h->d;
+  r.d_pad = h->d_pad;
+  r.N = nu_f64(h, b_out) + c0 * h->d_pad;
+  r.Ns = oz_rows(h, c0, b_out);
+  r.S = oz_slices(h);
+  r.KB = h->ozKB;
+  return r;
+}
+
 // Q rows [c0, c0 + Rp) = nu A'^T by the configured projection (nu from buffer b).
 // arcs (nullable, int8 projection only): fuse the arc construction into its epilogue
+// rng (nullable, int8 projection only): also draw nu_{t+1} in its epilogue warps
 cudaError_t launch_projection(const tmvn_ctx* h, int64_t c0, int64_t Rp, cudaStream_t st, int b = 0,
-                              double* Qout = nullptr, bool compact = false, const OzArcs* arcs = nullptr) {
+                              double* Qout = nullptr, bool compact = false, const OzArcs* arcs = nullptr,
+                              const OzRng* rng = nullptr) {
   double* Qb = (Qout ? Qout : h->Q) + c0 * h->m_pad;
   if (use_oz(h))
     return launch_ozaki_gemm(h->As, h->m_pad, oz_rows(h, c0, b), Rp, h->ozKB, oz_slices(h), h->rowscale,
-                             Qb, h->m_pad, st, compact, nullptr, arcs);
+                             Qb, h->m_pad, st, compact, nullptr, arcs, rng);
   return launch_gemm_tn(nu_f64(h, b) + c0 * h->d_pad, Rp, h->At, h->m_pad, h->d_pad, Qb, h->m_pad, st);
 }
 
@@ -537,22 +561,23 @@ bool recorded_iter(const tmvn_options& o, int64_t t) {
 // read t from h->d_tbase (set by a one-thread kernel before each replay) and
 // compute their record flag from t, so one graph serves every aligned block.
 tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K, double* Pc,
-                        double* Pn, bool ahead, uint64_t seed, cudaGraphExec_t* out) {
+                        double* Pn, bool ahead, bool gem, uint64_t seed, cudaGraphExec_t* out) {
   const int parity = Pc == h->P0 ? 0 : 1;
+  const bool twobuf = ahead || gem;  // nu_t in buffer t & 1
   EssParams p = base;
   p.t_dev = h->d_tbase;
   p.rec_dev = 1;
   // one graph serves blocks with and without recorded iterations: round-robin chains
   // whenever recording is on (the per-group moment rows need a fixed chain -> group map)
   p.dyn_use = h->opt.record ? 0 : 1;
-  p.gen_next = ahead ? 0 : 1;
-  if (ahead) p.Ns = nullptr;
+  p.gen_next = twobuf ? 0 : 1;
+  if (twobuf) p.Ns = nullptr;
   p.t = 0;
   p.P_cur = Pc;
   p.P_next = Pn;
   std::vector<unsigned char> sig(sizeof(EssParams) + 2 * sizeof(int64_t) + 2 * sizeof(void*) + 16);
   std::memcpy(sig.data() + sizeof(EssParams) + 16 + 2 * sizeof(void*), &seed, 8);
-  const int64_t ah = ahead ? 1 : 0;
+  const int64_t ah = (ahead ? 1 : 0) | (gem ? 2 : 0);
   std::memcpy(sig.data() + sizeof(EssParams) + 24 + 2 * sizeof(void*), &ah, 8);
   std::memcpy(sig.data(), &p, sizeof(EssParams));
   std::memcpy(sig.data() + sizeof(EssParams), &C, sizeof(int64_t));
@@ -584,12 +609,14 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
       if ((err = cudaEventRecord(h->ev_rng, h->rng_stream)) != cudaSuccess) break;
     }
     const OzArcs ga = arcs_for(h, 0, C, pc);
-    err = launch_projection(h, 0, Rp, cs, ahead ? (int)(i & 1) : 0, nullptr, false, p.arcs ? &ga : nullptr);
+    const OzRng gr = rng_for(h, 0, C, seed, (uint32_t)i, h->d_tbase, (int)((i + 1) & 1));
+    err = launch_projection(h, 0, Rp, cs, twobuf ? (int)(i & 1) : 0, nullptr, false, p.arcs ? &ga : nullptr,
+                            gem ? &gr : nullptr);
     if (err != cudaSuccess) break;
     p.t = (uint32_t)i;
     p.P_cur = pc;
     p.P_next = pn;
-    p.N = nu_f64(h, ahead ? (int)(i & 1) : 0);
+    p.N = nu_f64(h, twobuf ? (int)(i & 1) : 0);
     err = launch_ess_step(p, h->plan.grid, cs);
     if (err == cudaSuccess && ahead) err = cudaStreamWaitEvent(cs, h->ev_rng, 0);  // join: nu_{t+i+1} ready
     std::swap(pc, pn);
@@ -735,7 +762,10 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     tmvn_status rs = ensure_rng_stream(h);
     if (rs != TMVN_OK) return rs;
   }
-  CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st, ahead ? (int)(t0 & 1) : 0));
+  // nu_{t+1} drawn by the projection of iteration t (options.rng_gemm): nu_t in buffer t & 1
+  const bool gem = !ahead && rng_in_gemm(h);
+  const bool twobuf = ahead || gem;
+  CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st, twobuf ? (int)(t0 & 1) : 0));
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   // dynamic hand-out pays for long rows (W = 8); for short ones the atomic's latency
   // is comparable to a chain's work (config 2: 17 -> 22 us per launch), so auto = W == 8
@@ -813,7 +843,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     if (graphs && t % K == 0 && n_iter - it >= K) {  // a whole aligned block: replay
       Shard& x = sh[0];
       cudaGraphExec_t ge;
-      tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, ahead, seed, &ge);
+      tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, ahead, gem, seed, &ge);
       if (gs != TMVN_OK) return gs;
       Nvtx nv("graph block: (a2 projection, ess_kernel) x K, a3 refresh");
       KL(h, launch_set_u32(h->d_tbase, (uint32_t)t, st));
@@ -827,7 +857,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     for (int s = 0; s < S; ++s) {
       Shard& x = sh[s];
       const int64_t Rp = round_up(x.C, kTileR);
-      const int b = ahead ? (int)(t & 1) : 0;
+      const int b = twobuf ? (int)(t & 1) : 0;
       if (ahead && it + 1 < n_iter) {  // nu_{t+1} into the other buffer, beside this projection
         CK(h, cudaEventRecord(h->ev_pre, x.st));
         CK(h, cudaStreamWaitEvent(h->rng_stream, h->ev_pre, 0));
@@ -835,17 +865,19 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
         CK(h, cudaEventRecord(h->ev_rng, h->rng_stream));
       }
       const OzArcs xa = arcs_for(h, x.c0, x.C, x.Pc);
+      const OzRng xr = rng_for(h, x.c0, x.C, seed, (uint32_t)t, nullptr, b ^ 1);
       {
-        Nvtx nv("a2 projection Q = N A'^T");
+        Nvtx nv(gem ? "a2 projection Q = N A'^T (+ a1 nu_{t+1} in the epilogue)" : "a2 projection Q = N A'^T");
         TIMED(use_oz(h) ? 2 : 0, x.C, x.st,
-              launch_projection(h, x.c0, Rp, x.st, b, nullptr, false, x.p.arcs ? &xa : nullptr));
+              launch_projection(h, x.c0, Rp, x.st, b, nullptr, false, x.p.arcs ? &xa : nullptr,
+                                (gem && it + 1 < n_iter) ? &xr : nullptr));
       }
       x.p.P_cur = x.Pc;
       x.p.P_next = x.Pn;
       x.p.t = (uint32_t)t;
-      x.p.gen_next = (!ahead && it + 1 < n_iter) ? 1 : 0;
-      if (ahead) {
-        x.p.N = nu_f64(h, b);
+      x.p.gen_next = (!twobuf && it + 1 < n_iter) ? 1 : 0;
+      if (twobuf) {
+        x.p.N = nu_f64(h, b) + x.c0 * h->d_pad;
         x.p.Ns = nullptr;
       }
       x.p.record = (rec && !h->affine) ? 1 : 0;
@@ -1022,7 +1054,8 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->latency = 2;
   o->precision = 0;
   o->total_chains = 0;
-  o->fuse_arcs = 0;  // measured slower on B200 (the epilogue outgrows the MMAs)
+  o->fuse_arcs = 0;
+  o->rng_gemm = 0;  // measured neutral at config 3 (0.384 -> 0.383 ms / iteration), slower at config 5  // measured slower on B200 (the epilogue outgrows the MMAs)
   return TMVN_OK;
 }
 

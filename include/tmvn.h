@@ -208,6 +208,13 @@ typedef struct {
    * the per-chain kernel gains ~26 us at config 3, the projection loses ~21 us --
    * 0.384 vs 0.383 ms per iteration -- and config 5 loses 3 %). */
   int32_t rng_gemm;
+  /* 1: the fused per-chain kernel draws nu for t + 1 while the last lane of
+   * its highest warp computes theta (the other warps would idle at the
+   * barrier), into the other of two nu buffers; 0 (default): after the update
+   * (B200, config 3: 0.207 vs 0.211 ms per launch -- with four chain groups per
+   * SM the kernel is throughput-bound, not idle at that barrier).  Results do
+   * not depend on it (same counters, tested bitwise). */
+  int32_t rng_overlap;
 } tmvn_options;
 
 typedef struct {

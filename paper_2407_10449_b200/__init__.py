@@ -53,7 +53,7 @@ class options(ctypes.Structure):
                 ("schedule", ctypes.c_int32), ("pipeline", ctypes.c_int32),
                 ("latency", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("total_chains", ctypes.c_int64), ("fuse_arcs", ctypes.c_int32),
-                ("rng_gemm", ctypes.c_int32)]
+                ("rng_gemm", ctypes.c_int32), ("rng_overlap", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):

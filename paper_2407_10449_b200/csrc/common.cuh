@@ -282,7 +282,7 @@ __device__ __forceinline__ double fast_recip(double d) {
 }
 __device__ __forceinline__ double fast_atan2(double y, double x) {
   const double ax = fabs(x), ay = fabs(y);
-  const double mx = fmax(ax, ay), mn = fmin(ax, ay);
+  const double mx = ay > ax ? ay : ax, mn = ay > ax ? ax : ay;  // |x|, |y|: no NaN handling needed
   const bool big = mn > 0.41421356237309503 * mx;
   const double num = big ? mn - mx : mn;
   const double den = big ? mn + mx : mx;
@@ -304,8 +304,8 @@ __device__ __forceinline__ double fast_atan2(double y, double x) {
 __device__ __forceinline__ void fast_atan2_2(double y1, double x1, double y2, double x2, double& r1,
                                              double& r2) {
   const double ax1 = fabs(x1), ay1 = fabs(y1), ax2 = fabs(x2), ay2 = fabs(y2);
-  const double mx1 = fmax(ax1, ay1), mn1 = fmin(ax1, ay1);
-  const double mx2 = fmax(ax2, ay2), mn2 = fmin(ax2, ay2);
+  const double mx1 = ay1 > ax1 ? ay1 : ax1, mn1 = ay1 > ax1 ? ax1 : ay1;  // non-negative, no NaN
+  const double mx2 = ay2 > ax2 ? ay2 : ax2, mn2 = ay2 > ax2 ? ax2 : ay2;
   const bool big1 = mn1 > 0.41421356237309503 * mx1, big2 = mn2 > 0.41421356237309503 * mx2;
   const double num1 = big1 ? mn1 - mx1 : mn1, den1 = big1 ? mn1 + mx1 : mx1;
   const double num2 = big2 ? mn2 - mx2 : mn2, den2 = big2 ? mn2 + mx2 : mx2;
@@ -340,10 +340,24 @@ __device__ __forceinline__ bool arc_active(double p, double q, double b) {
   const double s2 = fma(p, p, fma(q, q, -b * b));  // p^2 + q^2 - b^2
   return b < 0.0 || s2 > 0.0;
 }
+// sqrt(x) for x >= 0 within ~1 ulp (not correctly rounded; the arcs' parity bar is 1e-10):
+// the MUFU reciprocal-square-root estimate, two Newton steps on it and one on the root --
+// ~13 instructions instead of the IEEE sqrt's ~35 with its slow-path call; tiny or zero
+// x (rare: near-tangent arcs) take the IEEE sqrt.
+__device__ __forceinline__ double arc_sqrt(double x) {
+  if (!(x >= 0x1p-1000)) return sqrt(x > 0.0 ? x : 0.0);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  const double r = x * y;
+  return fma(0.5 * y, fma(-r, r, x), r);
+}
+
 __device__ __forceinline__ bool arc_of(double p, double q, double b, double& alpha, double& beta) {
   const double s2 = fma(p, p, fma(q, q, -b * b));  // p^2 + q^2 - b^2 (as in arc_active)
   if (!(b < 0.0 || s2 > 0.0)) return false;
-  const double s = sqrt(fmax(s2, 0.0));
+  const double s = arc_sqrt(s2);
   double tau, delta;
   fast_atan2_2(q, p, s, b, tau, delta);
   double lo = __dsub_rn(tau, delta);

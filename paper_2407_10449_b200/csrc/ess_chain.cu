@@ -807,6 +807,9 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     if (g.tid == 0) ring_issue(0);
   }
 
+#ifdef TMVN_EXP_STAGGER  // experiment: de-phase the CTAs of an SM (4 per SM at config 3)
+  if (!kGiven) __nanosleep((unsigned)((blockIdx.x / gridDim.x * 0 + (blockIdx.x * 4 / gridDim.x)) * TMVN_EXP_STAGGER));
+#endif
   // iteration index and record flag (from device memory under CUDA-graph replay)
   const uint32_t t_it = p.t_dev ? *p.t_dev + p.t : p.t;
 #ifdef TMVN_TIMELINE
@@ -1153,9 +1156,23 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
 
     // ---------------- B + C: I_act by Alg. 3, then theta ----------------
     const bool fast = par_intervals(g, S, ctl, AS, NB, scale, gg, s_w64, s_w32);
+    // nu_{t+1} drawn while the highest warp's last lane computes theta (options.rng_overlap:
+    // the other W - 1 warps would wait at the barrier); into the other nu buffer (N_next),
+    // since phase D still reads nu_t
+    const bool rng_here = !kGiven && W > 1 && fast && p.gen_next && p.N_next != nullptr;
     if (fast && g.tid == T - 1) {  // theta on the highest warp (arbiter: highest warp id first)
       const double u = kGiven ? (p.g_u ? p.g_u[c] : 0.0) : ctl.u;
       theta_from_gaps(S, ctl, gg, u, p.eps);
+    } else if (rng_here && g.warp < W - 1) {
+      const int kpairs = (int)(p.d_pad / 2);
+      const int64_t xr = tiled_row(c, p.d_pad);
+      const int64_t zr = p.Ns ? oz_row(c, p.ozS, p.ozKB, kOzNuRows) : 0;
+      for (int pk = g.tid; pk < kpairs; pk += 32 * (W - 1)) {
+        const int k = 2 * pk;
+        const double2 nv = normal_pair_at(p.seed, t_it + 1, gchain, k, p.d);
+        *reinterpret_cast<double2*>(p.N_next + (xr + tiled_col(k))) = nv;
+        if (p.Ns) oz_put_nu_pair_s(p.Ns + (zr + oz_col(k, p.ozS, kOzNuRows)), nv.x, nv.y, p.ozS);
+      }
     }
     g.sync();
     PHASE(3);  // B (+C) on the parallel path
@@ -1288,13 +1305,14 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         *s1 = a1;
         *s2 = a2;
       }
-      if (p.gen_next) {
+      if (p.gen_next && !rng_here) {
 #ifdef TMVN_EXP_NO_RNG  // timing experiment only (wrong results): the kernel without drawing nu
         const double2 nv = make_double2(xv.y * 1e-3, xv.x * 1e-3);
 #else
         const double2 nv = normal_pair_at(p.seed, t_it + 1, gchain, k, p.d);
 #endif
-        *nr = nv;
+        if (p.N_next) *reinterpret_cast<double2*>(p.N_next + o) = nv;
+        else *nr = nv;
         if (p.Ns) oz_put_nu_pair_s(p.Ns + (zrow + oz_col(k, p.ozS, kOzNuRows)), nv.x, nv.y, p.ozS);
       }
     }

@@ -140,7 +140,9 @@ struct EssParams {
   const uint32_t* t_dev;  // graph replay: iteration base in device memory (nullable)
   int rec_dev;      // 1: record flag computed from t (t >= burn_in, (t - burn_in) % thin == 0)
   int64_t burn_in, thin;
-  int gen_next;     // 1: draw nu for t + 1 into N after the update
+  int gen_next;     // 1: draw nu for t + 1 (into N after the update, or into N_next)
+  double* N_next;   // non-null: nu_{t+1} goes to this buffer (options.rng_overlap: drawn while
+                    // theta is computed; N keeps nu_t for the update)
   int64_t group_base;  // scratch index of this launch's first group (split launches)
   int* dyn_ctr;     // non-null: chains handed out dynamically by atomicAdd on dyn_ctr[t & 63]
                     // (the launch for t zeroes the slot of t + 32); null: round-robin

@@ -561,23 +561,23 @@ bool recorded_iter(const tmvn_options& o, int64_t t) {
 // read t from h->d_tbase (set by a one-thread kernel before each replay) and
 // compute their record flag from t, so one graph serves every aligned block.
 tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K, double* Pc,
-                        double* Pn, bool ahead, bool gem, uint64_t seed, cudaGraphExec_t* out) {
+                        double* Pn, bool ahead, bool gem, bool ovl, uint64_t seed, cudaGraphExec_t* out) {
   const int parity = Pc == h->P0 ? 0 : 1;
-  const bool twobuf = ahead || gem;  // nu_t in buffer t & 1
+  const bool twobuf = ahead || gem || ovl;  // nu_t in buffer t & 1
   EssParams p = base;
   p.t_dev = h->d_tbase;
   p.rec_dev = 1;
   // one graph serves blocks with and without recorded iterations: round-robin chains
   // whenever recording is on (the per-group moment rows need a fixed chain -> group map)
   p.dyn_use = h->opt.record ? 0 : 1;
-  p.gen_next = twobuf ? 0 : 1;
+  p.gen_next = (twobuf && !ovl) ? 0 : 1;
   if (twobuf) p.Ns = nullptr;
   p.t = 0;
   p.P_cur = Pc;
   p.P_next = Pn;
   std::vector<unsigned char> sig(sizeof(EssParams) + 2 * sizeof(int64_t) + 2 * sizeof(void*) + 16);
   std::memcpy(sig.data() + sizeof(EssParams) + 16 + 2 * sizeof(void*), &seed, 8);
-  const int64_t ah = (ahead ? 1 : 0) | (gem ? 2 : 0);
+  const int64_t ah = (ahead ? 1 : 0) | (gem ? 2 : 0) | (ovl ? 4 : 0);
   std::memcpy(sig.data() + sizeof(EssParams) + 24 + 2 * sizeof(void*), &ah, 8);
   std::memcpy(sig.data(), &p, sizeof(EssParams));
   std::memcpy(sig.data() + sizeof(EssParams), &C, sizeof(int64_t));
@@ -617,6 +617,10 @@ tmvn_status block_graph(tmvn_ctx* h, const EssParams& base, int64_t C, int64_t K
     p.P_cur = pc;
     p.P_next = pn;
     p.N = nu_f64(h, twobuf ? (int)(i & 1) : 0);
+    if (ovl) {
+      p.N_next = nu_f64(h, (int)((i + 1) & 1));
+      p.Ns = use_oz(h) ? oz_rows(h, 0, (int)((i + 1) & 1)) : nullptr;
+    }
     err = launch_ess_step(p, h->plan.grid, cs);
     if (err == cudaSuccess && ahead) err = cudaStreamWaitEvent(cs, h->ev_rng, 0);  // join: nu_{t+i+1} ready
     std::swap(pc, pn);
@@ -764,7 +768,9 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
   }
   // nu_{t+1} drawn by the projection of iteration t (options.rng_gemm): nu_t in buffer t & 1
   const bool gem = !ahead && rng_in_gemm(h);
-  const bool twobuf = ahead || gem;
+  // nu_{t+1} drawn by the per-chain kernel while theta is computed (options.rng_overlap)
+  const bool ovl = !ahead && !gem && h->opt.rng_overlap != 0 && h->plan.W > 1;
+  const bool twobuf = ahead || gem || ovl;
   CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st, twobuf ? (int)(t0 & 1) : 0));
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   // dynamic hand-out pays for long rows (W = 8); for short ones the atomic's latency
@@ -843,7 +849,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     if (graphs && t % K == 0 && n_iter - it >= K) {  // a whole aligned block: replay
       Shard& x = sh[0];
       cudaGraphExec_t ge;
-      tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, ahead, gem, seed, &ge);
+      tmvn_status gs = block_graph(h, x.p, C, K, x.Pc, x.Pn, ahead, gem, ovl, seed, &ge);
       if (gs != TMVN_OK) return gs;
       Nvtx nv("graph block: (a2 projection, ess_kernel) x K, a3 refresh");
       KL(h, launch_set_u32(h->d_tbase, (uint32_t)t, st));
@@ -875,10 +881,14 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
       x.p.P_cur = x.Pc;
       x.p.P_next = x.Pn;
       x.p.t = (uint32_t)t;
-      x.p.gen_next = (!twobuf && it + 1 < n_iter) ? 1 : 0;
+      x.p.gen_next = ((!twobuf || ovl) && it + 1 < n_iter) ? 1 : 0;
       if (twobuf) {
         x.p.N = nu_f64(h, b) + x.c0 * h->d_pad;
         x.p.Ns = nullptr;
+      }
+      if (ovl) {  // nu_{t+1} (and its digits) into the other buffer
+        x.p.N_next = nu_f64(h, b ^ 1) + x.c0 * h->d_pad;
+        x.p.Ns = use_oz(h) ? oz_rows(h, x.c0, b ^ 1) : nullptr;
       }
       x.p.record = (rec && !h->affine) ? 1 : 0;
       x.p.dyn_use = x.p.record ? 0 : 1;  // recorded: round-robin (per-group moment rows)
@@ -1055,7 +1065,8 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->precision = 0;
   o->total_chains = 0;
   o->fuse_arcs = 0;
-  o->rng_gemm = 0;  // measured neutral at config 3 (0.384 -> 0.383 ms / iteration), slower at config 5  // measured slower on B200 (the epilogue outgrows the MMAs)
+  o->rng_gemm = 0;
+  o->rng_overlap = 0;  // measured slightly slower at config 3 (0.207 -> 0.211 ms per launch) and config 4  // measured neutral at config 3 (0.384 -> 0.383 ms / iteration), slower at config 5  // measured slower on B200 (the epilogue outgrows the MMAs)
   return TMVN_OK;
 }
 

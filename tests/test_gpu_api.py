@@ -235,11 +235,39 @@ def test_rng_ahead_and_projection_options_bitwise():
         o0 = tm.Sampler(A, b).sample(X0, n, seed=11)
         assert np.array_equal(o1, o0), n
     # resume at a multiple of recompute_every with nu drawn ahead (plain + graph blocks)
-    for kw in (dict(rng_ahead=1), dict(pipeline=1)):
+    for kw in (dict(rng_ahead=1), dict(pipeline=1), dict(rng_gemm=1), dict(rng_overlap=1)):
         s = tm.Sampler(A, b, **kw)
         a = s.sample(X0, 32, seed=11)
         a = s.sample(a, 38, seed=11)
         assert np.array_equal(a, ref), kw
+    # round-2 options: nu drawn by the projection's epilogue (rng_gemm), nu drawn while
+    # theta is computed (rng_overlap), arcs computed in the projection's epilogue
+    # (fuse_arcs), the P/Q ring; plain and graph launches, several W
+    for kw in (dict(rng_gemm=1), dict(rng_gemm=1, graphs=0), dict(rng_overlap=1), dict(rng_overlap=1, graphs=0),
+               dict(rng_overlap=1, chain_warps=2), dict(fuse_arcs=1), dict(fuse_arcs=1, graphs=0),
+               dict(fuse_arcs=1, chain_warps=4), dict(ring=1), dict(ring=1, graphs=0)):
+        out = tm.Sampler(A, b, **kw).sample(X0, 70, seed=11)
+        assert np.array_equal(out, ref), kw
+
+
+def test_odd_m_and_general_interval_path_on_default_options():
+    """The production per-chain kernel with the chain's P / Q rows in shared memory on an
+    odd m, and the S4.2 geometry, whose arcs crowd the first buckets so that
+    more than 256 arcs are live (the general, bitonic-sorted interval path): every step
+    against the oracle (north_star bar), feasibility, no rejections."""
+    from test_gpu_step import check_trace
+    A, b, x0 = synth.make_instance(3, m=301, d=70)
+    C, T = 130, 40
+    s = tm.Sampler(A, b, latency=0)
+    chains = np.array([0, 7, 64, 129])
+    trace, out = s.test_trace(np.tile(x0, (C, 1)), T, seed=5, chains=chains)
+    check_trace(A, b, trace, 5, chains, projection=1 if s.profile()["oz_guard_ratio"] <= 16 else 2)
+    A2, b2, x2 = synth.paper_random(600, seed=600)
+    s2 = tm.Sampler(A2, b2, latency=0)
+    chains = np.arange(20)
+    trace, out = s2.test_trace(np.tile(x2, (20, 1)), 12, seed=42, chains=chains)
+    check_trace(A2, b2, trace, 42, chains, projection=1 if s2.profile()["oz_guard_ratio"] <= 16 else 2)
+    assert s2.stats()["rejections"] == 0
 
 
 @pytest.mark.parametrize("latency", [0, 1])

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+make -s all > /dev/null 2>&1
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -k "arcs or step or stages or ozaki" > gpurun_out/t14.log 2>&1
+echo "tests rc=$?" >> gpurun_out/t14.log
+L="paper_2407_10449_b200/libtmvn.so build/libtmvn_c3.so"
+( REPS=1 python tools/ab_time.py 3 0 1 0 $L; REPS=1 python tools/ab_time.py 4 0 1 0 $L ) > gpurun_out/ab14.log 2>&1

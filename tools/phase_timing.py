@@ -14,7 +14,12 @@ k = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 cfg = synth.CONFIGS[k]
 A, b, x0 = synth.make_instance(k)
-s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"))
+if os.environ.get("PAPER_D"):  # the S4.2 geometry (synth.paper_random) with PAPER_C chains
+    import dataclasses
+    dd = int(os.environ["PAPER_D"])
+    A, b, x0 = synth.paper_random(dd, seed=dd)
+    cfg = dataclasses.replace(cfg, C=int(os.environ.get("PAPER_C", "20")))
+s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"), latency=0)
 s.set_options(streams=1, chain_warps=int(os.environ.get("W", "0")))
 X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
 s.sample(X, 40, cfg.chain_seed, out=X)

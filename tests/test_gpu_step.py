@@ -266,6 +266,26 @@ def test_full_size_config4_sampled():
         s.close()
 
 
+@pytest.mark.parametrize("k,T,nchains", [(4, 6, 8), (2, 40, 16), (1, 200, 16)])
+def test_full_size_default_options_trace(k, T, nchains):
+    """BASELINE configs 4 (m = 100000: arcs in global scratch, the sort-bound case), 2
+    (orthant: every constraint active every step; the dynamic-range guard takes DMMA for
+    A = -I) and 1 (tiny 2-D: the latency mode is the automatic choice, so the throughput
+    path is forced here) at full size on default options, traced and checked step by step
+    against the oracle (north_star: 1e-10)."""
+    A, b, x0 = synth.make_instance(k)
+    cfg = synth.CONFIGS[k]
+    s = tm.Sampler(A, b, latency=0)
+    rng = np.random.default_rng(k)
+    chains = np.unique(np.concatenate([[0, cfg.C - 1], rng.choice(cfg.C, size=nchains - 2, replace=False)]))
+    trace, out = s.test_trace(np.tile(x0, (cfg.C, 1)), T, seed=cfg.chain_seed, chains=chains)
+    log = []
+    check_trace(A, b, trace, cfg.chain_seed, chains, projection=s.profile()["projection_used"] or 2, log=log)
+    print("exempt steps", log)
+    assert s.stats()["rejections"] == 0
+    s.close()
+
+
 def test_full_size_config5_trace():
     """BASELINE config 5 at full single-GPU size (d=4096, m=16384, C=65536; ~45 GB of
     device state) through the production loop on the default options (int8 projection,

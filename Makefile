@@ -4,7 +4,7 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v
 PKG     := paper_2407_10449_b200
 CSRC    := $(PKG)/csrc
-SRCS    := $(CSRC)/gemm_f64.cu $(CSRC)/gemm_i8.cu $(CSRC)/latency.cu $(CSRC)/cp.cu $(CSRC)/ess_chain.cu $(CSRC)/aux_kernels.cu $(CSRC)/runtime.cu
+SRCS    := $(CSRC)/gemm_f64.cu $(CSRC)/gemm_i8.cu $(CSRC)/latency.cu $(CSRC)/small.cu $(CSRC)/cp.cu $(CSRC)/ess_chain.cu $(CSRC)/aux_kernels.cu $(CSRC)/runtime.cu
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS    := $(CSRC)/common.cuh $(CSRC)/internal.h include/tmvn.h
 

@@ -215,6 +215,19 @@ typedef struct {
    * SM the kernel is throughput-bound, not idle at that barrier).  Results do
    * not depend on it (same counters, tested bitwise). */
   int32_t rng_overlap;
+  /* Warp mode for small polytopes (small.cu): one warp per chain runs all n_iter
+   * iterations in one launch with A resident in shared memory (column-major),
+   * Q = A nu one lane per row, the arcs compacted by ballot, Alg. 3 as a warp
+   * bitonic sort + prefix max, the safeguard by ballot.  Needs FP64, no affine
+   * map, m <= 512 and A (d x 32 ceil(m / 32) doubles) plus one warp's state in
+   * shared memory.  2: whenever that holds with >= 4 warps per CTA and
+   * options.latency is automatic (2) -- decided from m and d only, so every shard
+   * of a job takes the same path; 1: whenever it holds; 0 (default): off (B200:
+   * config 1 5.0 us per iteration vs 6.1 in the latency mode, config 2 20 us vs
+   * 19 on the default path -- one warp's serial per-iteration work, ~5K
+   * instructions, with ~7 chains per SM, does not beat the other paths).   Dot products sum in index order: results agree
+   * with the other paths to rounding, not bitwise. */
+  int32_t warp_mode;
 } tmvn_options;
 
 typedef struct {
@@ -247,6 +260,7 @@ typedef struct {
    * tmvn_create / tmvn_set_affine (kept by tmvn_reset_stats). */
   double oz_guard_ratio;
   int32_t projection_used;    /* projection of the last throughput-path call: 1 int8, 2 DMMA */
+  int64_t warp_mode_calls;    /* tmvn_sample calls run in warp mode (options.warp_mode)        */
 } tmvn_profile;
 
 /* Fills *opt with the defaults listed above. */

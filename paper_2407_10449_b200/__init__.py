@@ -53,7 +53,8 @@ class options(ctypes.Structure):
                 ("schedule", ctypes.c_int32), ("pipeline", ctypes.c_int32),
                 ("latency", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("total_chains", ctypes.c_int64), ("fuse_arcs", ctypes.c_int32),
-                ("rng_gemm", ctypes.c_int32), ("rng_overlap", ctypes.c_int32)]
+                ("rng_gemm", ctypes.c_int32), ("rng_overlap", ctypes.c_int32),
+                ("warp_mode", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):
@@ -64,7 +65,8 @@ class profile(ctypes.Structure):
                 ("tc_ms", ctypes.c_double), ("tc_ops", ctypes.c_double),
                 ("tc_flops", ctypes.c_double), ("latency_calls", ctypes.c_int64),
                 ("latency_fallbacks", ctypes.c_int64), ("latency_grid_calls", ctypes.c_int64),
-                ("oz_guard_ratio", ctypes.c_double), ("projection_used", ctypes.c_int32)]
+                ("oz_guard_ratio", ctypes.c_double), ("projection_used", ctypes.c_int32),
+                ("warp_mode_calls", ctypes.c_int64)]
 
 
 class stats(ctypes.Structure):

@@ -119,6 +119,33 @@ int latency_cap(int64_t d_pad, int m, int cs, size_t smem_max);
 int latency_cluster_size(int C, int64_t m, int64_t d_pad, size_t smem_max, bool fp32, int* cap_out);
 cudaError_t launch_latency(const LatParams& p, int cs, cudaStream_t st);
 
+// ---- warp mode (small.cu): one warp per chain, all iterations, A in shared memory ----
+struct SmallParams {
+  const double* A;   // m x d row-major (A' = A: no affine change of variable)
+  const double* b;   // m
+  int m, d;
+  int64_t d_pad;
+  double* X;         // tiled C_pad x d_pad: x_{t0} in, final iterates out
+  int C;
+  uint32_t chain_offset;
+  uint64_t seed;
+  uint32_t t0;
+  int n_iter;
+  int64_t K;         // refresh period of P = A x
+  double eps;        // S3.3 trim
+  int record;
+  int64_t burn_in, thin;
+  double* S1;        // tiled moment rows (one per warp)
+  double* S2;
+  int64_t* rej;      // per chain
+  unsigned long long* startflag;  // non-null: check the start; lowest chain * m + i violating
+  int warp_bytes, n2;             // set by the launcher
+};
+// shared memory per warp; rows of A per lane (power of two, m <= 32 R)
+size_t small_warp_bytes(int m, int64_t d_pad);
+int small_rows(int m);
+cudaError_t launch_small(const SmallParams& p, int warps_per_cta, int grid, cudaStream_t st);
+
 // ---- fused per-chain ESS kernel (ess_chain.cu) -----------------------------
 struct EssParams {
   // P (= A x_t, incremental), Q (= A nu): C_pad x ldp row-major.

@@ -1066,7 +1066,8 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->total_chains = 0;
   o->fuse_arcs = 0;
   o->rng_gemm = 0;
-  o->rng_overlap = 0;  // measured slightly slower at config 3 (0.207 -> 0.211 ms per launch) and config 4  // measured neutral at config 3 (0.384 -> 0.383 ms / iteration), slower at config 5  // measured slower on B200 (the epilogue outgrows the MMAs)
+  o->rng_overlap = 0;
+  o->warp_mode = 0;  // measured: config 1 5.0 vs 6.1 us / iteration (latency mode), config 2 20 vs 19 us (default path)  // measured slightly slower at config 3 (0.207 -> 0.211 ms per launch) and config 4  // measured neutral at config 3 (0.384 -> 0.383 ms / iteration), slower at config 5  // measured slower on B200 (the epilogue outgrows the MMAs)
   return TMVN_OK;
 }
 
@@ -1300,6 +1301,77 @@ bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_ou
   return true;
 }
 
+// Warp mode (options.warp_mode, small.cu): FP64, no affine map, m <= 512 and A (d x
+// 32 R doubles, column-major) in shared memory beside >= 1 warp's state.  Decided from
+// (m, d) only, so every shard of a job takes the same path.  Warps per CTA: as few as
+// spread the job's chains over the SMs (up to 16).
+bool small_fits(tmvn_ctx* h, int64_t C, int* wpc_out, int* grid_out) {
+  if (h->opt.warp_mode == 0 || h->affine || h->opt.precision != 0 || h->m > 512) return false;
+  // auto only under the automatic path choice: latency = 0 / 1 ask for a specific path
+  if (h->opt.warp_mode == 2 && h->opt.latency != 2) return false;
+  int dev = 0, sms = 0, smem_max = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t a_bytes = (size_t)h->d * 32 * small_rows((int)h->m) * 8;
+  const size_t wb = small_warp_bytes((int)h->m, h->d_pad);
+  if (a_bytes + wb > (size_t)smem_max) return false;
+  int wmax = (int)std::min<size_t>(16, ((size_t)smem_max - a_bytes) / wb);
+  if (h->opt.warp_mode == 2 && wmax < 4) return false;  // auto: a few chains per CTA at least
+  int wpc = (int)std::min<int64_t>(wmax, std::max<int64_t>(1, (C + sms - 1) / sms));
+  int64_t grid = (C + wpc - 1) / wpc;
+  if (grid > sms) grid = sms;  // one CTA per SM (A per CTA); warps loop over their chains
+  *wpc_out = wpc;
+  *grid_out = (int)grid;
+  return true;
+}
+
+tmvn_status run_small(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int wpc, int grid,
+                      int64_t* n_recorded) {
+  cudaStream_t st = stream_of(h);
+  SmallParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.A = h->A_row;
+  p.b = h->b_eff;
+  p.m = (int)h->m;
+  p.d = (int)h->d;
+  p.d_pad = h->d_pad;
+  p.X = h->X;
+  p.C = (int)C;
+  p.chain_offset = (uint32_t)h->opt.chain_offset;
+  p.seed = seed;
+  p.t0 = (uint32_t)h->opt.iter_offset;
+  p.n_iter = (int)n_iter;
+  p.K = h->opt.recompute_every < 1 ? 1 : h->opt.recompute_every;
+  p.eps = h->opt.trim_eps;
+  p.record = h->opt.record;
+  p.burn_in = h->opt.burn_in;
+  p.thin = h->opt.thin;
+  p.S1 = h->S1;
+  p.S2 = h->S2;
+  p.rej = h->rej;
+  p.startflag = h->dflag;
+  CK(h, cudaMemsetAsync(h->dflag, 0xff, sizeof(unsigned long long), st));
+  KL(h, launch_small(p, wpc, grid, st));
+  unsigned long long* fp = reinterpret_cast<unsigned long long*>(h->pin);
+  CK(h, cudaMemcpyAsync(fp, h->dflag, sizeof(*fp), cudaMemcpyDeviceToHost, st));
+  CK(h, cudaStreamSynchronize(st));
+  const unsigned long long flag = *fp;
+  if (flag != ~0ull) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "infeasible start: chain %lld violates constraint %lld (a_i . x0 >= b_i; the start "
+             "must be strictly interior)",
+             (long long)(flag / h->m), (long long)(flag % h->m));
+    return fail(h, TMVN_E_INFEASIBLE_START, buf);
+  }
+  int64_t nrec = 0;
+  for (int64_t it = 0; it < n_iter; ++it) nrec += recorded_iter(h->opt, h->opt.iter_offset + it) ? 1 : 0;
+  *n_recorded = nrec;
+  h->prof.warp_mode_calls += 1;
+  return TMVN_OK;
+}
+
 // returns TMVN_OK with *overflow = true (nothing usable written) when some iteration had
 // more live arcs than the capacity: the caller restores X and runs the default path
 tmvn_status run_latency(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int cs, int cap, int gsz,
@@ -1417,6 +1489,17 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = plan_ess(h, C)) != TMVN_OK) return s;
   if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
+  int swpc = 0, sgrid = 0;
+  if (n_iter > 0 && small_fits(h, C, &swpc, &sgrid)) {  // warp mode: the kernel checks the start
+    Nvtx nw("warp mode (one warp per chain, all iterations, A in shared memory)");
+    if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
+    int64_t nrec = 0;
+    if ((s = run_small(h, C, n_iter, seed, swpc, sgrid, &nrec)) != TMVN_OK) return s;
+    if ((s = store_X(h, C, out)) != TMVN_OK) return s;
+    if ((s = finish_stats(h, C, n_iter, nrec)) != TMVN_OK) return s;
+    if (h->opt.auto_advance) h->opt.iter_offset += n_iter;
+    return TMVN_OK;
+  }
   int lcs = 0, lcap = 0;
   int lgsz = 0;
   const bool lat = n_iter > 0 && latency_fits(h, C, &lcs, &lcap, &lgsz);

@@ -270,19 +270,20 @@ def test_odd_m_and_general_interval_path_on_default_options():
     assert s2.stats()["rejections"] == 0
 
 
-@pytest.mark.parametrize("latency", [0, 1])
-def test_degenerate_inputs(latency):
+@pytest.mark.parametrize("latency", [0, 1, "warp"])
+def test_degenerate_inputs(latency):  # "warp": options.warp_mode = 1
+    kw = dict(warp_mode=1) if latency == "warp" else dict(latency=latency)
     """n_iter = 0, one chain, one dimension, no active constraint (every arc inactive:
     the whole ellipse, L = 2 pi), and a polytope whose every constraint is active at
     every step (orthant) -- on both execution paths."""
     A, b, x0 = synth.make_instance(3, m=40, d=7)
-    s = tm.Sampler(A, b, latency=latency)
+    s = tm.Sampler(A, b, **kw)
     X0 = np.tile(x0, (3, 1))
     out = s.sample(X0, 0, seed=1)
     assert np.array_equal(out, X0) and s.stats()["steps"] == 0
     # one chain, one dimension: N(0,1) on [-1, 3]
     A1, b1, x1 = synth.one_dim((-1.0, 3.0))
-    s1 = tm.Sampler(A1, b1, latency=latency)
+    s1 = tm.Sampler(A1, b1, **kw)
     o1 = s1.sample(x1[None, :], 5, seed=2)
     for t in range(5):
         xn, _ = oracle.step(A1, b1, x1, 2, t, 0)
@@ -291,7 +292,7 @@ def test_degenerate_inputs(latency):
     # no active constraint: b far outside the reachable ellipse
     Ab = A.copy()
     bb = np.full(40, 1e6)
-    s2 = tm.Sampler(Ab, bb, latency=latency, record=0)
+    s2 = tm.Sampler(Ab, bb, **kw, record=0)
     X = np.tile(x0, (4, 1))
     Xn = s2.sample(X, 1, seed=3)
     for c in range(4):

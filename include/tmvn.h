@@ -90,9 +90,11 @@ typedef struct {
   int32_t chain_warps;
   /* Chain shards run as independent GEMM -> ESS sequences on concurrent streams
    * (forked from / joined to `stream`), so the FP64 tensor GEMM of one shard
-   * can overlap the ALU-bound per-chain kernel of another.  0 (default) = 1
-   * (with the persistent GEMM filling every SM the overlap measured slower).
-   * Results do not depend on it. */
+   * can overlap the ALU-bound per-chain kernel of another.  0 (default) =
+   * automatic: 2 shards for >= 2048 chains, 4 for m >= 8192 and >= 1024 chains,
+   * 1 when d > 2048 (the projection dominates and every shard would re-stream
+   * its A' operand from HBM); measured on B200.  Results
+   * do not depend on it (tested bitwise). */
   int32_t streams;
   /* 1: stream each chain's P and Q rows into shared memory with cp.async.bulk
    * through a 2-slot mbarrier ring (the next chain's rows prefetched); 0

@@ -237,7 +237,20 @@ tmvn_status ensure_chains(tmvn_ctx* h, int64_t C) {
 // Shards, launch plan of the fused kernel (per shard) and its per-group scratch.
 tmvn_status plan_ess(tmvn_ctx* h, int64_t C) {
   int S = h->opt.streams;
-  if (S <= 0) S = 1;  // auto: the persistent GEMM fills every SM, overlap does not pay (profiles/r01)
+  if (S <= 0) {
+    // auto (measured on B200): chain shards as independent GEMM ->
+    // per-chain sequences on concurrent streams fill each other's tails (the persistent
+    // per-chain kernel's last round, the GEMM's last tiles) -- config 3 (4096 chains,
+    // d = 1000) 0.381 -> 0.359 ms per iteration with 2 shards, config 4 (1024 chains,
+    // m = 100000) 2.44 -> 1.98 ms with 4 -- unless the projection dominates and its A'
+    // operand exceeds L2 (config 5, d = 4096: every shard re-streams 470 MB of digits,
+    // 125 -> 145 ms with 2 shards)
+    S = 1;
+    if (h->d <= 2048) {
+      if (h->m >= 8192 && C >= 4 * 256) S = 4;
+      else if (C >= 2 * 1024) S = 2;
+    }
+  }
   if (h->trace_dev) S = 1;
   const int64_t per = round_up((C + S - 1) / S, kTileR);
   S = (int)((C + per - 1) / per);

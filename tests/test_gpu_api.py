@@ -245,9 +245,23 @@ def test_rng_ahead_and_projection_options_bitwise():
     # (fuse_arcs), the P/Q ring; plain and graph launches, several W
     for kw in (dict(rng_gemm=1), dict(rng_gemm=1, graphs=0), dict(rng_overlap=1), dict(rng_overlap=1, graphs=0),
                dict(rng_overlap=1, chain_warps=2), dict(fuse_arcs=1), dict(fuse_arcs=1, graphs=0),
-               dict(fuse_arcs=1, chain_warps=4), dict(ring=1), dict(ring=1, graphs=0)):
+               dict(fuse_arcs=1, chain_warps=4), dict(ring=1), dict(ring=1, graphs=0),
+               dict(streams=2), dict(streams=3), dict(streams=2, rng_overlap=1)):
         out = tm.Sampler(A, b, **kw).sample(X0, 70, seed=11)
         assert np.array_equal(out, ref), kw
+    # chain shards on concurrent streams (the automatic choice from 2048 chains): the same
+    # chains bitwise, moments to rounding (the per-group rows regroup)
+    C2 = 2304
+    X2 = np.tile(x0, (C2, 1))
+    s1 = tm.Sampler(A, b, streams=1)
+    r1 = s1.sample(X2, 40, seed=3)
+    for S in (0, 2, 4):
+        sS = tm.Sampler(A, b, streams=S)
+        rS = sS.sample(X2, 40, seed=3)
+        assert np.array_equal(rS, r1), S
+        for u, v in zip(sS.moments()[:2], s1.moments()[:2]):
+            assert np.allclose(u, v, rtol=1e-12, atol=1e-12)
+        assert sS.stats() == s1.stats()
 
 
 def test_odd_m_and_general_interval_path_on_default_options():

@@ -139,9 +139,10 @@ __device__ __forceinline__ T warp_incl_sum(T v) {
   return v;
 }
 // exclusive max-scan of v over the group's threads (init `init`); *total = max(init, all v)
+// tail_sync = false: the caller guarantees a group barrier before s_w is written again
 template <int W>
 __device__ uint64_t grp_excl_max(const Grp<W>& g, uint64_t v, uint64_t init, uint64_t* s_w,
-                                 uint64_t* total) {
+                                 uint64_t* total, bool tail_sync = true) {
   const uint64_t inc = warp_incl_max(v);
   uint64_t exc = __shfl_up_sync(0xffffffffu, inc, 1);
   if (g.lane == 0) exc = 0;
@@ -157,12 +158,12 @@ __device__ uint64_t grp_excl_max(const Grp<W>& g, uint64_t v, uint64_t init, uin
     if (i < g.warp) pre = pre > s_w[i] ? pre : s_w[i];
     tot = tot > s_w[i] ? tot : s_w[i];
   }
-  g.sync();
+  if (tail_sync) g.sync();
   *total = tot;
   return pre > exc ? pre : exc;
 }
 template <int W>
-__device__ int grp_excl_sum(const Grp<W>& g, int v, int* s_w, int* total) {
+__device__ int grp_excl_sum(const Grp<W>& g, int v, int* s_w, int* total, bool tail_sync = true) {
   const int inc = warp_incl_sum(v);
   if (W == 1) {
     *total = __shfl_sync(0xffffffffu, inc, 31);
@@ -175,7 +176,7 @@ __device__ int grp_excl_sum(const Grp<W>& g, int v, int* s_w, int* total) {
     if (i < g.warp) pre += s_w[i];
     tot += s_w[i];
   }
-  g.sync();
+  if (tail_sync) g.sync();
   *total = tot;
   return pre + inc - v;
 }
@@ -517,7 +518,9 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
   uint64_t lmax = 0;
   for (int j = j0; j < j1; ++j) lmax = lmax > S.Gx[j] ? lmax : S.Gx[j];
   uint64_t Gtot;
-  uint64_t run = grp_excl_max(g, lmax, dbits(ctl.G), s_w64, &Gtot);
+  // no trailing barriers in the two scans: s_w64 / s_w32 are next written after the
+  // barriers below (grp_excl_sum's, and the one after the offsets)
+  uint64_t run = grp_excl_max(g, lmax, dbits(ctl.G), s_w64, &Gtot, false);
   int lcount = 0;
   for (int j = j0; j < j1; ++j) {
     S.gin[j] = run;
@@ -527,8 +530,11 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
     run = run > S.Gx[j] ? run : S.Gx[j];
   }
   int total;
-  int o = grp_excl_sum(g, lcount, s_w32, &total);
-  if (total > kLiveCap) return false;  // uniform: the general path runs
+  int o = grp_excl_sum(g, lcount, s_w32, &total, false);
+  if (total > kLiveCap) {  // uniform: the general path runs (its first scan writes s_w64 / s_w32)
+    g.sync();
+    return false;
+  }
   for (int j = j0; j < j1; ++j) {
     const int cj = S.cnt[j];
     const bool live = cj > 0 && (S.maxA[j] | 0xFFFFFFFFull) > S.gin[j];
@@ -842,12 +848,10 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     }
     g.sync();
   }
-  for (int64_t cc = dyn ? (int64_t)ctl.next : gglobal; cc < p.C;
-       cc = dyn ? (int64_t)ctl.next : cc + ngroups) {
-    const int c = (int)cc;
-    const uint32_t gchain = p.chain_offset + (uint32_t)c;
-    g.sync();
-    PHASE(6);  // D2 of the previous chain (x, moments, next nu) + loop overhead
+  // per-chain state (bucket tables, control words), reset before the first chain and at
+  // the end of every chain, so that the loop-top barrier orders it before phase A
+  auto reset_chain_state = [&]() {
+    clear_buckets(g, S, NB);
     if (g.tid == 0) {
       ctl.n_act = 0;
       ctl.ngap = 0;
@@ -857,6 +861,14 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
       ctl.mode = 0;
       ctl.maxa_exact = 0;
     }
+  };
+  reset_chain_state();
+  for (int64_t cc = dyn ? (int64_t)ctl.next : gglobal; cc < p.C;
+       cc = dyn ? (int64_t)ctl.next : cc + ngroups) {
+    const int c = (int)cc;
+    const uint32_t gchain = p.chain_offset + (uint32_t)c;
+    g.sync();
+    PHASE(6);  // D2 of the previous chain (x, moments, next nu) + loop overhead
     if (!kGiven && g.tid == T - 1) {
       // u for this chain (Philox latency hidden behind phase A); the next chain's
       // P and Q rows are pulled into L2 now, so its phase A loads hit L2
@@ -886,8 +898,6 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p.N + o));
       }
     }
-    clear_buckets(g, S, NB);
-    g.sync();
     PHASE(0);  // init
 
     // ---------------- A: arcs -> stash + level-1 bucket statistics ----------------
@@ -1204,7 +1214,11 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         p.d_seg_hi[(int64_t)c * p.seg_cap + k] = gv.y;
       }
     }
-    if (kGiven) continue;
+    if (kGiven) {
+      g.sync();  // the dumps above read ctl and the gaps
+      reset_chain_state();
+      continue;
+    }
 
     // ---------------- D: safeguard, P', x update, moments, next nu ----------------
     const double L = ctl.L;
@@ -1320,6 +1334,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
       if (!accept) p.rej[c] += 1;
       if (p.d_accept) p.d_accept[c] = accept ? 1 : 0;
     }
+    reset_chain_state();  // phase D reads neither the bucket tables nor ctl's interval words
   }
 #ifdef TMVN_TIMELINE
   if (!kGiven && threadIdx.x == 0) atomicMax(&g_tl[t_it & 255][3], tl_now());

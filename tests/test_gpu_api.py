@@ -246,7 +246,8 @@ def test_rng_ahead_and_projection_options_bitwise():
     for kw in (dict(rng_gemm=1), dict(rng_gemm=1, graphs=0), dict(rng_overlap=1), dict(rng_overlap=1, graphs=0),
                dict(rng_overlap=1, chain_warps=2), dict(fuse_arcs=1), dict(fuse_arcs=1, graphs=0),
                dict(fuse_arcs=1, chain_warps=4), dict(ring=1), dict(ring=1, graphs=0),
-               dict(streams=2), dict(streams=3), dict(streams=2, rng_overlap=1)):
+               dict(streams=2), dict(streams=3), dict(streams=2, rng_overlap=1),
+               dict(streams=2, fuse_arcs=1), dict(streams=2, rng_gemm=1), dict(streams=3, ring=1)):
         out = tm.Sampler(A, b, **kw).sample(X0, 70, seed=11)
         assert np.array_equal(out, ref), kw
     # chain shards on concurrent streams (the automatic choice from 2048 chains): the same

@@ -86,7 +86,8 @@ typedef struct {
   int32_t profile;
   /* Warps of the fused per-chain kernel that own one chain: 1, 2, 4, 8 or 16
    * (16: one 512-thread CTA per chain); 0 (default) = chosen from C and m.
-   * Results do not depend on it. */
+   * Results do not depend on it.  A small W whose chain groups' bucket tables
+   * would not fit one CTA's shared memory (m in the thousands) is raised. */
   int32_t chain_warps;
   /* Chain shards run as independent GEMM -> ESS sequences on concurrent streams
    * (forked from / joined to `stream`), so the FP64 tensor GEMM of one shard
@@ -227,9 +228,18 @@ typedef struct {
    * of a job takes the same path; 1: whenever it holds; 0 (default): off (B200:
    * config 1 5.0 us per iteration vs 6.1 in the latency mode, config 2 20 us vs
    * 19 on the default path -- one warp's serial per-iteration work, ~5K
-   * instructions, with ~7 chains per SM, does not beat the other paths).   Dot products sum in index order: results agree
+   * instructions, with ~7 chains per SM, does not beat the other paths).  Dot products sum in index order: results agree
    * with the other paths to rounding, not bitwise. */
   int32_t warp_mode;
+  /* Level-1 buckets of the per-chain kernel's Alg. 3 (bucketed sort, Prop. 1): 1
+   * linear in alpha over [0, 2 pi]; 2 by octave of alpha (NB / 16 per octave over
+   * [2^-12, 8)), for geometries whose arcs crowd just after theta = 0 (the paper's
+   * S4.2 instances, unnormalised rows with b = A x0 + U[0, 1]); 0 (default):
+   * linear, switching to octaves for the rest of the call once more than 1/8 of a
+   * launch's chains went down the general (sorted) interval path or held more than
+   * 4 m / NB + 32 arcs in one bucket (tmvn_profile.buckets_used).  Any monotone
+   * bucketing gives the same I_act bit for bit: results do not depend on it. */
+  int32_t buckets;
 } tmvn_options;
 
 typedef struct {
@@ -263,6 +273,10 @@ typedef struct {
   double oz_guard_ratio;
   int32_t projection_used;    /* projection of the last throughput-path call: 1 int8, 2 DMMA */
   int64_t warp_mode_calls;    /* tmvn_sample calls run in warp mode (options.warp_mode)        */
+  /* level-1 bucket mapping the per-chain kernel ended the last call with: 1 linear,
+   * 2 by octave (options.buckets = 2, or the automatic switch turned it on); 0 before
+   * any throughput-path call.  Read from device memory by tmvn_get_profile (synchronises the device). */
+  int32_t buckets_used;
 } tmvn_profile;
 
 /* Fills *opt with the defaults listed above. */
@@ -393,6 +407,9 @@ tmvn_status tmvn_test_latency_cap(tmvn_handle h, int32_t cap);
 /* Latency mode's grid variant (a cooperative grid of SMs / C CTAs per chain instead
  * of a cluster): mode 1 forces it whenever it fits, -1 never, 0 automatic. */
 tmvn_status tmvn_test_latency_grid(tmvn_handle h, int32_t mode);
+/* Launch configuration of tmvn_test_intervals: warps per chain (0 = automatic; 1, 2,
+ * 4, 8, 16) and level-1 bucket mapping (1 linear, 2 by octave); process-wide. */
+tmvn_status tmvn_test_interval_config(int32_t chain_warps, int32_t bucket_mode);
 /* The production FP64 GEMM: out[R x S] = X[R x K] . W[S x K]^T (all row-major). */
 tmvn_status tmvn_test_gemm(const double* X, int64_t R, const double* W, int64_t S, int64_t K,
                            double* out);

@@ -30,7 +30,7 @@ EXPORTS = ["tmvn_default_options", "tmvn_create", "tmvn_set_affine", "tmvn_set_o
            "tmvn_get_options", "tmvn_sample", "tmvn_get_stats", "tmvn_get_moments",
            "tmvn_reset_stats", "tmvn_get_profile", "tmvn_last_error", "tmvn_version",
            "tmvn_destroy", "tmvn_test_philox", "tmvn_test_curand_philox", "tmvn_test_normals", "tmvn_test_arcs",
-           "tmvn_test_intervals", "tmvn_test_gemm", "tmvn_test_ozaki_gemm", "tmvn_test_step",
+           "tmvn_test_intervals", "tmvn_test_interval_config", "tmvn_test_gemm", "tmvn_test_ozaki_gemm", "tmvn_test_step",
            "tmvn_test_trace", "tmvn_test_latency_cap", "tmvn_test_latency_grid", "tmvn_cp_begin", "tmvn_cp_stats", "tmvn_cp_live",
            "tmvn_cp_theta", "tmvn_cp_commit", "tmvn_cp_end"]
 
@@ -54,7 +54,7 @@ class options(ctypes.Structure):
                 ("latency", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("total_chains", ctypes.c_int64), ("fuse_arcs", ctypes.c_int32),
                 ("rng_gemm", ctypes.c_int32), ("rng_overlap", ctypes.c_int32),
-                ("warp_mode", ctypes.c_int32)]
+                ("warp_mode", ctypes.c_int32), ("buckets", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):
@@ -66,7 +66,8 @@ class profile(ctypes.Structure):
                 ("tc_flops", ctypes.c_double), ("latency_calls", ctypes.c_int64),
                 ("latency_fallbacks", ctypes.c_int64), ("latency_grid_calls", ctypes.c_int64),
                 ("oz_guard_ratio", ctypes.c_double), ("projection_used", ctypes.c_int32),
-                ("warp_mode_calls", ctypes.c_int64)]
+                ("warp_mode_calls", ctypes.c_int64),
+                ("buckets_used", ctypes.c_int32)]
 
 
 class stats(ctypes.Structure):
@@ -113,6 +114,7 @@ def lib():
             "tmvn_test_normals": [u64, u64, i64, i64, i64, P, P],
             "tmvn_test_arcs": [P, P, P, i64, P, P, P],
             "tmvn_test_intervals": [P, P, i64, i64, P, f64, P, P, i64, P, P, P],
+            "tmvn_test_interval_config": [ctypes.c_int32, ctypes.c_int32],
             "tmvn_test_gemm": [P, i64, P, i64, i64, P],
             "tmvn_test_ozaki_gemm": [P, i64, P, i64, i64, ctypes.c_int32, P],
             "tmvn_test_step": [H, P, i64, u64, i64, P],
@@ -394,6 +396,12 @@ def test_arcs(p, q, b):
     al, be, act = np.zeros(n), np.zeros(n), np.zeros(n, np.uint8)
     _check(lib().tmvn_test_arcs(_ptr(p), _ptr(q), _ptr(b), n, _ptr(al), _ptr(be), _ptr(act)))
     return al, be, act.astype(bool)
+
+
+def test_interval_config(chain_warps=0, bucket_mode=1):
+    """Launch configuration of test_intervals (process-wide): warps per chain, level-1
+    buckets (1 linear, 2 by octave)."""
+    _check(lib().tmvn_test_interval_config(int(chain_warps), int(bucket_mode)))
 
 
 def test_intervals(alpha, beta, u=None, eps=0.0, seg_cap=None):

@@ -51,7 +51,9 @@ __device__ __forceinline__ double bitsd(uint64_t b) { return __longlong_as_doubl
 struct Ctl {
   uint64_t rlo, rhi, klo;
   uint64_t pqbar;       // mbarrier: the chain's P and Q rows bulk-copied into shared memory
-  int shift, mode;      // key: mode 0 linear on [0, 2 pi]; mode 1 (bits - klo) >> shift
+  int shift, mode;      // key: mode 0 linear on [0, 2 pi]; mode 1 (bits - klo) >> shift;
+                        // mode 2 by octave (bucket_key)
+  int oct_log2;         // mode 2: log2(buckets per octave)
   double G;             // running gamma: max beta over every arc already passed
   int n_act;
   int ngap;
@@ -63,6 +65,7 @@ struct Ctl {
   int maxa_exact;       // max/min alpha per bucket exact (refinement levels)
   int fast;             // 1: I_act built by the parallel level-1 path
   int ncand;            // gaps found by the parallel path
+  int crowd;            // a level-1 bucket held more than crowd_at arcs (par_intervals)
   int next;             // dynamic scheduling: the chain grabbed for the next round
   double u;             // u_{c,t} of "sample theta uniformly" (drawn at the chain's start)
 };
@@ -195,12 +198,24 @@ struct Smem {
   uint64_t* cand;  // 2 kLiveCap: gaps (alpha, gamma) found by the parallel path, unordered
 };
 
+// Level-1 keys: mode 0 linear on [0, 2 pi]; mode 2 by octave (NB / 16 buckets per octave
+// over [2^-12, 8) from the bit pattern, bucket 0 below -- for geometries whose arcs
+// crowd just after theta = 0, options.buckets / the automatic switch); mode 1: the
+// refinement levels' (bits - klo) >> shift.  All monotone in alpha, which is all that
+// Alg. 3's bucketed form needs (Prop. 1): I_act is bit-identical for any of them.
 __device__ __forceinline__ int bucket_key(double a, const Ctl& c, int NB, double scale) {
   if (c.mode == 0) {
     int k = (int)__dmul_rn(a, scale);
     return k < NB - 1 ? k : NB - 1;
   }
-  uint64_t k = (dbits(a) - c.klo) >> c.shift;
+  const uint64_t bits = dbits(a);
+  if (c.mode == 2) {
+    if (bits < 0x3F30000000000000ull) return 0;  // alpha < 2^-12
+    const int e = (int)(bits >> 52) - 1011;      // 0 .. 14 for alpha < 8
+    const int k = 1 + (e << c.oct_log2) + (int)((bits >> c.shift) & c.klo);
+    return k < NB - 1 ? k : NB - 1;
+  }
+  uint64_t k = (bits - c.klo) >> c.shift;
   return k < (uint64_t)(NB - 1) ? (int)k : NB - 1;
 }
 
@@ -508,9 +523,11 @@ __device__ void build_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const 
 // false, touching only gin / cand / fill, when more than kLiveCap arcs are live:
 // the general path (build_intervals) then runs on the untouched statistics.
 // ---------------------------------------------------------------------------
+
 template <int W, bool kRows>
 __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const ArcStore<kRows>& stash,
-                              int NB, double scale, double2* gg, uint64_t* s_w64, int* s_w32) {
+                              int NB, double scale, double2* gg, uint64_t* s_w64, int* s_w32,
+                              int crowd_at) {
   constexpr int T = Grp<W>::kThreads;
   const int per = (NB + T - 1) / T;
   const int j0 = g.tid * per, j1 = min(NB, j0 + per);
@@ -525,6 +542,7 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
   for (int j = j0; j < j1; ++j) {
     S.gin[j] = run;
     const int cj = S.cnt[j];
+    if (cj > crowd_at) ctl.crowd = 1;  // read after the closing barrier
     // level 1: only the high word of max alpha is exact -> conservative test
     if (cj > 0 && (S.maxA[j] | 0xFFFFFFFFull) > run) lcount += cj;
     run = run > S.Gx[j] ? run : S.Gx[j];
@@ -704,6 +722,11 @@ __device__ __forceinline__ void stash_arc(const Smem& S, Ctl& ctl, double2* stas
 #ifndef TMVN_ESS_W8_BLOCKS
 #define TMVN_ESS_W8_BLOCKS 4
 #endif
+// automatic level-1 bucket switch (options.buckets = 0): octave mapping once more than
+// C / 2^TMVN_GMODE_SHIFT chains of a launch took the general interval path
+#ifndef TMVN_GMODE_SHIFT
+#define TMVN_GMODE_SHIFT 3
+#endif
 // threads per CTA: 256 (8 / W chain groups), or one 32 W-thread group when W = 16
 __host__ __device__ constexpr int ess_threads(int W) { return W > 8 ? 32 * W : kEssThreads; }
 __host__ __device__ constexpr int ess_groups(int W) { return W >= 8 ? 1 : 8 / W; }
@@ -848,6 +871,26 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     }
     g.sync();
   }
+  // level-1 bucket mapping of this launch: linear, or by octave when chosen (options.buckets
+  // = 2) or when the automatic switch saw more than 1/8 of the previous launch's chains go
+  // down the general interval path or crowd a level-1 bucket (counters: launch t counts into
+  // slot t % 3, reads slot (t - 1) % 3, zeroes slot (t + 1) % 3; slot 3: sticky switch)
+  int l1_mode = p.bucket_mode == 2 ? 2 : 0;
+  if (!kGiven && p.bucket_mode == 0 && p.gmode != nullptr && NB >= 64) {
+    // one thread per chain group reads the counters (a single L2 line every CTA would
+    // otherwise hammer with 512 loads); the decision reaches the group through ctl.mode
+    if (g.tid == 0) {
+      const uint32_t tm3 = t_it % 3u;
+      if (blockIdx.x == 0 && g.gid == 0) p.gmode[(tm3 + 1) % 3] = 0;
+      const int prev = *(volatile int*)(p.gmode + (tm3 + 2) % 3);
+      const bool sticky = *(volatile int*)(p.gmode + 3) != 0;
+      const bool oct = sticky || ((int64_t)prev << TMVN_GMODE_SHIFT) > p.C;
+      if (oct && !sticky) p.gmode[3] = 1;  // written once: stores to the line every CTA reads cost
+      ctl.mode = oct ? 2 : 0;
+    }
+    g.sync();
+    l1_mode = ctl.mode;
+  }
   // per-chain state (bucket tables, control words), reset before the first chain and at
   // the end of every chain, so that the loop-top barrier orders it before phase A
   auto reset_chain_state = [&]() {
@@ -858,8 +901,14 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
       ctl.G = 0.0;  // gamma_0 = 0: the first segment is [0, alpha_{i_1}]
       ctl.rlo = 0;
       ctl.rhi = kTopBits;
-      ctl.mode = 0;
+      ctl.mode = l1_mode;
+      if (l1_mode == 2) {  // NB / 16 buckets per octave
+        ctl.oct_log2 = log2NB - 4;
+        ctl.shift = 52 - (log2NB - 4);
+        ctl.klo = (uint64_t)((NB >> 4) - 1);
+      }
       ctl.maxa_exact = 0;
+      ctl.crowd = 0;
     }
   };
   reset_chain_state();
@@ -1165,7 +1214,9 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     PHASE(2);  // low-word pass
 
     // ---------------- B + C: I_act by Alg. 3, then theta ----------------
-    const bool fast = par_intervals(g, S, ctl, AS, NB, scale, gg, s_w64, s_w32);
+    // a chain is crowded when one level-1 bucket holds 4 x the mean constraints per
+    // bucket + 32 arcs (phase A's bucket atomics and B3's scan serialise on it)
+    const bool fast = par_intervals(g, S, ctl, AS, NB, scale, gg, s_w64, s_w32, 4 * (m / NB) + 32);
     // nu_{t+1} drawn while the highest warp's last lane computes theta (options.rng_overlap:
     // the other W - 1 warps would wait at the barrier); into the other nu buffer (N_next),
     // since phase D still reads nu_t
@@ -1187,6 +1238,12 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     g.sync();
     PHASE(3);  // B (+C) on the parallel path
     PHASE_ADD(7, fast ? 0 : 1);
+    // automatic level-1 mapping: count the chains that went down the general path or
+    // crowded a level-1 bucket (arcs bunched in a few linear buckets); none once octave
+    if (!kGiven && l1_mode == 0 && p.gmode != nullptr && g.tid == 0 && (!fast || ctl.crowd)) {
+      atomicAdd(p.gmode + (t_it % 3u), 1);
+      ctl.crowd = 0;
+    }
     if (!fast) {
       build_intervals(g, S, ctl, AS, NB, log2NB, scale, gg, s_w64, s_w32);
       if (g.tid == 0) {
@@ -1443,6 +1500,13 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
   // buckets: about 16 constraints (~8 arcs) per level-1 bucket, 64 .. 1024
   int NB = 64;
   while (NB < m / 16 && NB < 1024) NB <<= 1;
+  // a requested W whose per-CTA chain groups' bucket tables would not fit in shared
+  // memory (e.g. W = 1, 8 groups, with 1024 level-1 buckets): more warps, fewer groups
+  auto min_bytes = [&](int w) {
+    return (size_t)ess_groups(w) *
+           ess_group_smem_bytes(m, NB, 0, ring_req ? std::min(256 * w, (m + 1) & ~1) : 0);
+  };
+  while (W < 8 && min_bytes(W) > 200 * 1024) W <<= 1;
   const int groups = ess_groups(W);
   // P/Q chunk: 256 W constraints (64 KB ring for a full CTA), never beyond the row;
   // CH = 0: no ring, P and Q are read from global memory

@@ -202,6 +202,9 @@ struct EssParams {
   int stash_smem;   // 1: arcs stashed in shared memory
   int CH;           // constraints per P/Q chunk streamed into shared memory (even)
   int grp_bytes, base_off, stash_off;  // per-group shared-memory layout (set by the launcher)
+  int bucket_mode;  // level-1 buckets: 0 automatic (linear, octave after a general-path-heavy
+                    // launch), 1 linear, 2 by octave
+  int* gmode;       // automatic switch state: [0..2] general-path counters by t % 3, [3] sticky
   // dumps (nullable)
   double* d_alpha;
   double* d_beta;

@@ -79,6 +79,7 @@ struct tmvn_ctx {
   // the RNG stream: nu_{t+1} is drawn beside the projection GEMM of iteration t
   cudaStream_t rng_stream = nullptr;
   int* dyn = nullptr;  // dynamic chain scheduling counters: 64 slots per shard
+  int* gmode = nullptr;  // level-1 bucket switch state: 4 ints per shard (EssParams.gmode)
   cudaEvent_t ev_pre = nullptr, ev_rng = nullptr;
   double *S1 = nullptr, *S2 = nullptr;       // tiled moments (u-space == x-space w/o affine)
   double *S1x = nullptr, *S2x = nullptr;     // row-major x-space moments (affine)
@@ -491,6 +492,8 @@ EssParams base_params(tmvn_ctx* h, int C) {
   p.Ns = use_oz(h) ? h->Ns : nullptr;
   p.ozS = oz_slices(h);
   p.ozKB = h->ozKB;
+  p.bucket_mode = h->opt.buckets;
+  p.gmode = h->gmode;
   if (fuse_arcs(h) && h->arcs) {
     p.arcs = h->arcs;
     p.ald = h->m_pad;
@@ -700,6 +703,9 @@ tmvn_status run_loop_pipe(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed,
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
   CK(h, cudaMemsetAsync(h->dyn, 0, sizeof(int) * 64 * 16, A));
   p.dyn_ctr = h->dyn;
+  if (!h->gmode) CK(h, dalloc(&h->gmode, (size_t)4 * 16));
+  CK(h, cudaMemsetAsync(h->gmode, 0, sizeof(int) * 4 * 16, A));
+  p.gmode = h->gmode;
   auto proj = [&](int64_t t) -> cudaError_t {
     return launch_projection(h, 0, Rp, B, (int)(t % 3), Qb[t & 1], oz);
   };
@@ -786,6 +792,8 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
   const bool twobuf = ahead || gem || ovl;
   CK(h, launch_first_nu(h, C, seed, (uint32_t)t0, st, twobuf ? (int)(t0 & 1) : 0));
   if (!h->dyn) CK(h, dalloc(&h->dyn, (size_t)64 * 16));
+  if (!h->gmode) CK(h, dalloc(&h->gmode, (size_t)4 * 16));
+  CK(h, cudaMemsetAsync(h->gmode, 0, sizeof(int) * 4 * 16, st));
   // dynamic hand-out pays for long rows (W = 8); for short ones the atomic's latency
   // is comparable to a chain's work (config 2: 17 -> 22 us per launch), so auto = W == 8
   const bool dyn = (h->opt.schedule == 2 || (h->opt.schedule == 0 && h->plan.W == 8)) && h->nshards <= 16;
@@ -814,6 +822,7 @@ tmvn_status run_loop(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, doub
     x.p.S2 = h->S2 + x.c0 * h->d_pad;
     x.p.rej = h->rej + x.c0;
     x.p.dyn_ctr = dyn ? h->dyn + 64 * s : nullptr;
+    x.p.gmode = h->gmode + 4 * (s % 16);
     x.p.chain_offset = (uint32_t)(h->opt.chain_offset + x.c0);
     x.p.gstash = h->gstash ? h->gstash + (size_t)s * h->plan.groups * ess_gstash_stride(h->m) : nullptr;
     x.p.ggaps = h->ggaps + (size_t)s * h->plan.groups * (h->m + 2);
@@ -1080,6 +1089,7 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->fuse_arcs = 0;
   o->rng_gemm = 0;
   o->rng_overlap = 0;
+  o->buckets = 0;
   o->warp_mode = 0;  // measured: config 1 5.0 vs 6.1 us / iteration (latency mode), config 2 20 vs 19 us (default path)  // measured slightly slower at config 3 (0.207 -> 0.211 ms per launch) and config 4  // measured neutral at config 3 (0.384 -> 0.383 ms / iteration), slower at config 5  // measured slower on B200 (the epilogue outgrows the MMAs)
   return TMVN_OK;
 }
@@ -1573,6 +1583,14 @@ tmvn_status tmvn_get_moments(tmvn_handle h, double* sum, double* sumsq, int64_t*
 tmvn_status tmvn_get_profile(tmvn_handle h, tmvn_profile* prof) {
   if (!h || !prof) return fail(h, TMVN_E_ARG, "null argument");
   *prof = h->prof;
+  prof->buckets_used = 0;
+  if (h->gmode) {  // slot 3 of every shard: the automatic switch's sticky flag
+    int g[4 * 16];
+    CK(h, cudaMemcpy(g, h->gmode, sizeof(g), cudaMemcpyDeviceToHost));
+    int oct = h->opt.buckets == 2 ? 1 : 0;
+    for (int s = 0; s < 16; ++s) oct |= g[4 * s + 3];
+    prof->buckets_used = oct ? 2 : 1;
+  }
   return TMVN_OK;
 }
 
@@ -1611,7 +1629,7 @@ void tmvn_destroy(tmvn_handle h) {
   if (h->At != h->A_tiled) dfree(h->At);
   dfree(h->A_tiled); dfree(h->A_row); dfree(h->A_pad); dfree(h->Xsnap); dfree(h->lat_gscratch); dfree(h->cp_tl); dfree(h->cp_arcs); dfree(h->cp_cur); dfree(h->A32); dfree(h->b32); dfree(h->b_orig); dfree(h->b_eff);
   dfree(h->mu); dfree(h->L); dfree(h->L_tiled);
-  dfree(h->dflag); dfree(h->dsum); dfree(h->msum);
+  dfree(h->dflag); dfree(h->dsum); dfree(h->msum); dfree(h->gmode);
   if (h->pin) cudaFreeHost(h->pin);
   dfree(h->As); dfree(h->rowscale);
   delete h;
@@ -1695,6 +1713,17 @@ tmvn_status tmvn_test_arcs(const double* p, const double* q, const double* b, in
 }
 
 static int g_test_chain_warps = 0;
+static int g_test_bucket_mode = 1;  // the intervals hook: 1 linear level-1 buckets, 2 by octave
+
+tmvn_status tmvn_test_interval_config(int32_t chain_warps, int32_t bucket_mode) {
+  if (chain_warps != 0 && chain_warps != 1 && chain_warps != 2 && chain_warps != 4 && chain_warps != 8 &&
+      chain_warps != 16)
+    return fail(nullptr, TMVN_E_ARG, "chain_warps must be 0, 1, 2, 4, 8 or 16");
+  if (bucket_mode != 1 && bucket_mode != 2) return fail(nullptr, TMVN_E_ARG, "bucket_mode must be 1 or 2");
+  g_test_chain_warps = chain_warps;
+  g_test_bucket_mode = bucket_mode;
+  return TMVN_OK;
+}
 
 tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t m, int64_t C,
                                 const double* u, double eps, double* seg_lo, double* seg_hi,
@@ -1729,6 +1758,7 @@ tmvn_status tmvn_test_intervals(const double* alpha, const double* beta, int64_t
   p.W = plan.W;
   p.CH = plan.CH;
   p.stash_smem = plan.stash_smem;
+  p.bucket_mode = g_test_bucket_mode;
   p.d_seg_lo = seg_cap ? dlo.p : nullptr;
   p.d_seg_hi = dhi.p;
   p.seg_cap = seg_cap;

@@ -247,7 +247,8 @@ def test_rng_ahead_and_projection_options_bitwise():
                dict(rng_overlap=1, chain_warps=2), dict(fuse_arcs=1), dict(fuse_arcs=1, graphs=0),
                dict(fuse_arcs=1, chain_warps=4), dict(ring=1), dict(ring=1, graphs=0),
                dict(streams=2), dict(streams=3), dict(streams=2, rng_overlap=1),
-               dict(streams=2, fuse_arcs=1), dict(streams=2, rng_gemm=1), dict(streams=3, ring=1)):
+               dict(streams=2, fuse_arcs=1), dict(streams=2, rng_gemm=1), dict(streams=3, ring=1),
+               dict(buckets=1), dict(buckets=2), dict(buckets=2, graphs=0), dict(buckets=2, streams=2)):
         out = tm.Sampler(A, b, **kw).sample(X0, 70, seed=11)
         assert np.array_equal(out, ref), kw
     # chain shards on concurrent streams (the automatic choice from 2048 chains): the same
@@ -263,6 +264,27 @@ def test_rng_ahead_and_projection_options_bitwise():
         for u, v in zip(sS.moments()[:2], s1.moments()[:2]):
             assert np.allclose(u, v, rtol=1e-12, atol=1e-12)
         assert sS.stats() == s1.stats()
+
+
+def test_bucket_mappings_bitwise_on_the_s42_geometry():
+    """S4.2's instance (arcs bunched just after theta = 0 from a start deep
+    inside): the octave level-1 buckets (options.buckets = 2) and the automatic switch
+    (0, which turns octave on after one launch of crowded chains) give bit-identical
+    chains to the linear mapping (any monotone bucketing: Prop. 1), one launch per
+    iteration and graphed blocks alike."""
+    A, b, x0 = synth.paper_random(400, seed=4)
+    X0 = np.tile(x0, (300, 1))
+    outs = {}
+    for bk in (1, 2, 0):
+        for g in (0, 1):
+            s = tm.Sampler(A, b, buckets=bk, graphs=g, latency=0)
+            outs[bk, g] = (s.sample(X0, 40, seed=3), s.moments(), s.stats())
+    ref = outs[1, 0]
+    for key, (X, mom, st) in outs.items():
+        assert np.array_equal(X, ref[0]), key
+        assert all(np.array_equal(u, v) for u, v in zip(mom, ref[1])), key
+        assert st == ref[2], key
+    assert np.max(ref[0] @ A.T - b) <= 0.0
 
 
 def test_odd_m_and_general_interval_path_on_default_options():

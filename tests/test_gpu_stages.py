@@ -160,3 +160,26 @@ def test_intervals_trim():
     al = rng.uniform(0, TWO_PI, (C, m))
     be = np.minimum(al + rng.exponential(0.05, (C, m)), TWO_PI)
     _check_intervals(al, be, rng.random(C), eps=1e-3)
+
+
+@pytest.mark.parametrize("warps,mode", [(0, 2), (8, 2), (2, 2), (1, 2), (16, 1), (4, 1)])
+def test_intervals_bucket_mappings_and_group_sizes(warps, mode):
+    """Alg. 3's bucketed form with the octave level-1 mapping (options.buckets = 2) and
+    other group sizes: bit-identical to Alg. 2 (any monotone bucketing, Prop. 1),
+    including arcs crowded just after theta = 0 (the S4.2 geometry the octave mapping
+    is for), ties, padding and the paper's worst case."""
+    tm.test_interval_config(warps, mode)
+    try:
+        rng = np.random.default_rng(11 + warps + 10 * mode)
+        C, m = 24, 600
+        al = 10.0 ** rng.uniform(-6, -1, (C, m))  # crowded near 0
+        be = np.minimum(al + 10.0 ** rng.uniform(-5, 0.5, (C, m)), TWO_PI)
+        al[:, ::9] = al[:, 1::9]  # ties
+        pad = rng.random((C, m)) < 0.2
+        al[pad] = 0.0
+        be[pad] = 0.0
+        _check_intervals(al, be, rng.random(C))
+        test_intervals_random_with_padding_and_ties()
+        test_intervals_paper_examples()
+    finally:
+        tm.test_interval_config(0, 1)

@@ -20,7 +20,7 @@ if os.environ.get("PAPER_D"):  # the S4.2 geometry (synth.paper_random) with PAP
     A, b, x0 = synth.paper_random(dd, seed=dd)
     cfg = dataclasses.replace(cfg, C=int(os.environ.get("PAPER_C", "20")))
 s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"), latency=0)
-s.set_options(streams=1, chain_warps=int(os.environ.get("W", "0")))
+s.set_options(streams=1, chain_warps=int(os.environ.get("W", "0")), buckets=int(os.environ.get("BUCKETS", "0")))
 X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
 s.sample(X, 40, cfg.chain_seed, out=X)
 buf = np.zeros(14, dtype=np.uint64)

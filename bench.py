@@ -352,14 +352,31 @@ def roofline_entries(prof, ms_iso, k, cfg, Cl, ips, steps, args, world, opts):
         g_ms = prof["gemm_ms"] / nG
         fl = prof["gemm_flops"] / nG
         ach = fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
-        kind = ("P = X A'^T refresh every recompute_every (int8: digit slicing + tcgen05 GEMM)"
-                if prof["tc_launches"] > 0 else "Q = N A^T and the P refresh, FP64 DMMA (mma.sync f64)")
-        ents.append({"bound": "tensor", "kernel": f"projection/refresh GEMMs ({kind})",
-                     "achieved": ach, "peak": peaks["dmma_tflops_w8"], "unit": "TFLOP/s (FP64-equivalent)",
-                     "frac": ach / peaks["dmma_tflops_w8"], "traffic": None,
-                     "peak_source": "measured FP64 DMMA pipe peak (profiles/peaks_fp64_r01.json)",
-                     "algorithmic_flops_per_launch": fl, "avg_launch_ms": g_ms, "launches": nG,
-                     "share_of_step": prof["gemm_ms"] / ms_iso})
+        if prof["tc_launches"] > 0:
+            # the refresh runs on the int8 tensor path too (digit slicing of X + the Ozaki GEMM
+            # with per-chain column scales): the int8 roofline, like the projection's
+            S = 4 if args.precision else (opts.ozaki_slices or 7)
+            ops = fl * S * (S + 1) / 2
+            ents.append({"bound": "tensor",
+                         "kernel": f"refresh P = X A'^T every recompute_every (digit slicing of X + "
+                                   f"ozaki_gemm_kernel, {S} digits)",
+                         "achieved": ops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0, "peak": 2.0 * bf16,
+                         "unit": "TOP/s (int8)",
+                         "frac": (ops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0) / (2.0 * bf16), "traffic": None,
+                         "peak_source": psrc + " bf16_tflops (burst) x 2 (the nominal int8 / bf16 dense ratio)",
+                         "algorithmic_ops_per_launch": ops,
+                         "algorithmic_ops_rule": "S(S+1)/2 digit-pair products x 2 C m d per launch; the "
+                                                 "launch time includes the slicing kernel of X",
+                         "fp64_equivalent_tflops": ach, "avg_launch_ms": g_ms, "launches": nG,
+                         "share_of_step": prof["gemm_ms"] / ms_iso})
+        else:
+            ents.append({"bound": "tensor",
+                         "kernel": "projection/refresh GEMMs (Q = N A^T and the P refresh, FP64 DMMA, mma.sync f64)",
+                         "achieved": ach, "peak": peaks["dmma_tflops_w8"], "unit": "TFLOP/s (FP64)",
+                         "frac": ach / peaks["dmma_tflops_w8"], "traffic": None,
+                         "peak_source": "measured FP64 DMMA pipe peak (profiles/peaks_fp64_r01.json)",
+                         "algorithmic_flops_per_launch": fl, "avg_launch_ms": g_ms, "launches": nG,
+                         "share_of_step": prof["gemm_ms"] / ms_iso})
     ents.sort(key=lambda e: -e["share_of_step"])
     return ents
 

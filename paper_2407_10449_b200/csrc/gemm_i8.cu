@@ -16,11 +16,14 @@
 // d <= 4096).  The S(S+1)/2 int8 MMAs per K step are exact; the pairs with
 // k + l > S + 1 are dropped (weight <= 2^(-8S)).  The epilogue forms
 //     q_i = 2^(e_i + e_nu - 14) * sum_{D} acc_D 2^(-8(D-2))
-// by FP64 Horner from the least significant diagonal.  Error bound (stated in
+// by summing the diagonals exactly in two 64-bit integers (the low one < 2^47: its
+// conversion is exact; the high one is exact below 2^53) and one FP64 FMA.  Error
+// bound (stated in
 // include/tmvn.h, tested in tests/test_gpu_ozaki.py):
 //     |q - a.nu| <= 2^(e_i + e_nu) d (S + 1) 2^(2 - 8S) + 2^-51 |q|
 // (per product: truncation of both operands < 2^(1 - (8S-1)); dropped diagonals
-// D >= S + 2: < (S - 1) 2^(2 - 8S) per unit of d; Horner rounding), i.e.
+// D >= S + 2: < (S - 1) 2^(2 - 8S) per unit of d; the reconstruction's two
+// roundings, <= 2^-52 |q|), i.e.
 // FP64-class accuracy relative to max_j |a_ij| * 2^e_nu * d, independent
 // of C; the result is a deterministic function of (A', nu) (no split-K, fixed
 // reconstruction order), so chains are bitwise independent of the sharding.
@@ -38,7 +41,7 @@
 //                  to tmem_full)
 //   warps 2-5:     A loaders (digit slices 0-3 of each stage into TMEM,
 //                  tcgen05.st, double-buffered)
-//   warps 6-13:    epilogue (tcgen05.ld 32x32b, FP64 Horner, coalesced stores
+//   warps 6-13:    epilogue (tcgen05.ld 32x32b, integer + FP64 reconstruction, coalesced stores
 //                  of Q[chain][constraint]), then arrive on tmem_empty;
 //                  with options.fuse_arcs also the arcs of eq:roots.
 #include <cstdint>
@@ -78,6 +81,10 @@ __host__ __device__ constexpr int oz_stages(int S) {
   return (226 * 1024) / oz_stage_bytes(S) > TMVN_OZ_MAX_STAGES ? TMVN_OZ_MAX_STAGES
                                                                  : (226 * 1024) / oz_stage_bytes(S);
 }
+
+// 2^(-8 k), k = 0 .. 4 (epilogue reconstruction)
+__device__ constexpr double kOzInvPow2[5] = {1.0, 0.00390625, 1.52587890625e-05, 5.9604644775390625e-08,
+                                             2.3283064365386962890625e-10};
 
 // ---- tcgen05 / mbarrier wrappers -------------------------------------------
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -436,11 +443,21 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          double h = (double)acc[S - 1][j];
+          // the diagonals combined exactly in two 64-bit integers (IMAD.WIDE), then two
+          // conversions and one FMA (S int32 -> FP64 conversions per output cost 26 % more
+          // epilogue cycles, tools/oz_timing.py): hi = sum_{D < H} acc_D 2^(8(H-1-D))
+          // (|hi| < 2^55), lo = sum_{D >= H} acc_D 2^(8(S-1-D)),
+          // h = (hi + lo 2^(-8(S-H))) 2^(-8(H-1))
+          constexpr int H = (S + 1) / 2;
+          long long hi = (long long)acc[H - 1][j], lo = (long long)acc[S - 1][j];
 #pragma unroll
-          for (int D = S - 2; D >= 0; --D) h = __fma_rn(h, 0.00390625, (double)acc[D][j]);  // 2^-8
+          for (int D = H - 2; D >= 0; --D) hi += (long long)acc[D][j] * (1ll << (8 * (H - 1 - D)));
+#pragma unroll
+          for (int D = S - 2; D >= H; --D) lo += (long long)acc[D][j] * (1ll << (8 * (S - 1 - D)));
+          const double h = __fma_rn(__ll2double_rn(lo), kOzInvPow2[S - H], __ll2double_rn(hi));
+          const double sc0 = scale * kOzInvPow2[H - 1];  // exact: powers of two
           // per-column power of two (refresh of P = X A'^T: 2^(e_c - 4) per chain), exact
-          const double sc = CS ? __dmul_rn(scale, __ldg(colscale + (int64_t)nb * kOzBN + cc + j)) : scale;
+          const double sc = CS ? __dmul_rn(sc0, __ldg(colscale + (int64_t)nb * kOzBN + cc + j)) : sc0;
           qcol[(int64_t)(cc + j) * ldq] = __dmul_rn(h, sc);
         }
       }

@@ -213,9 +213,11 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint4& a, const u
 
 // Role timing (timing build -DTMVN_PHASE_TIMING only; tools/oz_timing.py):
 // [0] MMA wait full, [1] MMA wait tmem_empty, [2] MMA issue, [3] epilogue wait
-// tmem_full, [4] epilogue work, [5] producer wait empty, [6] tiles, [7] CTA cycles
+// tmem_full, [4] epilogue work, [5] producer wait empty, [6] tiles, [7] CTA cycles,
+// [8] MMA wait for the A loaders (included in [0]), [9] A loaders wait for the MMAs
+// to release a TMEM A buffer
 #ifdef TMVN_PHASE_TIMING
-__device__ unsigned long long g_oz_cycles[8];
+__device__ unsigned long long g_oz_cycles[10];
 #define OZT(var) const long long var = clock64()
 #define OZADD(i, v) atomicAdd(&g_oz_cycles[i], (unsigned long long)(v))
 #else
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #endif
   OZT(t_start);
 #ifdef TMVN_PHASE_TIMING
-  long long acc0 = 0, acc1 = 0, acc2 = 0;
+  long long acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
 #endif
 
   if (warp == 0) {
@@ -350,11 +352,13 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           const int b = it & 1;
           OZT(f0);
           mbar_wait(&full[s], (it / kOzStages) & 1);
+          OZT(fa);
           if (NTS > 0) mbar_wait(&afull[b], (it >> 1) & 1);
           tc_fence_after();
           OZT(f1);
 #ifdef TMVN_PHASE_TIMING
           acc0 += f1 - f0;
+          acc3 += f1 - fa;
 #endif
           const uint64_t so = (uint64_t)((s * kStage) >> 4);
           const uint32_t abuf = b ? oz_acol<S>(1, 0) : oz_acol<S>(0, 0);
@@ -387,7 +391,11 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           const int s = it % kOzStages;
           const int b = it & 1;
           mbar_wait(&full[s], (it / kOzStages) & 1);
+          OZT(la);
           if (it >= 2) mbar_wait(&aempty[b], ((it >> 1) - 1) & 1);
+#ifdef TMVN_PHASE_TIMING
+          acc3 += clock64() - la;
+#endif
           tc_fence_after();
           const unsigned char* st = ring + s * kStage + roff;
 #pragma unroll
@@ -507,7 +515,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #ifdef TMVN_PHASE_TIMING
   if (lane == 0) {
     if (warp == 0) OZADD(5, acc0);
-    if (warp == 1) { OZADD(0, acc0); OZADD(1, acc1); OZADD(2, acc2); }
+    if (warp == 1) { OZADD(0, acc0); OZADD(1, acc1); OZADD(2, acc2); OZADD(8, acc3); }
+    if (warp == 2) OZADD(9, acc3);
     if (warp == 6) { OZADD(3, acc0); OZADD(4, acc1); }
     if (threadIdx.x == 0) OZADD(7, clock64() - t_start);
   }
@@ -559,11 +568,11 @@ __global__ void oz_slice_kernel(const double* __restrict__ src, int R, int d, in
 }  // namespace
 
 #ifdef TMVN_PHASE_TIMING
-void oz_cycles(unsigned long long* out8, bool reset) {
+void oz_cycles(unsigned long long* out10, bool reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out8, g_oz_cycles, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out10, g_oz_cycles, sizeof(unsigned long long) * 10);
   if (reset) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[10] = {0};
     cudaMemcpyToSymbol(g_oz_cycles, z, sizeof(z));
   }
 }

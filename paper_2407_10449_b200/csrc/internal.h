@@ -258,7 +258,7 @@ void tl_access_ess(unsigned long long* out, bool reset);
 #ifdef TMVN_PHASE_TIMING
 void lat_cycles(unsigned long long* out16, bool reset);
 void phase_cycles(unsigned long long* out10, bool reset);
-void oz_cycles(unsigned long long* out8, bool reset);
+void oz_cycles(unsigned long long* out10, bool reset);
 #endif
 
 // ---- auxiliary kernels (aux_kernels.cu) -------------------------------------

@@ -2061,8 +2061,8 @@ tmvn_status tmvn_test_lat_cycles(uint64_t* out16, int reset) {
   tmvn::lat_cycles(reinterpret_cast<unsigned long long*>(out16), reset != 0);
   return TMVN_OK;
 }
-tmvn_status tmvn_test_oz_cycles(uint64_t* out8, int reset) {
-  tmvn::oz_cycles(reinterpret_cast<unsigned long long*>(out8), reset != 0);
+tmvn_status tmvn_test_oz_cycles(uint64_t* out10, int reset) {
+  tmvn::oz_cycles(reinterpret_cast<unsigned long long*>(out10), reset != 0);
   return TMVN_OK;
 }
 #endif

@@ -17,13 +17,13 @@ A, b, x0 = synth.make_instance(k)
 s = tm.Sampler(torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda"), projection=1, graphs=0)
 X = torch.tensor(np.tile(x0, (cfg.C, 1)), device="cuda")
 s.sample(X, 4, cfg.chain_seed, out=X)
-buf = np.zeros(8, dtype=np.uint64)
+buf = np.zeros(10, dtype=np.uint64)
 L.tmvn_test_oz_cycles(buf.ctypes.data_as(ctypes.c_void_p), 1)
 s.sample(X, iters, cfg.chain_seed, out=X)
 L.tmvn_test_oz_cycles(buf.ctypes.data_as(ctypes.c_void_p), 0)
 tiles = float(buf[6])
 names = ["MMA wait full", "MMA wait tmem_empty", "MMA issue", "epi wait tmem_full", "epi work",
-         "producer wait empty", "tiles", "CTA cycles"]
+         "producer wait empty", "tiles", "CTA cycles", "MMA wait A loaders", "loaders wait A buf"]
 for i, n in enumerate(names):
     if i == 6:
         print(f"  {n:22s} {buf[i]:.0f}")

@@ -369,6 +369,9 @@ tmvn_status tmvn_cp_end(tmvn_handle h, int64_t n_iter, double* out);
  * tmvn_create when h is NULL).  Valid until the next call on the handle. */
 const char* tmvn_last_error(tmvn_handle h);
 const char* tmvn_version(void);
+/* sizeof of the ABI structs, for bindings to check their layouts: out[0..3] =
+ * tmvn_options, tmvn_stats, tmvn_profile, tmvn_step_dump.  Host-only (no device call). */
+tmvn_status tmvn_struct_sizes(int64_t* out4);
 void tmvn_destroy(tmvn_handle h);
 
 /* ------------------------------------------------------------------------ */

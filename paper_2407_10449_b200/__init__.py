@@ -28,7 +28,7 @@ STATUS = {0: "TMVN_OK", -1: "TMVN_E_ARG", -2: "TMVN_E_EMPTY_POLYTOPE",
 
 EXPORTS = ["tmvn_default_options", "tmvn_create", "tmvn_set_affine", "tmvn_set_options",
            "tmvn_get_options", "tmvn_sample", "tmvn_get_stats", "tmvn_get_moments",
-           "tmvn_reset_stats", "tmvn_get_profile", "tmvn_last_error", "tmvn_version",
+           "tmvn_reset_stats", "tmvn_get_profile", "tmvn_last_error", "tmvn_version", "tmvn_struct_sizes",
            "tmvn_destroy", "tmvn_test_philox", "tmvn_test_curand_philox", "tmvn_test_normals", "tmvn_test_arcs",
            "tmvn_test_intervals", "tmvn_test_interval_config", "tmvn_test_gemm", "tmvn_test_ozaki_gemm", "tmvn_test_step",
            "tmvn_test_trace", "tmvn_test_latency_cap", "tmvn_test_latency_grid", "tmvn_cp_begin", "tmvn_cp_stats", "tmvn_cp_live",
@@ -109,6 +109,7 @@ def lib():
             "tmvn_get_moments": [H, P, P, P],
             "tmvn_reset_stats": [H],
             "tmvn_get_profile": [H, P],
+            "tmvn_struct_sizes": [P],
             "tmvn_test_philox": [P, P, i64, P],
             "tmvn_test_curand_philox": [P, P, i64, P],
             "tmvn_test_normals": [u64, u64, i64, i64, i64, P, P],

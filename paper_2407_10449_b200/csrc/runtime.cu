@@ -1094,6 +1094,15 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   return TMVN_OK;
 }
 
+tmvn_status tmvn_struct_sizes(int64_t* out4) {
+  if (!out4) return fail(nullptr, TMVN_E_ARG, "null argument");
+  out4[0] = (int64_t)sizeof(tmvn_options);
+  out4[1] = (int64_t)sizeof(tmvn_stats);
+  out4[2] = (int64_t)sizeof(tmvn_profile);
+  out4[3] = (int64_t)sizeof(tmvn_step_dump);
+  return TMVN_OK;
+}
+
 const char* tmvn_version(void) { return "tmvn-b200 0.2 (sm_100a, FP64 DMMA + int8 tcgen05 Ozaki)"; }
 
 const char* tmvn_last_error(tmvn_handle h) { return h ? h->err.c_str() : g_create_error.c_str(); }

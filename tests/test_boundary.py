@@ -97,3 +97,13 @@ def test_header_is_plain_c(tmp_path):
     r = subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(root, "include"),
                         "-c", str(src), "-o", str(tmp_path / "h.o")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_binding_struct_layouts_match_the_library():
+    """The ctypes mirrors of the ABI structs have the C sizes (a field added on one side
+    only would shift every later field): tmvn_struct_sizes is host-only."""
+    import paper_2407_10449_b200 as tm
+    out = (ctypes.c_int64 * 4)()
+    assert tm.lib().tmvn_struct_sizes(out) == 0
+    assert list(out) == [ctypes.sizeof(tm.options), ctypes.sizeof(tm.stats), ctypes.sizeof(tm.profile),
+                         ctypes.sizeof(tm.step_dump)]

@@ -7,7 +7,7 @@ sys.path.insert(0, ROOT)
 import torch
 import paper_2407_10449_b200 as tm
 from paper_2407_10449_b200 import synth
-tm.LIB_PATH = os.path.join(ROOT, "build", "libtmvn_timing.so")
+tm.LIB_PATH = os.environ.get("TIMING_LIB", os.path.join(ROOT, "build", "libtmvn_timing.so"))
 L = tm.lib()
 L.tmvn_test_phase_cycles.argtypes = [ctypes.c_void_p, ctypes.c_int]
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 3

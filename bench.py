@@ -69,6 +69,9 @@ def parse(argv=None):
     ap.add_argument("--projection", type=int, default=0,
                     help="options.projection: 0 auto (int8 when d <= 4096), 1 int8 Ozaki split on "
                          "tcgen05 (FP64-accurate), 2 FP64 DMMA")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="options.streams: 0 auto (chain shards on concurrent streams); 1 one launch per "
+                         "kernel over all chains (the ncu captures behind the roofline traffic use it)")
     ap.add_argument("--precision", type=int, default=0,
                     help="options.precision: 0 FP64 (the BASELINE metric), 1 the paper's FP32-class "
                          "mode (int8 projection at 4 digits / FP32 latency kernel; trim_eps 1e-5)")
@@ -404,6 +407,8 @@ def run_workload(k, args, rank, world, dev, primary, host):
     stream = torch.cuda.Stream(device=dev)
     s = tm.Sampler(torch.tensor(A, device=dev), torch.tensor(b, device=dev), **opts)
     s.set_options(stream=stream, projection=args.projection)
+    if args.streams:
+        s.set_options(streams=args.streams)
     if args.precision:
         s.set_options(precision=1, trim_eps=1e-5)
     X = torch.tensor(np.tile(x0, (C, 1)), device=dev)

@@ -716,6 +716,10 @@ __device__ __forceinline__ void stash_arc(const Smem& S, Ctl& ctl, double2* stas
 // CTAs per SM the register allocation must allow: 4 (64 registers) for the config-3
 // path (W = 8, arcs stashed in shared memory: 4 x 56 KB fit, no spills), 3 (80
 // registers) elsewhere (at 64 those variants spill 100-200 bytes)
+// global-stash path: per-warp queues of active constraints in shared memory (phase A)
+#ifndef TMVN_ESS_AQUEUE
+#define TMVN_ESS_AQUEUE 1
+#endif
 #ifndef TMVN_ESS_MIN_BLOCKS
 #define TMVN_ESS_MIN_BLOCKS 3
 #endif
@@ -1128,8 +1132,96 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
           p.d_active[(int64_t)c * m + i] = 1;
         }
       }
+          } else if (TMVN_ESS_AQUEUE) {
+      // global stash (long rows): one pass -- the active test (C3/C25) on every constraint
+      // pair; each warp queues its active constraints (p, q, index) in shared memory and
+      // computes their arcs 32 at a time with every lane busy, straight into the stash
+      // (no (p, q) round trip through global memory; ~40-75 % of the constraints are
+      // inactive and would otherwise idle their lanes through two atan2)
+      const double2* P2 = reinterpret_cast<const double2*>(Prow);
+      const double2* Q2 = reinterpret_cast<const double2*>(Qrow);
+      const double2* B2 = reinterpret_cast<const double2*>(p.b);
+      unsigned char* qbase = gbase + p.stash_off + (size_t)g.warp * kAQueueBytes;
+      double* qP = reinterpret_cast<double*>(qbase);
+      double* qQ = qP + kAQueue;
+      int* qI = reinterpret_cast<int*>(qQ + kAQueue);
+      int qn = 0;  // warp-uniform
+      auto drain = [&](int n) {  // the arcs of the queue's first n <= 32 entries
+        __syncwarp();
+        const bool mine = g.lane < n;
+        double al = 0.0, be = 0.0;
+        int i = 0;
+        if (mine) {
+          i = qI[g.lane];
+          arc_of(qP[g.lane], qQ[g.lane], __ldg(p.b + i), al, be);  // active by the test: same predicate
+        }
+        int sb = 0;
+        if (g.lane == 0) sb = atomicAdd(&ctl.n_act, n);
+        sb = __shfl_sync(0xffffffffu, sb, 0);
+        if (mine) {
+          stash[sb + g.lane] = make_double2(al, be);
+          bucket_add<false>(S, bucket_key(al, ctl, NB, scale), al, be);
+          if (p.d_alpha) {
+            p.d_alpha[(int64_t)c * m + i] = al;
+            p.d_beta[(int64_t)c * m + i] = be;
+            p.d_active[(int64_t)c * m + i] = 1;
+          }
+        }
+        __syncwarp();
+      };
+      const int npairs = (m + 1) / 2;
+      const int npr = (npairs + T - 1) / T * T;  // whole warps stay in the loop (ballots)
+      for (int base = 0; base < npr; base += kBatchA1 * T) {
+        double2 pp[kBatchA1], qq[kBatchA1], bb[kBatchA1];
+#pragma unroll
+        for (int u = 0; u < kBatchA1; ++u) {
+          const int pi = base + u * T + g.tid;
+          if (pi < npairs) {
+            pp[u] = P2[pi];
+            qq[u] = Q2[pi];
+            bb[u] = __ldg(B2 + pi);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatchA1; ++u) {
+          if (base + u * T >= npr) break;  // uniform
+          const int pi = base + u * T + g.tid;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = 2 * pi + h;
+            const double pv = h ? pp[u].y : pp[u].x, qv = h ? qq[u].y : qq[u].x, bv = h ? bb[u].y : bb[u].x;
+            const bool act = pi < npairs && i < m && arc_active(pv, qv, bv);
+            if (p.d_alpha && pi < npairs && i < m && !act) {
+              p.d_alpha[(int64_t)c * m + i] = 0.0;
+              p.d_beta[(int64_t)c * m + i] = 0.0;
+              p.d_active[(int64_t)c * m + i] = 0;
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, act);
+            if (act) {
+              const int pos = qn + __popc(mask & ((1u << g.lane) - 1u));
+              qP[pos] = pv;
+              qQ[pos] = qv;
+              qI[pos] = i;
+            }
+            qn += __popc(mask);
+            if (qn >= 32) {  // a full warp of arcs; the rest (< 32) moves to the front
+              drain(32);
+              const int rest = qn - 32;
+              if (g.lane < rest) {
+                qP[g.lane] = qP[32 + g.lane];
+                qQ[g.lane] = qQ[32 + g.lane];
+                qI[g.lane] = qI[32 + g.lane];
+              }
+              __syncwarp();
+              qn = rest;
+            }
+          }
+        }
+      }
+      if (qn > 0) drain(qn);
+      PHASE(10);  // A1: active test + arcs (one pass here; slot 1 gets the barrier)
           } else {
-      // two passes: (1) the active test (C3/C25) on every constraint pair, active
+      // (TMVN_ESS_AQUEUE = 0) two passes: (1) the active test (C3/C25) on every constraint pair, active
       // (p, q) and the index compacted into the stash; (2) the arcs of the active
       // constraints only, every lane busy (about 40 % of the constraints are
       // inactive at config 3 and would idle their lanes through two atan2)
@@ -1432,7 +1524,7 @@ template <bool kGiven>
 cudaError_t launch_any(const EssParams& p0, int grid, cudaStream_t st) {
   if (grid < 1) return cudaSuccess;
   EssParams p = p0;
-  p.grp_bytes = (int)ess_group_smem_bytes(p.m, p.NB, p.stash_smem, p.CH);
+  p.grp_bytes = (int)ess_group_smem_bytes(p.m, p.NB, p.stash_smem, p.CH, p.W);
   p.base_off = (int)ess_ring_bytes(p.CH);
   p.stash_off = p.base_off + (int)ess_group_base_bytes(p.NB);
   const size_t smem = (size_t)ess_groups(p.W) * (size_t)p.grp_bytes;
@@ -1504,7 +1596,7 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
   // memory (e.g. W = 1, 8 groups, with 1024 level-1 buckets): more warps, fewer groups
   auto min_bytes = [&](int w) {
     return (size_t)ess_groups(w) *
-           ess_group_smem_bytes(m, NB, 0, ring_req ? std::min(256 * w, (m + 1) & ~1) : 0);
+           ess_group_smem_bytes(m, NB, 0, ring_req ? std::min(256 * w, (m + 1) & ~1) : 0, w);
   };
   while (W < 8 && min_bytes(W) > 200 * 1024) W <<= 1;
   const int groups = ess_groups(W);
@@ -1517,7 +1609,7 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
   // stash in shared memory when 2 CTAs per SM still fit
   int stash_smem = 0;
   if ((size_t)groups * ess_group_smem_bytes(m, NB, 1, CH) <= 112 * 1024) stash_smem = 1;
-  const size_t smem = (size_t)groups * ess_group_smem_bytes(m, NB, stash_smem, CH);
+  const size_t smem = (size_t)groups * ess_group_smem_bytes(m, NB, stash_smem, CH, W);
   int per_sm = 0;
   switch (W) {
     case 1: per_sm = occupancy_w<1>(smem, CH > 0, stash_smem); break;

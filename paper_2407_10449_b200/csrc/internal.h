@@ -231,11 +231,16 @@ __host__ __device__ inline size_t ess_group_base_bytes(int NB) {
              (size_t)kLiveCap * 16 + (size_t)NB * 3 * 4;
   return (s + 15) / 16 * 16;
 }
-__host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_smem, int CH) {
+// global-stash path (TMVN_ESS_AQUEUE): per warp, a queue of kAQueue active constraints
+// (p, q doubles, index int) in shared memory where the stash would be
+constexpr int kAQueue = 64;
+constexpr int kAQueueBytes = kAQueue * 20;
+__host__ __device__ inline size_t ess_group_smem_bytes(int m, int NB, int stash_smem, int CH, int W = 16) {
   size_t s = ess_ring_bytes(CH) + ess_group_base_bytes(NB);
   // stash: the arcs + constraint index (phase A compaction), or the chain's P and Q rows
-  // (even length) + the compacted active indices
+  // (even length) + the compacted active indices; else (global stash) the warps' queues
   if (stash_smem) s += (size_t)((m + 1) & ~1) * 16 + (size_t)m * 4;
+  else s += (size_t)W * kAQueueBytes;
   return (s + 15) / 16 * 16;
 }
 

@@ -279,7 +279,14 @@ def test_bucket_mappings_bitwise_on_the_s42_geometry():
         for g in (0, 1):
             s = tm.Sampler(A, b, buckets=bk, graphs=g, latency=0)
             outs[bk, g] = (s.sample(X0, 40, seed=3), s.moments(), s.stats())
+            # the automatic switch turns octave on here (every chain crowds bucket 0)
+            assert s.profile()["buckets_used"] == (1 if bk == 1 else 2), (bk, g)
     ref = outs[1, 0]
+    # a unit-row random polytope from x0 = 0 (config 3's structure) does not crowd: linear
+    A3, b3, x3 = synth.make_instance(3, m=600, d=200)
+    s3 = tm.Sampler(A3, b3, latency=0)
+    s3.sample(np.tile(x3, (300, 1)), 20, seed=3)
+    assert s3.profile()["buckets_used"] == 1
     for key, (X, mom, st) in outs.items():
         assert np.array_equal(X, ref[0]), key
         assert all(np.array_equal(u, v) for u, v in zip(mom, ref[1])), key

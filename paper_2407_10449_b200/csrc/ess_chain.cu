@@ -259,9 +259,21 @@ __device__ __forceinline__ uint32_t* lo_word(uint64_t* a) { return reinterpret_c
 __device__ __forceinline__ uint32_t hi32(double x) { return (uint32_t)(dbits(x) >> 32); }
 __device__ __forceinline__ uint32_t lo32(double x) { return (uint32_t)dbits(x); }
 
-template <bool kExact>
+// kCas: max beta exact in this pass by a 64-bit compare-and-swap, taken only while the
+// value beats the bucket's current max (a plain 64-bit load first: about ln n swaps per
+// bucket of n arcs), so that no low-word pass over the stash is needed (global stash)
+__device__ __forceinline__ void max_u64_cas(uint64_t* a, uint64_t v) {
+  uint64_t cur = *reinterpret_cast<volatile uint64_t*>(a);
+  while (v > cur) {
+    const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(a), cur, v);
+    if (prev == cur) break;
+    cur = prev;
+  }
+}
+template <bool kExact, bool kCas = false>
 __device__ __forceinline__ void bucket_add(const Smem& S, int k, double a, double b) {
-  atomicMax(hi_word(&S.Gx[k]), hi32(b));
+  if (kCas) max_u64_cas(&S.Gx[k], dbits(b));
+  else atomicMax(hi_word(&S.Gx[k]), hi32(b));
   atomicMax(hi_word(&S.maxA[k]), hi32(a));
   if (kExact) atomicMin(hi_word(&S.minA[k]), hi32(a));
   atomicAdd(&S.cnt[k], 1);
@@ -716,9 +728,13 @@ __device__ __forceinline__ void stash_arc(const Smem& S, Ctl& ctl, double2* stas
 // CTAs per SM the register allocation must allow: 4 (64 registers) for the config-3
 // path (W = 8, arcs stashed in shared memory: 4 x 56 KB fit, no spills), 3 (80
 // registers) elsewhere (at 64 those variants spill 100-200 bytes)
-// global-stash path: per-warp queues of active constraints in shared memory (phase A)
+// global-stash path: per-warp queues of active constraints in shared memory (phase A),
+// and the buckets' max beta by CAS (no low-word pass)
 #ifndef TMVN_ESS_AQUEUE
 #define TMVN_ESS_AQUEUE 1
+#endif
+#ifndef TMVN_ESS_CASMAX
+#define TMVN_ESS_CASMAX 1
 #endif
 #ifndef TMVN_ESS_MIN_BLOCKS
 #define TMVN_ESS_MIN_BLOCKS 3
@@ -786,6 +802,9 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
   // into the stash region while the previous chain runs phases D; phase A tests and
   // computes the arcs from there
   constexpr bool kRows = !kGiven && kSrc == 0 && kSmemStash;
+  // the queue path of phase A (global stash) takes the exact max beta by CAS: no
+  // low-word pass re-reading the stash from global memory
+  constexpr bool kCasPath = !kGiven && kSrc == 0 && !kSmemStash && TMVN_ESS_AQUEUE && TMVN_ESS_CASMAX;
   const int mm = (m + 1) & ~1;
   ArcStore<kRows> AS;
   AS.st = stash;
@@ -1160,7 +1179,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         sb = __shfl_sync(0xffffffffu, sb, 0);
         if (mine) {
           stash[sb + g.lane] = make_double2(al, be);
-          bucket_add<false>(S, bucket_key(al, ctl, NB, scale), al, be);
+          bucket_add<false, kCasPath>(S, bucket_key(al, ctl, NB, scale), al, be);
           if (p.d_alpha) {
             p.d_alpha[(int64_t)c * m + i] = al;
             p.d_beta[(int64_t)c * m + i] = be;
@@ -1295,7 +1314,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     // level-1 bucket ranges (exclusive scan of the counts), then one pass over the
     // stash: resolve the low words of max beta (see bucket_add) and scatter every arc
     // into its bucket's range (counting sort by bucket)
-    {
+    if (!kCasPath) {
       const int n_act = ctl.n_act;
       for (int idx = g.tid; idx < n_act; idx += T) {
         const double2 ab = AS.get(idx);

@@ -539,7 +539,7 @@ __device__ void build_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const 
 template <int W, bool kRows>
 __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const ArcStore<kRows>& stash,
                               int NB, double scale, double2* gg, uint64_t* s_w64, int* s_w32,
-                              int crowd_at) {
+                              int crowd_at, const int* akey) {
   constexpr int T = Grp<W>::kThreads;
   const int per = (NB + T - 1) / T;
   const int j0 = g.tid * per, j1 = min(NB, j0 + per);
@@ -576,8 +576,18 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
   // B2: gather the live buckets' arcs, grouped by bucket
   const int n_act = ctl.n_act;
   for (int idx = g.tid; idx < n_act; idx += T) {
-    const double2 ab = stash.get(idx);
-    const int k = bucket_key(ab.x, ctl, NB, scale);
+    // akey (global stash): each arc's level-1 bucket, stored by phase A, so that only the
+    // arcs of live buckets are read back from global memory
+    int k;
+    double2 ab;
+    if (akey) {
+      k = akey[idx];
+      if (S.off[k] < 0) continue;
+      ab = stash.get(idx);
+    } else {
+      ab = stash.get(idx);
+      k = bucket_key(ab.x, ctl, NB, scale);
+    }
     const int ok = S.off[k];
     if (ok >= 0) {
       const int pos = ok + atomicAdd(&S.fill[k], 1);
@@ -806,6 +816,8 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
   // low-word pass re-reading the stash from global memory
   constexpr bool kCasPath = !kGiven && kSrc == 0 && !kSmemStash && TMVN_ESS_AQUEUE && TMVN_ESS_CASMAX;
   const int mm = (m + 1) & ~1;
+  // the queue path's level-1 bucket of every stashed arc (the stash's m ints after its arcs)
+  int* akey = kCasPath ? reinterpret_cast<int*>(stash + m) : nullptr;
   ArcStore<kRows> AS;
   AS.st = stash;
   AS.Ps = reinterpret_cast<double*>(stash);
@@ -1179,7 +1191,9 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         sb = __shfl_sync(0xffffffffu, sb, 0);
         if (mine) {
           stash[sb + g.lane] = make_double2(al, be);
-          bucket_add<false, kCasPath>(S, bucket_key(al, ctl, NB, scale), al, be);
+          const int k = bucket_key(al, ctl, NB, scale);
+          if (kCasPath) akey[sb + g.lane] = k;
+          bucket_add<false, kCasPath>(S, k, al, be);
           if (p.d_alpha) {
             p.d_alpha[(int64_t)c * m + i] = al;
             p.d_beta[(int64_t)c * m + i] = be;
@@ -1327,7 +1341,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     // ---------------- B + C: I_act by Alg. 3, then theta ----------------
     // a chain is crowded when one level-1 bucket holds 4 x the mean constraints per
     // bucket + 32 arcs (phase A's bucket atomics and B3's scan serialise on it)
-    const bool fast = par_intervals(g, S, ctl, AS, NB, scale, gg, s_w64, s_w32, 4 * (m / NB) + 32);
+    const bool fast = par_intervals(g, S, ctl, AS, NB, scale, gg, s_w64, s_w32, 4 * (m / NB) + 32, akey);
     // nu_{t+1} drawn while the highest warp's last lane computes theta (options.rng_overlap:
     // the other W - 1 warps would wait at the barrier); into the other nu buffer (N_next),
     // since phase D still reads nu_t

@@ -328,7 +328,11 @@ __device__ void grp_sort(const Grp<W>& g, const Smem& S, int n) {
 //   kRows = false: stash[slot] = (alpha, beta) (shared or global memory);
 //   kRows = true:  the chain's P and Q rows in shared memory (bulk-copied ahead of the
 //                  chain), the arc of constraint i written over (Ps[i], Qs[i]), and
-//                  idx[slot] = i.
+//                  idx[slot] = i (packed with the bucket, below).
+// kRows: idx[slot] = constraint index | level-1 bucket << kIdxBits (set with the arc in
+// phase A), so the live gather skips dead buckets' arcs without reading them
+constexpr int kIdxBits = 21;
+constexpr int kIdxMask = (1 << kIdxBits) - 1;
 template <bool kRows>
 struct ArcStore {
   double2* st;
@@ -337,7 +341,7 @@ struct ArcStore {
   int* idx;
   __device__ __forceinline__ double2 get(int slot) const {
     if (kRows) {
-      const int i = idx[slot];
+      const int i = idx[slot] & kIdxMask;
       return make_double2(Ps[i], Qs[i]);
     }
     return st[slot];
@@ -580,7 +584,12 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
     // arcs of live buckets are read back from global memory
     int k;
     double2 ab;
-    if (akey) {
+    if (kRows) {
+      const int ik = stash.idx[idx];
+      k = ik >> kIdxBits;
+      if (S.off[k] < 0) continue;
+      ab = make_double2(stash.Ps[ik & kIdxMask], stash.Qs[ik & kIdxMask]);
+    } else if (akey) {
       k = akey[idx];
       if (S.off[k] < 0) continue;
       ab = stash.get(idx);
@@ -1156,7 +1165,9 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         arc_of(AS.Ps[i], AS.Qs[i], __ldg(p.b + i), al, be);  // active by pass 1: same predicate
         AS.Ps[i] = al;
         AS.Qs[i] = be;
-        bucket_add<false>(S, bucket_key(al, ctl, NB, scale), al, be);
+        const int k = bucket_key(al, ctl, NB, scale);
+        sidx[slot] = i | (k << kIdxBits);
+        bucket_add<false>(S, k, al, be);
         if (p.d_alpha) {
           p.d_alpha[(int64_t)c * m + i] = al;
           p.d_beta[(int64_t)c * m + i] = be;

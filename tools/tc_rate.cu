@@ -178,6 +178,7 @@ int main() {
   run<64, false>("SS");
   run<128, false>("SS");
   run<256, false>("SS");
+  run<32, true>("TS");
   run<64, true>("TS");
   run<128, true>("TS");
   return 0;

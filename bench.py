@@ -42,8 +42,12 @@ sys.path.insert(0, ROOT)
 METRIC = "constraint-evals/sec (chain-iterations/sec x m), FP64, whole job"
 METRIC32 = "constraint-evals/sec (chain-iterations/sec x m), FP32-class (--precision 1), whole job"
 UNIT = "constraint-evals/s"
-# iterations per step (one tmvn_sample call) per config: a step of ~10-700 ms
-IPS = {1: 2000, 2: 500, 3: 100, 4: 20, 5: 5, 6: 200, 7: 100}
+# iterations per step (one tmvn_sample call) per config: a step of ~10 ms - 4 s.  Every
+# call starts with the strict start check, P = X A'^T in full (a projection-sized GEMM),
+# so a step should be a good fraction of the config's run (T in BASELINE.json): config 5
+# (T = 100) at 25 iterations per call pays it once per 25 (at 5 it added ~15 % per
+# iteration); the refresh cadence inside a call is recompute_every = 32
+IPS = {1: 2000, 2: 500, 3: 100, 4: 20, 5: 25, 6: 200, 7: 100}
 # algorithmic HBM bytes per constraint-eval of the per-chain kernel --
 # P read + write (16 B) and the Q round trip between the projection and it (16 B)
 ESS_ALG_BYTES_PER_EVAL = 32.0

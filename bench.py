@@ -47,7 +47,7 @@ UNIT = "constraint-evals/s"
 # so a step should be a good fraction of the config's run (T in BASELINE.json): config 5
 # (T = 100) at 25 iterations per call pays it once per 25 (at 5 it added ~15 % per
 # iteration); the refresh cadence inside a call is recompute_every = 32
-IPS = {1: 2000, 2: 500, 3: 100, 4: 20, 5: 25, 6: 200, 7: 100}
+IPS = {1: 2000, 2: 500, 3: 100, 4: 50, 5: 25, 6: 200, 7: 100}
 # algorithmic HBM bytes per constraint-eval of the per-chain kernel --
 # P read + write (16 B) and the Q round trip between the projection and it (16 B)
 ESS_ALG_BYTES_PER_EVAL = 32.0

@@ -3,7 +3,11 @@
 //
 //   A  arcs      per constraint i: r = |(p, q)|, the infeasible arc
 //                (alpha_i, beta_i) of eq:roots (C1-C5); inactive
-//                constraints (r <= b) are compacted away.
+//                constraints (r <= b) are compacted away (rows in shared
+//                memory: compacted indices, arcs over their (P, Q) entries; long
+//                rows: per-warp queues of active constraints, arcs 32 at a time
+//                into the global stash) while the level-1 bucket statistics of B
+//                are gathered (linear or octave keys on alpha).
 //   B  I_act     Alg. 3 / Prop. 1: sort the alphas, cumulative max
 //                of the co-sorted betas, gaps [gamma_{k-1}, alpha_{i_k}] and
 //                [gamma_m, 2 pi].  The sort is an MSD bucket sort on alpha whose
@@ -13,8 +17,9 @@
 //                hold no gap (Prop. 1), so only "live" buckets are gathered;
 //                each live arc finds gamma before it within its own bucket
 //                (group-parallel, no sort; par_intervals), or, when many arcs
-//                are live, batches are bitonic-sorted and max-scanned.  Comparisons only: bit-identical to Alg. 2 on the
-//                same arcs.  Oversized buckets are refined.
+//                are live, batches are bitonic-sorted and max-scanned.
+//                Comparisons only: bit-identical to Alg. 2 on the same arcs
+//                (P:400-402).  Oversized buckets are refined.
 //   C  theta     canonical segments, S3.3 trim (C7), L = sum of lengths in
 //                ascending order, theta = inverse CDF at u (C10).
 //   D  update    P' = P cos(theta) + Q sin(theta) (Eq. 1), safeguard

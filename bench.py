@@ -277,6 +277,13 @@ def _peaks():
     return hbm, bf16, bf16s, src
 
 
+def _fp64_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")))["dfma_tflops_t1024"])
+    except Exception:
+        return 34.2
+
+
 def _traffic(k, kernel, args, world):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at config k from the
     committed ncu --set full capture of this round (profiles/r02/ncu_traffic.json)."""
@@ -310,6 +317,23 @@ def roofline_entries(prof, ms_iso, k, cfg, Cl, ips, steps, args, world, opts):
                                     "bytes counted) streams from L2: a bandwidth-equivalent figure",
                      "algorithmic_bytes_per_launch": abytes, "avg_launch_ms": launch_ms, "share_of_step": 1.0,
                      "latency_calls": prof["latency_calls"], "latency_fallbacks": prof["latency_fallbacks"]})
+        return ents
+    if prof.get("warp_mode_calls", 0) > 0:
+        # warp mode: one launch per call, A in shared memory, nothing per iteration in HBM;
+        # the bound is the FP64 pipe (FMA) behind the groups' latency: Q = A nu (2 m d flops
+        # per chain-iteration, the algorithmic count) against the measured DFMA peak
+        launch_ms = ms_iso / steps
+        flops = 2.0 * float(Cl) * ips * m * d
+        peak = _fp64_peak()
+        ents.append({"bound": "alu", "kernel": "small_kernel (warp mode: a group of warps per chain, all "
+                                               "iterations, A in shared memory: nu, A nu, arcs, bitonic Alg. 3, "
+                                               "theta, P', safeguard, x update, moments)",
+                     "achieved": flops / (launch_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s (FP64)",
+                     "frac": flops / (launch_ms * 1e-3) / 1e12 / peak, "traffic": None,
+                     "peak_source": "profiles/peaks_fp64_r01.json dfma_tflops_t1024 (measured FP64 FMA pipe, non-tensor); "
+                                    "the projection's 2 m d flops per chain-iteration counted",
+                     "algorithmic_flops_per_launch": flops, "avg_launch_ms": launch_ms, "share_of_step": 1.0,
+                     "warp_mode_calls": prof["warp_mode_calls"]})
         return ents
     # the fused per-chain kernel: HBM roofline at SURVEY 8(d)'s 32 B per constraint-eval
     nE = max(1, prof["ess_launches"])
@@ -486,12 +510,14 @@ def run_workload(k, args, rank, world, dev, primary, host):
     torch.cuda.empty_cache()
     oz = args.projection == 1 or (args.projection == 0 and d <= 4096)
     lat = prof["latency_calls"] > 0
+    warp = prof.get("warp_mode_calls", 0) > 0
     dtype = (("f32-class (int8 x4 projection, f64 elsewhere)" if not lat else "f32") if args.precision
-             else ("f64+i8" if oz and not lat else "f64"))
+             else ("f64+i8" if oz and not lat and not warp else "f64"))
     return {"k": k, "value": value, "ms_per_step": ms_max / steps, "steps": steps, "warmup": warm,
             "chain_iters_per_s": rate_iters, "evals_per_s_per_gpu": value / world, "dtype": dtype,
             "config": config_dict(cfg, k, ips, world, args.scaling), "rejections": rej_all, "recorded": n_all,
-            "path": "latency mode" if lat else "throughput path (projection GEMM + ess_kernel per iteration)",
+            "path": ("latency mode" if lat else "warp mode (small_kernel, all iterations per launch)" if warp
+                     else "throughput path (projection GEMM + ess_kernel per iteration)"),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": prof_main["launches"],
             "clocks": clocks,
             "options": {"projection": o.projection, "ozaki_slices": o.ozaki_slices, "chain_warps": o.chain_warps,

@@ -218,18 +218,20 @@ typedef struct {
    * SM the kernel is throughput-bound, not idle at that barrier).  Results do
    * not depend on it (same counters, tested bitwise). */
   int32_t rng_overlap;
-  /* Warp mode for small polytopes (small.cu): one warp per chain runs all n_iter
-   * iterations in one launch with A resident in shared memory (column-major),
-   * Q = A nu one lane per row, the arcs compacted by ballot, Alg. 3 as a warp
-   * bitonic sort + prefix max, the safeguard by ballot.  Needs FP64, no affine
-   * map, m <= 512 and A (d x 32 ceil(m / 32) doubles) plus one warp's state in
-   * shared memory.  2: whenever that holds with >= 4 warps per CTA and
-   * options.latency is automatic (2) -- decided from m and d only, so every shard
-   * of a job takes the same path; 1: whenever it holds; 0 (default): off (B200:
-   * config 1 5.0 us per iteration vs 6.1 in the latency mode, config 2 20 us vs
-   * 19 on the default path -- one warp's serial per-iteration work, ~5K
-   * instructions, with ~7 chains per SM, does not beat the other paths).  Dot products sum in index order: results agree
-   * with the other paths to rounding, not bitwise. */
+  /* Warp mode for small polytopes (small.cu): a group of 1-8 warps per chain
+   * (options.small_warps) runs all n_iter iterations in one launch with A resident
+   * in shared memory (column-major), Q = A nu one thread per row, the arcs
+   * compacted by ballot, Alg. 3 as a bitonic sort + prefix max, the safeguard by a
+   * group OR.  Needs FP64, no affine map, m <= 512 and A (d x 32 ceil(m / 32)
+   * doubles) plus 4 groups' state in shared memory.  2 (default): whenever that
+   * holds, options.latency is automatic (2) and the job is small --
+   * total chains x (m d + 32 m) <= 1.6e7 -- decided from m, d and
+   * options.total_chains (else this call's C), so every shard of a job takes the
+   * same path (B200, per iteration: BASELINE config 2, 1024 chains, 14.5 us vs
+   * 22.8 on the throughput path; config 1 4.9 vs 6.2 in the latency mode; the
+   * S4.1 interval with 2000 chains 5.6 vs 14.8); 1: whenever it fits; 0: off.  Dot
+   * products sum in index order: results agree with the other paths to rounding,
+   * not bitwise. */
   int32_t warp_mode;
   /* Level-1 buckets of the per-chain kernel's Alg. 3 (bucketed sort, Prop. 1): 1
    * linear in alpha over [0, 2 pi]; 2 by octave of alpha (NB / 16 per octave over
@@ -240,6 +242,14 @@ typedef struct {
    * 4 m / NB + 32 arcs in one bucket (tmvn_profile.buckets_used).  Any monotone
    * bucketing gives the same I_act bit for bit: results do not depend on it. */
   int32_t buckets;
+  /* Warp mode: warps per chain group (1, 2, 4 or 8, at most ceil(m / 32) rounded up to
+   * a power of two).  0 (default): automatic -- one warp per chain when the job's
+   * chains fill the SMs, else groups of up to 8 warps that split each chain's rows
+   * of A, arcs, sort and coordinates (~32 resident warps per SM).  Trajectories do
+   * not depend on it (every row's dot product sums in index order; the sorted arcs
+   * give the same gaps); moment sums may differ in the last bits (their per-group
+   * partial order follows the group layout). */
+  int32_t small_warps;
 } tmvn_options;
 
 typedef struct {

@@ -54,7 +54,8 @@ class options(ctypes.Structure):
                 ("latency", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("total_chains", ctypes.c_int64), ("fuse_arcs", ctypes.c_int32),
                 ("rng_gemm", ctypes.c_int32), ("rng_overlap", ctypes.c_int32),
-                ("warp_mode", ctypes.c_int32), ("buckets", ctypes.c_int32)]
+                ("warp_mode", ctypes.c_int32), ("buckets", ctypes.c_int32),
+                ("small_warps", ctypes.c_int32)]
 
 
 class profile(ctypes.Structure):

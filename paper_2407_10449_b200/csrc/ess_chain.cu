@@ -338,15 +338,33 @@ __device__ void grp_sort(const Grp<W>& g, const Smem& S, int n) {
 // phase A), so the live gather skips dead buckets' arcs without reading them
 constexpr int kIdxBits = 21;
 constexpr int kIdxMask = (1 << kIdxBits) - 1;
+// TMVN_ESS_KEEPPQ (kRows): the arcs are not written over the rows; the rows stay in shared
+// memory through phase D1 (P' read from there, no global re-read of P and Q), the buckets'
+// max beta is exact by CAS in phase A (no low-word pass), and a reader of an arc
+// recomputes it from (Ps[i], Qs[i], b[i]) by the same arc_of (bit-identical): only the live
+// buckets' arcs on the parallel path, every pass of the (rare) general path
+// Measured on B200 at config 3 (one shard, ncu): DRAM per launch 372 -> 331 MB, but the
+// launch 205 -> 212 us (the next chain's rows are issued only after D1, and the live
+// arcs are recomputed behind an extra barrier): off by default.
+#ifndef TMVN_ESS_KEEPPQ
+#define TMVN_ESS_KEEPPQ 0
+#endif
+constexpr bool kKeepPQ = TMVN_ESS_KEEPPQ != 0;
 template <bool kRows>
 struct ArcStore {
   double2* st;
   double* Ps;
   double* Qs;
   int* idx;
+  const double* b;
   __device__ __forceinline__ double2 get(int slot) const {
     if (kRows) {
       const int i = idx[slot] & kIdxMask;
+      if (kKeepPQ) {
+        double al, be;
+        arc_of(Ps[i], Qs[i], __ldg(b + i), al, be);  // active by phase A: same predicate
+        return make_double2(al, be);
+      }
       return make_double2(Ps[i], Qs[i]);
     }
     return st[slot];
@@ -589,7 +607,14 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
     // arcs of live buckets are read back from global memory
     int k;
     double2 ab;
-    if (kRows) {
+    if (kRows && kKeepPQ) {  // the live arcs' constraint indices, their arcs below
+      const int ik = stash.idx[idx];
+      k = ik >> kIdxBits;
+      const int ok = S.off[k];
+      if (ok < 0) continue;
+      S.keys[ok + atomicAdd(&S.fill[k], 1)] = (uint64_t)(ik & kIdxMask);
+      continue;
+    } else if (kRows) {
       const int ik = stash.idx[idx];
       k = ik >> kIdxBits;
       if (S.off[k] < 0) continue;
@@ -610,6 +635,16 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
     }
   }
   g.sync();
+  if (kRows && kKeepPQ) {  // the gathered arcs recomputed densely (at most one per thread)
+    for (int e = g.tid; e < total; e += T) {
+      const int i = (int)S.keys[e];
+      double al, be;
+      arc_of(stash.Ps[i], stash.Qs[i], __ldg(stash.b + i), al, be);
+      S.keys[e] = dbits(al);
+      S.vals[e] = be;
+    }
+    g.sync();
+  }
   // B3: gamma before every live arc from its own bucket; gaps to cand (unordered)
   for (int e = g.tid; e < total; e += T) {
     const uint64_t key = S.keys[e];
@@ -837,6 +872,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
   AS.Ps = reinterpret_cast<double*>(stash);
   AS.Qs = AS.Ps + mm;
   AS.idx = reinterpret_cast<int*>(AS.Qs + mm);
+  AS.b = p.b;
   uint32_t pqphase = 0;
   auto pq_issue = [&](int64_t cn) {  // one thread
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1158,7 +1194,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
       }
       g.sync();
       PHASE(10);  // A1: active test + compaction (the rest of phase A goes to slot 1)
-      if (g.tid == T - 1) {  // phase D's P and Q rows (global) back into L2 before it reads them
+      if (!kKeepPQ && g.tid == T - 1) {  // phase D's P and Q rows (global) back into L2 before it reads them
         const uint32_t bytes = (uint32_t)mm * 8u;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Prow), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Qrow), "r"(bytes) : "memory");
@@ -1168,11 +1204,13 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         const int i = sidx[slot];
         double al, be;
         arc_of(AS.Ps[i], AS.Qs[i], __ldg(p.b + i), al, be);  // active by pass 1: same predicate
-        AS.Ps[i] = al;
-        AS.Qs[i] = be;
+        if (!kKeepPQ) {
+          AS.Ps[i] = al;
+          AS.Qs[i] = be;
+        }
         const int k = bucket_key(al, ctl, NB, scale);
         sidx[slot] = i | (k << kIdxBits);
-        bucket_add<false>(S, k, al, be);
+        bucket_add<false, kKeepPQ>(S, k, al, be);
         if (p.d_alpha) {
           p.d_alpha[(int64_t)c * m + i] = al;
           p.d_beta[(int64_t)c * m + i] = be;
@@ -1344,7 +1382,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     // level-1 bucket ranges (exclusive scan of the counts), then one pass over the
     // stash: resolve the low words of max beta (see bucket_add) and scatter every arc
     // into its bucket's range (counting sort by bucket)
-    if (!kCasPath) {
+    if (!kCasPath && !(kRows && kKeepPQ)) {
       const int n_act = ctl.n_act;
       for (int idx = g.tid; idx < n_act; idx += T) {
         const double2 ab = AS.get(idx);
@@ -1395,7 +1433,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     }
     PHASE(4);  // B + C on the general path (rare)
     PHASE_ADD(9, ctl.ngap);
-    if (kRows && g.tid == T - 1) {  // stash free: the next chain's P and Q rows, beside phase D
+    if (kRows && !kKeepPQ && g.tid == T - 1) {  // stash free: the next chain's P and Q rows, beside phase D
       const int64_t cn = dyn ? (int64_t)ctl.next : cc + ngroups;
       if (cn < p.C) pq_issue(cn);
     }
@@ -1460,9 +1498,12 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
       }
     }
     if (!kRing && L > 0.0) {
-      const double2* Q2 = reinterpret_cast<const double2*>(Qrow);
+      // the rows still in shared memory (TMVN_ESS_KEEPPQ), else from global memory
+      const double2* Ps2 = (kRows && kKeepPQ) ? reinterpret_cast<const double2*>(AS.Ps) : P2;
+      const double2* Q2 = (kRows && kKeepPQ) ? reinterpret_cast<const double2*>(AS.Qs)
+                                             : reinterpret_cast<const double2*>(Qrow);
       for (int pi = g.tid; pi < npairs; pi += T) {
-        const double2 pv = P2[pi], qv = Q2[pi], bv = __ldg(B2 + pi);
+        const double2 pv = Ps2[pi], qv = Q2[pi], bv = __ldg(B2 + pi);
         double2 pn;
         pn.x = pv.x * ct + qv.x * st;
         pn.y = pv.y * ct + qv.y * st;
@@ -1474,6 +1515,10 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
     }
     const int any_viol = g.sync_or(viol);
     const bool accept = (L > 0.0) && !any_viol;
+    if (kRows && kKeepPQ && g.tid == T - 1) {  // rows read (barrier above): the next chain's, beside D2
+      const int64_t cn = dyn ? (int64_t)ctl.next : cc + ngroups;
+      if (cn < p.C) pq_issue(cn);
+    }
     PHASE(5);  // D1: P' and the safeguard
     if (p.d_slack) {
       // group max of the slack (dump only)

@@ -135,7 +135,7 @@ struct SmallParams {
   double eps;        // S3.3 trim
   int record;
   int64_t burn_in, thin;
-  double* S1;        // tiled moment rows (one per warp)
+  double* S1;        // tiled moment rows (one per chain group)
   double* S2;
   int64_t* rej;      // per chain
   unsigned long long* startflag;  // non-null: check the start; lowest chain * m + i violating
@@ -144,7 +144,10 @@ struct SmallParams {
 // shared memory per warp; rows of A per lane (power of two, m <= 32 R)
 size_t small_warp_bytes(int m, int64_t d_pad);
 int small_rows(int m);
-cudaError_t launch_small(const SmallParams& p, int warps_per_cta, int grid, cudaStream_t st);
+// warps per CTA the kernel allows (its register bound) with nw warps per chain
+int small_max_warps(int m, int nw);
+// groups_per_cta chain groups of nw warps (power of two, <= small_rows(m)) per CTA
+cudaError_t launch_small(const SmallParams& p, int groups_per_cta, int nw, int grid, cudaStream_t st);
 
 // ---- fused per-chain ESS kernel (ess_chain.cu) -----------------------------
 struct EssParams {

@@ -1090,7 +1090,8 @@ tmvn_status tmvn_default_options(tmvn_options* o) {
   o->rng_gemm = 0;
   o->rng_overlap = 0;
   o->buckets = 0;
-  o->warp_mode = 0;  // measured: config 1 5.0 vs 6.1 us / iteration (latency mode), config 2 20 vs 19 us (default path)  // measured slightly slower at config 3 (0.207 -> 0.211 ms per launch) and config 4  // measured neutral at config 3 (0.384 -> 0.383 ms / iteration), slower at config 5  // measured slower on B200 (the epilogue outgrows the MMAs)
+  o->small_warps = 0;
+  o->warp_mode = 2;  // auto (small polytopes, few chains: small_fits)
   return TMVN_OK;
 }
 
@@ -1239,6 +1240,9 @@ tmvn_status tmvn_set_options(tmvn_handle h, const tmvn_options* o) {
   if (o->precision < 0 || o->precision > 1) return fail(h, TMVN_E_ARG, "precision must be 0 (FP64) or 1 (FP32)");
   if (o->ozaki_slices != 0 && (o->ozaki_slices < 6 || o->ozaki_slices > 8))
     return fail(h, TMVN_E_ARG, "ozaki_slices must be 0, 6, 7 or 8");
+  if (o->small_warps != 0 && o->small_warps != 1 && o->small_warps != 2 && o->small_warps != 4 &&
+      o->small_warps != 8)
+    return fail(h, TMVN_E_ARG, "small_warps must be 0, 1, 2, 4 or 8");
   if (o->projection == 1 && h->d > 4096)
     return fail(h, TMVN_E_ARG, "projection = 1 (int8 tcgen05) needs d <= 4096 (int32 accumulator headroom)");
   h->opt = *o;
@@ -1337,7 +1341,8 @@ bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_ou
 // 32 R doubles, column-major) in shared memory beside >= 1 warp's state.  Decided from
 // (m, d) only, so every shard of a job takes the same path.  Warps per CTA: as few as
 // spread the job's chains over the SMs (up to 16).
-bool small_fits(tmvn_ctx* h, int64_t C, int* wpc_out, int* grid_out) {
+constexpr double kWarpAutoWork = 1.6e7;
+bool small_fits(tmvn_ctx* h, int64_t C, int* wpc_out, int* nw_out, int* grid_out) {
   if (h->opt.warp_mode == 0 || h->affine || h->opt.precision != 0 || h->m > 512) return false;
   // auto only under the automatic path choice: latency = 0 / 1 ask for a specific path
   if (h->opt.warp_mode == 2 && h->opt.latency != 2) return false;
@@ -1350,15 +1355,34 @@ bool small_fits(tmvn_ctx* h, int64_t C, int* wpc_out, int* grid_out) {
   if (a_bytes + wb > (size_t)smem_max) return false;
   int wmax = (int)std::min<size_t>(16, ((size_t)smem_max - a_bytes) / wb);
   if (h->opt.warp_mode == 2 && wmax < 4) return false;  // auto: a few chains per CTA at least
+  // auto: only while the job's GEMV + sort work per iteration is small (B200, warp mode vs
+  // the throughput path, tools/warp_vs_default.py: BASELINE config 2 at 1024 chains --
+  // 1.35e7 below -- 14.5 vs 22.8 us per iteration, at 4096 chains 58.9 vs 46.1 us); from
+  // the job's total chains, so that every shard takes the same path
+  const int64_t Ctot = h->opt.total_chains > 0 ? h->opt.total_chains : C;
+  if (h->opt.warp_mode == 2 && (double)Ctot * ((double)h->m * (double)h->d + 32.0 * (double)h->m) > kWarpAutoWork)
+    return false;
   int wpc = (int)std::min<int64_t>(wmax, std::max<int64_t>(1, (C + sms - 1) / sms));
+  // warps per chain: a group of nw warps when the chains alone leave the SMs short of
+  // ~32 resident warps (each chain's rows, arcs, sort and coordinates split nw ways; the
+  // trajectories do not depend on nw), at most one row of A per thread
+  int nw = 1;
+  const int mi = (int)h->m;
+  while (nw < 8 && 2 * nw <= small_rows(mi) && wpc * 2 * nw <= small_max_warps(mi, 2 * nw) && wpc <= 15) nw *= 2;
+  if (h->opt.small_warps > 0 && h->opt.small_warps <= small_rows(mi)) {  // requested (run_small checks the rest)
+    nw = h->opt.small_warps;
+    wpc = std::min(wpc, std::max(1, small_max_warps(mi, nw) / nw));
+    if (nw > 1) wpc = std::min(wpc, 15);
+  }
   int64_t grid = (C + wpc - 1) / wpc;
-  if (grid > sms) grid = sms;  // one CTA per SM (A per CTA); warps loop over their chains
+  if (grid > sms) grid = sms;  // one CTA per SM (A per CTA); groups loop over their chains
   *wpc_out = wpc;
+  *nw_out = nw;
   *grid_out = (int)grid;
   return true;
 }
 
-tmvn_status run_small(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int wpc, int grid,
+tmvn_status run_small(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int wpc, int nw, int grid,
                       int64_t* n_recorded) {
   cudaStream_t st = stream_of(h);
   SmallParams p;
@@ -1384,7 +1408,9 @@ tmvn_status run_small(tmvn_ctx* h, int64_t C, int64_t n_iter, uint64_t seed, int
   p.rej = h->rej;
   p.startflag = h->dflag;
   CK(h, cudaMemsetAsync(h->dflag, 0xff, sizeof(unsigned long long), st));
-  KL(h, launch_small(p, wpc, grid, st));
+  if (h->opt.small_warps > small_rows((int)h->m))
+    return fail(h, TMVN_E_ARG, "options.small_warps exceeds the rows of A per warp (ceil(m / 32) rounded up to a power of two)");
+  KL(h, launch_small(p, wpc, nw, grid, st));
   unsigned long long* fp = reinterpret_cast<unsigned long long*>(h->pin);
   CK(h, cudaMemcpyAsync(fp, h->dflag, sizeof(*fp), cudaMemcpyDeviceToHost, st));
   CK(h, cudaStreamSynchronize(st));
@@ -1521,12 +1547,12 @@ tmvn_status tmvn_sample(tmvn_handle h, const double* X0, int64_t C, int64_t n_it
   if ((s = plan_ess(h, C)) != TMVN_OK) return s;
   if ((s = ensure_ozaki(h)) != TMVN_OK) return s;
   if ((s = load_X(h, X0, C)) != TMVN_OK) return s;
-  int swpc = 0, sgrid = 0;
-  if (n_iter > 0 && small_fits(h, C, &swpc, &sgrid)) {  // warp mode: the kernel checks the start
+  int swpc = 0, snw = 1, sgrid = 0;
+  if (n_iter > 0 && small_fits(h, C, &swpc, &snw, &sgrid)) {  // warp mode: the kernel checks the start
     Nvtx nw("warp mode (one warp per chain, all iterations, A in shared memory)");
     if ((s = clear_accumulators(h, n_iter)) != TMVN_OK) return s;
     int64_t nrec = 0;
-    if ((s = run_small(h, C, n_iter, seed, swpc, sgrid, &nrec)) != TMVN_OK) return s;
+    if ((s = run_small(h, C, n_iter, seed, swpc, snw, sgrid, &nrec)) != TMVN_OK) return s;
     if ((s = store_X(h, C, out)) != TMVN_OK) return s;
     if ((s = finish_stats(h, C, n_iter, nrec)) != TMVN_OK) return s;
     if (h->opt.auto_advance) h->opt.iter_offset += n_iter;

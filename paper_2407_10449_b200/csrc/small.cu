@@ -81,44 +81,139 @@ __device__ void small_theta(double2* gaps, int ngap, double u, double eps, doubl
   }
 }
 
-// v_out[i] = sum_j A[i][j] v[j] for the R rows i = lane + 32 r of this lane (A_T column-
-// major with ms = 32 R rows per column; rows >= m are zero in A_T)
-template <int R>
-__device__ __forceinline__ void small_gemv(const double* __restrict__ AT, const double* v, int d, int lane,
-                                           double (&out)[R]) {
+// A group of NW warps owning one chain (NW = 1: the warp mode proper; NW > 1 when the job
+// has too few chains to fill the SMs one warp each): named barrier gid + 1 over its
+// 32 NW threads, or warp-synchronous.
+template <int NW>
+struct SGrp {
+  static constexpr int T = 32 * NW;
+  int gid, tid, warp, lane;
+  __device__ __forceinline__ void sync() const {
+    if (NW == 1) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(gid + 1), "r"(T) : "memory");
+  }
+  // group-wide OR of v (a barrier)
+  __device__ __forceinline__ int sync_or(int v) const {
+    if (NW == 1) return __any_sync(0xffffffffu, v);
+    int r;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.s32 p, %1, 0;\n bar.red.or.pred q, %2, %3, p;\n"
+        " selp.s32 %0, 1, 0, q;\n}\n"
+        : "=r"(r)
+        : "r"(v), "r"(gid + 1), "r"(T)
+        : "memory");
+    return r;
+  }
+};
+
+// exclusive prefix (max of uint64 / sum of int) over the group's threads in thread order,
+// the group total in *tot; scr: NW words, not rewritten before the group's next barrier
+template <int NW>
+__device__ __forceinline__ uint64_t sgrp_excl_max(const SGrp<NW>& g, uint64_t v, uint64_t* scr, uint64_t* tot) {
+  uint64_t inc = v;
 #pragma unroll
-  for (int r = 0; r < R; ++r) out[r] = 0.0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t nb = __shfl_up_sync(0xffffffffu, inc, o);
+    if (g.lane >= o) inc = inc > nb ? inc : nb;
+  }
+  uint64_t exc = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (g.lane == 0) exc = 0;
+  if (NW == 1) {
+    *tot = __shfl_sync(0xffffffffu, inc, 31);
+    return exc;
+  }
+  if (g.lane == 31) scr[g.warp] = inc;
+  g.sync();
+  uint64_t pre = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const uint64_t sw = scr[w];
+    if (w < g.warp) pre = pre > sw ? pre : sw;
+    all = all > sw ? all : sw;
+  }
+  *tot = all;
+  return pre > exc ? pre : exc;
+}
+template <int NW>
+__device__ __forceinline__ int sgrp_excl_sum(const SGrp<NW>& g, int v, int* scr, int* tot) {
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int nb = __shfl_up_sync(0xffffffffu, inc, o);
+    if (g.lane >= o) inc += nb;
+  }
+  if (NW == 1) {
+    *tot = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - v;
+  }
+  if (g.lane == 31) scr[g.warp] = inc;
+  g.sync();
+  int pre = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int sw = scr[w];
+    if (w < g.warp) pre += sw;
+    all += sw;
+  }
+  *tot = all;
+  return pre + inc - v;
+}
+
+// v_out[i] = sum_j A[i][j] v[j] (in index order j = 0, 1, ...) for the RT rows
+// i = tid + T r of this thread (A_T column-major with MS rows per column; rows >= m are
+// zero in A_T).  Each row's sum is the same whichever thread computes it.
+template <int RT, int T, int MS>
+__device__ __forceinline__ void small_gemv(const double* __restrict__ AT, const double* v, int d, int tid,
+                                           double (&out)[RT]) {
+#pragma unroll
+  for (int r = 0; r < RT; ++r) out[r] = 0.0;
   for (int j = 0; j < d; ++j) {
     const double vj = v[j];
-    const double* col = AT + (size_t)j * (32 * R) + lane;
+    const double* col = AT + (size_t)j * MS + tid;
 #pragma unroll
-    for (int r = 0; r < R; ++r) out[r] = fma(col[32 * r], vj, out[r]);
+    for (int r = 0; r < RT; ++r) out[r] = fma(col[T * r], vj, out[r]);
   }
 }
 
 struct SmallWarp {
   double* x;     // d_pad
   double* nu;    // d_pad
-  double* M1;    // d_pad (moments over this warp's chains)
+  double* M1;    // d_pad (moments over this group's chains)
   double* M2;
   uint64_t* key; // n2: alpha bits (sort keys)
   double* val;   // n2: beta
   double2* gaps; // m + 2
+  uint64_t* scr64;  // 8: group scan scratch
+  int* scr32;       // 8
+  double* ctl;      // [0] u, [1] theta, [2] L; n_act at ictl[0]
+  int* ictl;
 };
 
-template <int R>
-__global__ void __launch_bounds__(512, 1) small_kernel(const SmallParams p) {
+// Group control words after the per-warp state of small_warp_bytes
+constexpr int kSmallCtlBytes = 8 * 8 + 8 * 4 + 4 * 8 + 16;
+
+// threads per CTA: up to 1024 (64 registers) with at most 4 rows of A per thread, else
+// up to 512 (small_max_warps)
+template <int R, int NW>
+__global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(const SmallParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int m = p.m, d = p.d;
+  constexpr int T = 32 * NW;
+  constexpr int RT = R / NW;  // rows of A per thread
   constexpr int MS = 32 * R;
+  SGrp<NW> g;
+  g.gid = threadIdx.x / T;
+  g.tid = threadIdx.x % T;
+  g.warp = g.tid >> 5;
+  g.lane = threadIdx.x & 31;
+  const int ngr = blockDim.x / T;  // groups in the CTA
+  const int m = p.m, d = p.d;
   double* AT = reinterpret_cast<double*>(smem);  // d x MS, column j = A[:, j] (zero rows >= m)
   // A' into shared memory, transposed (rows of the row-major input are strided reads)
   for (int e = threadIdx.x; e < d * MS; e += blockDim.x) {
     const int j = e / MS, i = e % MS;
     AT[e] = i < m ? p.A[(int64_t)i * d + j] : 0.0;
   }
-  unsigned char* wbase = smem + (size_t)d * MS * 8 + (size_t)wib * p.warp_bytes;
+  unsigned char* wbase = smem + (size_t)d * MS * 8 + (size_t)g.gid * p.warp_bytes;
   SmallWarp W;
   W.x = reinterpret_cast<double*>(wbase);
   W.nu = W.x + p.d_pad;
@@ -127,78 +222,96 @@ __global__ void __launch_bounds__(512, 1) small_kernel(const SmallParams p) {
   W.key = reinterpret_cast<uint64_t*>(W.M2 + p.d_pad);
   W.val = reinterpret_cast<double*>(W.key + p.n2);
   W.gaps = reinterpret_cast<double2*>(W.val + p.n2);
-  for (int j = lane; j < p.d_pad; j += 32) {
+  W.scr64 = reinterpret_cast<uint64_t*>(wbase + p.warp_bytes - kSmallCtlBytes);
+  W.scr32 = reinterpret_cast<int*>(W.scr64 + 8);
+  W.ctl = reinterpret_cast<double*>(W.scr32 + 8);
+  W.ictl = reinterpret_cast<int*>(W.ctl + 4);
+  for (int j = g.tid; j < p.d_pad; j += T) {
     W.M1[j] = 0.0;
     W.M2[j] = 0.0;
   }
   __syncthreads();
-  double bv[R];
+  double bv[RT];
 #pragma unroll
-  for (int r = 0; r < R; ++r) bv[r] = lane + 32 * r < m ? p.b[lane + 32 * r] : HUGE_VAL;
-  const int64_t gw = (int64_t)blockIdx.x * nw + wib;  // this warp's global index (moment row)
-  const int64_t nwarps = (int64_t)gridDim.x * nw;
+  for (int r = 0; r < RT; ++r) bv[r] = g.tid + T * r < m ? p.b[g.tid + T * r] : HUGE_VAL;
+  const int64_t gw = (int64_t)blockIdx.x * ngr + g.gid;  // this group's global index (moment row)
+  const int64_t ngroups = (int64_t)gridDim.x * ngr;
   const int kpairs = (int)(p.d_pad / 2);
   bool recorded_any = false;
 
-  for (int64_t c = gw; c < p.C; c += nwarps) {
+  for (int64_t c = gw; c < p.C; c += ngroups) {
     const uint32_t gchain = p.chain_offset + (uint32_t)c;
     const int64_t xrow = tiled_row(c, p.d_pad);
-    for (int j = lane; j < p.d_pad; j += 32) W.x[j] = j < d ? p.X[xrow + tiled_col(j)] : 0.0;
-    __syncwarp();
-    double P[R], Q[R];
-    small_gemv<R>(AT, W.x, d, lane, P);
+    for (int j = g.tid; j < p.d_pad; j += T) W.x[j] = j < d ? p.X[xrow + tiled_col(j)] : 0.0;
+    g.sync();
+    double P[RT], Q[RT];
+    small_gemv<RT, T, MS>(AT, W.x, d, g.tid, P);
     int n_iter = p.n_iter;
     if (p.startflag) {  // strict start a_i . x0 < b_i (C18): lowest (chain, constraint) to the host
       bool bad = false;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
+      for (int r = 0; r < RT; ++r) {
+        const int i = g.tid + T * r;
         if (i < m && !(P[r] - bv[r] < 0.0)) {
           atomicMin(p.startflag, (unsigned long long)c * (unsigned long long)m + (unsigned long long)i);
           bad = true;
         }
       }
-      if (__any_sync(0xffffffffu, bad)) n_iter = 0;
+      if (g.sync_or(bad)) n_iter = 0;
     }
     int64_t rej = 0;
     for (int it = 0; it < n_iter; ++it) {
       const uint32_t t = p.t0 + (uint32_t)it;
       // nu_t and u_t (C12)
-      for (int pk = lane; pk < kpairs; pk += 32) {
+      for (int pk = g.tid; pk < kpairs; pk += T) {
         const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
         W.nu[2 * pk] = v.x;
         W.nu[2 * pk + 1] = v.y;
       }
-      const double u = __shfl_sync(0xffffffffu, lane == 0 ? theta_uniform(p.seed, t, gchain) : 0.0, 0);
-      __syncwarp();
-      small_gemv<R>(AT, W.nu, d, lane, Q);
-      // arcs of the active constraints (eq:roots, C1-C5), compacted by ballot
-      int n_act = 0;
+      if (g.tid == 0) {
+        W.ctl[0] = theta_uniform(p.seed, t, gchain);
+        W.ictl[0] = 0;
+      }
+      g.sync();
+      small_gemv<RT, T, MS>(AT, W.nu, d, g.tid, Q);
+      // arcs of the active constraints (eq:roots, C1-C5), compacted (any order: sorted below)
+      int n_w = 0;  // NW = 1: the running count in a register
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
+      for (int r = 0; r < RT; ++r) {
+        const int i = g.tid + T * r;
         double al = 0.0, be = 0.0;
         const bool act = i < m && arc_of(P[r], Q[r], bv[r], al, be);
         const unsigned mask = __ballot_sync(0xffffffffu, act);
-        if (act) {
-          const int slot = n_act + __popc(mask & ((1u << lane) - 1u));
-          W.key[slot] = sbits(al);
-          W.val[slot] = be;
+        if (mask) {
+          int base = n_w;
+          if (NW > 1) {
+            if (g.lane == 0) base = atomicAdd(&W.ictl[0], __popc(mask));
+            base = __shfl_sync(0xffffffffu, base, 0);
+          }
+          if (act) {
+            const int slot = base + __popc(mask & ((1u << g.lane) - 1u));
+            W.key[slot] = sbits(al);
+            W.val[slot] = be;
+          }
+          n_w += __popc(mask);
         }
-        n_act += __popc(mask);
       }
+      g.sync();
+      const int n_act = NW == 1 ? n_w : W.ictl[0];
       // Alg. 3: sort by alpha (bitonic, padded with +inf keys), prefix max of beta, gaps
       int n2 = 1;
       while (n2 < n_act) n2 <<= 1;
       if (n2 < 32) n2 = 32;
-      for (int e = n_act + lane; e < n2; e += 32) {
+      for (int e = n_act + g.tid; e < n2; e += T) {
         W.key[e] = 0x7FF0000000000000ull;
         W.val[e] = 0.0;
       }
-      __syncwarp();
+      g.sync();
+      // compare-exchange stages: a stride below 32 keeps both elements in the owning warp
+      // (element e belongs to thread e mod T); a barrier around every stride >= 32
       for (int k = 2; k <= n2; k <<= 1) {
         for (int jj = k >> 1; jj > 0; jj >>= 1) {
-          for (int e = lane; e < n2; e += 32) {
+          for (int e = g.tid; e < n2; e += T) {
             const int l = e ^ jj;
             if (l > e) {
               const bool up = (e & k) == 0;
@@ -212,97 +325,90 @@ __global__ void __launch_bounds__(512, 1) small_kernel(const SmallParams p) {
               }
             }
           }
-          __syncwarp();
+          const int jn = jj > 1 ? jj >> 1 : k;  // the next stage's stride
+          if (NW > 1 && (jj >= 32 || jn >= 32)) g.sync();
+          else __syncwarp();
         }
       }
-      // lane owns the sorted elements [lane E, lane E + E): gamma before each element is
+      if (NW > 1) g.sync();
+      // thread owns the sorted elements [tid E, tid E + E): gamma before each element is
       // max(0, prefix max of beta of the earlier ones) (gamma_0 = 0: [0, alpha_1] first)
-      const int E = n2 / 32;
-      const int e0 = lane * E;
+      const int E = n2 >= T ? n2 / T : 1;
+      const int e0 = g.tid * E;
+      const int e1 = min(e0 + E, n_act);
       uint64_t lmax = 0;
-      for (int e = e0; e < e0 + E && e < n_act; ++e) lmax = lmax > sbits(W.val[e]) ? lmax : sbits(W.val[e]);
-      uint64_t incl = lmax;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t nb = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl = incl > nb ? incl : nb;
-      }
-      uint64_t run = __shfl_up_sync(0xffffffffu, incl, 1);
-      if (lane == 0) run = 0;  // gamma_0 = 0 (bits of +0.0)
-      const uint64_t Gtot = __shfl_sync(0xffffffffu, incl, 31);
+      for (int e = e0; e < e1; ++e) lmax = lmax > sbits(W.val[e]) ? lmax : sbits(W.val[e]);
+      uint64_t Gtot;
+      const uint64_t run = sgrp_excl_max<NW>(g, lmax, W.scr64, &Gtot);
       int mine = 0;
       {
-        uint64_t g = run;
-        for (int e = e0; e < e0 + E && e < n_act; ++e) {
-          if (W.key[e] > g) ++mine;  // alpha_k > gamma_{k-1}: a gap (Prop. 1)
+        uint64_t gm = run;
+        for (int e = e0; e < e1; ++e) {
+          if (W.key[e] > gm) ++mine;  // alpha_k > gamma_{k-1}: a gap (Prop. 1)
           const uint64_t vb = sbits(W.val[e]);
-          g = g > vb ? g : vb;
+          gm = gm > vb ? gm : vb;
         }
       }
-      int before = mine;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int nb = __shfl_up_sync(0xffffffffu, before, o);
-        if (lane >= o) before += nb;
-      }
-      const int ngap0 = __shfl_sync(0xffffffffu, before, 31);
-      before -= mine;
+      int ngap0;
+      const int before = sgrp_excl_sum<NW>(g, mine, W.scr32, &ngap0);
       {
-        uint64_t g = run;
+        uint64_t gm = run;
         int pos = before;
-        for (int e = e0; e < e0 + E && e < n_act; ++e) {
-          if (W.key[e] > g) W.gaps[pos++] = make_double2(sbitsd(g), sbitsd(W.key[e]));
+        for (int e = e0; e < e1; ++e) {
+          if (W.key[e] > gm) W.gaps[pos++] = make_double2(sbitsd(gm), sbitsd(W.key[e]));
           const uint64_t vb = sbits(W.val[e]);
-          g = g > vb ? g : vb;
+          gm = gm > vb ? gm : vb;
         }
       }
-      __syncwarp();
-      double theta = 0.0, L = 0.0;
-      if (lane == 0) {
+      g.sync();
+      if (g.tid == 0) {
         int ng = ngap0;
         const double G = sbitsd(Gtot);
         if (G < kTwoPi) W.gaps[ng++] = make_double2(G, kTwoPi);  // [gamma_n, 2 pi]
-        small_theta(W.gaps, ng, u, p.eps, &theta, &L);
+        double theta = 0.0, L = 0.0;
+        small_theta(W.gaps, ng, W.ctl[0], p.eps, &theta, &L);
+        W.ctl[1] = theta;
+        W.ctl[2] = L;
       }
-      theta = __shfl_sync(0xffffffffu, theta, 0);
-      L = __shfl_sync(0xffffffffu, L, 0);
+      g.sync();
+      const double theta = W.ctl[1], L = W.ctl[2];
       // P' = P cos + Q sin, the safeguard (C8), the update
       double st = 0.0, ct = 1.0;
       if (L > 0.0) sincos(theta, &st, &ct);
       bool viol = false;
-      double Pn[R];
+      double Pn[RT];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        Pn[r] = P[r] * ct + Q[r] * st;
+      for (int r = 0; r < RT; ++r) {
+        Pn[r] = fma(Q[r], st, __dmul_rn(P[r], ct));  // contraction fixed: the same in every instantiation
         viol |= (Pn[r] - bv[r]) > 0.0;  // b is +inf beyond m
       }
-      const bool accept = (L > 0.0) && !__any_sync(0xffffffffu, viol);
+      const bool accept = (L > 0.0) && !g.sync_or(viol);
       if (accept) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) P[r] = Pn[r];
-        for (int j = lane; j < d; j += 32) W.x[j] = W.x[j] * ct + W.nu[j] * st;
+        for (int r = 0; r < RT; ++r) P[r] = Pn[r];
+        for (int j = g.tid; j < d; j += T) W.x[j] = fma(W.nu[j], st, __dmul_rn(W.x[j], ct));
       } else {
         ++rej;
       }
       const int64_t tt = (int64_t)t;
       if (p.record && tt >= p.burn_in && ((tt - p.burn_in) % (p.thin < 1 ? 1 : p.thin)) == 0) {
         recorded_any = true;
-        for (int j = lane; j < d; j += 32) {
+        for (int j = g.tid; j < d; j += T) {
           const double xv = W.x[j];
           W.M1[j] += xv;
-          W.M2[j] += xv * xv;
+          W.M2[j] = fma(xv, xv, W.M2[j]);
         }
       }
-      __syncwarp();
-      if ((tt + 1) % p.K == 0) small_gemv<R>(AT, W.x, d, lane, P);  // refresh P = A x (C13)
+      g.sync();
+      if ((tt + 1) % p.K == 0) small_gemv<RT, T, MS>(AT, W.x, d, g.tid, P);  // refresh P = A x (C13)
     }
-    for (int j = lane; j < d; j += 32) p.X[xrow + tiled_col(j)] = W.x[j];
-    if (lane == 0) p.rej[c] = rej;
-    __syncwarp();
+    for (int j = g.tid; j < d; j += T) p.X[xrow + tiled_col(j)] = W.x[j];
+    if (g.tid == 0) p.rej[c] = rej;
+    g.sync();
   }
-  if (recorded_any) {  // this warp's moment row (rows < C; zeroed by the host)
+  if (recorded_any) {  // this group's moment row (rows < C; zeroed by the host)
     const int64_t mrow = tiled_row(gw, p.d_pad);
-    for (int j = lane; j < d; j += 32) {
+    for (int j = g.tid; j < d; j += T) {
       p.S1[mrow + tiled_col(j)] = W.M1[j];
       p.S2[mrow + tiled_col(j)] = W.M2[j];
     }
@@ -314,7 +420,7 @@ __global__ void __launch_bounds__(512, 1) small_kernel(const SmallParams p) {
 size_t small_warp_bytes(int m, int64_t d_pad) {
   int n2 = 32;
   while (n2 < m) n2 <<= 1;
-  return (size_t)(4 * d_pad * 8 + (size_t)n2 * 16 + (size_t)(m + 2) * 16 + 15) / 16 * 16;
+  return (size_t)(4 * d_pad * 8 + (size_t)n2 * 16 + (size_t)(m + 2) * 16 + kSmallCtlBytes + 15) / 16 * 16;
 }
 
 int small_rows(int m) {
@@ -323,28 +429,42 @@ int small_rows(int m) {
   return R;
 }
 
-cudaError_t launch_small(const SmallParams& p0, int warps_per_cta, int grid, cudaStream_t st) {
+int small_max_warps(int m, int nw) { return small_rows(m) / nw >= 8 ? 16 : 32; }
+
+cudaError_t launch_small(const SmallParams& p0, int groups_per_cta, int nw, int grid, cudaStream_t st) {
   SmallParams p = p0;
   const int R = small_rows(p.m);
+  if (nw < 1 || nw > R || (nw & (nw - 1)) != 0 || groups_per_cta * nw > small_max_warps(p.m, nw))
+    return cudaErrorInvalidValue;
   p.warp_bytes = (int)small_warp_bytes(p.m, p.d_pad);
   int n2 = 32;
   while (n2 < p.m) n2 <<= 1;
   p.n2 = n2;
-  const size_t smem = (size_t)p.d * 32 * R * 8 + (size_t)warps_per_cta * p.warp_bytes;
+  const size_t smem = (size_t)p.d * 32 * R * 8 + (size_t)groups_per_cta * p.warp_bytes;
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 32 * warps_per_cta, smem, st>>>(p);
+    kern<<<grid, 32 * nw * groups_per_cta, smem, st>>>(p);
     return cudaGetLastError();
   };
+#define TMVN_SMALL_CASE(RR)                                  \
+  case RR:                                                   \
+    switch (nw) {                                            \
+      case 1: return go(small_kernel<RR, 1>);                \
+      case 2: if constexpr (RR >= 2) return go(small_kernel<RR, (RR >= 2 ? 2 : 1)>); break; \
+      case 4: if constexpr (RR >= 4) return go(small_kernel<RR, (RR >= 4 ? 4 : 1)>); break; \
+      case 8: if constexpr (RR >= 8) return go(small_kernel<RR, (RR >= 8 ? 8 : 1)>); break; \
+    }                                                        \
+    return cudaErrorInvalidValue;
   switch (R) {
-    case 1: return go(small_kernel<1>);
-    case 2: return go(small_kernel<2>);
-    case 4: return go(small_kernel<4>);
-    case 8: return go(small_kernel<8>);
-    case 16: return go(small_kernel<16>);
+    TMVN_SMALL_CASE(1)
+    TMVN_SMALL_CASE(2)
+    TMVN_SMALL_CASE(4)
+    TMVN_SMALL_CASE(8)
+    TMVN_SMALL_CASE(16)
     default: return cudaErrorInvalidValue;
   }
+#undef TMVN_SMALL_CASE
 }
 
 }  // namespace tmvn

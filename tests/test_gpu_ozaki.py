@@ -134,7 +134,7 @@ def test_dynamic_range_guard_under_default_options():
     A = rng.standard_normal((m, d)) * 10.0 ** rng.uniform(-8, 0, size=(m, d))
     b = rng.uniform(0.3, 1.0, m)
     x0 = np.zeros(d)
-    s = tm.Sampler(A, b)
+    s = tm.Sampler(A, b, warp_mode=0)  # the throughput path (small jobs default to the warp mode)
     pr = s.profile()
     assert pr["oz_guard_ratio"] > 16
     X = np.tile(x0, (C, 1))
@@ -149,7 +149,7 @@ def test_dynamic_range_guard_under_default_options():
     assert s.profile()["projection_used"] == 2
     # unit Gaussian rows: int8
     Ag, bg, xg = synth.make_instance(3, m=90, d=60)
-    sg = tm.Sampler(Ag, bg)
+    sg = tm.Sampler(Ag, bg, warp_mode=0)
     assert sg.profile()["oz_guard_ratio"] <= 16
     sg.sample(np.tile(xg, (C, 1)), 3, seed=seed)
     assert sg.profile()["projection_used"] == 1

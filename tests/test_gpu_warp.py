@@ -1,5 +1,5 @@
-"""The warp mode (options.warp_mode, small.cu; opt-in): one warp per chain runs every
-iteration with A in shared memory, for small polytopes (BASELINE configs 1 and 2, the
+"""The warp mode (options.warp_mode, small.cu; automatic for small jobs): a group of
+1-8 warps per chain runs every iteration with A in shared memory, for small polytopes (BASELINE configs 1 and 2, the
 S4.1 intervals).  Parity with the oracle step by step (north_star: next
 iterate within 1e-10 relative, exemptions only for SURVEY 8(c)'s readings), over short
 runs, moments, sharding / resume invariance, the strict start, and warps looping over
@@ -98,8 +98,48 @@ def test_warp_mode_start_check_and_options():
     with pytest.raises(tm.TmvnError) as ei:
         s.sample(X, 3, seed=1)
     assert ei.value.status == -3 and "chain 17 violates constraint 5" in str(ei.value)
-    # automatic warp mode only under the automatic latency choice; off by default
-    for kw in (dict(latency=0, warp_mode=2), dict(), dict(latency=1, warp_mode=2)):
+    # automatic warp mode (the default) only under the automatic latency choice and for
+    # small jobs (total chains x (m d + 32 m) <= 1.6e7, from options.total_chains)
+    for kw in (dict(latency=0, warp_mode=2), dict(warp_mode=0), dict(latency=1, warp_mode=2),
+               dict(total_chains=4096)):
         s2 = tm.Sampler(A, b, **kw)
         s2.sample(np.tile(x0, (40, 1)), 3, seed=1)
         assert s2.profile()["warp_mode_calls"] == 0, kw
+    for kw in (dict(), dict(total_chains=1024)):
+        s2 = tm.Sampler(A, b, **kw)
+        s2.sample(np.tile(x0, (40, 1)), 3, seed=1)
+        assert s2.profile()["warp_mode_calls"] == 1, kw
+
+
+@pytest.mark.parametrize("name,C", [("orthant", 1024), ("random", 300), ("orthant", 37)])
+def test_chain_groups_are_bitwise_one_warp(name, C):
+    """options.small_warps: a chain owned by 1, 2, 4 or 8 warps (rows of A, arcs, the
+    sort and the coordinates split over the group) gives the same iterates and
+    rejections bit for bit -- every row's dot product sums in index order and the sorted
+    arcs give the same gaps whatever the compaction order; the moment sums agree to
+    rounding (their per-group partial order follows the group layout).  The automatic
+    choice (0) is among them and passes the oracle checks above."""
+    A, b, x0 = CASES[name][0]()
+    X0 = np.tile(x0, (C, 1))
+    R = 1
+    while 32 * R < A.shape[0]:
+        R *= 2
+    ref = None
+    for nw in [1, 2, 4, 8, 0]:
+        if nw > R:
+            continue
+        s = tm.Sampler(A, b, warp_mode=1, small_warps=nw, burn_in=5, thin=3)
+        X = s.sample(X0, 70, seed=21)  # refresh at K = 32 crossed twice
+        st = s.stats()
+        mom = s.moments()
+        assert s.profile()["warp_mode_calls"] == 1
+        if ref is None:
+            ref = (X, st, mom)
+            continue
+        assert np.array_equal(X, ref[0]), nw
+        assert st == ref[1], nw
+        assert mom[2] == ref[2][2]
+        for a, r in zip(mom[:2], ref[2][:2]):
+            assert np.max(np.abs(a - r)) <= 1e-12 * max(1.0, np.max(np.abs(r))), nw
+    with pytest.raises(tm.TmvnError):  # more warps than rows of A per warp
+        tm.Sampler(A, b, warp_mode=1, small_warps=2 * R).sample(X0, 2, seed=1)

@@ -30,6 +30,8 @@ for path in sys.argv[5:] * reps:
             s.set_options(rng_overlap=int(os.environ["OVL"]))
         if "RNG_GEMM" in os.environ:
             s.set_options(rng_gemm=int(os.environ["RNG_GEMM"]))
+        if "WARP" in os.environ:
+            s.set_options(warp_mode=int(os.environ["WARP"]), small_warps=int(os.environ.get("SW", "0")))
         if "BUCKETS" in os.environ:
             s.set_options(buckets=int(os.environ["BUCKETS"]))
         if "FUSE" in os.environ:
@@ -41,7 +43,7 @@ for path in sys.argv[5:] * reps:
         s.sample(X, iters, cfg.chain_seed, out=X)
         torch.cuda.synchronize(); dt = time.perf_counter() - t0
         pr = s.profile()
-        print(f"{os.path.basename(path)} g={os.environ.get('GRAPHS', '-')} ovl={os.environ.get('OVL', '-')} rg={os.environ.get('RNG_GEMM', '-')} fuse={os.environ.get('FUSE', '-')} bk={os.environ.get('BUCKETS', '-')} rec={os.environ.get('RECORD', '1')} rng_ahead={os.environ.get('RNG_AHEAD', '0')} sched={os.environ.get('SCHED', '0')} pipe={os.environ.get('PIPE', '0')} lat={os.environ.get('LATENCY', '0')} W={W} S={S} R={R} cfg{k}: {dt/iters*1e3:.3f} ms/iter  gemm "
+        print(f"{os.path.basename(path)} g={os.environ.get('GRAPHS', '-')} ovl={os.environ.get('OVL', '-')} rg={os.environ.get('RNG_GEMM', '-')} fuse={os.environ.get('FUSE', '-')} bk={os.environ.get('BUCKETS', '-')} warp={os.environ.get('WARP', '-')}/{os.environ.get('SW', '-')} rec={os.environ.get('RECORD', '1')} rng_ahead={os.environ.get('RNG_AHEAD', '0')} sched={os.environ.get('SCHED', '0')} pipe={os.environ.get('PIPE', '0')} lat={os.environ.get('LATENCY', '0')} W={W} S={S} R={R} cfg{k}: {dt/iters*1e3:.3f} ms/iter  gemm "
               f"{pr['gemm_ms']/max(1,pr['gemm_launches']):.3f} ms  tc {pr['tc_ms']/max(1,pr['tc_launches']):.3f} ms"
               f"  ess {pr['ess_ms']/max(1,pr['ess_launches']):.3f} ms"
               f"  evals/s {cfg.C*cfg.m*iters/dt:.3e}  l1={pr['buckets_used']}", flush=True)

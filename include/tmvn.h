@@ -225,11 +225,11 @@ typedef struct {
    * group OR.  Needs FP64, no affine map, m <= 512 and A (d x 32 ceil(m / 32)
    * doubles) plus 4 groups' state in shared memory.  2 (default): whenever that
    * holds, options.latency is automatic (2) and the job is small --
-   * total chains x (m d + 32 m) <= 1.6e7 -- decided from m, d and
+   * total chains x (m d + 32 m) <= 3.2e7 -- decided from m, d and
    * options.total_chains (else this call's C), so every shard of a job takes the
-   * same path (B200, per iteration: BASELINE config 2, 1024 chains, 14.5 us vs
-   * 22.8 on the throughput path; config 1 4.9 vs 6.2 in the latency mode; the
-   * S4.1 interval with 2000 chains 5.6 vs 14.8); 1: whenever it fits; 0: off.  Dot
+   * same path (B200, per iteration: BASELINE config 2, 1024 chains, 11.4 us vs
+   * 19.6 on the throughput path; config 1 3.9 vs 6.2 in the latency mode; the
+   * S4.1 interval with 2000 chains 4.7 vs 14.5); 1: whenever it fits; 0: off.  Dot
    * products sum in index order: results agree with the other paths to rounding,
    * not bitwise. */
   int32_t warp_mode;

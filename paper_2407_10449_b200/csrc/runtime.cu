@@ -1341,7 +1341,7 @@ bool latency_fits(tmvn_ctx* h, int64_t C, int* cs_out, int* cap_out, int* gsz_ou
 // 32 R doubles, column-major) in shared memory beside >= 1 warp's state.  Decided from
 // (m, d) only, so every shard of a job takes the same path.  Warps per CTA: as few as
 // spread the job's chains over the SMs (up to 16).
-constexpr double kWarpAutoWork = 1.6e7;
+constexpr double kWarpAutoWork = 3.2e7;
 bool small_fits(tmvn_ctx* h, int64_t C, int* wpc_out, int* nw_out, int* grid_out) {
   if (h->opt.warp_mode == 0 || h->affine || h->opt.precision != 0 || h->m > 512) return false;
   // auto only under the automatic path choice: latency = 0 / 1 ask for a specific path
@@ -1356,9 +1356,10 @@ bool small_fits(tmvn_ctx* h, int64_t C, int* wpc_out, int* nw_out, int* grid_out
   int wmax = (int)std::min<size_t>(16, ((size_t)smem_max - a_bytes) / wb);
   if (h->opt.warp_mode == 2 && wmax < 4) return false;  // auto: a few chains per CTA at least
   // auto: only while the job's GEMV + sort work per iteration is small (B200, warp mode vs
-  // the throughput path, tools/warp_vs_default.py: BASELINE config 2 at 1024 chains --
-  // 1.35e7 below -- 14.5 vs 22.8 us per iteration, at 4096 chains 58.9 vs 46.1 us); from
-  // the job's total chains, so that every shard takes the same path
+  // the throughput path, tools/warp_vs_default.py, BASELINE config 2 shapes: 1024 chains --
+  // 1.35e7 below -- 11.4 vs 19.6 us per iteration, 2048 chains (2.7e7) 22.8 vs 28.9 us,
+  // 4096 chains (5.4e7) 64.8 vs 39.0 us); from the job's total chains, so that every
+  // shard takes the same path
   const int64_t Ctot = h->opt.total_chains > 0 ? h->opt.total_chains : C;
   if (h->opt.warp_mode == 2 && (double)Ctot * ((double)h->m * (double)h->d + 32.0 * (double)h->m) > kWarpAutoWork)
     return false;

@@ -185,7 +185,7 @@ struct SmallWarp {
   double2* gaps; // m + 2
   uint64_t* scr64;  // 8: group scan scratch
   int* scr32;       // 8
-  double* ctl;      // [0] u, [1] theta, [2] L; n_act at ictl[0]
+  double* ctl;      // [0] u, [1] sin theta, [2] L, [3] cos theta; n_act at ictl[0]
   int* ictl;
 };
 
@@ -302,35 +302,73 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
       int n2 = 1;
       while (n2 < n_act) n2 <<= 1;
       if (n2 < 32) n2 = 32;
-      for (int e = n_act + g.tid; e < n2; e += T) {
-        W.key[e] = 0x7FF0000000000000ull;
-        W.val[e] = 0.0;
-      }
-      g.sync();
-      // compare-exchange stages: a stride below 32 keeps both elements in the owning warp
-      // (element e belongs to thread e mod T); a barrier around every stride >= 32
-      for (int k = 2; k <= n2; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-          for (int e = g.tid; e < n2; e += T) {
-            const int l = e ^ jj;
-            if (l > e) {
-              const bool up = (e & k) == 0;
-              const uint64_t ke = W.key[e], kl = W.key[l];
-              if ((ke > kl) == up) {
-                W.key[e] = kl;
-                W.key[l] = ke;
-                const double tv = W.val[e];
-                W.val[e] = W.val[l];
-                W.val[l] = tv;
-              }
+      if (n2 <= T) {
+        // one element per thread in registers, T of them (pads beyond n_act): strides below
+        // 32 exchange by shuffles, strides >= 32 through W.key / W.val between barriers;
+        // the pair's two threads take the same swap decision (ties may land in either
+        // order -- the gaps do not depend on it, see the header)
+        n2 = T;
+        uint64_t kk = g.tid < n_act ? W.key[g.tid] : 0x7FF0000000000000ull;
+        double vv = g.tid < n_act ? W.val[g.tid] : 0.0;
+#pragma unroll 1
+        for (int k = 2; k <= T; k <<= 1) {
+#pragma unroll 1
+          for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            uint64_t ok;
+            double ov;
+            if (jj >= 32) {
+              g.sync();
+              W.key[g.tid] = kk;
+              W.val[g.tid] = vv;
+              g.sync();
+              ok = W.key[g.tid ^ jj];
+              ov = W.val[g.tid ^ jj];
+            } else {
+              ok = __shfl_xor_sync(0xffffffffu, kk, jj);
+              ov = __shfl_xor_sync(0xffffffffu, vv, jj);
+            }
+            const bool lower = (g.tid & jj) == 0, up = (g.tid & k) == 0;
+            const uint64_t klo = lower ? kk : ok, khi = lower ? ok : kk;
+            if ((klo > khi) == up) {
+              kk = ok;
+              vv = ov;
             }
           }
-          const int jn = jj > 1 ? jj >> 1 : k;  // the next stage's stride
-          if (NW > 1 && (jj >= 32 || jn >= 32)) g.sync();
-          else __syncwarp();
         }
+        g.sync();  // the last cross-warp exchange read before the write-back
+        W.key[g.tid] = kk;  // each thread reads back only its own element below (E = 1)
+        W.val[g.tid] = vv;
+      } else {
+        for (int e = n_act + g.tid; e < n2; e += T) {
+          W.key[e] = 0x7FF0000000000000ull;
+          W.val[e] = 0.0;
+        }
+        g.sync();
+        // compare-exchange stages: a stride below 32 keeps both elements in the owning warp
+        // (element e belongs to thread e mod T); a barrier around every stride >= 32
+        for (int k = 2; k <= n2; k <<= 1) {
+          for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int e = g.tid; e < n2; e += T) {
+              const int l = e ^ jj;
+              if (l > e) {
+                const bool up = (e & k) == 0;
+                const uint64_t ke = W.key[e], kl = W.key[l];
+                if ((ke > kl) == up) {
+                  W.key[e] = kl;
+                  W.key[l] = ke;
+                  const double tv = W.val[e];
+                  W.val[e] = W.val[l];
+                  W.val[l] = tv;
+                }
+              }
+            }
+            const int jn = jj > 1 ? jj >> 1 : k;  // the next stage's stride
+            if (NW > 1 && (jj >= 32 || jn >= 32)) g.sync();
+            else __syncwarp();
+          }
+        }
+        if (NW > 1) g.sync();
       }
-      if (NW > 1) g.sync();
       // thread owns the sorted elements [tid E, tid E + E): gamma before each element is
       // max(0, prefix max of beta of the earlier ones) (gamma_0 = 0: [0, alpha_1] first)
       const int E = n2 >= T ? n2 / T : 1;
@@ -367,14 +405,15 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
         if (G < kTwoPi) W.gaps[ng++] = make_double2(G, kTwoPi);  // [gamma_n, 2 pi]
         double theta = 0.0, L = 0.0;
         small_theta(W.gaps, ng, W.ctl[0], p.eps, &theta, &L);
-        W.ctl[1] = theta;
+        double st0 = 0.0, ct0 = 1.0;
+        if (L > 0.0) sincos(theta, &st0, &ct0);  // once per chain, not per thread
+        W.ctl[1] = st0;
         W.ctl[2] = L;
+        W.ctl[3] = ct0;
       }
       g.sync();
-      const double theta = W.ctl[1], L = W.ctl[2];
+      const double st = W.ctl[1], L = W.ctl[2], ct = W.ctl[3];
       // P' = P cos + Q sin, the safeguard (C8), the update
-      double st = 0.0, ct = 1.0;
-      if (L > 0.0) sincos(theta, &st, &ct);
       bool viol = false;
       double Pn[RT];
 #pragma unroll

@@ -99,7 +99,7 @@ def test_warp_mode_start_check_and_options():
         s.sample(X, 3, seed=1)
     assert ei.value.status == -3 and "chain 17 violates constraint 5" in str(ei.value)
     # automatic warp mode (the default) only under the automatic latency choice and for
-    # small jobs (total chains x (m d + 32 m) <= 1.6e7, from options.total_chains)
+    # small jobs (total chains x (m d + 32 m) <= 3.2e7, from options.total_chains)
     for kw in (dict(latency=0, warp_mode=2), dict(warp_mode=0), dict(latency=1, warp_mode=2),
                dict(total_chains=4096)):
         s2 = tm.Sampler(A, b, **kw)

@@ -185,12 +185,12 @@ struct SmallWarp {
   double2* gaps; // m + 2
   uint64_t* scr64;  // 8: group scan scratch
   int* scr32;       // 8
-  double* ctl;      // [0] u, [1] sin theta, [2] L, [3] cos theta; n_act at ictl[0]
+  double* ctl;      // [1] sin theta, [2] L, [3] cos theta, [4 + (t & 1)] u_t; n_act at ictl[0]
   int* ictl;
 };
 
 // Group control words after the per-warp state of small_warp_bytes
-constexpr int kSmallCtlBytes = 8 * 8 + 8 * 4 + 4 * 8 + 16;
+constexpr int kSmallCtlBytes = 8 * 8 + 8 * 4 + 6 * 8 + 16;
 
 // threads per CTA: up to 1024 (64 registers) with at most 4 rows of A per thread, else
 // up to 512 (small_max_warps)
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
   SmallWarp W;
   W.x = reinterpret_cast<double*>(wbase);
   W.nu = W.x + p.d_pad;
-  W.M1 = W.nu + p.d_pad;
+  W.M1 = W.nu + 2 * p.d_pad;  // nu double-buffered: nu_t at W.nu + (t & 1) d_pad
   W.M2 = W.M1 + p.d_pad;
   W.key = reinterpret_cast<uint64_t*>(W.M2 + p.d_pad);
   W.val = reinterpret_cast<double*>(W.key + p.n2);
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
   W.scr64 = reinterpret_cast<uint64_t*>(wbase + p.warp_bytes - kSmallCtlBytes);
   W.scr32 = reinterpret_cast<int*>(W.scr64 + 8);
   W.ctl = reinterpret_cast<double*>(W.scr32 + 8);
-  W.ictl = reinterpret_cast<int*>(W.ctl + 4);
+  W.ictl = reinterpret_cast<int*>(W.ctl + 6);
   for (int j = g.tid; j < p.d_pad; j += T) {
     W.M1[j] = 0.0;
     W.M2[j] = 0.0;
@@ -262,18 +262,19 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
     int64_t rej = 0;
     for (int it = 0; it < n_iter; ++it) {
       const uint32_t t = p.t0 + (uint32_t)it;
-      // nu_t and u_t (C12)
-      for (int pk = g.tid; pk < kpairs; pk += T) {
-        const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
-        W.nu[2 * pk] = v.x;
-        W.nu[2 * pk + 1] = v.y;
+      // nu_t and u_t (C12); with NW > 1 drawn during theta of t - 1 (below) after the first
+      double* nu = W.nu + (t & 1) * p.d_pad;
+      if (NW == 1 || it == 0) {
+        for (int pk = g.tid; pk < kpairs; pk += T) {
+          const double2 v = normal_pair_at(p.seed, t, gchain, 2 * pk, d);
+          nu[2 * pk] = v.x;
+          nu[2 * pk + 1] = v.y;
+        }
+        if (g.tid == 0) W.ctl[4 + (t & 1)] = theta_uniform(p.seed, t, gchain);
       }
-      if (g.tid == 0) {
-        W.ctl[0] = theta_uniform(p.seed, t, gchain);
-        W.ictl[0] = 0;
-      }
+      if (g.tid == 0) W.ictl[0] = 0;
       g.sync();
-      small_gemv<RT, T, MS>(AT, W.nu, d, g.tid, Q);
+      small_gemv<RT, T, MS>(AT, nu, d, g.tid, Q);
       // arcs of the active constraints (eq:roots, C1-C5), compacted (any order: sorted below)
       int n_w = 0;  // NW = 1: the running count in a register
 #pragma unroll
@@ -404,12 +405,22 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
         const double G = sbitsd(Gtot);
         if (G < kTwoPi) W.gaps[ng++] = make_double2(G, kTwoPi);  // [gamma_n, 2 pi]
         double theta = 0.0, L = 0.0;
-        small_theta(W.gaps, ng, W.ctl[0], p.eps, &theta, &L);
+        small_theta(W.gaps, ng, W.ctl[4 + (t & 1)], p.eps, &theta, &L);
         double st0 = 0.0, ct0 = 1.0;
         if (L > 0.0) sincos(theta, &st0, &ct0);  // once per chain, not per thread
         W.ctl[1] = st0;
         W.ctl[2] = L;
         W.ctl[3] = ct0;
+      } else if (NW > 1 && g.warp > 0 && it + 1 < n_iter) {
+        // nu_{t+1}, u_{t+1} while one thread computes theta (the other buffer: nu_t is read
+        // by the update below)
+        double* nn = W.nu + ((t + 1) & 1) * p.d_pad;
+        for (int pk = g.tid - 32; pk < kpairs; pk += T - 32) {
+          const double2 v = normal_pair_at(p.seed, t + 1, gchain, 2 * pk, d);
+          nn[2 * pk] = v.x;
+          nn[2 * pk + 1] = v.y;
+        }
+        if (g.tid == 32) W.ctl[4 + ((t + 1) & 1)] = theta_uniform(p.seed, t + 1, gchain);
       }
       g.sync();
       const double st = W.ctl[1], L = W.ctl[2], ct = W.ctl[3];
@@ -425,7 +436,7 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
       if (accept) {
 #pragma unroll
         for (int r = 0; r < RT; ++r) P[r] = Pn[r];
-        for (int j = g.tid; j < d; j += T) W.x[j] = fma(W.nu[j], st, __dmul_rn(W.x[j], ct));
+        for (int j = g.tid; j < d; j += T) W.x[j] = fma(nu[j], st, __dmul_rn(W.x[j], ct));
       } else {
         ++rej;
       }
@@ -459,7 +470,7 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
 size_t small_warp_bytes(int m, int64_t d_pad) {
   int n2 = 32;
   while (n2 < m) n2 <<= 1;
-  return (size_t)(4 * d_pad * 8 + (size_t)n2 * 16 + (size_t)(m + 2) * 16 + kSmallCtlBytes + 15) / 16 * 16;
+  return (size_t)(5 * d_pad * 8 + (size_t)n2 * 16 + (size_t)(m + 2) * 16 + kSmallCtlBytes + 15) / 16 * 16;
 }
 
 int small_rows(int m) {

@@ -308,11 +308,15 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
         // 32 exchange by shuffles, strides >= 32 through W.key / W.val between barriers;
         // the pair's two threads take the same swap decision (ties may land in either
         // order -- the gaps do not depend on it, see the header)
+        // (the network spans S = the power of two >= n_act only: the elements beyond are
+        // +inf pads that stay in place, so the first S come out ascending)
+        int S = 2;
+        while (S < n_act) S <<= 1;
         n2 = T;
         uint64_t kk = g.tid < n_act ? W.key[g.tid] : 0x7FF0000000000000ull;
         double vv = g.tid < n_act ? W.val[g.tid] : 0.0;
 #pragma unroll 1
-        for (int k = 2; k <= T; k <<= 1) {
+        for (int k = 2; k <= S; k <<= 1) {
 #pragma unroll 1
           for (int jj = k >> 1; jj > 0; jj >>= 1) {
             uint64_t ok;

@@ -313,34 +313,39 @@ __global__ void __launch_bounds__(R / NW >= 8 ? 512 : 1024, 1) small_kernel(cons
         int S = 2;
         while (S < n_act) S <<= 1;
         n2 = T;
+        // (key, slot) pairs: the slot (32 bits, one shuffle) indexes beta in W.val, which
+        // the sort leaves in place; the cross-warp slot exchange goes through W.gaps
+        // (free until the gaps are emitted; (m + 2) 16 >= 4 T whenever T > 32)
+        int* xs = reinterpret_cast<int*>(W.gaps);
         uint64_t kk = g.tid < n_act ? W.key[g.tid] : 0x7FF0000000000000ull;
-        double vv = g.tid < n_act ? W.val[g.tid] : 0.0;
+        int ii = g.tid < n_act ? g.tid : -1;
 #pragma unroll 1
         for (int k = 2; k <= S; k <<= 1) {
 #pragma unroll 1
           for (int jj = k >> 1; jj > 0; jj >>= 1) {
             uint64_t ok;
-            double ov;
+            int oi;
             if (jj >= 32) {
               g.sync();
               W.key[g.tid] = kk;
-              W.val[g.tid] = vv;
+              xs[g.tid] = ii;
               g.sync();
               ok = W.key[g.tid ^ jj];
-              ov = W.val[g.tid ^ jj];
+              oi = xs[g.tid ^ jj];
             } else {
               ok = __shfl_xor_sync(0xffffffffu, kk, jj);
-              ov = __shfl_xor_sync(0xffffffffu, vv, jj);
+              oi = __shfl_xor_sync(0xffffffffu, ii, jj);
             }
             const bool lower = (g.tid & jj) == 0, up = (g.tid & k) == 0;
             const uint64_t klo = lower ? kk : ok, khi = lower ? ok : kk;
             if ((klo > khi) == up) {
               kk = ok;
-              vv = ov;
+              ii = oi;
             }
           }
         }
-        g.sync();  // the last cross-warp exchange read before the write-back
+        const double vv = ii >= 0 ? W.val[ii] : 0.0;
+        g.sync();  // every beta read (and the last cross-warp exchange) before the write-back
         W.key[g.tid] = kk;  // each thread reads back only its own element below (E = 1)
         W.val[g.tid] = vv;
       } else {

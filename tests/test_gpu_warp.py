@@ -143,3 +143,29 @@ def test_chain_groups_are_bitwise_one_warp(name, C):
             assert np.max(np.abs(a - r)) <= 1e-12 * max(1.0, np.max(np.abs(r))), nw
     with pytest.raises(tm.TmvnError):  # more warps than rows of A per warp
         tm.Sampler(A, b, warp_mode=1, small_warps=2 * R).sample(X0, 2, seed=1)
+
+
+@pytest.mark.parametrize("eps,K", [(1e-5, 32), (0.0, 1), (0.05, 3)])
+def test_warp_mode_trim_and_refresh_period_vs_oracle(eps, K):
+    """S3.3 trim (reading C7: interior endpoints only, untrimmed fallback) and the refresh
+    period K (C13) in the warp mode, per step against the oracle with the same eps, on
+    the orthant (config 2) and a random polytope with ragged m, d (several 32-row blocks,
+    a partial last block) -- chain groups of 4 and 8 warps."""
+    cases = [synth.make_instance(2), synth.make_instance(3, m=211, d=37)]
+    for A, b, x0 in cases:
+        C = 96
+        s = tm.Sampler(A, b, record=0, warp_mode=1, trim_eps=eps, recompute_every=K)
+        X = np.tile(x0, (C, 1))
+        r = oracle.run(A, b, X[:24], 6, seed=4, eps=eps)  # a few chains away from x0
+        X[:24] = r["X"]
+        for t in range(5):
+            Xn = s.sample(X, 1, seed=4)
+            for c in range(0, C, 7):
+                xn, o = oracle.step(A, b, X[c], 4, t, c, eps=eps)
+                err = np.max(np.abs(Xn[c] - xn))
+                if err > REL * max(1.0, np.max(np.abs(xn))):
+                    why = step_exemption(A, b, X[c], o, projection=2, gpu_accept=not np.array_equal(Xn[c], X[c]))
+                    assert why is not None, (eps, K, t, c, err)
+            assert np.max(Xn @ A.T - b) <= 0.0
+            X = Xn
+        assert s.profile()["warp_mode_calls"] == 5

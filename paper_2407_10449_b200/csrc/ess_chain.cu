@@ -346,6 +346,14 @@ constexpr int kIdxMask = (1 << kIdxBits) - 1;
 // Measured on B200 at config 3 (one shard, ncu): DRAM per launch 372 -> 331 MB, but the
 // launch 205 -> 212 us (the next chain's rows are issued only after D1, and the live
 // arcs are recomputed behind an extra barrier): off by default.
+// L2 bulk prefetch of the next chain's P and Q rows on the global-stash path (long rows):
+// off -- measured on B200 at config 4 (one launch over 1024 chains, ncu): DRAM reads 3.58 ->
+// 3.39 GB, 1.68 -> 1.66 ms (the rows of every group's next chain, ~300 x 1.6 MB, do not
+// stay in the 126 MB L2 until they are read); config 5 +0.5 %; config 3 takes the
+// shared-memory path (its rows are bulk-copied into shared memory instead)
+#ifndef TMVN_ESS_NEXT_PREFETCH
+#define TMVN_ESS_NEXT_PREFETCH 0
+#endif
 #ifndef TMVN_ESS_KEEPPQ
 #define TMVN_ESS_KEEPPQ 0
 #endif
@@ -1015,7 +1023,7 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.arcs + cn * p.ald),
                      "r"((uint32_t)m * 16u) : "memory");
       }
-      if (!kRing && !kArcsIn && !kRows && cn < p.C) {
+      if (TMVN_ESS_NEXT_PREFETCH && !kRing && !kArcsIn && !kRows && cn < p.C) {
         const uint32_t bytes = (uint32_t)(((int64_t)m * 8 + 15) & ~15ll);
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.P_cur + cn * p.ldp), "r"(bytes)
                      : "memory");

@@ -33,6 +33,8 @@ def load(path):
 def bytes_of(m):
     return m["value"] * UNIT.get(m["unit"], 1)
 if __name__ == "__main__":
+    if len(sys.argv) < 2:  # never overwrite the committed traffic file with nothing
+        sys.exit("usage: python tools/ncu_summarize.py tag=raw.csv [tag=raw.csv ...]")
     traffic = {}
     for arg in sys.argv[1:]:
         tag, path = arg.split("=")

@@ -1,22 +1,27 @@
-// small.cu -- the warp mode (options.warp_mode): one warp per chain runs every
-// iteration of Alg. 1 for its chains in a single launch, with A resident in
-// shared memory.  For small polytopes (m <= 512 and A small enough for shared
-// memory: BASELINE configs 1 and 2, m * d <= ~20K) the throughput path is bound by
-// two launches per iteration and the latency mode by cluster barriers; here a warp
-// owns a chain for all n_iter iterations:
-//   nu_t (Philox + Box-Muller, C12) into shared memory, u_t;
-//   Q = A nu, one lane per row (A stored column-major: lane-contiguous, no bank
+// small.cu -- the warp mode (options.warp_mode): a group of NW
+// warps (NW = 1, 2, 4, 8; options.small_warps) per chain runs every iteration of Alg. 1
+// for its chains in a single launch, with A resident in shared memory.  For
+// small polytopes (m <= 512 and A small enough for shared memory: BASELINE configs 1
+// and 2) the throughput path is bound by two launches per iteration and the latency
+// mode by cluster barriers; here a group owns a chain for all n_iter iterations:
+//   nu_t (Philox + Box-Muller, C12) into shared memory, u_t (with NW > 1 drawn by
+//     warps 1..NW-1 while thread 0 computes theta of t - 1: nu double-buffered);
+//   Q = A nu, one thread per row (A stored column-major: thread-contiguous, no bank
 //     conflicts; nu broadcast), P = A x maintained incrementally (Eq. 1) and
 //     recomputed every K (C13);
-//   the arcs of eq:roots (C1-C5, the shared arc_of), compacted by ballot;
-//   Alg. 3 literally: a warp bitonic sort of the arcs by alpha, the inclusive
-//     prefix max of beta (warp scan), gaps [gamma_{k-1}, alpha_k] where
+//   the arcs of eq:roots (C1-C5, the shared arc_of), compacted by ballot + a group
+//     counter (any order);
+//   Alg. 3 literally: a bitonic sort of (alpha, slot) by alpha -- one element per
+//     thread in registers, shuffles below stride 32, shared memory across warps --,
+//     the inclusive prefix max of beta (group scan), gaps [gamma_{k-1}, alpha_k] where
 //     alpha_k > gamma_{k-1} (Prop. 1) and [gamma_n, 2 pi];
-//   one lane: merge touching segments, trim (C7), L, theta = inverse CDF (C10);
-//   P' = P cos + Q sin, the safeguard (C8) by ballot, x update, moments.
-// No block barriers (warp-synchronous), no cross-warp state except A.  The dot products
-// sum in index order (with FMA), so trajectories agree with the other paths and the
-// oracle to rounding, not bitwise.
+//   one thread: merge touching segments, trim (C7), L, theta = inverse CDF (C10),
+//     sin / cos of theta;
+//   P' = P cos + Q sin, the safeguard (C8) by a group OR, x update, moments.
+// Named barriers per group (warp-synchronous when NW = 1), no cross-group state except
+// A.  The dot products sum in index order (FMA, contraction fixed), so trajectories do
+// not depend on NW and agree with the other paths and the oracle to rounding, not
+// bitwise.
 #include <cfloat>
 
 #include "common.cuh"

@@ -351,6 +351,11 @@ constexpr int kIdxMask = (1 << kIdxBits) - 1;
 // 3.39 GB, 1.68 -> 1.66 ms (the rows of every group's next chain, ~300 x 1.6 MB, do not
 // stay in the 126 MB L2 until they are read); config 5 +0.5 %; config 3 takes the
 // shared-memory path (its rows are bulk-copied into shared memory instead)
+// constraints per level-1 bucket (ess_plan); B200, config 3 (NB = 128 at 16): 8 -> 0.216 ms,
+// 32 -> 0.208 ms, 16 -> 0.204 ms per launch; config 4 (1024 buckets either way) unchanged
+#ifndef TMVN_ESS_NB_DIV
+#define TMVN_ESS_NB_DIV 16
+#endif
 #ifndef TMVN_ESS_NEXT_PREFETCH
 #define TMVN_ESS_NEXT_PREFETCH 0
 #endif
@@ -1693,7 +1698,7 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
   }
   // buckets: about 16 constraints (~8 arcs) per level-1 bucket, 64 .. 1024
   int NB = 64;
-  while (NB < m / 16 && NB < 1024) NB <<= 1;
+  while (NB < m / TMVN_ESS_NB_DIV && NB < 1024) NB <<= 1;
   // a requested W whose per-CTA chain groups' bucket tables would not fit in shared
   // memory (e.g. W = 1, 8 groups, with 1024 level-1 buckets): more warps, fewer groups
   auto min_bytes = [&](int w) {

@@ -192,8 +192,10 @@ __device__ __forceinline__ void issue_stage(uint64_t da, uint64_t dn, uint32_t a
 // blocks.  With A' digits larger than L2 (config 5: 470 MB) the plain
 // constraint-fastest order streamed them once per chain block.  Results do not
 // depend on the order (every tile sums its whole K range).
+// band of 16 chain blocks (1024 chains): B200, config 5 136.4 vs 137.7 ms per
+// iteration with 8 (32: 137.6); config 3 unchanged
 #ifndef TMVN_OZ_BAND
-#define TMVN_OZ_BAND 8
+#define TMVN_OZ_BAND 16
 #endif
 __device__ __forceinline__ void oz_tile(int tile, int MB, int NBt, int& mb, int& nb) {
   constexpr int GN = TMVN_OZ_BAND;

@@ -356,6 +356,19 @@ constexpr int kIdxMask = (1 << kIdxBits) - 1;
 #ifndef TMVN_ESS_NB_DIV
 #define TMVN_ESS_NB_DIV 16
 #endif
+// Global-stash path (long rows): each thread prefetches into L2 (prefetch.global.L2: no
+// registers, no spills) the P and Q pairs it will load TMVN_ESS_PF_DIST passes later in the
+// active-test loop of phase A and in the P' loop of phase D1, so that more of the row is
+// in flight than the one pair per thread the register budget allows.  B200 (one launch over
+// all chains): config 4 1.647 -> 1.410 ms per launch at distance 2 (1: 1.420; 3: 1.421,
+// 4: 1.425, 6: 1.436, 12: 1.552), config 5 -4 %.  TMVN_ESS_PF_ROWS: the same in D1 on the
+// shared-memory path (config 3): 0.205 -> 0.207-0.209 ms, off.
+#ifndef TMVN_ESS_PF_DIST
+#define TMVN_ESS_PF_DIST 2
+#endif
+#ifndef TMVN_ESS_PF_ROWS
+#define TMVN_ESS_PF_ROWS 0
+#endif
 #ifndef TMVN_ESS_NEXT_PREFETCH
 #define TMVN_ESS_NEXT_PREFETCH 0
 #endif
@@ -1272,6 +1285,13 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
       const int npairs = (m + 1) / 2;
       const int npr = (npairs + T - 1) / T * T;  // whole warps stay in the loop (ballots)
       for (int base = 0; base < npr; base += kBatchA1 * T) {
+        if (TMVN_ESS_PF_DIST > 0) {  // the rows TMVN_ESS_PF_DIST passes ahead into L2 (no registers)
+          const int pf = base + g.tid + TMVN_ESS_PF_DIST * kBatchA1 * T;
+          if (pf < npairs) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P2 + pf));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(Q2 + pf));
+          }
+        }
         double2 pp[kBatchA1], qq[kBatchA1], bb[kBatchA1];
 #pragma unroll
         for (int u = 0; u < kBatchA1; ++u) {
@@ -1516,6 +1536,13 @@ __global__ void __launch_bounds__(ess_threads(W), (ess_min_blocks<W, kSrc == 1, 
       const double2* Q2 = (kRows && kKeepPQ) ? reinterpret_cast<const double2*>(AS.Qs)
                                              : reinterpret_cast<const double2*>(Qrow);
       for (int pi = g.tid; pi < npairs; pi += T) {
+        if (TMVN_ESS_PF_DIST > 0 && (!kRows || TMVN_ESS_PF_ROWS)) {
+          const int pf = pi + TMVN_ESS_PF_DIST * T;
+          if (pf < npairs) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(Ps2 + pf));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(Q2 + pf));
+          }
+        }
         const double2 pv = Ps2[pi], qv = Q2[pi], bv = __ldg(B2 + pi);
         double2 pn;
         pn.x = pv.x * ct + qv.x * st;

@@ -366,6 +366,11 @@ constexpr int kIdxMask = (1 << kIdxBits) - 1;
 #ifndef TMVN_ESS_PF_DIST
 #define TMVN_ESS_PF_DIST 2
 #endif
+// the same for the live gather's stream of stored bucket keys (par_intervals B2, global
+// stash): config 4 1.413 -> 1.364 ms per launch at distance 2 (4: 1.365), config 5 -2 %
+#ifndef TMVN_ESS_PF_AKEY
+#define TMVN_ESS_PF_AKEY 2
+#endif
 #ifndef TMVN_ESS_PF_ROWS
 #define TMVN_ESS_PF_ROWS 0
 #endif
@@ -646,6 +651,8 @@ __device__ bool par_intervals(const Grp<W>& g, const Smem& S, Ctl& ctl, const Ar
       if (S.off[k] < 0) continue;
       ab = make_double2(stash.Ps[ik & kIdxMask], stash.Qs[ik & kIdxMask]);
     } else if (akey) {
+      if (TMVN_ESS_PF_AKEY && idx + TMVN_ESS_PF_AKEY * T < n_act)  // the stream of bucket keys ahead
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(akey + idx + TMVN_ESS_PF_AKEY * T));
       k = akey[idx];
       if (S.off[k] < 0) continue;
       ab = stash.get(idx);

@@ -1729,6 +1729,10 @@ EssLaunch ess_plan(int C, int m, int W_req, int ring_req) {
     // up to two chains per SM with long rows: a 512-thread CTA per chain (C = 80..256,
     // d = m = 1000: 5-9 % per iteration; beyond 2 x SMs chains, 16 warps lose)
     if (C <= 2 * g_sms && m >= 512) W = 16;
+    // very long rows (the global-stash path with the streaming L2 prefetch): a 512-thread
+    // CTA per chain whatever the chain count (B200, one launch over all chains: config 4
+    // 1.364 -> 1.096 ms, config 5 25.3 -> 24.0 ms per launch)
+    if (m >= 8192) W = 16;
   }
   // buckets: about 16 constraints (~8 arcs) per level-1 bucket, 64 .. 1024
   int NB = 64;

@@ -246,9 +246,11 @@ tmvn_status plan_ess(tmvn_ctx* h, int64_t C) {
     // m = 100000) 2.44 -> 1.98 ms with 4 -- unless the projection dominates and its A'
     // operand exceeds L2 (config 5, d = 4096: every shard re-streams 470 MB of digits,
     // 125 -> 145 ms with 2 shards)
+    // (with 512-thread CTAs per chain for m >= 8192 and the streaming L2 prefetch, config 4
+    // measured best at 2 shards: 1.396 ms per iteration vs 1.446 at 4, 1.578 at 1)
     S = 1;
     if (h->d <= 2048) {
-      if (h->m >= 8192 && C >= 4 * 256) S = 4;
+      if (h->m >= 8192 && C >= 2 * 256) S = 2;
       else if (C >= 2 * 1024) S = 2;
     }
   }

@@ -360,8 +360,9 @@ constexpr int kIdxMask = (1 << kIdxBits) - 1;
 // registers, no spills) the P and Q pairs it will load TMVN_ESS_PF_DIST passes later in the
 // active-test loop of phase A and in the P' loop of phase D1, so that more of the row is
 // in flight than the one pair per thread the register budget allows.  B200 (one launch over
-// all chains): config 4 1.647 -> 1.410 ms per launch at distance 2 (1: 1.420; 3: 1.421,
-// 4: 1.425, 6: 1.436, 12: 1.552), config 5 -4 %.  TMVN_ESS_PF_ROWS: the same in D1 on the
+// all chains, W = 8): config 4 1.647 -> 1.410 ms per launch at distance 2 (1: 1.420; 3: 1.421,
+// 4: 1.425, 6: 1.436, 12: 1.552; with W = 16 for long rows, 2 stays best: 1 and 3 lose
+// 1-2 % at config 4), config 5 -4 %.  TMVN_ESS_PF_ROWS: the same in D1 on the
 // shared-memory path (config 3): 0.205 -> 0.207-0.209 ms, off.
 #ifndef TMVN_ESS_PF_DIST
 #define TMVN_ESS_PF_DIST 2
